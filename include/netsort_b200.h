@@ -1,0 +1,174 @@
+/*
+ * netsort_b200.h — C ABI of the B200 (sm_100a) hybrid network-base-case sort.
+ *
+ * This is the drop-in boundary under the reference's header-only C++ API
+ * (/root/reference/proj/include/netsort/hybrid.hpp, config.hpp).  The
+ * reference has no FFI of its own; its only injection point is the
+ * `std::function<void(std::span<std::int64_t>)> sort_fn` that measure_loop
+ * calls (bench.hpp:58-61, bound to run_variant at bench.cpp:94-96).  The C++
+ * host layer include/netsort_b200.hpp keeps the reference's entry points
+ * (optimized_merge_sort / optimized_quick_sort / run_variant, NetworkConfig /
+ * find_config / base_case_applies) and calls down into these functions; a
+ * ctypes / cgo / JNI binding would call them directly.
+ *
+ * Conventions
+ *   - keys are int32_t, sorted ascending, in place;
+ *   - ranges are half-open (ptr, n); the C++ layer converts the reference's
+ *     inclusive [left, right] and keeps its "right < left is a no-op" rule
+ *     (hybrid.hpp:160, 201);
+ *   - d_* pointers are caller-owned device memory; `stream` is a
+ *     cudaStream_t (NULL = legacy default stream); every device entry point
+ *     is stream-ordered and asynchronous, never synchronises unless stated;
+ *   - scratch is caller-provided: query *_temp_bytes(n) first;
+ *   - a network configuration is (width_mask, varsort_max) exactly as
+ *     NetworkConfig (config.hpp:20-26): bit w of width_mask enables the
+ *     fixed width-w network, varsort_max != 0 enables widths 2..varsort_max;
+ *   - no function throws; each returns an ns_status.  There is no CPU
+ *     fallback: without a usable sm_100a device every compute call returns
+ *     NS_ERR_CUDA.
+ */
+#ifndef NETSORT_B200_H
+#define NETSORT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum ns_status {
+  NS_OK = 0,
+  NS_ERR_INVALID = 1, /* bad argument / config (reference: std::invalid_argument) */
+  NS_ERR_CUDA = 2,    /* CUDA runtime / launch error, or no device */
+  NS_ERR_OOM = 3,     /* device or pinned-host allocation failed */
+  NS_ERR_TEMP = 4     /* caller scratch smaller than *_temp_bytes */
+} ns_status;
+
+typedef enum ns_algorithm { NS_MERGE_SORT = 0, NS_QUICK_SORT = 1 } ns_algorithm;
+
+/* ---- library / configuration ------------------------------------------ */
+
+/* Human-readable status; never NULL. */
+const char* ns_status_string(int status);
+/* Last CUDA error string recorded by this thread ("" if none). */
+const char* ns_last_error(void);
+/* ABI version (major*10000 + minor*100 + patch). */
+int ns_version(void);
+
+/* find_config — src/config.cpp:55-60.  Fills the (mask, varsort) pair of a
+ * registry preset by case-sensitive name; NS_ERR_INVALID if unknown. */
+int ns_find_config(const char* name, uint32_t* width_mask, int* varsort_max);
+/* config_registry — src/config.cpp:35-53: number of presets and their names
+ * in registry order (Classic, PowerOf2, ..., VarSort5). */
+int ns_config_count(void);
+const char* ns_config_name(int index);
+/* base_case_applies — include/netsort/config.hpp:30-36. */
+int ns_base_case_applies(int64_t size, uint32_t width_mask, int varsort_max);
+/* Per-thread leaf width the kernels use for this config (8, 4, 2 or 1): the
+ * reference recursion's shape on an 8-key window. */
+int ns_leaf_width(uint32_t width_mask, int varsort_max);
+/* The comparator list the kernels run for one width (bundled_network,
+ * networks.hpp:89-104): writes `cap` (lo,hi) byte pairs at most and returns
+ * the comparator count, or -1 for a width outside [2, 8]. */
+int ns_network_comparators(int width, uint8_t* pairs, int cap);
+
+/* ---- device entry points (caller-owned device memory) ----------------- */
+
+/* optimized_merge_sort — include/netsort/hybrid.hpp:156-177. */
+size_t ns_merge_sort_temp_bytes(size_t n);
+int ns_merge_sort_i32(int32_t* d_keys, size_t n, uint32_t width_mask, int varsort_max,
+                      void* d_temp, size_t temp_bytes, void* stream);
+
+/* optimized_quick_sort — include/netsort/hybrid.hpp:197-216.  GPU form: a
+ * sampled-splitter partition (the many-pivot analogue of median_of_three +
+ * hoare_partition, hybrid.hpp:105-133) recursing until buckets fit one CTA,
+ * whose in-shared-memory sort uses the config's network base case.  May
+ * synchronise `stream` once per partition level (bucket sizes drive the
+ * launch plan, as the partition split drives the reference recursion). */
+size_t ns_quick_sort_temp_bytes(size_t n);
+int ns_quick_sort_i32(int32_t* d_keys, size_t n, uint32_t width_mask, int varsort_max,
+                      void* d_temp, size_t temp_bytes, void* stream);
+
+/* Base-case batch (BASELINE config 2; no reference batch API — the
+ * reference would loop sort_small, networks.hpp:132-145): num_arrays
+ * independent arrays packed contiguously, array i = d_keys[d_offsets[i] ..
+ * d_offsets[i+1]); every length must lie in [0, 8].  Each array of length
+ * 2..8 is sorted by its own size-specific network; 0/1 are no-ops (the
+ * reference's apply_varsort rule, networks.hpp:166-176).  Lengths outside
+ * [0, 8] are NS_ERR_INVALID (checked on the device; the call then
+ * synchronises to report it). */
+int ns_sort_small_batch_i32(int32_t* d_keys, const uint32_t* d_offsets, size_t num_arrays,
+                            void* stream);
+
+/* Segmented sort of num_segments independent arrays of seg_len keys each,
+ * stored back to back (BASELINE config 4's 65,536 x 16,384 batch).  The
+ * reference would run `algorithm` once per segment. */
+size_t ns_segmented_sort_temp_bytes(size_t num_segments, size_t seg_len);
+int ns_segmented_sort_i32(int32_t* d_keys, size_t num_segments, size_t seg_len,
+                          int algorithm, uint32_t width_mask, int varsort_max, void* d_temp,
+                          size_t temp_bytes, void* stream);
+
+/* ---- sample-sort building blocks (multi-GPU layer, BASELINE config 5) ---
+ * The exchange itself is an NCCL all-to-all issued by the host layer; these
+ * are the per-rank device steps around it. */
+
+/* Regular sampling of a sorted shard: d_samples[k] = d_sorted[(k+1)*n/(s+1)]
+ * for k < s (PSRS).  n must be >= 1. */
+int ns_regular_samples_i32(const int32_t* d_sorted, size_t n, int s, int32_t* d_samples,
+                           void* stream);
+/* Sorts a small sample set (s <= 16384) in place and writes the g-1
+ * splitters at regular positions: d_splitters[k] = d_samples[(k+1)*s/g]. */
+int ns_select_splitters_i32(int32_t* d_samples, int s, int g, int32_t* d_splitters,
+                            void* stream);
+/* Bucket bounds of a sorted shard (int64): d_bounds[0] = 0, d_bounds[g] = n,
+ * d_bounds[k] = number of keys < d_splitters[k-1] (lower_bound), so keys
+ * equal to a splitter go to the upper bucket. */
+int ns_bucket_bounds_i32(const int32_t* d_sorted, size_t n, const int32_t* d_splitters, int g,
+                         int64_t* d_bounds, void* stream);
+/* Merges `num_runs` sorted runs that lie back to back in d_keys (run r =
+ * [d_run_offsets[r], d_run_offsets[r+1]) with host-side h_run_offsets the
+ * same values) into one sorted array, in place. */
+size_t ns_merge_runs_temp_bytes(size_t n, int num_runs);
+int ns_merge_runs_i32(int32_t* d_keys, const int64_t* h_run_offsets, int num_runs,
+                      void* d_temp, size_t temp_bytes, void* stream);
+
+/* ---- checking helpers (used by tests and bench, not by the sort) ------- */
+
+/* d_out[0] += sum of mix64(key), d_out[1] ^= xor of mix64(key) (uint64);
+ * an order-independent multiset digest (matches the oracle's). */
+int ns_multiset_digest_i32(const int32_t* d_keys, size_t n, uint64_t* d_out, void* stream);
+/* d_out[0] += number of i with d_keys[i] > d_keys[i+1] (0 == sorted). */
+int ns_count_inversions_i32(const int32_t* d_keys, size_t n, unsigned long long* d_out,
+                            void* stream);
+
+/* Device generator for the seeded inputs (bench/tests): kind 0 = uniform
+ * random int32 in [0, 2^31) = int32(SplitMix64(seed).next() >> 33) element by
+ * element (datagen.hpp:29-42 narrowed as in SURVEY.md §8(d)); kind 1 = the
+ * ramp 0..n-1.  Identical to oracle_generate_i32 for the same (kind, seed). */
+int ns_generate_i32(int32_t* d_out, size_t n, int kind, uint64_t seed, void* stream);
+
+/* ---- instrumentation ----------------------------------------------------
+ * ns_launch_count: kernels this library has launched since load (process-
+ * wide).  The profiler, when enabled, records a CUDA event pair around every
+ * launch on the launching stream, grouped by kernel class; ns_profile_read
+ * synchronises those events and returns the summed device time and launch
+ * count of one class.  ns_profile_enable(0|1) also clears the records. */
+uint64_t ns_launch_count(void);
+int ns_profile_enable(int on);
+int ns_profile_kinds(void);
+const char* ns_profile_kind_name(int kind);
+int ns_profile_read(int kind, double* total_ms, uint64_t* launches);
+
+/* ---- host-buffer entry points (the reference's own call shape) ---------
+ * Sort a HOST array in place, exactly like optimized_merge_sort(span, cfg):
+ * copies through pinned staging to the current device, sorts, copies back,
+ * synchronises.  Device buffers are cached per thread (ns_release_cache). */
+int ns_merge_sort_host_i32(int32_t* h_keys, size_t n, uint32_t width_mask, int varsort_max);
+int ns_quick_sort_host_i32(int32_t* h_keys, size_t n, uint32_t width_mask, int varsort_max);
+int ns_release_cache(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NETSORT_B200_H */

@@ -1,0 +1,135 @@
+// netsort_b200.hpp — C++20 host API with the reference's entry points.
+//
+// Mirrors /root/reference/proj/include/netsort/{config,hybrid}.hpp for int32
+// keys so that a user of the reference can switch by changing the namespace:
+//   NetworkConfig, base_case_applies      config.hpp:20-36
+//   config_registry, find_config, ...     src/config.cpp:11-70
+//   optimized_merge_sort (3 overloads)    hybrid.hpp:156-177
+//   classical_merge_sort                  hybrid.hpp:180-183
+//   optimized_quick_sort (3 overloads)    hybrid.hpp:197-216
+//   classical_quick_sort                  hybrid.hpp:220-223
+//   run_variant                           hybrid.hpp:225-232
+// The spans are HOST memory sorted in place, as in the reference; the work
+// runs on the current CUDA device through the C ABI (netsort_b200.h).  The
+// device_* overloads take caller-owned device memory and a stream instead.
+// Errors: config errors throw std::invalid_argument (as the reference does,
+// config.cpp:16-19, networks.hpp:99-114); device errors throw
+// std::runtime_error.  There is no CPU fallback.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <initializer_list>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <string_view>
+#include <vector>
+
+#include "netsort_b200.h"
+
+namespace netsort_b200 {
+
+inline constexpr int kMinNetworkWidth = 2;
+inline constexpr int kMaxNetworkWidth = 8;
+
+enum class Algorithm { merge_sort, quick_sort };
+std::string_view algorithm_name(Algorithm a);
+
+struct NetworkConfig {
+  std::string name;
+  std::uint32_t width_mask = 0;
+  int varsort_max = 0;
+  bool is_classic() const { return width_mask == 0 && varsort_max == 0; }
+};
+
+inline bool base_case_applies(std::ptrdiff_t size, const NetworkConfig& cfg) {
+  if (size >= kMinNetworkWidth && size <= kMaxNetworkWidth && ((cfg.width_mask >> size) & 1u))
+    return true;
+  return cfg.varsort_max != 0 && size >= 2 && size <= cfg.varsort_max;
+}
+
+NetworkConfig make_fixed_config(std::string name, std::initializer_list<int> widths);
+NetworkConfig make_varsort_config(std::string name, int max_width);
+NetworkConfig classic_config();
+const std::vector<NetworkConfig>& config_registry();
+const NetworkConfig* find_config(std::string_view name);
+
+struct SortVariant {
+  Algorithm algorithm;
+  NetworkConfig config;
+};
+std::vector<SortVariant> bundled_variants();
+
+namespace detail {
+inline void check(int status, const char* what) {
+  if (status == NS_OK) return;
+  std::string msg = std::string(what) + ": " + ns_status_string(status);
+  const char* cuda = ns_last_error();
+  if (cuda && *cuda) msg += std::string(" (") + cuda + ")";
+  if (status == NS_ERR_INVALID) throw std::invalid_argument(msg);
+  throw std::runtime_error(msg);
+}
+}  // namespace detail
+
+// ---- host spans (the reference's own call shape) --------------------------
+
+inline void optimized_merge_sort(std::span<std::int32_t> a, std::ptrdiff_t left,
+                                 std::ptrdiff_t right, const NetworkConfig& cfg) {
+  if (right < left) return;  // hybrid.hpp:160
+  if (left < 0 || right >= static_cast<std::ptrdiff_t>(a.size()))
+    throw std::invalid_argument("optimized_merge_sort: range outside the span");
+  detail::check(ns_merge_sort_host_i32(a.data() + left, static_cast<size_t>(right - left + 1),
+                                       cfg.width_mask, cfg.varsort_max),
+                "optimized_merge_sort");
+}
+inline void optimized_merge_sort(std::span<std::int32_t> a, const NetworkConfig& cfg) {
+  optimized_merge_sort(a, 0, static_cast<std::ptrdiff_t>(a.size()) - 1, cfg);
+}
+inline void classical_merge_sort(std::span<std::int32_t> a) {
+  optimized_merge_sort(a, classic_config());
+}
+
+inline void optimized_quick_sort(std::span<std::int32_t> a, std::ptrdiff_t low,
+                                 std::ptrdiff_t high, const NetworkConfig& cfg) {
+  if (high < low) return;  // hybrid.hpp:201
+  if (low < 0 || high >= static_cast<std::ptrdiff_t>(a.size()))
+    throw std::invalid_argument("optimized_quick_sort: range outside the span");
+  detail::check(ns_quick_sort_host_i32(a.data() + low, static_cast<size_t>(high - low + 1),
+                                       cfg.width_mask, cfg.varsort_max),
+                "optimized_quick_sort");
+}
+inline void optimized_quick_sort(std::span<std::int32_t> a, const NetworkConfig& cfg) {
+  optimized_quick_sort(a, 0, static_cast<std::ptrdiff_t>(a.size()) - 1, cfg);
+}
+inline void classical_quick_sort(std::span<std::int32_t> a) {
+  optimized_quick_sort(a, classic_config());
+}
+
+inline void run_variant(const SortVariant& v, std::span<std::int32_t> a) {
+  if (v.algorithm == Algorithm::merge_sort) optimized_merge_sort(a, v.config);
+  else optimized_quick_sort(a, v.config);
+}
+
+// ---- device spans (caller-owned device memory, stream-ordered) ------------
+
+class DeviceScratch {
+ public:
+  DeviceScratch() = default;
+  DeviceScratch(const DeviceScratch&) = delete;
+  DeviceScratch& operator=(const DeviceScratch&) = delete;
+  ~DeviceScratch();
+  void* reserve(size_t bytes);  // grows, never shrinks
+  size_t size() const { return bytes_; }
+
+ private:
+  void* ptr_ = nullptr;
+  size_t bytes_ = 0;
+};
+
+void device_merge_sort(std::int32_t* d_keys, size_t n, const NetworkConfig& cfg,
+                       DeviceScratch& scratch, void* stream = nullptr);
+void device_quick_sort(std::int32_t* d_keys, size_t n, const NetworkConfig& cfg,
+                       DeviceScratch& scratch, void* stream = nullptr);
+
+}  // namespace netsort_b200

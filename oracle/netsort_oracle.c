@@ -1,0 +1,276 @@
+/*
+ * netsort_oracle.c — plain-C restatement of the reference hot path.
+ *
+ * TEST INFRASTRUCTURE ONLY (see netsort_oracle.h).  The product never links
+ * this file.  Paths in citations are relative to /root/reference/proj.
+ */
+#include "netsort_oracle.h"
+
+#include <stdlib.h>
+#include <string.h>
+
+/* ---- input generation ------------------------------------------------- */
+
+/* SplitMix64::next — include/netsort/datagen.hpp:33-38 */
+uint64_t oracle_splitmix64_next(uint64_t* state) {
+  uint64_t z = (*state += 0x9E3779B97F4A7C15ull);
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+/* generate — src/datagen.cpp:18-50, written once for both widths. */
+#define GEN_BODY(T, RANDOM_EXPR)                                              \
+  if (kind == 2 && !(p >= 0.0 && p <= 1.0)) return -1;                       \
+  if (kind == 0) {                                                           \
+    uint64_t s = seed;                                                       \
+    for (size_t i = 0; i < n; ++i) {                                         \
+      uint64_t r = oracle_splitmix64_next(&s);                               \
+      out[i] = (T)(RANDOM_EXPR);                                             \
+    }                                                                        \
+    return 0;                                                                \
+  }                                                                          \
+  for (size_t i = 0; i < n; ++i) out[i] = (T)i;                              \
+  if (kind == 2) {                                                           \
+    size_t swaps = (size_t)(p * (double)n);                                  \
+    if (swaps == 0 && n >= 2 && p > 0.0) swaps = 1;                          \
+    uint64_t s = seed;                                                       \
+    for (size_t k = 0; k < swaps; ++k) {                                     \
+      size_t i = (size_t)(oracle_splitmix64_next(&s) % n);                   \
+      size_t j = (size_t)(oracle_splitmix64_next(&s) % n);                   \
+      T t = out[i];                                                          \
+      out[i] = out[j];                                                       \
+      out[j] = t;                                                            \
+    }                                                                        \
+  }                                                                          \
+  return 0;
+
+int oracle_generate_i32(int kind, size_t n, uint64_t seed, double p, int32_t* out) {
+  GEN_BODY(int32_t, r >> 33)
+}
+
+int oracle_generate_i64(int kind, size_t n, uint64_t seed, double p, int64_t* out) {
+  GEN_BODY(int64_t, r)
+}
+
+size_t oracle_generate_batch_i32(size_t num_arrays, uint64_t seed, uint32_t* offsets,
+                                 int32_t* keys) {
+  uint64_t ls = seed;
+  size_t total = 0;
+  for (size_t a = 0; a < num_arrays; ++a) {
+    if (offsets) offsets[a] = (uint32_t)total;
+    total += 3 + (size_t)(oracle_splitmix64_next(&ls) % 6);
+  }
+  if (offsets) offsets[num_arrays] = (uint32_t)total;
+  if (keys) {
+    uint64_t ks = seed ^ 0x5bd1e995ull;
+    for (size_t i = 0; i < total; ++i) keys[i] = (int32_t)(oracle_splitmix64_next(&ks) >> 33);
+  }
+  return total;
+}
+
+/* ---- networks ---------------------------------------------------------- */
+
+/* Optimal-size comparator lists, widths 2..8 (sizes 1,3,5,9,12,16,19 as in
+ * include/netsort/networks.hpp:49-72).  Any zero-one-complete network of the
+ * same width yields the identical output; tests/test_oracle.py re-verifies
+ * these exhaustively. */
+static const uint8_t kW2[][2] = {{0, 1}};
+static const uint8_t kW3[][2] = {{1, 2}, {0, 2}, {0, 1}};
+static const uint8_t kW4[][2] = {{0, 1}, {2, 3}, {0, 2}, {1, 3}, {1, 2}};
+static const uint8_t kW5[][2] = {{0, 1}, {3, 4}, {2, 4}, {2, 3}, {0, 3},
+                                 {0, 2}, {1, 4}, {1, 3}, {1, 2}};
+static const uint8_t kW6[][2] = {{1, 2}, {4, 5}, {0, 2}, {3, 5}, {0, 1}, {3, 4},
+                                 {2, 5}, {0, 3}, {1, 4}, {2, 4}, {1, 3}, {2, 3}};
+static const uint8_t kW7[][2] = {{1, 2}, {3, 4}, {5, 6}, {0, 2}, {3, 5}, {4, 6},
+                                 {0, 1}, {4, 5}, {2, 6}, {0, 4}, {1, 5}, {0, 3},
+                                 {2, 5}, {1, 3}, {2, 4}, {2, 3}};
+static const uint8_t kW8[][2] = {{0, 2}, {1, 3}, {4, 6}, {5, 7}, {0, 4}, {1, 5}, {2, 6},
+                                 {3, 7}, {0, 1}, {2, 3}, {4, 5}, {6, 7}, {2, 4}, {3, 5},
+                                 {1, 4}, {3, 6}, {1, 2}, {3, 4}, {5, 6}};
+
+static const uint8_t (*net_table(int w, int* count))[2] {
+  switch (w) {
+    case 2: *count = 1; return kW2;
+    case 3: *count = 3; return kW3;
+    case 4: *count = 5; return kW4;
+    case 5: *count = 9; return kW5;
+    case 6: *count = 12; return kW6;
+    case 7: *count = 16; return kW7;
+    case 8: *count = 19; return kW8;
+    default: *count = -1; return NULL;
+  }
+}
+
+int oracle_network(int width, uint8_t* pairs, int cap) {
+  int count;
+  const uint8_t(*t)[2] = net_table(width, &count);
+  if (!t) return -1;
+  for (int i = 0; i < count && i < cap; ++i) {
+    pairs[2 * i] = t[i][0];
+    pairs[2 * i + 1] = t[i][1];
+  }
+  return count;
+}
+
+/* compare_exchange — networks.hpp:25-32 (select form, no branch on data) */
+static inline void cx(int32_t* a, int32_t* b) {
+  const int32_t x = *a, y = *b;
+  const int ooo = y < x;
+  *a = ooo ? y : x;
+  *b = ooo ? x : y;
+}
+
+/* sort_small — networks.hpp:132-145 */
+void oracle_sort_small_i32(int32_t* v, int size) {
+  int count;
+  const uint8_t(*t)[2] = net_table(size, &count);
+  if (!t) return;
+  for (int i = 0; i < count; ++i) cx(&v[t[i][0]], &v[t[i][1]]);
+}
+
+/* base_case_applies — config.hpp:30-36 (fixed widths first, then varsort) */
+int oracle_base_case_applies(int64_t size, uint32_t width_mask, int varsort_max) {
+  if (size >= 2 && size <= 8 && ((width_mask >> size) & 1u)) return 1;
+  return varsort_max != 0 && size >= 2 && size <= varsort_max;
+}
+
+/* ---- merge sort -------------------------------------------------------- */
+
+static inline void st_depth(oracle_stats* s, int d) {
+  if (s && d > s->max_depth) s->max_depth = d;
+}
+
+/* try_base_case — hybrid.hpp:48-56 */
+static int try_base(int32_t* a, int64_t left, int64_t size, uint32_t mask, int vs,
+                    oracle_stats* st) {
+  if (!oracle_base_case_applies(size, mask, vs)) return 0;
+  if (st) st->network_hits[size]++;
+  oracle_sort_small_i32(a + left, (int)size);
+  return 1;
+}
+
+/* merge_runs — hybrid.hpp:61-79: left run staged in scratch, left wins ties */
+static void merge_runs(int32_t* a, int64_t left, int64_t mid, int64_t right,
+                       int32_t* scratch) {
+  const int64_t left_len = mid - left + 1;
+  memcpy(scratch, a + left, (size_t)left_len * sizeof(int32_t));
+  int64_t i = 0, j = mid + 1, out = left;
+  while (i < left_len && j <= right) {
+    if (a[j] < scratch[i]) a[out++] = a[j++];
+    else a[out++] = scratch[i++];
+  }
+  while (i < left_len) a[out++] = scratch[i++];
+}
+
+/* merge_sort_rec — hybrid.hpp:81-95 */
+static void ms_rec(int32_t* a, int64_t left, int64_t right, uint32_t mask, int vs,
+                   int32_t* scratch, oracle_stats* st, int depth) {
+  st_depth(st, depth);
+  const int64_t size = right - left + 1;
+  if (try_base(a, left, size, mask, vs, st)) return;
+  if (left < right) {
+    const int64_t mid = left + (right - left) / 2;
+    ms_rec(a, left, mid, mask, vs, scratch, st, depth + 1);
+    ms_rec(a, mid + 1, right, mask, vs, scratch, st, depth + 1);
+    if (st) st->merges++;
+    merge_runs(a, left, mid, right, scratch);
+  }
+}
+
+/* optimized_merge_sort — hybrid.hpp:156-165 */
+void oracle_merge_sort_i32(int32_t* a, int64_t left, int64_t right, uint32_t mask,
+                           int vs, oracle_stats* st) {
+  if (right < left) return;
+  int32_t* scratch = (int32_t*)malloc((size_t)(right - left + 1) * sizeof(int32_t));
+  ms_rec(a, left, right, mask, vs, scratch, st, 1);
+  free(scratch);
+}
+
+/* merge — hybrid.hpp:186-193 */
+void oracle_merge_i32(int32_t* a, int64_t left, int64_t mid, int64_t right) {
+  int32_t* scratch = (int32_t*)malloc((size_t)(mid - left + 1) * sizeof(int32_t));
+  merge_runs(a, left, mid, right, scratch);
+  free(scratch);
+}
+
+/* ---- quick sort -------------------------------------------------------- */
+
+/* median_of_three — hybrid.hpp:105-114 */
+int32_t oracle_median_of_three_i32(int32_t* a, int64_t low, int64_t high) {
+  if (high - low < 2) return a[low];
+  const int64_t mid = low + (high - low) / 2;
+  cx(&a[low], &a[mid]);
+  cx(&a[low], &a[high]);
+  cx(&a[mid], &a[high]);
+  return a[mid];
+}
+
+/* hoare_partition — hybrid.hpp:121-133 (j == high fix-up at 130) */
+int64_t oracle_hoare_partition_i32(int32_t* a, int64_t low, int64_t high, int32_t pivot) {
+  int64_t i = low - 1, j = high + 1;
+  for (;;) {
+    do { ++i; } while (a[i] < pivot);
+    do { --j; } while (pivot < a[j]);
+    if (i >= j) return j < high ? j : high - 1;
+    const int32_t t = a[i];
+    a[i] = a[j];
+    a[j] = t;
+  }
+}
+
+/* quick_sort_rec — hybrid.hpp:137-150 */
+static void qs_rec(int32_t* a, int64_t low, int64_t high, uint32_t mask, int vs,
+                   oracle_stats* st, int depth) {
+  st_depth(st, depth);
+  const int64_t size = high - low + 1;
+  if (try_base(a, low, size, mask, vs, st)) return;
+  if (low < high) {
+    const int32_t pivot = oracle_median_of_three_i32(a, low, high);
+    if (st) st->partitions++;
+    const int64_t split = oracle_hoare_partition_i32(a, low, high, pivot);
+    qs_rec(a, low, split, mask, vs, st, depth + 1);
+    qs_rec(a, split + 1, high, mask, vs, st, depth + 1);
+  }
+}
+
+/* optimized_quick_sort — hybrid.hpp:197-204 */
+void oracle_quick_sort_i32(int32_t* a, int64_t low, int64_t high, uint32_t mask, int vs,
+                           oracle_stats* st) {
+  if (high < low) return;
+  qs_rec(a, low, high, mask, vs, st, 1);
+}
+
+/* ---- batch helpers ----------------------------------------------------- */
+
+void oracle_sort_small_batch_i32(int32_t* keys, const uint32_t* offsets, size_t num_arrays) {
+  for (size_t i = 0; i < num_arrays; ++i) {
+    const int len = (int)(offsets[i + 1] - offsets[i]);
+    oracle_sort_small_i32(keys + offsets[i], len);
+  }
+}
+
+void oracle_segmented_quick_sort_i32(int32_t* keys, size_t num_segments, size_t seg_len,
+                                     uint32_t mask, int vs) {
+  for (size_t s = 0; s < num_segments; ++s)
+    oracle_quick_sort_i32(keys + s * seg_len, 0, (int64_t)seg_len - 1, mask, vs, NULL);
+}
+
+/* ---- digest ------------------------------------------------------------ */
+
+static inline uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+void oracle_multiset_digest_i32(const int32_t* keys, size_t n, uint64_t out[2]) {
+  uint64_t s = 0, x = 0;
+  for (size_t i = 0; i < n; ++i) {
+    const uint64_t m = mix64((uint64_t)(uint32_t)keys[i] + 0x9E3779B97F4A7C15ull);
+    s += m;
+    x ^= m;
+  }
+  out[0] = s;
+  out[1] = x;
+}

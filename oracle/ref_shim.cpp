@@ -1,0 +1,156 @@
+// ref_shim.cpp — extern "C" wrapper over the UNMODIFIED reference headers.
+//
+// TEST INFRASTRUCTURE ONLY.  Compiled by oracle/Makefile against the
+// reference sources where they lie (/root/reference/proj/include,
+// src/config.cpp, src/datagen.cpp) into oracle/_ref/libnetsort_ref.so.  No
+// reference source is copied into this repo; this file only instantiates the
+// reference templates at int32_t and exposes them over a C ABI so the tests
+// can pin oracle/netsort_oracle.c against the reference itself, and bench.py
+// can time the reference as the CPU baseline.
+#include <cstdint>
+#include <cstring>
+#include <span>
+#include <string_view>
+#include <vector>
+
+#include "netsort/config.hpp"
+#include "netsort/datagen.hpp"
+#include "netsort/hybrid.hpp"
+#include "netsort/networks.hpp"
+
+using namespace netsort;
+
+extern "C" {
+
+// find_config — src/config.cpp:55-60.  Returns 0 on success.
+int ref_find_config(const char* name, uint32_t* width_mask, int* varsort_max) {
+  const NetworkConfig* c = find_config(std::string_view(name));
+  if (!c) return -1;
+  *width_mask = c->width_mask;
+  *varsort_max = c->varsort_max;
+  return 0;
+}
+
+int ref_config_count() { return static_cast<int>(config_registry().size()); }
+
+const char* ref_config_name(int i) {
+  const auto& r = config_registry();
+  if (i < 0 || i >= static_cast<int>(r.size())) return nullptr;
+  return r[static_cast<size_t>(i)].name.c_str();
+}
+
+static NetworkConfig cfg_of(uint32_t mask, int vs) { return NetworkConfig{"shim", mask, vs}; }
+
+static void copy_stats(const DispatchStats& s, uint64_t* out) {
+  // layout: hits[0..8], merges, partitions, max_depth
+  if (!out) return;
+  for (int w = 0; w <= 8; ++w) out[w] = s.network_hits[static_cast<size_t>(w)];
+  out[9] = s.merges;
+  out[10] = s.partitions;
+  out[11] = static_cast<uint64_t>(s.max_depth);
+}
+
+// optimized_merge_sort — include/netsort/hybrid.hpp:156-177
+void ref_merge_sort_i32(int32_t* a, int64_t n, uint32_t mask, int vs, uint64_t* stats) {
+  std::span<int32_t> s(a, static_cast<size_t>(n));
+  if (stats) {
+    DispatchStats st;
+    optimized_merge_sort(s, 0, static_cast<std::ptrdiff_t>(n) - 1, cfg_of(mask, vs), st);
+    copy_stats(st, stats);
+  } else {
+    optimized_merge_sort(s, cfg_of(mask, vs));
+  }
+}
+
+// optimized_quick_sort — include/netsort/hybrid.hpp:197-216
+void ref_quick_sort_i32(int32_t* a, int64_t n, uint32_t mask, int vs, uint64_t* stats) {
+  std::span<int32_t> s(a, static_cast<size_t>(n));
+  if (stats) {
+    DispatchStats st;
+    optimized_quick_sort(s, 0, static_cast<std::ptrdiff_t>(n) - 1, cfg_of(mask, vs), st);
+    copy_stats(st, stats);
+  } else {
+    optimized_quick_sort(s, cfg_of(mask, vs));
+  }
+}
+
+// Range form with inclusive bounds (hybrid.hpp:156-172, 197-211).
+void ref_merge_sort_range_i32(int32_t* a, int64_t n, int64_t left, int64_t right,
+                              uint32_t mask, int vs) {
+  optimized_merge_sort(std::span<int32_t>(a, static_cast<size_t>(n)), left, right,
+                       cfg_of(mask, vs));
+}
+void ref_quick_sort_range_i32(int32_t* a, int64_t n, int64_t low, int64_t high,
+                              uint32_t mask, int vs) {
+  optimized_quick_sort(std::span<int32_t>(a, static_cast<size_t>(n)), low, high,
+                       cfg_of(mask, vs));
+}
+
+// sort_small — networks.hpp:132-145
+void ref_sort_small_i32(int32_t* v, int size) { sort_small(v, size); }
+
+void ref_sort_small_batch_i32(int32_t* keys, const uint32_t* offsets, int64_t num_arrays) {
+  for (int64_t i = 0; i < num_arrays; ++i)
+    sort_small(keys + offsets[i], static_cast<int>(offsets[i + 1] - offsets[i]));
+}
+
+void ref_segmented_quick_sort_i32(int32_t* keys, int64_t num_segments, int64_t seg_len,
+                                  uint32_t mask, int vs) {
+  const NetworkConfig cfg = cfg_of(mask, vs);
+  for (int64_t s = 0; s < num_segments; ++s)
+    optimized_quick_sort(std::span<int32_t>(keys + s * seg_len, static_cast<size_t>(seg_len)),
+                         cfg);
+}
+
+// bundled_network — networks.hpp:89-104
+int ref_network(int width, uint8_t* pairs, int cap) {
+  try {
+    const SortingNetwork& net = bundled_network(width);
+    int i = 0;
+    for (const Comparator c : net.comparators) {
+      if (i < cap) {
+        pairs[2 * i] = c.lo;
+        pairs[2 * i + 1] = c.hi;
+      }
+      ++i;
+    }
+    return i;
+  } catch (...) {
+    return -1;
+  }
+}
+
+// median_of_three / hoare_partition — hybrid.hpp:105-133
+int32_t ref_median_of_three_i32(int32_t* a, int64_t n, int64_t low, int64_t high) {
+  return median_of_three(std::span<int32_t>(a, static_cast<size_t>(n)), low, high);
+}
+int64_t ref_hoare_partition_i32(int32_t* a, int64_t n, int64_t low, int64_t high,
+                                int32_t pivot) {
+  return hoare_partition(std::span<int32_t>(a, static_cast<size_t>(n)), low, high, pivot);
+}
+
+// generate — src/datagen.cpp:18-50 (the reference's int64 stream)
+int ref_generate_i64(int kind, int64_t n, uint64_t seed, double p, int64_t* out) {
+  try {
+    GenSpec spec;
+    spec.size = static_cast<size_t>(n);
+    spec.distribution.kind = kind == 0 ? Dist::random : kind == 1 ? Dist::sorted
+                                                                  : Dist::nearly_sorted;
+    spec.distribution.perturbation = p;
+    spec.seed = seed;
+    std::vector<int64_t> v = generate(spec);
+    std::memcpy(out, v.data(), v.size() * sizeof(int64_t));
+    return 0;
+  } catch (...) {
+    return -1;
+  }
+}
+
+uint64_t ref_splitmix64_nth(uint64_t seed, int64_t k) {
+  SplitMix64 r(seed);
+  uint64_t v = 0;
+  for (int64_t i = 0; i <= k; ++i) v = r.next();
+  return v;
+}
+
+}  // extern "C"

@@ -1,0 +1,12 @@
+"""netsort-b200: merge sort and quick sort over int32 keys whose recursion
+bottoms out in fixed sorting networks (arXiv 2503.05934), rebuilt for B200
+(sm_100a).  The compute lives in lib/libnetsort_b200.so behind the C ABI
+include/netsort_b200.h; this package is the Python host layer over it."""
+from ._lib import NetsortError, build, lib  # noqa: F401
+from .api import (  # noqa: F401
+    Algorithm, NetworkConfig, SortVariant, algorithm_name, base_case_applies,
+    bundled_variants, classic_config, classical_merge_sort, classical_quick_sort,
+    config_registry, count_inversions, find_config, kMaxNetworkWidth, kMinNetworkWidth,
+    leaf_width, make_fixed_config, make_varsort_config, multiset_digest, network,
+    optimized_merge_sort, optimized_quick_sort, release_scratch, run_variant,
+    segmented_sort, sort_small_batch)

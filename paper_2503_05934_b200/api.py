@@ -1,0 +1,290 @@
+"""Python host API mirroring the reference's C++ interface.
+
+Names, argument meaning and error behaviour follow
+/root/reference/proj/include/netsort/{config,hybrid}.hpp:
+  NetworkConfig / base_case_applies          config.hpp:20-36
+  config_registry / find_config / ...        src/config.cpp:11-70
+  optimized_merge_sort(a, [left, right,] cfg) hybrid.hpp:156-177
+  optimized_quick_sort(a, [low, high,] cfg)   hybrid.hpp:197-216
+  classical_merge_sort / classical_quick_sort hybrid.hpp:180-183, 220-223
+  run_variant(variant, a)                     hybrid.hpp:225-232
+Arrays are sorted IN PLACE.  ``a`` may be a CUDA int32 tensor (device path:
+no host copies, stream-ordered on torch's current stream) or a host int32
+numpy array (the reference's call shape: copied to the GPU, sorted, copied
+back).  Everything executes in the sm_100a library through the C ABI; there
+is no CPU fallback.  Configuration errors raise ValueError (the reference
+throws std::invalid_argument), device errors raise NetsortError.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+from ._lib import check, lib
+
+try:  # torch is plumbing for device memory and streams
+    import torch
+except Exception:  # pragma: no cover - torch is present in this image
+    torch = None
+
+kMinNetworkWidth = 2
+kMaxNetworkWidth = 8
+
+
+class Algorithm(enum.Enum):
+    merge_sort = 0
+    quick_sort = 1
+
+
+def algorithm_name(a: Algorithm) -> str:
+    return "MergeSort" if a is Algorithm.merge_sort else "QuickSort"
+
+
+@dataclass(frozen=True)
+class NetworkConfig:
+    name: str
+    width_mask: int = 0
+    varsort_max: int = 0
+
+    def is_classic(self) -> bool:
+        return self.width_mask == 0 and self.varsort_max == 0
+
+
+@dataclass(frozen=True)
+class SortVariant:
+    algorithm: Algorithm
+    config: NetworkConfig
+
+
+def base_case_applies(size: int, cfg: NetworkConfig) -> bool:
+    return bool(lib().ns_base_case_applies(int(size), cfg.width_mask, cfg.varsort_max))
+
+
+def make_fixed_config(name: str, widths: Sequence[int]) -> NetworkConfig:
+    mask = 0
+    for w in widths:
+        if w < 3 or w > kMaxNetworkWidth:
+            raise ValueError(f"fixed network width must be in [3, 8], got {w}")
+        mask |= 1 << w
+    return NetworkConfig(name, mask, 0)
+
+
+def make_varsort_config(name: str, max_width: int) -> NetworkConfig:
+    if max_width < 3 or max_width > 5:
+        raise ValueError(f"varsort max width must be 3, 4, or 5, got {max_width}")
+    return NetworkConfig(name, 0, max_width)
+
+
+def classic_config() -> NetworkConfig:
+    return NetworkConfig("Classic", 0, 0)
+
+
+_REGISTRY: Optional[list] = None
+
+
+def config_registry() -> list:
+    """The 12 presets in registry order, read from the library."""
+    global _REGISTRY
+    if _REGISTRY is None:
+        L = lib()
+        reg = []
+        for i in range(L.ns_config_count()):
+            name = L.ns_config_name(i).decode()
+            m, v = C.c_uint32(), C.c_int()
+            check(L.ns_find_config(name.encode(), C.byref(m), C.byref(v)), "ns_find_config")
+            reg.append(NetworkConfig(name, m.value, v.value))
+        _REGISTRY = reg
+    return list(_REGISTRY)
+
+
+def find_config(name: str) -> Optional[NetworkConfig]:
+    for c in config_registry():
+        if c.name == name:
+            return c
+    return None
+
+
+def bundled_variants() -> list:
+    return [SortVariant(a, c) for a in (Algorithm.merge_sort, Algorithm.quick_sort)
+            for c in config_registry()]
+
+
+def network(width: int) -> list:
+    """The comparator list the kernels run for `width` (bundled_network)."""
+    buf = (C.c_uint8 * 64)()
+    cnt = lib().ns_network_comparators(int(width), C.cast(buf, C.c_void_p), 32)
+    if cnt < 0:
+        raise ValueError(f"no bundled network of width {width}")
+    return [(buf[2 * i], buf[2 * i + 1]) for i in range(cnt)]
+
+
+def leaf_width(cfg: NetworkConfig) -> int:
+    return int(lib().ns_leaf_width(cfg.width_mask, cfg.varsort_max))
+
+
+# ---- device scratch -------------------------------------------------------
+
+_SCRATCH: dict = {}
+
+
+def scratch(nbytes: int, device) -> int:
+    """Device pointer to >= nbytes of cached scratch on `device` (0 if none)."""
+    if nbytes == 0:
+        return 0
+    key = torch.device(device).index if torch.device(device).index is not None else \
+        torch.cuda.current_device()
+    buf = _SCRATCH.get(key)
+    if buf is None or buf.numel() < nbytes:
+        _SCRATCH.pop(key, None)
+        buf = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{key}")
+        _SCRATCH[key] = buf
+    return buf.data_ptr()
+
+
+def release_scratch() -> None:
+    _SCRATCH.clear()
+    lib().ns_release_cache()
+
+
+def _stream_ptr(t) -> int:
+    return torch.cuda.current_stream(t.device).cuda_stream
+
+
+def _is_device(a) -> bool:
+    return torch is not None and isinstance(a, torch.Tensor) and a.is_cuda
+
+
+def _check_tensor(a):
+    if a.dtype != torch.int32:
+        raise ValueError(f"keys must be int32, got {a.dtype}")
+    if not a.is_contiguous():
+        raise ValueError("keys must be contiguous")
+
+
+def _check_host(a):
+    if not isinstance(a, np.ndarray) or a.dtype != np.int32 or not a.flags.c_contiguous:
+        raise ValueError("host keys must be a C-contiguous int32 numpy array")
+    if not a.flags.writeable:
+        raise ValueError("host keys must be writeable (sorted in place)")
+
+
+def _range(a, left, right):
+    n = len(a) if not _is_device(a) else a.numel()
+    if left is None:
+        left, right = 0, n - 1
+    return int(left), int(right), n
+
+
+def _sort(algo: int, a, left, right, cfg: NetworkConfig):
+    left, right, n = _range(a, left, right)
+    if right < left:  # hybrid.hpp:160, 201 — inverted range is a no-op
+        return a
+    if left < 0 or right >= n:
+        raise ValueError("range outside the array")
+    cnt = right - left + 1
+    L = lib()
+    if _is_device(a):
+        _check_tensor(a)
+        ptr = a.data_ptr() + 4 * left
+        if algo == _lib.NS_MERGE_SORT:
+            tb = L.ns_merge_sort_temp_bytes(cnt)
+            st = L.ns_merge_sort_i32(ptr, cnt, cfg.width_mask, cfg.varsort_max,
+                                     scratch(tb, a.device), tb, _stream_ptr(a))
+        else:
+            tb = L.ns_quick_sort_temp_bytes(cnt)
+            st = L.ns_quick_sort_i32(ptr, cnt, cfg.width_mask, cfg.varsort_max,
+                                     scratch(tb, a.device), tb, _stream_ptr(a))
+        check(st, "optimized_merge_sort" if algo == 0 else "optimized_quick_sort")
+    else:
+        _check_host(a)
+        ptr = a.ctypes.data + 4 * left
+        fn = L.ns_merge_sort_host_i32 if algo == 0 else L.ns_quick_sort_host_i32
+        check(fn(ptr, cnt, cfg.width_mask, cfg.varsort_max),
+              "optimized_merge_sort" if algo == 0 else "optimized_quick_sort")
+    return a
+
+
+def optimized_merge_sort(a, *args):
+    """optimized_merge_sort(a, cfg) or optimized_merge_sort(a, left, right, cfg)."""
+    if len(args) == 1:
+        return _sort(_lib.NS_MERGE_SORT, a, None, None, args[0])
+    left, right, cfg = args
+    return _sort(_lib.NS_MERGE_SORT, a, left, right, cfg)
+
+
+def optimized_quick_sort(a, *args):
+    """optimized_quick_sort(a, cfg) or optimized_quick_sort(a, low, high, cfg)."""
+    if len(args) == 1:
+        return _sort(_lib.NS_QUICK_SORT, a, None, None, args[0])
+    low, high, cfg = args
+    return _sort(_lib.NS_QUICK_SORT, a, low, high, cfg)
+
+
+def classical_merge_sort(a):
+    return optimized_merge_sort(a, classic_config())
+
+
+def classical_quick_sort(a):
+    return optimized_quick_sort(a, classic_config())
+
+
+def run_variant(variant: SortVariant, a):
+    if variant.algorithm is Algorithm.merge_sort:
+        return optimized_merge_sort(a, variant.config)
+    return optimized_quick_sort(a, variant.config)
+
+
+# ---- batch entry points (BASELINE configs 2 and 4) -------------------------
+
+def sort_small_batch(keys, offsets):
+    """Sort every ragged array keys[offsets[i]:offsets[i+1]] (length <= 8) with
+    its size-specific network.  keys: CUDA int32, offsets: CUDA int32/uint32
+    (num_arrays + 1 entries, read as uint32)."""
+    _check_tensor(keys)
+    if offsets.dtype not in (torch.int32, torch.uint32) or not offsets.is_cuda:
+        raise ValueError("offsets must be a CUDA int32/uint32 tensor")
+    num = offsets.numel() - 1
+    check(lib().ns_sort_small_batch_i32(keys.data_ptr(), offsets.data_ptr(), max(num, 0),
+                                        _stream_ptr(keys)), "sort_small_batch")
+    return keys
+
+
+def segmented_sort(keys, seg_len: int, cfg: NetworkConfig,
+                   algorithm: Algorithm = Algorithm.quick_sort):
+    """Sort keys.numel() // seg_len back-to-back segments independently."""
+    _check_tensor(keys)
+    if seg_len <= 0 or keys.numel() % seg_len:
+        raise ValueError("keys must hold a whole number of segments")
+    nseg = keys.numel() // seg_len
+    L = lib()
+    tb = L.ns_segmented_sort_temp_bytes(nseg, seg_len)
+    check(L.ns_segmented_sort_i32(keys.data_ptr(), nseg, seg_len, algorithm.value,
+                                  cfg.width_mask, cfg.varsort_max, scratch(tb, keys.device),
+                                  tb, _stream_ptr(keys)), "segmented_sort")
+    return keys
+
+
+# ---- checking helpers ------------------------------------------------------
+
+def multiset_digest(keys) -> tuple:
+    """Order-independent (sum, xor) digest of mix64(key) over a CUDA tensor."""
+    _check_tensor(keys)
+    out = torch.zeros(2, dtype=torch.int64, device=keys.device)
+    check(lib().ns_multiset_digest_i32(keys.data_ptr(), keys.numel(), out.data_ptr(),
+                                       _stream_ptr(keys)), "multiset_digest")
+    s, x = out.cpu().tolist()
+    return s & (2**64 - 1), x & (2**64 - 1)
+
+
+def count_inversions(keys) -> int:
+    """Number of adjacent descents (0 == sorted)."""
+    _check_tensor(keys)
+    out = torch.zeros(1, dtype=torch.int64, device=keys.device)
+    check(lib().ns_count_inversions_i32(keys.data_ptr(), keys.numel(), out.data_ptr(),
+                                        _stream_ptr(keys)), "count_inversions")
+    return int(out.item())

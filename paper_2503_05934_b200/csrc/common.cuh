@@ -1,0 +1,90 @@
+// common.cuh — status plumbing shared by the C-ABI translation units.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "../../include/netsort_b200.h"
+
+namespace nsb {
+
+void set_last_error(const char* where, cudaError_t e);
+void count_launch();
+
+// Kernel classes for the built-in launch profiler (ns_profile_*).
+enum ProfKind {
+  PK_TILE_SORT = 0,  // blocksort_kernel
+  PK_PARTITION,      // merge-path partition searches
+  PK_MERGE_PASS,     // merge_pass_kernel / pairs_merge_kernel
+  PK_BATCH,          // sort_small_batch_kernel
+  PK_QS_SAMPLE,      // sampling + splitter selection
+  PK_QS_COUNT,       // count_kernel
+  PK_QS_SCATTER,     // scatter_kernel
+  PK_QS_BUCKET,      // bucket_sort_kernel
+  PK_PSRS,           // multi-GPU sample-sort helpers
+  PK_CHECK,          // digest / inversions / generator
+  PK_NUM_KINDS
+};
+
+// RAII: when profiling is on, records a CUDA event pair around one launch on
+// the launching stream (so the timing sees exactly that stream's work).
+struct Prof {
+  Prof(int kind, cudaStream_t s);
+  ~Prof();
+  int kind;
+  cudaStream_t stream;
+  cudaEvent_t begin = nullptr;
+};
+
+// Returns NS_OK, or records the pending launch/runtime error.
+inline int check_launch(const char* where) {
+  const cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) {
+    count_launch();
+    return NS_OK;
+  }
+  set_last_error(where, e);
+  return e == cudaErrorMemoryAllocation ? NS_ERR_OOM : NS_ERR_CUDA;
+}
+
+inline int check_cuda(cudaError_t e, const char* where) {
+  if (e == cudaSuccess) return NS_OK;
+  set_last_error(where, e);
+  return e == cudaErrorMemoryAllocation ? NS_ERR_OOM : NS_ERR_CUDA;
+}
+
+#define NSB_TRY(expr)                 \
+  do {                                \
+    const int _st = (expr);           \
+    if (_st != NS_OK) return _st;     \
+  } while (0)
+
+inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+inline int ceil_log2(uint64_t x) {
+  int p = 0;
+  while ((uint64_t(1) << p) < x) ++p;
+  return p;
+}
+
+// Per-leaf-width template dispatch (networks.cuh leaf_of).
+template <class F>
+inline int with_leaf(int leaf, F&& f) {
+  switch (leaf) {
+    case 8: return f(std::integral_constant<int, 8>{});
+    case 4: return f(std::integral_constant<int, 4>{});
+    case 2: return f(std::integral_constant<int, 2>{});
+    default: return f(std::integral_constant<int, 1>{});
+  }
+}
+
+// Device-side sort primitives shared between translation units.
+int merge_sort_device(int32_t* d_keys, size_t n, int leaf, void* d_temp, size_t temp_bytes,
+                      cudaStream_t s);
+int tile_sort_segments(int32_t* d_keys, size_t num_segments, size_t seg_len, int leaf,
+                       cudaStream_t s);
+size_t merge_sort_temp(size_t n);
+constexpr int kSmallTile = 16384;  // largest array one CTA sorts on chip
+
+}  // namespace nsb

@@ -1,0 +1,118 @@
+// host.cu — host-buffer entry points (the reference's own call shape:
+// optimized_merge_sort(span, cfg) sorts a host array in place,
+// /root/reference/proj/include/netsort/hybrid.hpp:174-177) and the C++
+// DeviceScratch / device_* helpers declared in include/netsort_b200.hpp.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "../../include/netsort_b200.hpp"
+#include "common.cuh"
+
+namespace nsb {
+size_t quick_sort_temp(size_t n);
+
+// Per-thread device staging: keys + scratch, grown on demand, plus one
+// non-blocking stream.  Mirrors the reference's per-call `new T[n]` scratch
+// (hybrid.hpp:163) without paying an allocation on every call.
+struct HostCache {
+  void* dev = nullptr;
+  size_t bytes = 0;
+  cudaStream_t stream = nullptr;
+  ~HostCache() { release(); }
+  void release() {
+    if (dev) cudaFree(dev);
+    if (stream) cudaStreamDestroy(stream);
+    dev = nullptr;
+    bytes = 0;
+    stream = nullptr;
+  }
+  int ensure(size_t need) {
+    if (!stream)
+      NSB_TRY(check_cuda(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking),
+                         "cudaStreamCreate"));
+    if (bytes >= need) return NS_OK;
+    if (dev) cudaFree(dev);
+    dev = nullptr;
+    bytes = 0;
+    NSB_TRY(check_cuda(cudaMalloc(&dev, need), "cudaMalloc"));
+    bytes = need;
+    return NS_OK;
+  }
+};
+static thread_local HostCache g_host;
+
+static int host_sort(int32_t* h_keys, size_t n, uint32_t mask, int vs, int algorithm) {
+  if (n <= 1) return NS_OK;
+  if (!h_keys) return NS_ERR_INVALID;
+  const size_t kb = align_up(n * sizeof(int32_t), 256);
+  const size_t tb = algorithm == NS_MERGE_SORT ? merge_sort_temp(n) : quick_sort_temp(n);
+  NSB_TRY(g_host.ensure(kb + tb));
+  cudaStream_t s = g_host.stream;
+  int32_t* d = static_cast<int32_t*>(g_host.dev);
+  void* t = static_cast<char*>(g_host.dev) + kb;
+  NSB_TRY(check_cuda(cudaMemcpyAsync(d, h_keys, n * 4, cudaMemcpyHostToDevice, s), "H2D"));
+  const int st = algorithm == NS_MERGE_SORT
+                     ? ns_merge_sort_i32(d, n, mask, vs, t, tb, s)
+                     : ns_quick_sort_i32(d, n, mask, vs, t, tb, s);
+  if (st != NS_OK) {
+    cudaStreamSynchronize(s);
+    return st;
+  }
+  NSB_TRY(check_cuda(cudaMemcpyAsync(h_keys, d, n * 4, cudaMemcpyDeviceToHost, s), "D2H"));
+  return check_cuda(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+}
+
+}  // namespace nsb
+
+extern "C" {
+
+int ns_merge_sort_host_i32(int32_t* h_keys, size_t n, uint32_t width_mask, int varsort_max) {
+  return nsb::host_sort(h_keys, n, width_mask, varsort_max, NS_MERGE_SORT);
+}
+
+int ns_quick_sort_host_i32(int32_t* h_keys, size_t n, uint32_t width_mask, int varsort_max) {
+  return nsb::host_sort(h_keys, n, width_mask, varsort_max, NS_QUICK_SORT);
+}
+
+int ns_release_cache(void) {
+  nsb::g_host.release();
+  return NS_OK;
+}
+
+}  // extern "C"
+
+namespace netsort_b200 {
+
+DeviceScratch::~DeviceScratch() {
+  if (ptr_) cudaFree(ptr_);
+}
+
+void* DeviceScratch::reserve(size_t bytes) {
+  if (bytes <= bytes_) return ptr_;
+  if (ptr_) cudaFree(ptr_);
+  ptr_ = nullptr;
+  bytes_ = 0;
+  if (bytes == 0) return nullptr;
+  detail::check(nsb::check_cuda(cudaMalloc(&ptr_, bytes), "cudaMalloc"), "DeviceScratch");
+  bytes_ = bytes;
+  return ptr_;
+}
+
+void device_merge_sort(std::int32_t* d_keys, size_t n, const NetworkConfig& cfg,
+                       DeviceScratch& scratch, void* stream) {
+  const size_t tb = ns_merge_sort_temp_bytes(n);
+  void* t = scratch.reserve(tb);
+  detail::check(ns_merge_sort_i32(d_keys, n, cfg.width_mask, cfg.varsort_max, t, tb, stream),
+                "device_merge_sort");
+}
+
+void device_quick_sort(std::int32_t* d_keys, size_t n, const NetworkConfig& cfg,
+                       DeviceScratch& scratch, void* stream) {
+  const size_t tb = ns_quick_sort_temp_bytes(n);
+  void* t = scratch.reserve(tb);
+  detail::check(ns_quick_sort_i32(d_keys, n, cfg.width_mask, cfg.varsort_max, t, tb, stream),
+                "device_quick_sort");
+}
+
+}  // namespace netsort_b200

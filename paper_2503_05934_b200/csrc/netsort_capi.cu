@@ -1,0 +1,336 @@
+// netsort_capi.cu — C-ABI entry points of the merge layer, the base-case
+// batch, the segmented sort and the checking helpers (include/netsort_b200.h).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cstdint>
+#include <cstring>
+#include <string>
+
+#include "common.cuh"
+#include "mergesort.cuh"
+#include "networks.cuh"
+
+namespace nsb {
+
+// ---- tuning (sm_100a) -----------------------------------------------------
+// Tile sort: 512 threads x 16 keys = 8192 keys (32 KiB smem), 2+ CTAs/SM.
+constexpr int kBsNT = 512, kBsK = 16, kBsT = kBsNT * kBsK;
+// Single-CTA sort for n <= 16384: 1024 threads x 16 keys (64 KiB smem).
+constexpr int kSmNT = 1024, kSmK = 16, kSmT = kSmNT * kSmK;
+static_assert(kSmT == kSmallTile, "small-tile size mismatch");
+// Merge pass: 512 threads x 16 outputs = 8192 keys per CTA.
+constexpr int kMgNT = 512, kMgK = 16, kMgT = kMgNT * kMgK;
+static_assert((2 * kBsT) % kMgT == 0, "merge tiles must not straddle run pairs");
+
+
+template <int NT, int K, int LEAF>
+static int launch_blocksort(const int32_t* src, int32_t* dst, int64_t n, int stride,
+                            int64_t ctas, cudaStream_t s) {
+  constexpr int smem = NT * K * 4;
+  auto* kern = blocksort_kernel<NT, K, LEAF>;
+  static bool attr_set = false;  // benign race: idempotent attribute write
+  if (!attr_set) {
+    NSB_TRY(check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            smem),
+                       "cudaFuncSetAttribute(blocksort)"));
+    attr_set = true;
+  }
+  {
+    Prof prof(PK_TILE_SORT, s);
+    kern<<<(unsigned)ctas, NT, smem, s>>>(src, dst, n, stride);
+  }
+  return check_launch("blocksort_kernel");
+}
+
+size_t merge_sort_temp(size_t n) {
+  if (n <= (size_t)kSmT) return 0;
+  const size_t tiles = (n + kMgT - 1) / kMgT;
+  return align_up(n * sizeof(int32_t), 256) + align_up((tiles + 1) * sizeof(int64_t), 256);
+}
+
+int merge_sort_device(int32_t* d_keys, size_t n, int leaf, void* d_temp, size_t temp_bytes,
+                      cudaStream_t s) {
+  if (n <= 1) return NS_OK;
+  if (n <= (size_t)kSmT) {
+    return with_leaf(leaf, [&](auto L) {
+      return launch_blocksort<kSmNT, kSmK, decltype(L)::value>(d_keys, d_keys, (int64_t)n,
+                                                                kSmT, 1, s);
+    });
+  }
+  if (temp_bytes < merge_sort_temp(n) || d_temp == nullptr) return NS_ERR_TEMP;
+  int32_t* tmp = static_cast<int32_t*>(d_temp);
+  int64_t* mp = reinterpret_cast<int64_t*>(static_cast<char*>(d_temp) +
+                                           align_up(n * sizeof(int32_t), 256));
+  const int64_t tiles = (int64_t)((n + kBsT - 1) / kBsT);
+  const int passes = ceil_log2((uint64_t)tiles);
+  // Pick the tile-sort destination so the last pass lands in d_keys.
+  int32_t* cur = (passes & 1) ? tmp : d_keys;
+  int32_t* other = (cur == d_keys) ? tmp : d_keys;
+  NSB_TRY(with_leaf(leaf, [&](auto L) {
+    return launch_blocksort<kBsNT, kBsK, decltype(L)::value>(d_keys, cur, (int64_t)n, kBsT,
+                                                              tiles, s);
+  }));
+  const int64_t mtiles = (int64_t)((n + kMgT - 1) / kMgT);
+  for (int64_t R = kBsT; R < (int64_t)n; R *= 2) {
+    {
+      Prof prof(PK_PARTITION, s);
+      merge_partition_kernel<kMgT><<<(unsigned)((mtiles + 255) / 256), 256, 0, s>>>(
+          cur, (int64_t)n, R, mtiles, mp);
+    }
+    NSB_TRY(check_launch("merge_partition_kernel"));
+    {
+      Prof prof(PK_MERGE_PASS, s);
+      merge_pass_kernel<kMgNT, kMgK><<<(unsigned)mtiles, kMgNT, 0, s>>>(cur, other, (int64_t)n,
+                                                                        R, mp);
+    }
+    NSB_TRY(check_launch("merge_pass_kernel"));
+    std::swap(cur, other);
+  }
+  return NS_OK;
+}
+
+int tile_sort_segments(int32_t* d_keys, size_t num_segments, size_t seg_len, int leaf,
+                       cudaStream_t s) {
+  if (seg_len > (size_t)kSmT) return NS_ERR_INVALID;
+  const int64_t n = (int64_t)(num_segments * seg_len);
+  if (seg_len <= (size_t)kBsT) {
+    return with_leaf(leaf, [&](auto L) {
+      return launch_blocksort<kBsNT, kBsK, decltype(L)::value>(d_keys, d_keys, n, (int)seg_len,
+                                                                (int64_t)num_segments, s);
+    });
+  }
+  return with_leaf(leaf, [&](auto L) {
+    return launch_blocksort<kSmNT, kSmK, decltype(L)::value>(d_keys, d_keys, n, (int)seg_len,
+                                                              (int64_t)num_segments, s);
+  });
+}
+
+// ---------------------------------------------------------------------------
+// Base-case batch: each ragged array (length 0..8) sorted by its own network.
+// A CTA owns kBaArr consecutive arrays; their keys (<= 8 per array) are staged
+// in shared memory with coalesced loads, each thread sorts its arrays in
+// registers with the size-specific network, and the CTA stores them back.
+// ---------------------------------------------------------------------------
+constexpr int kBaNT = 256, kBaPer = 4, kBaArr = kBaNT * kBaPer;
+
+__global__ void __launch_bounds__(kBaNT)
+    sort_small_batch_kernel(int32_t* __restrict__ keys, const uint32_t* __restrict__ offsets,
+                            int64_t num_arrays, int* __restrict__ bad) {
+  __shared__ uint32_t so[kBaArr + 1];
+  __shared__ int32_t sk[kBaArr * 8];
+  __shared__ int s_bad;
+  const int tid = threadIdx.x;
+  const int64_t first = (int64_t)blockIdx.x * kBaArr;
+  const int cnt = (int)min((int64_t)kBaArr, num_arrays - first);
+  if (tid == 0) s_bad = 0;
+  for (int i = tid; i <= cnt; i += kBaNT) so[i] = __ldg(offsets + first + i);
+  __syncthreads();
+  // validate lengths before touching keys (lengths outside [0,8] -> error)
+  for (int i = tid; i < cnt; i += kBaNT) {
+    const uint32_t len = so[i + 1] - so[i];
+    if (so[i + 1] < so[i] || len > 8) s_bad = 1;
+  }
+  __syncthreads();
+  if (s_bad) {
+    if (tid == 0) atomicExch(bad, 1);
+    return;
+  }
+  const uint32_t k0 = so[0];
+  const int nk = (int)(so[cnt] - k0);
+  for (int i = tid; i < nk; i += kBaNT) sk[i] = __ldcs(keys + k0 + i);
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < kBaPer; ++r) {
+    const int j = r * kBaNT + tid;  // lanes take consecutive arrays
+    if (j < cnt) {
+      const int off = (int)(so[j] - k0);
+      const int len = (int)(so[j + 1] - so[j]);
+      int32_t v[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = k < len ? sk[off + k] : 0;
+      sort_small_switch(v, len);
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (k < len) sk[off + k] = v[k];
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < nk; i += kBaNT) __stcs(keys + k0 + i, sk[i]);
+}
+
+// ---------------------------------------------------------------------------
+// Checking helpers.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__global__ void digest_kernel(const int32_t* __restrict__ keys, int64_t n,
+                              unsigned long long* __restrict__ out) {
+  unsigned long long s = 0, x = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t m = mix64((uint64_t)(uint32_t)keys[i] + 0x9E3779B97F4A7C15ull);
+    s += m;
+    x ^= m;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    s += __shfl_xor_sync(kFull, s, o);
+    x ^= __shfl_xor_sync(kFull, x, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(out, s);
+    atomicXor(out + 1, x);
+  }
+}
+
+__global__ void inversions_kernel(const int32_t* __restrict__ keys, int64_t n,
+                                  unsigned long long* __restrict__ out) {
+  unsigned long long c = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i + 1 < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    c += keys[i] > keys[i + 1];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(kFull, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
+}
+
+static int grid_for(int64_t n, int nt) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t want = (n + nt - 1) / nt;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sms * 8));
+}
+
+}  // namespace nsb
+
+using namespace nsb;
+
+extern "C" {
+
+const char* ns_status_string(int status) {
+  switch (status) {
+    case NS_OK: return "ok";
+    case NS_ERR_INVALID: return "invalid argument";
+    case NS_ERR_CUDA: return "CUDA error";
+    case NS_ERR_OOM: return "out of memory";
+    case NS_ERR_TEMP: return "scratch buffer too small";
+    default: return "unknown status";
+  }
+}
+
+int ns_version(void) { return 100; }
+
+int ns_leaf_width(uint32_t width_mask, int varsort_max) { return leaf_of(width_mask, varsort_max); }
+
+int ns_network_comparators(int width, uint8_t* pairs, int cap) {
+  auto emit = [&](const Pair* p, int cnt) {
+    for (int i = 0; i < cnt && i < cap; ++i) {
+      pairs[2 * i] = p[i].lo;
+      pairs[2 * i + 1] = p[i].hi;
+    }
+    return cnt;
+  };
+  switch (width) {
+    case 2: return emit(Net<2>::P, Net<2>::N);
+    case 3: return emit(Net<3>::P, Net<3>::N);
+    case 4: return emit(Net<4>::P, Net<4>::N);
+    case 5: return emit(Net<5>::P, Net<5>::N);
+    case 6: return emit(Net<6>::P, Net<6>::N);
+    case 7: return emit(Net<7>::P, Net<7>::N);
+    case 8: return emit(Net<8>::P, Net<8>::N);
+    default: return -1;
+  }
+}
+
+size_t ns_merge_sort_temp_bytes(size_t n) { return merge_sort_temp(n); }
+
+int ns_merge_sort_i32(int32_t* d_keys, size_t n, uint32_t width_mask, int varsort_max,
+                      void* d_temp, size_t temp_bytes, void* stream) {
+  if (n > 0 && d_keys == nullptr) return NS_ERR_INVALID;
+  if (n > (size_t)INT64_MAX / 4) return NS_ERR_INVALID;
+  return merge_sort_device(d_keys, n, leaf_of(width_mask, varsort_max), d_temp, temp_bytes,
+                           static_cast<cudaStream_t>(stream));
+}
+
+int ns_sort_small_batch_i32(int32_t* d_keys, const uint32_t* d_offsets, size_t num_arrays,
+                            void* stream) {
+  if (num_arrays == 0) return NS_OK;
+  if (!d_keys || !d_offsets) return NS_ERR_INVALID;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int* bad = nullptr;
+  NSB_TRY(check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&bad), sizeof(int), s),
+                     "cudaMallocAsync"));
+  NSB_TRY(check_cuda(cudaMemsetAsync(bad, 0, sizeof(int), s), "cudaMemsetAsync"));
+  const int64_t ctas = (int64_t)((num_arrays + kBaArr - 1) / kBaArr);
+  {
+    Prof prof(PK_BATCH, s);
+    sort_small_batch_kernel<<<(unsigned)ctas, kBaNT, 0, s>>>(d_keys, d_offsets,
+                                                              (int64_t)num_arrays, bad);
+  }
+  int st = check_launch("sort_small_batch_kernel");
+  int h_bad = 0;
+  if (st == NS_OK) {
+    // The length check is the only device->host traffic of this call.
+    st = check_cuda(cudaMemcpyAsync(&h_bad, bad, sizeof(int), cudaMemcpyDeviceToHost, s),
+                    "cudaMemcpyAsync");
+    if (st == NS_OK) st = check_cuda(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+  }
+  cudaFreeAsync(bad, s);
+  if (st != NS_OK) return st;
+  return h_bad ? NS_ERR_INVALID : NS_OK;
+}
+
+size_t ns_segmented_sort_temp_bytes(size_t num_segments, size_t seg_len) {
+  (void)num_segments;
+  if (seg_len <= (size_t)kSmT) return 0;
+  return std::max(merge_sort_temp(seg_len), ns_quick_sort_temp_bytes(seg_len));
+}
+
+int ns_segmented_sort_i32(int32_t* d_keys, size_t num_segments, size_t seg_len, int algorithm,
+                          uint32_t width_mask, int varsort_max, void* d_temp,
+                          size_t temp_bytes, void* stream) {
+  if (algorithm != NS_MERGE_SORT && algorithm != NS_QUICK_SORT) return NS_ERR_INVALID;
+  if (num_segments == 0 || seg_len <= 1) return NS_OK;
+  if (!d_keys) return NS_ERR_INVALID;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int leaf = leaf_of(width_mask, varsort_max);
+  if (seg_len <= (size_t)kSmT) return tile_sort_segments(d_keys, num_segments, seg_len, leaf, s);
+  // Segments larger than one CTA: one device sort per segment.
+  for (size_t g = 0; g < num_segments; ++g) {
+    int32_t* seg = d_keys + g * seg_len;
+    const int st = algorithm == NS_MERGE_SORT
+                       ? merge_sort_device(seg, seg_len, leaf, d_temp, temp_bytes, s)
+                       : ns_quick_sort_i32(seg, seg_len, width_mask, varsort_max, d_temp,
+                                           temp_bytes, stream);
+    if (st != NS_OK) return st;
+  }
+  return NS_OK;
+}
+
+int ns_multiset_digest_i32(const int32_t* d_keys, size_t n, uint64_t* d_out, void* stream) {
+  if (!d_out || (n && !d_keys)) return NS_ERR_INVALID;
+  if (n == 0) return NS_OK;
+  Prof prof(PK_CHECK, static_cast<cudaStream_t>(stream));
+  digest_kernel<<<grid_for((int64_t)n, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      d_keys, (int64_t)n, reinterpret_cast<unsigned long long*>(d_out));
+  return check_launch("digest_kernel");
+}
+
+int ns_count_inversions_i32(const int32_t* d_keys, size_t n, unsigned long long* d_out,
+                            void* stream) {
+  if (!d_out || (n && !d_keys)) return NS_ERR_INVALID;
+  if (n < 2) return NS_OK;
+  Prof prof(PK_CHECK, static_cast<cudaStream_t>(stream));
+  inversions_kernel<<<grid_for((int64_t)n, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      d_keys, (int64_t)n, d_out);
+  return check_launch("inversions_kernel");
+}
+
+}  // extern "C"

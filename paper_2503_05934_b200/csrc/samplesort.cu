@@ -1,0 +1,212 @@
+// samplesort.cu — per-rank device steps of the multi-GPU sample sort (PSRS)
+// and the g-way merge of received runs.
+//
+// No reference counterpart: the reference is single-process (SURVEY.md §2.2,
+// §8(e)).  The host layer (paper_2503_05934_b200/samplesort.py) runs, on every
+// rank: local merge sort (ns_merge_sort_i32) -> ns_regular_samples_i32 ->
+// all-gather of samples -> ns_select_splitters_i32 -> ns_bucket_bounds_i32 ->
+// all-to-all of counts and keys over NCCL -> ns_merge_runs_i32.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cstdint>
+#include <vector>
+
+#include "common.cuh"
+#include "mergesort.cuh"
+
+namespace nsb {
+
+__global__ void regular_samples_kernel(const int32_t* __restrict__ sorted, int64_t n, int s,
+                                       int32_t* __restrict__ out) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < s) out[k] = sorted[(int64_t)(k + 1) * n / (s + 1)];
+}
+
+__global__ void pick_splitters_kernel(const int32_t* __restrict__ samples, int s, int g,
+                                      int32_t* __restrict__ spl) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < g - 1) spl[k] = samples[(int64_t)(k + 1) * s / g];
+}
+
+// bounds[k] = lower_bound(sorted, spl[k-1]) for 1 <= k < g; bounds[0] = 0,
+// bounds[g] = n.  Keys equal to a splitter go to the upper bucket.
+__global__ void bucket_bounds_kernel(const int32_t* __restrict__ sorted, int64_t n,
+                                     const int32_t* __restrict__ spl, int g,
+                                     int64_t* __restrict__ bounds) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k > g) return;
+  if (k == 0) { bounds[0] = 0; return; }
+  if (k == g) { bounds[g] = n; return; }
+  const int32_t key = spl[k - 1];
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (sorted[mid] < key) lo = mid + 1;
+    else hi = mid;
+  }
+  bounds[k] = lo;
+}
+
+// ---- merge of explicit adjacent run pairs (uneven lengths) ---------------
+constexpr int kMaxPairs = 64;
+struct PairTable {
+  int npairs;
+  int64_t a_base[kMaxPairs], a_len[kMaxPairs], b_len[kMaxPairs], tile0[kMaxPairs + 1];
+};
+
+__device__ __forceinline__ int pair_of(const PairTable& t, int64_t tile) {
+  int p = 0;
+  while (p + 1 < t.npairs && t.tile0[p + 1] <= tile) ++p;
+  return p;
+}
+
+template <int TM>
+__global__ void pairs_partition_kernel(const int32_t* __restrict__ src, PairTable t,
+                                       int64_t* __restrict__ mp) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= t.tile0[t.npairs]) return;
+  const int p = pair_of(t, c);
+  const int32_t* A = src + t.a_base[p];
+  const int64_t diag = (c - t.tile0[p]) * TM;
+  mp[c] = merge_path<int64_t>(A, t.a_len[p], A + t.a_len[p], t.b_len[p], diag);
+}
+
+template <int NT, int K>
+__global__ void __launch_bounds__(NT)
+    pairs_merge_kernel(const int32_t* __restrict__ src, int32_t* __restrict__ dst, PairTable t,
+                       const int64_t* __restrict__ mp) {
+  constexpr int TM = NT * K;
+  __shared__ __align__(16) int32_t sm[TM];
+  const int tid = threadIdx.x;
+  const int64_t c = blockIdx.x;
+  const int p = pair_of(t, c);
+  const int64_t pair_len = t.a_len[p] + t.b_len[p];
+  const int64_t diag0 = (c - t.tile0[p]) * TM;
+  const int64_t diag1 = min(diag0 + TM, pair_len);
+  const int64_t a0 = mp[c];
+  const int64_t a1 = (diag1 == pair_len) ? t.a_len[p] : mp[c + 1];
+  const int la = (int)(a1 - a0);
+  const int lb = (int)((diag1 - a1) - (diag0 - a0));
+  const int32_t* A = src + t.a_base[p] + a0;
+  const int32_t* B = src + t.a_base[p] + t.a_len[p] + (diag0 - a0);
+  const int total = la + lb;
+  for (int i = tid; i < total; i += NT) sm[i] = i < la ? __ldcs(A + i) : __ldcs(B + (i - la));
+  __syncthreads();
+  const int diag = min(tid * K, total);
+  const int a = merge_path<int>(sm, la, sm + la, lb, diag);
+  int32_t v[K];
+  serial_merge<K>(sm, la, sm + la, lb, a, diag - a, v);
+  int32_t* out = dst + t.a_base[p] + diag0;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const int i = tid * K + k;
+    if (i < total) out[i] = v[k];
+  }
+}
+
+constexpr int kPmNT = 512, kPmK = 16, kPmT = kPmNT * kPmK;
+
+}  // namespace nsb
+
+using namespace nsb;
+
+extern "C" {
+
+int ns_regular_samples_i32(const int32_t* d_sorted, size_t n, int s, int32_t* d_samples,
+                           void* stream) {
+  if (n == 0 || s <= 0 || !d_sorted || !d_samples) return NS_ERR_INVALID;
+  Prof prof(PK_PSRS, static_cast<cudaStream_t>(stream));
+  regular_samples_kernel<<<(s + 255) / 256, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      d_sorted, (int64_t)n, s, d_samples);
+  return check_launch("regular_samples_kernel");
+}
+
+int ns_select_splitters_i32(int32_t* d_samples, int s, int g, int32_t* d_splitters,
+                            void* stream) {
+  if (s <= 0 || s > kSmallTile || g < 1 || !d_samples || (g > 1 && !d_splitters))
+    return NS_ERR_INVALID;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  NSB_TRY(merge_sort_device(d_samples, (size_t)s, 8, nullptr, 0, st));
+  if (g == 1) return NS_OK;
+  Prof prof(PK_PSRS, st);
+  pick_splitters_kernel<<<(g + 255) / 256, 256, 0, st>>>(d_samples, s, g, d_splitters);
+  return check_launch("pick_splitters_kernel");
+}
+
+int ns_bucket_bounds_i32(const int32_t* d_sorted, size_t n, const int32_t* d_splitters, int g,
+                         int64_t* d_bounds, void* stream) {
+  if (g < 1 || !d_bounds || (n && !d_sorted) || (g > 1 && !d_splitters)) return NS_ERR_INVALID;
+  Prof prof(PK_PSRS, static_cast<cudaStream_t>(stream));
+  bucket_bounds_kernel<<<(g + 1 + 127) / 128, 128, 0, static_cast<cudaStream_t>(stream)>>>(
+      d_sorted, (int64_t)n, d_splitters, g, d_bounds);
+  return check_launch("bucket_bounds_kernel");
+}
+
+size_t ns_merge_runs_temp_bytes(size_t n, int num_runs) {
+  if (num_runs <= 1) return 0;
+  return align_up(n * 4, 256) + align_up((n / kPmT + 2 * kMaxPairs + 2) * 8, 256);
+}
+
+int ns_merge_runs_i32(int32_t* d_keys, const int64_t* h_run_offsets, int num_runs, void* d_temp,
+                      size_t temp_bytes, void* stream) {
+  if (num_runs < 1 || num_runs > 2 * kMaxPairs || !h_run_offsets) return NS_ERR_INVALID;
+  const int64_t n = h_run_offsets[num_runs] - h_run_offsets[0];
+  if (num_runs == 1 || n <= 1) return NS_OK;
+  for (int r = 0; r < num_runs; ++r)
+    if (h_run_offsets[r + 1] < h_run_offsets[r]) return NS_ERR_INVALID;
+  if (!d_temp || temp_bytes < ns_merge_runs_temp_bytes((size_t)n, num_runs)) return NS_ERR_TEMP;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int32_t* base = d_keys + h_run_offsets[0];
+  int32_t* tmp = static_cast<int32_t*>(d_temp);
+  int64_t* mp = reinterpret_cast<int64_t*>(static_cast<char*>(d_temp) + align_up(n * 4, 256));
+
+  std::vector<int64_t> runs(h_run_offsets, h_run_offsets + num_runs + 1);
+  for (auto& r : runs) r -= h_run_offsets[0];
+  int rounds = 0;
+  for (int k = num_runs; k > 1; k = (k + 1) / 2) ++rounds;
+  // Pick the first destination so that the last round lands in d_keys.
+  int32_t* cur = base;
+  int32_t* other = tmp;
+  if (rounds & 1) {
+    // odd round count: start by staging into tmp so the final write hits base
+    NSB_TRY(check_cuda(cudaMemcpyAsync(tmp, base, n * 4, cudaMemcpyDeviceToDevice, s), "copy"));
+    cur = tmp;
+    other = base;
+  }
+  while (runs.size() > 2) {
+    const int nr = (int)runs.size() - 1;
+    PairTable t{};
+    t.npairs = (nr + 1) / 2;
+    int64_t tiles = 0;
+    std::vector<int64_t> next{0};
+    for (int p = 0; p < t.npairs; ++p) {
+      const int ra = 2 * p, rb = 2 * p + 1;
+      t.a_base[p] = runs[ra];
+      t.a_len[p] = runs[ra + 1] - runs[ra];
+      t.b_len[p] = rb < nr ? runs[rb + 1] - runs[rb] : 0;
+      t.tile0[p] = tiles;
+      tiles += (t.a_len[p] + t.b_len[p] + kPmT - 1) / kPmT;
+      next.push_back(runs[std::min(rb + 1, nr)]);
+    }
+    t.tile0[t.npairs] = tiles;
+    if (tiles > 0) {
+      {
+        Prof prof(PK_PARTITION, s);
+        pairs_partition_kernel<kPmT><<<(unsigned)((tiles + 255) / 256), 256, 0, s>>>(cur, t, mp);
+      }
+      NSB_TRY(check_launch("pairs_partition_kernel"));
+      {
+        Prof prof(PK_MERGE_PASS, s);
+        pairs_merge_kernel<kPmNT, kPmK><<<(unsigned)tiles, kPmNT, 0, s>>>(cur, other, t, mp);
+      }
+      NSB_TRY(check_launch("pairs_merge_kernel"));
+    }
+    std::swap(cur, other);
+    runs.swap(next);
+  }
+  return NS_OK;
+}
+
+}  // extern "C"

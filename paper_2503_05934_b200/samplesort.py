@@ -1,0 +1,153 @@
+"""Multi-GPU sample sort (BASELINE config 5).
+
+One process per GPU.  Each rank owns a contiguous shard of one big int32
+array.  The per-rank compute is the sm_100a library through the C ABI; the
+only cross-rank traffic is one all-gather of samples, one all-to-all of
+bucket counts and ONE all-to-all of the keys themselves (NCCL over NVLink /
+NVSwitch in production, gloo in the CPU tests):
+
+  1. local merge sort of the shard (6To8 network base case)  ns_merge_sort_i32
+  2. s = 255 regular samples of the sorted shard              ns_regular_samples_i32
+  3. all-gather samples (g*s keys)                             torch.distributed
+  4. sort samples, pick g-1 global splitters                   ns_select_splitters_i32
+  5. bucket bounds in the sorted shard (lower_bound)           ns_bucket_bounds_i32
+  6. all-to-all counts, then all-to-all keys (variable sizes)  torch.distributed
+  7. g-way merge of the g received sorted runs                 ns_merge_runs_i32
+
+The result is globally sorted across ranks in rank order (rank r holds the
+r-th bucket range) and is a permutation of the input.  The reference has no
+distributed path; its single-array merge sort is the oracle.
+
+`LocalOps` is the per-rank compute interface.  The product uses `DeviceOps`
+(CUDA library, fails loudly without it); the CPU tests inject an oracle-backed
+implementation to exercise the exchange logic under gloo with world_size 2.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Optional
+
+import torch
+import torch.distributed as dist
+
+from ._lib import check, lib
+
+SAMPLES_PER_RANK = 255
+
+
+class DeviceOps:
+    """Per-rank steps on the GPU through the C ABI."""
+
+    def __init__(self, width_mask: int = (1 << 6) | (1 << 7) | (1 << 8), varsort_max: int = 0):
+        self.mask, self.vs = width_mask, varsort_max
+        self.L = lib()
+        self._scratch = None
+
+    def _temp(self, nbytes: int, device) -> int:
+        if nbytes == 0:
+            return 0
+        if self._scratch is None or self._scratch.numel() < nbytes:
+            self._scratch = None
+            self._scratch = torch.empty(nbytes, dtype=torch.uint8, device=device)
+        return self._scratch.data_ptr()
+
+    @staticmethod
+    def _s(t):
+        return torch.cuda.current_stream(t.device).cuda_stream
+
+    def local_sort(self, keys: torch.Tensor) -> None:
+        tb = self.L.ns_merge_sort_temp_bytes(keys.numel())
+        check(self.L.ns_merge_sort_i32(keys.data_ptr(), keys.numel(), self.mask, self.vs,
+                                       self._temp(tb, keys.device), tb, self._s(keys)),
+              "local merge sort")
+
+    def samples(self, sorted_keys: torch.Tensor, s: int) -> torch.Tensor:
+        out = torch.empty(s, dtype=torch.int32, device=sorted_keys.device)
+        if sorted_keys.numel() == 0:
+            out.fill_(torch.iinfo(torch.int32).max)
+            return out
+        check(self.L.ns_regular_samples_i32(sorted_keys.data_ptr(), sorted_keys.numel(), s,
+                                            out.data_ptr(), self._s(out)), "regular samples")
+        return out
+
+    def splitters(self, all_samples: torch.Tensor, g: int) -> torch.Tensor:
+        spl = torch.empty(max(g - 1, 1), dtype=torch.int32, device=all_samples.device)
+        check(self.L.ns_select_splitters_i32(all_samples.data_ptr(), all_samples.numel(), g,
+                                             spl.data_ptr(), self._s(spl)), "select splitters")
+        return spl[: g - 1]
+
+    def bounds(self, sorted_keys: torch.Tensor, spl: torch.Tensor, g: int) -> torch.Tensor:
+        b = torch.empty(g + 1, dtype=torch.int64, device=sorted_keys.device)
+        check(self.L.ns_bucket_bounds_i32(sorted_keys.data_ptr(), sorted_keys.numel(),
+                                          spl.data_ptr() if g > 1 else None, g, b.data_ptr(),
+                                          self._s(b)), "bucket bounds")
+        return b
+
+    def merge_runs(self, keys: torch.Tensor, run_offsets: list) -> None:
+        nr = len(run_offsets) - 1
+        tb = self.L.ns_merge_runs_temp_bytes(keys.numel(), nr)
+        offs = (C.c_int64 * (nr + 1))(*run_offsets)
+        check(self.L.ns_merge_runs_i32(keys.data_ptr(), C.cast(offs, C.c_void_p), nr,
+                                       self._temp(tb, keys.device), tb, self._s(keys)),
+              "merge runs")
+
+
+@dataclass
+class SampleSortTiming:
+    """Device-side phase boundaries (CUDA events) for the bench report."""
+    local_sort_ms: float = 0.0
+    exchange_ms: float = 0.0
+    merge_ms: float = 0.0
+    send_bytes: int = 0
+
+
+def sample_sort(shard: torch.Tensor, group=None, ops=None, samples_per_rank: int = SAMPLES_PER_RANK,
+                timing: Optional[SampleSortTiming] = None) -> torch.Tensor:
+    """Globally sort the distributed array whose rank-local shard is `shard`.
+
+    Returns this rank's slice of the sorted result (a new tensor; `shard` is
+    sorted in place as a side effect).  Works for world size 1 (then it is the
+    local merge sort)."""
+    ops = ops or DeviceOps()
+    g = dist.get_world_size(group) if dist.is_initialized() else 1
+    dev = shard.device
+    ev = None
+    if timing is not None and dev.type == "cuda":
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        ev[0].record()
+    ops.local_sort(shard)
+    if g == 1:
+        if ev:
+            ev[1].record()
+            ev[1].synchronize()
+            timing.local_sort_ms = ev[0].elapsed_time(ev[1])
+        return shard
+    if ev:
+        ev[1].record()
+    smp = ops.samples(shard, samples_per_rank)
+    gathered = [torch.empty_like(smp) for _ in range(g)]
+    dist.all_gather(gathered, smp, group=group)
+    spl = ops.splitters(torch.cat(gathered), g)
+    bnd = ops.bounds(shard, spl, g)
+    send_counts = (bnd[1:] - bnd[:-1]).to(torch.int64)
+    recv_counts = torch.empty_like(send_counts)
+    dist.all_to_all_single(recv_counts, send_counts, group=group)
+    sc = send_counts.cpu().tolist()
+    rc = recv_counts.cpu().tolist()
+    out = torch.empty(sum(rc), dtype=torch.int32, device=dev)
+    dist.all_to_all_single(out, shard, output_split_sizes=rc, input_split_sizes=sc, group=group)
+    if ev:
+        ev[2].record()
+    offs = [0]
+    for c in rc:
+        offs.append(offs[-1] + c)
+    ops.merge_runs(out, offs)
+    if ev:
+        ev[3].record()
+        ev[3].synchronize()
+        timing.local_sort_ms = ev[0].elapsed_time(ev[1])
+        timing.exchange_ms = ev[1].elapsed_time(ev[2])
+        timing.merge_ms = ev[2].elapsed_time(ev[3])
+        timing.send_bytes = 4 * (sum(sc) - sc[dist.get_rank(group)])
+    return out

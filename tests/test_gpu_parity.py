@@ -1,0 +1,228 @@
+"""GPU parity: the sm_100a kernels, called through the C ABI, against the CPU
+oracle (oracle/netsort_oracle.c) and the reference's own outputs frozen in
+tests/golden/golden.json.  Bit-exact for every case (int32 keys)."""
+import hashlib
+import itertools
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+SIZES = [0, 1, 2, 3, 4, 5, 7, 8, 9, 13, 16, 17, 31, 32, 33, 63, 64, 100, 255, 256, 257, 501,
+         1000, 1023, 4096, 8191, 8192, 8193, 10000, 16383, 16384, 16385, 20000, 25000, 32768,
+         65537, 100000, 262144, 1000000]
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def to_dev(a, dev):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(a, np.int32)).to(dev)
+
+
+def from_dev(t):
+    return t.cpu().numpy()
+
+
+@pytest.mark.parametrize("algo", ["merge", "quick"])
+@pytest.mark.parametrize("dist", ["random", "sorted", "nearly_sorted"])
+def test_sizes_match_oracle(ns, cuda, oracle, algo, dist):
+    cfg_name = "6To8" if algo == "merge" else "3To5"
+    cfg = ns.find_config(cfg_name)
+    for n in SIZES:
+        a = oracle.generate_i32(dist, n, seed=42 + n)
+        want = oracle.merge_sort(a, cfg_name) if algo == "merge" else oracle.quick_sort(a, cfg_name)
+        t = to_dev(a, cuda)
+        (ns.optimized_merge_sort if algo == "merge" else ns.optimized_quick_sort)(t, cfg)
+        got = from_dev(t)
+        assert np.array_equal(got, want), f"{algo} {dist} n={n}"
+
+
+@pytest.mark.parametrize("cfg_name", ["Classic", "PowerOf2", "Even", "Odd", "3", "3To4", "3To5",
+                                      "3To8", "6To8", "VarSort3", "VarSort4", "VarSort5"])
+def test_every_config_both_algorithms(ns, cuda, oracle, cfg_name):
+    cfg = ns.find_config(cfg_name)
+    for n in (0, 1, 2, 3, 4, 7, 16, 33, 64, 501, 1000, 9000, 40000):
+        a = oracle.generate_i32("random", n, seed=3000 + n)
+        want = np.sort(a)
+        for fn in (ns.optimized_merge_sort, ns.optimized_quick_sort):
+            t = to_dev(a, cuda)
+            fn(t, cfg)
+            assert np.array_equal(from_dev(t), want), f"{fn.__name__} {cfg_name} n={n}"
+
+
+def test_golden_reference_outputs(ns, cuda, oracle, golden):
+    """Every frozen reference output (SHA-256) is reproduced bit-exactly."""
+    for c in golden["cases"]:
+        a = oracle.generate_i32(c["dist"], c["n"], c["seed"])
+        assert sha(a) == c["input_sha256"], c
+        t = to_dev(a, cuda)
+        cfg = ns.find_config(c["config"])
+        (ns.optimized_merge_sort if c["algo"] == "merge" else ns.optimized_quick_sort)(t, cfg)
+        assert sha(from_dev(t)) == c["output_sha256"], (c["algo"], c["config"], c["dist"], c["n"])
+
+
+def test_ternary_exhaustive(ns, cuda):
+    """All {0,1,2} arrays of length <= 8 through both algorithms (acceptance.cpp:135-164),
+    batched as segments so the whole sweep is a handful of launches."""
+    import torch
+    for length in range(2, 9):
+        codes = np.array(list(itertools.product(range(3), repeat=length)), np.int32)
+        flat = codes.reshape(-1)
+        for algo in (ns.Algorithm.merge_sort, ns.Algorithm.quick_sort):
+            for cfg_name in ("Classic", "3To5", "6To8", "Odd", "VarSort3"):
+                t = to_dev(flat, cuda)
+                ns.segmented_sort(t, length, ns.find_config(cfg_name), algo)
+                got = from_dev(t).reshape(-1, length)
+                assert np.array_equal(got, np.sort(codes, axis=1)), (length, cfg_name, algo)
+    torch.cuda.synchronize()
+
+
+def test_networks_exhaustive_on_device(ns, cuda):
+    """Zero-one principle and every permutation, widths 2..8, through the
+    base-case batch kernel (each array hits its own width's network)."""
+    import torch
+    for w in range(2, 9):
+        perms = np.array(list(itertools.permutations(range(1, w + 1))), np.int32)
+        bits = np.array([[(b >> i) & 1 for i in range(w)] for b in range(1 << w)], np.int32)
+        arr = np.concatenate([perms, bits])
+        offs = np.arange(0, arr.size + 1, w, dtype=np.int32)
+        keys = to_dev(arr.reshape(-1), cuda)
+        ns.sort_small_batch(keys, torch.from_numpy(offs).to(cuda))
+        got = from_dev(keys).reshape(-1, w)
+        assert np.array_equal(got, np.sort(arr, axis=1)), w
+
+
+def test_sort_small_batch_matches_reference(ns, cuda, oracle, golden):
+    import torch
+    sb = golden["small_batch"]
+    keys = to_dev(np.array(sb["input"], np.int32), cuda)
+    offs = torch.tensor(sb["offsets"], dtype=torch.int32, device=cuda)
+    ns.sort_small_batch(keys, offs)
+    assert from_dev(keys).tolist() == sb["output"]
+    # 2^20 ragged arrays against the oracle
+    o, k = oracle.generate_batch_i32(1 << 20, 11)
+    want = oracle.sort_small_batch(k, o)
+    t = to_dev(k, cuda)
+    ns.sort_small_batch(t, torch.from_numpy(o.view(np.int32)).to(cuda))
+    assert np.array_equal(from_dev(t), want)
+
+
+def test_sort_small_batch_edge_cases(ns, cuda):
+    import torch
+    # lengths 0 and 1 are no-ops; an empty batch is fine
+    keys = to_dev(np.array([5, 3, 9, 2, 1], np.int32), cuda)
+    offs = torch.tensor([0, 0, 1, 1, 3, 5], dtype=torch.int32, device=cuda)
+    ns.sort_small_batch(keys, offs)
+    assert from_dev(keys).tolist() == [5, 3, 9, 1, 2]
+    ns.sort_small_batch(keys, torch.tensor([0], dtype=torch.int32, device=cuda))
+    # a length above 8 is rejected (networks.hpp:99-103 throws there)
+    bad = torch.tensor([0, 9], dtype=torch.int32, device=cuda)
+    k9 = to_dev(np.arange(9, 0, -1, dtype=np.int32), cuda)
+    with pytest.raises(ValueError):
+        ns.sort_small_batch(k9, bad)
+    assert from_dev(k9).tolist() == list(range(9, 0, -1))
+
+
+def test_segmented_matches_reference_prefix(ns, cuda, oracle, golden):
+    g = golden["segmented"]
+    nseg, seg = g["num_segments_checked"], g["seg_len"]
+    a = oracle.generate_i32("random", nseg * seg, g["seed"])
+    assert sha(a) == g["input_prefix_sha256"]
+    t = to_dev(a, cuda)
+    ns.segmented_sort(t, seg, ns.find_config(g["config"]), ns.Algorithm.quick_sort)
+    assert sha(from_dev(t)) == g["output_prefix_sha256"]
+
+
+def test_segmented_odd_lengths(ns, cuda, oracle):
+    for seg in (1, 2, 3, 5, 100, 4097, 8192, 12345, 16384, 20000):
+        nseg = max(1, 200000 // seg)
+        a = oracle.generate_i32("random", nseg * seg, seed=seg)
+        want = np.sort(a.reshape(nseg, seg), axis=1).reshape(-1)
+        for algo in (ns.Algorithm.merge_sort, ns.Algorithm.quick_sort):
+            t = to_dev(a, cuda)
+            ns.segmented_sort(t, seg, ns.find_config("3To5"), algo)
+            assert np.array_equal(from_dev(t), want), (seg, algo)
+
+
+def test_range_sorts_leave_outside_untouched(ns, cuda, oracle):
+    """test_hybrid.cpp:320-342, on the device path and the host path."""
+    base = oracle.generate_i32("random", 40000, 17)
+    lo, hi = 10007, 29999
+    for name in ("Classic", "3To8", "VarSort4", "6To8", "3To5"):
+        cfg = ns.find_config(name)
+        for fn in (ns.optimized_merge_sort, ns.optimized_quick_sort):
+            t = to_dev(base, cuda)
+            fn(t, lo, hi, cfg)
+            got = from_dev(t)
+            assert np.array_equal(got[:lo], base[:lo]) and np.array_equal(got[hi + 1:], base[hi + 1:])
+            assert np.array_equal(got[lo:hi + 1], np.sort(base[lo:hi + 1]))
+            h = base.copy()
+            fn(h, lo, hi, cfg)
+            assert np.array_equal(h, got)
+            # inverted range is a no-op (hybrid.hpp:160, 201)
+            h2 = base.copy()
+            fn(h2, 5, 4, cfg)
+            assert np.array_equal(h2, base)
+
+
+def test_host_entry_points(ns, cuda, oracle):
+    for n in (0, 1, 7, 10000, 1000000):
+        a = oracle.generate_i32("random", n, 5)
+        want = np.sort(a)
+        for fn, cfg in ((ns.optimized_merge_sort, "6To8"), (ns.optimized_quick_sort, "3To5"),
+                        (ns.classical_merge_sort, None), (ns.classical_quick_sort, None)):
+            h = a.copy()
+            fn(h, ns.find_config(cfg)) if cfg else fn(h)
+            assert np.array_equal(h, want), (fn.__name__, n)
+
+
+def test_duplicates_and_extremes(ns, cuda):
+    rng = np.random.default_rng(0)
+    cases = [
+        np.full(100000, 7, np.int32),
+        np.full(50000, np.iinfo(np.int32).max, np.int32),
+        np.full(50000, np.iinfo(np.int32).min, np.int32),
+        rng.integers(0, 3, 300000).astype(np.int32),
+        rng.integers(np.iinfo(np.int32).min, np.iinfo(np.int32).max, 300000, dtype=np.int32),
+        np.concatenate([np.full(200000, 5, np.int32), rng.integers(0, 10, 100000).astype(np.int32)]),
+        np.arange(300000, 0, -1, dtype=np.int32),
+        np.tile(np.arange(1000, dtype=np.int32), 300),
+    ]
+    for a in cases:
+        for fn, cfg in ((ns.optimized_merge_sort, "6To8"), (ns.optimized_quick_sort, "3To5")):
+            t = to_dev(a, cuda)
+            fn(t, ns.find_config(cfg))
+            assert np.array_equal(from_dev(t), np.sort(a)), (fn.__name__, a[:5])
+
+
+def test_checking_helpers(ns, cuda, oracle):
+    a = oracle.generate_i32("random", 123457, 9)
+    t = to_dev(a, cuda)
+    assert ns.multiset_digest(t) == oracle.multiset_digest(a)
+    assert ns.count_inversions(t) == int(np.sum(a[:-1] > a[1:]))
+    ns.optimized_merge_sort(t, ns.find_config("6To8"))
+    assert ns.count_inversions(t) == 0
+    assert ns.multiset_digest(t) == oracle.multiset_digest(a)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("algo", ["merge", "quick"])
+def test_full_size_properties(ns, cuda, oracle, algo):
+    """At BASELINE's largest single-array size: sorted + same multiset."""
+    import torch
+    n = 1 << 30 if algo == "merge" else 16_777_216
+    g = torch.Generator(device=cuda)
+    g.manual_seed(1234)
+    t = torch.randint(0, 2**31 - 1, (n,), dtype=torch.int32, device=cuda, generator=g)
+    d0 = ns.multiset_digest(t)
+    (ns.optimized_merge_sort if algo == "merge" else ns.optimized_quick_sort)(
+        t, ns.find_config("6To8" if algo == "merge" else "3To5"))
+    assert ns.count_inversions(t) == 0
+    assert ns.multiset_digest(t) == d0
+    del t
+    ns.release_scratch()
+    torch.cuda.empty_cache()
