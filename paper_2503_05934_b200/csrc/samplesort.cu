@@ -78,7 +78,7 @@ __global__ void __launch_bounds__(NT)
     pairs_merge_kernel(const int32_t* __restrict__ src, int32_t* __restrict__ dst, PairTable t,
                        const int64_t* __restrict__ mp) {
   constexpr int TM = NT * K;
-  __shared__ __align__(16) int32_t sm[TM];
+  __shared__ __align__(16) int32_t sm[TM + 4];  // +pad: an exhausted B side may be peeked at sm[TM]
   const int tid = threadIdx.x;
   const int64_t c = blockIdx.x;
   const int p = pair_of(t, c);
