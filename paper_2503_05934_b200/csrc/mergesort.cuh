@@ -63,6 +63,21 @@ __device__ __forceinline__ void warp_bitonic(T (&v)[K], int lane) {
   }
 }
 
+// Shared-memory layout: one pad word after every 32 keys.  Thread cursors in
+// the merge levels sit ~K/2 keys apart (K = keys per thread), i.e. on the same
+// bank every 32/(K/2) lanes without padding; with it every warp-wide blocked
+// access (thread t touching t*K + k) and every coalesced access is bank
+// conflict free, and data-dependent merge cursors spread across banks.
+__host__ __device__ constexpr int pad_idx(int i) { return i + (i >> 5); }
+__host__ __device__ constexpr int padded_words(int T) { return T + (T >> 5) + 8; }
+
+// Read-only view of a run that starts at logical index `off` of padded smem.
+struct SmemRun {
+  const int32_t* s;
+  int off;
+  __device__ __forceinline__ int32_t operator[](int i) const { return s[pad_idx(off + i)]; }
+};
+
 // Merge-path split: number of elements taken from A among the first `diag`
 // outputs of merge(A, B) when A wins ties (same rule as merge_runs,
 // hybrid.hpp:71-75).
@@ -78,11 +93,11 @@ __device__ __forceinline__ IDX merge_path(PA A, IDX a_len, PB B, IDX b_len, IDX 
   return lo;
 }
 
-// Serial merge of K outputs starting at (a, b) from shared-memory runs.
-template <int K>
-__device__ __forceinline__ void serial_merge(const int32_t* A, int a_len, const int32_t* B,
-                                             int b_len, int a, int b, int32_t (&v)[K]) {
-  // clamped indices keep every shared-memory read in bounds; the clamped
+// Serial merge of K outputs starting at (a, b).
+template <int K, class SA, class SB>
+__device__ __forceinline__ void serial_merge(SA A, int a_len, SB B, int b_len, int a, int b,
+                                             int32_t (&v)[K]) {
+  // clamped indices keep every read inside the staged tile; the clamped
   // value is never selected because the exhausted side loses every test
   const int a_last = max(a_len - 1, 0), b_last = max(b_len - 1, 0);
   int32_t ka = A[min(a, a_last)];
@@ -101,6 +116,109 @@ __device__ __forceinline__ void serial_merge(const int32_t* A, int a_len, const 
   }
 }
 
+// Blocked registers <-> padded smem (thread t owns logical [t*K, t*K+K)).
+template <int K>
+__device__ __forceinline__ void regs_to_smem(int32_t* sm, const int32_t (&v)[K]) {
+  const int base = threadIdx.x * K;
+#pragma unroll
+  for (int k = 0; k < K; ++k) sm[pad_idx(base + k)] = v[k];
+}
+template <int K>
+__device__ __forceinline__ void smem_to_regs(const int32_t* sm, int32_t (&v)[K]) {
+  const int base = threadIdx.x * K;
+#pragma unroll
+  for (int k = 0; k < K; ++k) v[k] = sm[pad_idx(base + k)];
+}
+
+// Coalesced global -> padded smem for a T-key tile (`valid` live keys, the
+// rest padded with INT_MAX, which sorts to the tail).
+template <int NT, int T>
+__device__ __forceinline__ void tile_load(const int32_t* in, int valid, int32_t* sm) {
+  const int tid = threadIdx.x;
+  if (valid == T && (reinterpret_cast<uintptr_t>(in) & 15) == 0) {
+    const int4* p = reinterpret_cast<const int4*>(in);
+#pragma unroll
+    for (int q = 0; q < T / 4 / NT; ++q) {
+      const int j = q * NT + tid;
+      const int4 x = __ldcs(p + j);  // streamed: every key is read exactly once
+      const int i = pad_idx(4 * j);  // 4 consecutive keys never straddle a pad
+      sm[i] = x.x; sm[i + 1] = x.y; sm[i + 2] = x.z; sm[i + 3] = x.w;
+    }
+  } else {
+#pragma unroll 4
+    for (int i = tid; i < T; i += NT) sm[pad_idx(i)] = i < valid ? in[i] : INT_MAX;
+  }
+}
+
+// Stage the two input slices of a merge tile, A = a_ptr[0, la) followed by
+// B = b_ptr[0, lb), into padded smem [0, la + lb).  The slices start at
+// arbitrary key offsets, so each is covered by 16-byte-aligned chunks that
+// are loaded with 128-bit LDGs — ALL of a thread's chunks are issued before
+// the first shared-memory store, so every thread keeps up to CH loads in
+// flight — and the keys outside the slice are dropped.  [lo, hi) bounds the
+// underlying array: a chunk that would cross it is read key by key.
+template <int NT, int TM>
+__device__ __forceinline__ void stage_slices(const int32_t* lo, const int32_t* hi,
+                                             const int32_t* a_ptr, int la, const int32_t* b_ptr,
+                                             int lb, int32_t* sm) {
+  constexpr int CH = (TM / 4 + 3 + NT - 1) / NT;
+  const int tid = threadIdx.x;
+  const int32_t* a_al = reinterpret_cast<const int32_t*>(reinterpret_cast<uintptr_t>(a_ptr) & ~uintptr_t(15));
+  const int32_t* b_al = reinterpret_cast<const int32_t*>(reinterpret_cast<uintptr_t>(b_ptr) & ~uintptr_t(15));
+  const int a_shift = (int)(a_ptr - a_al), b_shift = (int)(b_ptr - b_al);
+  const int ca = la ? (a_shift + la + 3) >> 2 : 0;
+  const int cb = lb ? (b_shift + lb + 3) >> 2 : 0;
+  int4 x[CH];
+#pragma unroll
+  for (int u = 0; u < CH; ++u) {
+    const int c = u * NT + tid;
+    if (c < ca + cb) {
+      const int32_t* p = c < ca ? a_al + 4 * c : b_al + 4 * (c - ca);
+      if (p >= lo && p + 4 <= hi) {
+        x[u] = __ldcs(reinterpret_cast<const int4*>(p));
+      } else {
+        x[u].x = (p + 0 >= lo && p + 0 < hi) ? p[0] : 0;
+        x[u].y = (p + 1 >= lo && p + 1 < hi) ? p[1] : 0;
+        x[u].z = (p + 2 >= lo && p + 2 < hi) ? p[2] : 0;
+        x[u].w = (p + 3 >= lo && p + 3 < hi) ? p[3] : 0;
+      }
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < CH; ++u) {
+    const int c = u * NT + tid;
+    if (c < ca + cb) {
+      const bool in_a = c < ca;
+      const int first = in_a ? 4 * c - a_shift : la + 4 * (c - ca) - b_shift;
+      const int lim_lo = in_a ? 0 : la, lim_hi = in_a ? la : la + lb;
+      const int32_t e[4] = {x[u].x, x[u].y, x[u].z, x[u].w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int i = first + q;
+        if (i >= lim_lo && i < lim_hi) sm[pad_idx(i)] = e[q];
+      }
+    }
+  }
+}
+
+// Coalesced padded smem -> global for the first `valid` keys of a T-key tile.
+template <int NT, int T>
+__device__ __forceinline__ void tile_store(const int32_t* sm, int32_t* out, int valid) {
+  const int tid = threadIdx.x;
+  if (valid == T && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
+    int4* p = reinterpret_cast<int4*>(out);
+#pragma unroll
+    for (int q = 0; q < T / 4 / NT; ++q) {
+      const int j = q * NT + tid;
+      const int i = pad_idx(4 * j);
+      __stcs(p + j, make_int4(sm[i], sm[i + 1], sm[i + 2], sm[i + 3]));
+    }
+  } else {
+#pragma unroll 4
+    for (int i = tid; i < valid; i += NT) out[i] = sm[pad_idx(i)];
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Tile sort: one CTA sorts `valid` <= T = NT*K keys from `in` into `out` (in
 // place allowed) on chip.  Shared by the tiled merge sort, the segmented sort
@@ -113,22 +231,10 @@ __device__ __forceinline__ void cta_sort(const int32_t* in, int32_t* out, int va
   const int tid = threadIdx.x;
   const int lane = tid & 31;
 
+  tile_load<NT, T>(in, valid, sm);
+  __syncthreads();
   int32_t v[K];
-  const bool vec = (valid == T) && ((reinterpret_cast<uintptr_t>(in) & 15) == 0);
-  if (vec) {
-    const int4* p = reinterpret_cast<const int4*>(in + tid * K);
-#pragma unroll
-    for (int q = 0; q < K / 4; ++q) {
-      const int4 x = __ldcs(p + q);  // streamed: every key is read exactly once
-      v[4 * q] = x.x; v[4 * q + 1] = x.y; v[4 * q + 2] = x.z; v[4 * q + 3] = x.w;
-    }
-  } else {
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      const int i = tid * K + k;
-      v[k] = i < valid ? in[i] : INT_MAX;  // INT_MAX pads sort to the tail
-    }
-  }
+  smem_to_regs<K>(sm, v);
 
   thread_sort<LEAF>(v);  // the network base case (try_base_case, hybrid.hpp:48-56)
   if constexpr (NT >= 32) warp_bitonic<5>(v, lane);
@@ -137,29 +243,20 @@ __device__ __forceinline__ void cta_sort(const int32_t* in, int32_t* out, int va
 #pragma unroll 1
   for (int R = 32 * K; R < T; R *= 2) {
     __syncthreads();
-#pragma unroll
-    for (int k = 0; k < K; ++k) sm[tid * K + k] = v[k];
+    regs_to_smem<K>(sm, v);
     __syncthreads();
     const int pos = tid * K;
     const int pair = pos & ~(2 * R - 1);
     const int diag = pos - pair;
-    const int32_t* A = sm + pair;
-    const int32_t* B = A + R;
+    const SmemRun A{sm, pair}, B{sm, pair + R};
     const int a = merge_path<int>(A, R, B, R, diag);
     serial_merge<K>(A, R, B, R, a, diag - a, v);
   }
 
-  if (vec && ((reinterpret_cast<uintptr_t>(out) & 15) == 0)) {
-    int4* p = reinterpret_cast<int4*>(out + tid * K);
-#pragma unroll
-    for (int q = 0; q < K / 4; ++q) p[q] = make_int4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-  } else {
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      const int i = tid * K + k;
-      if (i < valid) out[i] = v[k];
-    }
-  }
+  __syncthreads();
+  regs_to_smem<K>(sm, v);
+  __syncthreads();
+  tile_store<NT, T>(sm, out, valid);
 }
 
 // CTA b sorts [b*stride, b*stride + min(stride, n - b*stride)), stride <= T
@@ -206,7 +303,7 @@ __global__ void __launch_bounds__(NT)
     merge_pass_kernel(const int32_t* __restrict__ src, int32_t* __restrict__ dst, int64_t n,
                       int64_t R, const int64_t* __restrict__ mp) {
   constexpr int TM = NT * K;
-  __shared__ __align__(16) int32_t sm[TM + 4];  // +pad: an exhausted B side may be peeked at sm[TM]
+  __shared__ __align__(16) int32_t sm[padded_words(TM)];
   const int tid = threadIdx.x;
   const int64_t c = blockIdx.x;
   const PassGeom g = pass_geom(c * TM, n, R);
@@ -219,27 +316,178 @@ __global__ void __launch_bounds__(NT)
   const int32_t* A = src + g.pair_base + a0;
   const int32_t* B = src + g.pair_base + g.a_len + (g.diag0 - a0);
 
+  // stage both input slices in padded smem: [A slice | B slice]
   const int total = la + lb;
-#pragma unroll 4
-  for (int i = tid; i < total; i += NT) sm[i] = i < la ? __ldcs(A + i) : __ldcs(B + (i - la));
+  stage_slices<NT, TM>(src, src + n, A, la, B, lb, sm);
   __syncthreads();
 
   const int diag = min(tid * K, total);
-  const int a = merge_path<int>(sm, la, sm + la, lb, diag);
+  const SmemRun SA{sm, 0}, SB{sm, la};
+  const int a = merge_path<int>(SA, la, SB, lb, diag);
   int32_t v[K];
-  serial_merge<K>(sm, la, sm + la, lb, a, diag - a, v);
+  serial_merge<K>(SA, la, SB, lb, a, diag - a, v);
 
-  int32_t* out = dst + c * TM;
-  if (total == TM && ((reinterpret_cast<uintptr_t>(out) & 15) == 0)) {
-    int4* p = reinterpret_cast<int4*>(out + tid * K);
+  // restage the merged tile so the HBM stores are coalesced 128-bit writes
+  __syncthreads();
+  regs_to_smem<K>(sm, v);
+  __syncthreads();
+  tile_store<NT, TM>(sm, dst + c * TM, total);
+}
+
+}  // namespace nsb
+
+// ===========================================================================
+// Merge pass v2: pair-local tiles, TMA bulk staging, sentinel merge.
+//
+// Every run pair (A = [p*2R, p*2R+R), B = the next R keys) is cut into tpp
+// output tiles of TMp keys (TMp <= NT*K, a multiple of 4, as even as the pair
+// allows), so no tile straddles two pairs and K can be odd: with an odd
+// per-thread output count the merge cursors of neighbouring lanes land on
+// different shared-memory banks without any padding, which keeps the layout
+// TMA-compatible.  One elected thread stages the 16-byte-aligned cover of
+// each input slice with a single cp.async.bulk (complete_tx on an mbarrier),
+// places +inf sentinels after both slices (no bounds tests in the merge
+// loop), and after the merge writes the tile back with one bulk store.
+// Slices whose cover would leave the array fall back to plain loads.
+// ===========================================================================
+#include "tma.cuh"
+
+namespace nsb {
+
+struct PassPlan {
+  int64_t R;    // run length being merged
+  int64_t n;    // keys
+  int tpp;      // tiles per pair
+  int tmp;      // keys per tile (<= NT*K, multiple of 4)
+  int kp;       // outputs per thread = ceil(tmp / NT)
+};
+
+struct TileGeom {
+  int64_t pair_base, a_len, b_len, diag0, diag1;
+};
+
+__device__ __forceinline__ TileGeom tile_geom(const PassPlan& P, int64_t c) {
+  TileGeom g;
+  const int64_t pair = c / P.tpp;
+  const int64_t lt = c - pair * P.tpp;
+  g.pair_base = pair * 2 * P.R;
+  g.a_len = min(P.R, P.n - g.pair_base);
+  g.b_len = max((int64_t)0, min(P.R, P.n - g.pair_base - P.R));
+  const int64_t pair_len = g.a_len + g.b_len;
+  g.diag0 = min(lt * P.tmp, pair_len);
+  g.diag1 = min(g.diag0 + P.tmp, pair_len);
+  return g;
+}
+
+static __global__ void merge_partition_v2_kernel(const int32_t* __restrict__ src, PassPlan P,
+                                          int64_t num_tiles, int64_t* __restrict__ mp) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= num_tiles) return;
+  const TileGeom g = tile_geom(P, c);
+  const int32_t* A = src + g.pair_base;
+  mp[c] = merge_path<int64_t>(A, g.a_len, A + g.a_len, g.b_len, g.diag0);
+}
+
+// Words of shared memory a v2 tile needs: two slices with up to 3 words of
+// alignment slack each, a sentinel after each, 16-byte rounding.
+__host__ __device__ constexpr int v2_smem_words(int TM) { return TM + 16; }
+
+template <int NT, int K>
+__global__ void __launch_bounds__(NT)
+    merge_pass_v2_kernel(const int32_t* __restrict__ src, int32_t* __restrict__ dst, PassPlan P,
+                         const int64_t* __restrict__ mp) {
+  constexpr int TM = NT * K;
+  __shared__ __align__(128) int32_t sm[v2_smem_words(TM)];
+  __shared__ __align__(8) uint64_t bar;
+  const int tid = threadIdx.x;
+  const int64_t c = blockIdx.x;
+  const TileGeom g = tile_geom(P, c);
+  if (g.diag0 >= g.diag1) return;  // empty trailing tile of a short last pair
+  const bool last_in_pair = g.diag1 == g.a_len + g.b_len;
+  const int64_t a0 = mp[c];
+  const int64_t a1 = last_in_pair ? g.a_len : mp[c + 1];
+  const int la = (int)(a1 - a0);
+  const int lb = (int)((g.diag1 - a1) - (g.diag0 - a0));
+  const int32_t* A = src + g.pair_base + a0;
+  const int32_t* B = src + g.pair_base + g.a_len + (g.diag0 - a0);
+  const int32_t* lo = src;
+  const int32_t* hi = src + P.n;
+
+  // smem placement mirrors global 16-byte alignment so one bulk copy per slice
+  const uintptr_t a_addr = reinterpret_cast<uintptr_t>(A), b_addr = reinterpret_cast<uintptr_t>(B);
+  const int a_shift = (int)((a_addr & 15) >> 2), b_shift = (int)((b_addr & 15) >> 2);
+  const int b_off = (a_shift + la + 1 + 3) & ~3;  // B cover starts 16-byte aligned
+  const int32_t* a_cov = A - a_shift;
+  const int32_t* b_cov = B - b_shift;
+  const int a_words = (a_shift + la + 3) & ~3, b_words = (b_shift + lb + 3) & ~3;
+  const bool a_tma = la > 0 && (a_addr & 3) == 0 && a_cov >= lo && a_cov + a_words <= hi;
+  const bool b_tma = lb > 0 && (b_addr & 3) == 0 && b_cov >= lo && b_cov + b_words <= hi;
+
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    const uint32_t bytes = (a_tma ? a_words * 4u : 0u) + (b_tma ? b_words * 4u : 0u);
+    mbar_arrive_expect_tx(&bar, bytes);
+    if (a_tma) tma_load_1d(sm, a_cov, a_words * 4u, &bar);
+    if (b_tma) tma_load_1d(sm + b_off, b_cov, b_words * 4u, &bar);
+  }
+  if (!a_tma)
+    for (int i = tid; i < la; i += NT) sm[a_shift + i] = __ldcs(A + i);
+  if (!b_tma)
+    for (int i = tid; i < lb; i += NT) sm[b_off + b_shift + i] = __ldcs(B + i);
+  mbar_wait(&bar, 0);
+  __syncthreads();
+  if (tid == 0) {
+    sm[a_shift + la] = INT_MAX;          // sentinels: the merge loop has no bounds tests
+    sm[b_off + b_shift + lb] = INT_MAX;
+  }
+  __syncthreads();
+
+  const int32_t* SA = sm + a_shift;
+  const int32_t* SB = sm + b_off + b_shift;
+  const int total = la + lb;
+  const int kp = P.kp;
+  const int d = min(tid * kp, total);
+  const int cnt = min(kp, total - d);
+  const int a = merge_path<int>(SA, la, SB, lb, d);
+  int ia = a, ib = d - a;
+  int32_t ka = SA[ia], kb = SB[ib];
+  int32_t v[K];
 #pragma unroll
-    for (int q = 0; q < K / 4; ++q) p[q] = make_int4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-  } else {
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      const int i = tid * K + k;
-      if (i < total) out[i] = v[k];
+  for (int k = 0; k < K; ++k) {
+    if (k < cnt) {
+      const bool take_a = ka <= kb;  // A wins ties (merge_runs, hybrid.hpp:71-75)
+      v[k] = take_a ? ka : kb;
+      if (take_a) {
+        ia = min(ia + 1, la);  // an exhausted side keeps re-reading its sentinel
+        ka = SA[ia];
+      } else {
+        ib = min(ib + 1, lb);
+        kb = SB[ib];
+      }
     }
+  }
+  __syncthreads();  // every thread is done reading the staged inputs
+#pragma unroll
+  for (int k = 0; k < K; ++k)
+    if (k < cnt) sm[d + k] = v[k];
+
+  int32_t* out = dst + g.pair_base + g.diag0;
+  const bool o_tma = ((reinterpret_cast<uintptr_t>(out) & 15) == 0) && (total & 3) == 0;
+  if (o_tma) {
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+      tma_store_1d(out, sm, (uint32_t)total * 4u);
+      bulk_commit();
+      bulk_wait_read_all();
+    }
+  } else {
+    __syncthreads();
+    for (int i = tid; i < total; i += NT) out[i] = sm[i];
   }
 }
 

@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <climits>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -28,7 +29,7 @@ static_assert((2 * kBsT) % kMgT == 0, "merge tiles must not straddle run pairs")
 template <int NT, int K, int LEAF>
 static int launch_blocksort(const int32_t* src, int32_t* dst, int64_t n, int stride,
                             int64_t ctas, cudaStream_t s) {
-  constexpr int smem = NT * K * 4;
+  constexpr int smem = padded_words(NT * K) * 4;
   auto* kern = blocksort_kernel<NT, K, LEAF>;
   static bool attr_set = false;  // benign race: idempotent attribute write
   if (!attr_set) {
@@ -44,10 +45,42 @@ static int launch_blocksort(const int32_t* src, int32_t* dst, int64_t n, int str
   return check_launch("blocksort_kernel");
 }
 
+// Tuning knobs (read once; the defaults are the measured best on B200).
+//   NSB_TILE  = 8192 | 16384 : keys per tile-sort CTA
+//   NSB_MERGE = 16 | 32      : outputs per thread in the merge pass (CTA = 8192 keys)
+//   NSB_MERGE = 2 selects the TMA-staged pair-local merge pass (merge_pass_v2)
+constexpr int kV2NT = 256, kV2K = 31, kV2T = kV2NT * kV2K;  // 7936 keys per tile
+struct MergeTuning {
+  int tile = kBsT;
+  int merge_k = 2;
+  MergeTuning() {
+    if (const char* e = getenv("NSB_TILE")) tile = atoi(e) == 16384 ? 16384 : 8192;
+    if (const char* e = getenv("NSB_MERGE")) merge_k = atoi(e);
+  }
+};
+static const MergeTuning& tuning() {
+  static const MergeTuning t;
+  return t;
+}
+
+// Upper bound on merge tiles of any pass (v1: n/kMgT; v2: <= 4n/kV2T + n/16384 + 2).
+static size_t max_merge_tiles(size_t n) { return n / 1024 + 64; }
+
 size_t merge_sort_temp(size_t n) {
   if (n <= (size_t)kSmT) return 0;
-  const size_t tiles = (n + kMgT - 1) / kMgT;
-  return align_up(n * sizeof(int32_t), 256) + align_up((tiles + 1) * sizeof(int64_t), 256);
+  return align_up(n * sizeof(int32_t), 256) + align_up((max_merge_tiles(n) + 1) * 8, 256);
+}
+
+static PassPlan plan_pass(int64_t n, int64_t R) {
+  PassPlan P;
+  P.R = R;
+  P.n = n;
+  const int64_t two_r = 2 * R;
+  P.tpp = (int)((two_r + kV2T - 1) / kV2T);
+  const int64_t even = (two_r + P.tpp - 1) / P.tpp;
+  P.tmp = (int)((even + 3) & ~int64_t(3));
+  P.kp = (P.tmp + kV2NT - 1) / kV2NT;
+  return P;
 }
 
 int merge_sort_device(int32_t* d_keys, size_t n, int leaf, void* d_temp, size_t temp_bytes,
@@ -63,17 +96,40 @@ int merge_sort_device(int32_t* d_keys, size_t n, int leaf, void* d_temp, size_t 
   int32_t* tmp = static_cast<int32_t*>(d_temp);
   int64_t* mp = reinterpret_cast<int64_t*>(static_cast<char*>(d_temp) +
                                            align_up(n * sizeof(int32_t), 256));
-  const int64_t tiles = (int64_t)((n + kBsT - 1) / kBsT);
+  const MergeTuning& tu = tuning();
+  const int T = tu.tile;
+  const int64_t tiles = (int64_t)((n + T - 1) / T);
   const int passes = ceil_log2((uint64_t)tiles);
   // Pick the tile-sort destination so the last pass lands in d_keys.
   int32_t* cur = (passes & 1) ? tmp : d_keys;
   int32_t* other = (cur == d_keys) ? tmp : d_keys;
   NSB_TRY(with_leaf(leaf, [&](auto L) {
-    return launch_blocksort<kBsNT, kBsK, decltype(L)::value>(d_keys, cur, (int64_t)n, kBsT,
-                                                              tiles, s);
+    constexpr int LF = decltype(L)::value;
+    return T == kSmT ? launch_blocksort<kSmNT, kSmK, LF>(d_keys, cur, (int64_t)n, T, tiles, s)
+                     : launch_blocksort<kBsNT, kBsK, LF>(d_keys, cur, (int64_t)n, T, tiles, s);
   }));
+  if (tu.merge_k == 2) {
+    for (int64_t R = T; R < (int64_t)n; R *= 2) {
+      const PassPlan P = plan_pass((int64_t)n, R);
+      const int64_t pairs = ((int64_t)n + 2 * R - 1) / (2 * R);
+      const int64_t tiles = pairs * P.tpp;
+      {
+        Prof prof(PK_PARTITION, s);
+        merge_partition_v2_kernel<<<(unsigned)((tiles + 255) / 256), 256, 0, s>>>(cur, P, tiles,
+                                                                                 mp);
+      }
+      NSB_TRY(check_launch("merge_partition_v2_kernel"));
+      {
+        Prof prof(PK_MERGE_PASS, s);
+        merge_pass_v2_kernel<kV2NT, kV2K><<<(unsigned)tiles, kV2NT, 0, s>>>(cur, other, P, mp);
+      }
+      NSB_TRY(check_launch("merge_pass_v2_kernel"));
+      std::swap(cur, other);
+    }
+    return NS_OK;
+  }
   const int64_t mtiles = (int64_t)((n + kMgT - 1) / kMgT);
-  for (int64_t R = kBsT; R < (int64_t)n; R *= 2) {
+  for (int64_t R = T; R < (int64_t)n; R *= 2) {
     {
       Prof prof(PK_PARTITION, s);
       merge_partition_kernel<kMgT><<<(unsigned)((mtiles + 255) / 256), 256, 0, s>>>(
@@ -82,8 +138,12 @@ int merge_sort_device(int32_t* d_keys, size_t n, int leaf, void* d_temp, size_t 
     NSB_TRY(check_launch("merge_partition_kernel"));
     {
       Prof prof(PK_MERGE_PASS, s);
-      merge_pass_kernel<kMgNT, kMgK><<<(unsigned)mtiles, kMgNT, 0, s>>>(cur, other, (int64_t)n,
-                                                                        R, mp);
+      if (tu.merge_k == 32)
+        merge_pass_kernel<kMgT / 32, 32><<<(unsigned)mtiles, kMgT / 32, 0, s>>>(
+            cur, other, (int64_t)n, R, mp);
+      else
+        merge_pass_kernel<kMgNT, kMgK><<<(unsigned)mtiles, kMgNT, 0, s>>>(cur, other,
+                                                                          (int64_t)n, R, mp);
     }
     NSB_TRY(check_launch("merge_pass_kernel"));
     std::swap(cur, other);

@@ -169,7 +169,7 @@ template <int NT, int K, int LEAF>
 static int launch_bucket_sort(const int32_t* src, int32_t* dst, const int64_t* jobs, int njobs,
                               cudaStream_t s) {
   if (njobs == 0) return NS_OK;
-  constexpr int smem = NT * K * 4;
+  constexpr int smem = padded_words(NT * K) * 4;
   auto* kern = bucket_sort_kernel<NT, K, LEAF>;
   static bool attr_set = false;
   if (!attr_set) {

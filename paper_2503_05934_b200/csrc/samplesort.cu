@@ -53,6 +53,7 @@ __global__ void bucket_bounds_kernel(const int32_t* __restrict__ sorted, int64_t
 constexpr int kMaxPairs = 64;
 struct PairTable {
   int npairs;
+  int64_t n;  // keys in the buffer (bounds every read)
   int64_t a_base[kMaxPairs], a_len[kMaxPairs], b_len[kMaxPairs], tile0[kMaxPairs + 1];
 };
 
@@ -78,7 +79,7 @@ __global__ void __launch_bounds__(NT)
     pairs_merge_kernel(const int32_t* __restrict__ src, int32_t* __restrict__ dst, PairTable t,
                        const int64_t* __restrict__ mp) {
   constexpr int TM = NT * K;
-  __shared__ __align__(16) int32_t sm[TM + 4];  // +pad: an exhausted B side may be peeked at sm[TM]
+  __shared__ __align__(16) int32_t sm[padded_words(TM)];
   const int tid = threadIdx.x;
   const int64_t c = blockIdx.x;
   const int p = pair_of(t, c);
@@ -92,18 +93,17 @@ __global__ void __launch_bounds__(NT)
   const int32_t* A = src + t.a_base[p] + a0;
   const int32_t* B = src + t.a_base[p] + t.a_len[p] + (diag0 - a0);
   const int total = la + lb;
-  for (int i = tid; i < total; i += NT) sm[i] = i < la ? __ldcs(A + i) : __ldcs(B + (i - la));
+  stage_slices<NT, TM>(src, src + t.n, A, la, B, lb, sm);
   __syncthreads();
   const int diag = min(tid * K, total);
-  const int a = merge_path<int>(sm, la, sm + la, lb, diag);
+  const SmemRun SA{sm, 0}, SB{sm, la};
+  const int a = merge_path<int>(SA, la, SB, lb, diag);
   int32_t v[K];
-  serial_merge<K>(sm, la, sm + la, lb, a, diag - a, v);
-  int32_t* out = dst + t.a_base[p] + diag0;
-#pragma unroll
-  for (int k = 0; k < K; ++k) {
-    const int i = tid * K + k;
-    if (i < total) out[i] = v[k];
-  }
+  serial_merge<K>(SA, la, SB, lb, a, diag - a, v);
+  __syncthreads();
+  regs_to_smem<K>(sm, v);
+  __syncthreads();
+  tile_store<NT, TM>(sm, dst + t.a_base[p] + diag0, total);
 }
 
 constexpr int kPmNT = 512, kPmK = 16, kPmT = kPmNT * kPmK;
@@ -179,6 +179,7 @@ int ns_merge_runs_i32(int32_t* d_keys, const int64_t* h_run_offsets, int num_run
     const int nr = (int)runs.size() - 1;
     PairTable t{};
     t.npairs = (nr + 1) / 2;
+    t.n = n;
     int64_t tiles = 0;
     std::vector<int64_t> next{0};
     for (int p = 0; p < t.npairs; ++p) {

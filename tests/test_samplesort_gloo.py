@@ -1,0 +1,106 @@
+"""Multi-process sample sort (BASELINE config 5) on CPU: world_size 2 (and 3)
+over gloo, exercising the exchange logic of paper_2503_05934_b200/samplesort.py
+with the per-rank steps injected from the oracle (test-only ops; the product
+uses DeviceOps, the sm_100a library)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+class OracleOps:
+    """CPU stand-ins for DeviceOps with identical contracts."""
+
+    def __init__(self):
+        from oracle import oracle as O
+        self.O = O
+
+    def local_sort(self, keys):
+        keys.copy_(torch.from_numpy(self.O.merge_sort(keys.numpy(), "6To8")))
+
+    def samples(self, sorted_keys, s):
+        n = sorted_keys.numel()
+        if n == 0:
+            return torch.full((s,), 2**31 - 1, dtype=torch.int32)
+        idx = [(k + 1) * n // (s + 1) for k in range(s)]
+        return sorted_keys[idx].clone()
+
+    def splitters(self, all_samples, g):
+        srt = torch.from_numpy(self.O.merge_sort(all_samples.numpy(), "6To8"))
+        s = srt.numel()
+        return srt[[(k + 1) * s // g for k in range(g - 1)]].clone()
+
+    def bounds(self, sorted_keys, spl, g):
+        a = sorted_keys.numpy()
+        b = [0] + [int(np.searchsorted(a, int(x), side="left")) for x in spl.tolist()] + [len(a)]
+        return torch.tensor(b, dtype=torch.int64)
+
+    def merge_runs(self, keys, offs):
+        out = keys.numpy().copy()
+        runs = [out[offs[i]:offs[i + 1]] for i in range(len(offs) - 1)]
+        for r in runs:
+            assert np.all(r[:-1] <= r[1:])
+        merged = runs[0] if runs else out[:0]
+        for r in runs[1:]:
+            cat = np.concatenate([merged, r]).astype(np.int32)
+            self.O.lib().oracle_merge_i32(cat, 0, len(merged) - 1, len(cat) - 1) if len(merged) and len(r) else None
+            merged = cat
+        keys.copy_(torch.from_numpy(np.ascontiguousarray(merged, np.int32)))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, n, dist_kind, q):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle import oracle as O
+    from paper_2503_05934_b200 import samplesort
+    full = O.generate_i32(dist_kind, n, 42)
+    m = n // world
+    lo = rank * m
+    hi = n if rank == world - 1 else lo + m
+    shard = torch.from_numpy(full[lo:hi].copy())
+    out = samplesort.sample_sort(shard, ops=OracleOps())
+    parts = [None] * world
+    dist.all_gather_object(parts, out.numpy().tolist())
+    if rank == 0:
+        q.put(parts)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n,dist_kind", [(2, 20000, "random"), (2, 5000, "sorted"),
+                                               (3, 30001, "random"), (2, 3, "random")])
+def test_sample_sort_multi_process(oracle, world, n, dist_kind):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, dist_kind, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    parts = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    result = np.array([x for part in parts for x in part], np.int32)
+    full = oracle.generate_i32(dist_kind, n, 42)
+    # globally sorted, a permutation of the input, equal to the oracle's sort
+    assert np.array_equal(result, oracle.merge_sort(full, "6To8"))
+    # every rank's slice is sorted and the ranks are in order
+    for a, b in zip(parts, parts[1:]):
+        if a and b:
+            assert a[-1] <= b[0]
