@@ -59,7 +59,18 @@ struct MergeTuning {
   }
 };
 static const MergeTuning& tuning() {
-  static const MergeTuning t;
+  static const MergeTuning t = [] {
+    MergeTuning m;
+    if (const char* e = getenv("NSB_TS_STAGE")) {
+      const int st = atoi(e);
+      cudaMemcpyToSymbol(g_ts_stage, &st, sizeof(int));
+    }
+    if (const char* e = getenv("NSB_TS_KB")) {
+      const int kb = atoi(e);
+      cudaMemcpyToSymbol(g_ts_kb, &kb, sizeof(int));
+    }
+    return m;
+  }();
   return t;
 }
 
@@ -154,6 +165,7 @@ int merge_sort_device(int32_t* d_keys, size_t n, int leaf, void* d_temp, size_t 
 int tile_sort_segments(int32_t* d_keys, size_t num_segments, size_t seg_len, int leaf,
                        cudaStream_t s) {
   if (seg_len > (size_t)kSmT) return NS_ERR_INVALID;
+  (void)tuning();
   const int64_t n = (int64_t)(num_segments * seg_len);
   if (seg_len <= (size_t)kBsT) {
     return with_leaf(leaf, [&](auto L) {
