@@ -7,10 +7,12 @@
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 
 #include "common.cuh"
 #include "mergesort.cuh"
+#include "kway.cuh"
 #include "networks.cuh"
 
 namespace nsb {
@@ -50,12 +52,18 @@ static int launch_blocksort(const int32_t* src, int32_t* dst, int64_t n, int str
 //   NSB_MERGE = 16 | 32      : outputs per thread in the merge pass (CTA = 8192 keys)
 //   NSB_MERGE = 2 selects the TMA-staged pair-local merge pass (merge_pass_v2)
 constexpr int kV2NT = 256, kV2K = 31, kV2T = kV2NT * kV2K;  // 7936 keys per tile
+//   NSB_KWAY  = 0 | 4 | 8 : widest k-way merge pass (0 = pairwise only, default)
+//   NSB_KWAY_MIN = n below which only pairwise passes are used
 struct MergeTuning {
   int tile = kBsT;
   int merge_k = 2;
+  int kway = 0;  // measured: k-way passes are merge-compute bound, no faster
+  int64_t kway_min = int64_t(1) << 22;
   MergeTuning() {
     if (const char* e = getenv("NSB_TILE")) tile = atoi(e) == 16384 ? 16384 : 8192;
     if (const char* e = getenv("NSB_MERGE")) merge_k = atoi(e);
+    if (const char* e = getenv("NSB_KWAY")) kway = atoi(e);
+    if (const char* e = getenv("NSB_KWAY_MIN")) kway_min = atoll(e);
   }
 };
 static const MergeTuning& tuning() {
@@ -77,9 +85,108 @@ static const MergeTuning& tuning() {
 // Upper bound on merge tiles of any pass (v1: n/kMgT; v2: <= 4n/kV2T + n/16384 + 2).
 static size_t max_merge_tiles(size_t n) { return n / 1024 + 64; }
 
+// k-way scratch: raw + 2 merged sample buffers (u64), their merge-path splits,
+// and the tile cuts (int32 per run per tile).
+static size_t kway_max_samples(size_t n) { return n / kKwS + 1024; }
+// sample-merge splits: tiles of >= 128 samples (2 * Ls, Ls = R / 128 >= 64)
+static size_t kway_max_cuts(size_t n) { return (n / 4096 + 1024) * 8; }
+static size_t kway_temp(size_t n) {
+  return 3 * align_up(kway_max_samples(n) * 8, 256) +
+         align_up((kway_max_samples(n) / 128 + 64) * 8, 256) +
+         align_up(kway_max_cuts(n) * 4, 256);
+}
+
 size_t merge_sort_temp(size_t n) {
   if (n <= (size_t)kSmT) return 0;
-  return align_up(n * sizeof(int32_t), 256) + align_up((max_merge_tiles(n) + 1) * 8, 256);
+  return align_up(n * sizeof(int32_t), 256) + align_up((max_merge_tiles(n) + 1) * 8, 256) +
+         kway_temp(n);
+}
+
+struct KwScratch {
+  uint64_t *raw, *m1, *m2;
+  int64_t* smp;
+  int32_t* cuts;
+};
+
+static KwScratch carve_kway(char* p, size_t n) {
+  KwScratch k;
+  const size_t sb = align_up(kway_max_samples(n) * 8, 256);
+  k.raw = reinterpret_cast<uint64_t*>(p);
+  k.m1 = reinterpret_cast<uint64_t*>(p + sb);
+  k.m2 = reinterpret_cast<uint64_t*>(p + 2 * sb);
+  k.smp = reinterpret_cast<int64_t*>(p + 3 * sb);
+  k.cuts = reinterpret_cast<int32_t*>(p + 3 * sb +
+                                      align_up((kway_max_samples(n) / 128 + 64) * 8, 256));
+  return k;
+}
+
+template <int K>
+static int launch_kway_merge(const int32_t* src, int32_t* dst, const KwPlan& P,
+                             const int32_t* cuts, cudaStream_t s) {
+  constexpr int smem = 2 * kway_buf_words(K) * 4;
+  auto* kern = kway_merge_kernel<K>;
+  static bool attr = false;
+  if (!attr) {
+    NSB_TRY(check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            smem),
+                       "cudaFuncSetAttribute(kway)"));
+    attr = true;
+  }
+  {
+    Prof prof(PK_MERGE_PASS, s);
+    kern<<<(unsigned)P.tiles, kKwNT, smem, s>>>(src, dst, P, cuts);
+  }
+  return check_launch("kway_merge_kernel");
+}
+
+// One k-way pass: runs of R in src -> runs of k*R in dst.
+static int kway_pass(const int32_t* src, int32_t* dst, int64_t n, int64_t R, int k,
+                     const KwScratch& ks, cudaStream_t s) {
+  KwPlan P;
+  P.n = n;
+  P.R = R;
+  P.k = k;
+  P.Ls = R / kKwS;
+  const int64_t nruns = (n + R - 1) / R;
+  const int64_t last_len = n - (nruns - 1) * R;
+  P.S = (nruns - 1) * P.Ls + (last_len + kKwS - 1) / kKwS;
+  const int m = kway_m(k);
+  P.tiles_full = (int)((k * P.Ls + m - 1) / m);
+  P.groups = (nruns + k - 1) / k;
+  P.tiles = P.groups * P.tiles_full;
+  {
+    Prof prof(PK_PARTITION, s);
+    kway_sample_kernel<<<(unsigned)((P.S + 255) / 256), 256, 0, s>>>(src, P, ks.raw);
+  }
+  NSB_TRY(check_launch("kway_sample_kernel"));
+  // merge the k sample sub-runs of every group: log2(k) pairwise rounds
+  const uint64_t* cur = ks.raw;
+  uint64_t* bufs[2] = {ks.m1, ks.m2};
+  int bi = 0;
+  constexpr int SNT = 256, SK = 8, STM = SNT * SK;
+  for (int64_t r = P.Ls; r < (int64_t)k * P.Ls; r *= 2) {
+    const int tm = (int)std::min<int64_t>(STM, 2 * r);  // divides 2r: no tile straddles pairs
+    const int64_t tiles = (P.S + tm - 1) / tm;
+    {
+      Prof prof(PK_PARTITION, s);
+      simple_partition_kernel<uint64_t><<<(unsigned)((tiles + 255) / 256), 256, 0, s>>>(
+          cur, P.S, r, tm, tiles, ks.smp);
+      simple_merge_pass_kernel<uint64_t, SNT, SK><<<(unsigned)tiles, SNT, 0, s>>>(
+          cur, bufs[bi], P.S, r, tm, ks.smp);
+    }
+    NSB_TRY(check_launch("simple_merge_pass_kernel"));
+    cur = bufs[bi];
+    bi ^= 1;
+  }
+  {
+    Prof prof(PK_PARTITION, s);
+    const int64_t threads = P.tiles * k;
+    kway_boundary_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(src, ks.raw, cur, P,
+                                                                           m, ks.cuts);
+  }
+  NSB_TRY(check_launch("kway_boundary_kernel"));
+  return k == 8 ? launch_kway_merge<8>(src, dst, P, ks.cuts, s)
+                : launch_kway_merge<4>(src, dst, P, ks.cuts, s);
 }
 
 static PassPlan plan_pass(int64_t n, int64_t R) {
@@ -110,7 +217,18 @@ int merge_sort_device(int32_t* d_keys, size_t n, int leaf, void* d_temp, size_t 
   const MergeTuning& tu = tuning();
   const int T = tu.tile;
   const int64_t tiles = (int64_t)((n + T - 1) / T);
-  const int passes = ceil_log2((uint64_t)tiles);
+  // pass schedule: k-way passes (k = 8 for 5+ runs, 4 for 3-4) on large
+  // inputs, pairwise v2 passes otherwise
+  int sched[64];
+  int npass = 0;
+  for (int64_t runs = tiles; runs > 1;) {
+    int k = 2;
+    if (tu.merge_k == 2 && tu.kway >= 4 && (int64_t)n >= tu.kway_min && runs >= 3)
+      k = (tu.kway >= 8 && runs >= 5) ? 8 : 4;
+    sched[npass++] = k;
+    runs = (runs + k - 1) / k;
+  }
+  const int passes = tu.merge_k == 2 ? npass : ceil_log2((uint64_t)tiles);
   // Pick the tile-sort destination so the last pass lands in d_keys.
   int32_t* cur = (passes & 1) ? tmp : d_keys;
   int32_t* other = (cur == d_keys) ? tmp : d_keys;
@@ -120,22 +238,33 @@ int merge_sort_device(int32_t* d_keys, size_t n, int leaf, void* d_temp, size_t 
                      : launch_blocksort<kBsNT, kBsK, LF>(d_keys, cur, (int64_t)n, T, tiles, s);
   }));
   if (tu.merge_k == 2) {
-    for (int64_t R = T; R < (int64_t)n; R *= 2) {
+    const KwScratch ks = carve_kway(reinterpret_cast<char*>(mp) +
+                                        align_up((max_merge_tiles(n) + 1) * 8, 256),
+                                    n);
+    int64_t R = T;
+    for (int pi = 0; pi < npass; ++pi) {
+      const int k = sched[pi];
+      if (k > 2) {
+        NSB_TRY(kway_pass(cur, other, (int64_t)n, R, k, ks, s));
+        std::swap(cur, other);
+        R *= k;
+        continue;
+      }
       const PassPlan P = plan_pass((int64_t)n, R);
       const int64_t pairs = ((int64_t)n + 2 * R - 1) / (2 * R);
-      const int64_t tiles = pairs * P.tpp;
+      const int64_t mt = pairs * P.tpp;
       {
         Prof prof(PK_PARTITION, s);
-        merge_partition_v2_kernel<<<(unsigned)((tiles + 255) / 256), 256, 0, s>>>(cur, P, tiles,
-                                                                                 mp);
+        merge_partition_v2_kernel<<<(unsigned)((mt + 255) / 256), 256, 0, s>>>(cur, P, mt, mp);
       }
       NSB_TRY(check_launch("merge_partition_v2_kernel"));
       {
         Prof prof(PK_MERGE_PASS, s);
-        merge_pass_v2_kernel<kV2NT, kV2K><<<(unsigned)tiles, kV2NT, 0, s>>>(cur, other, P, mp);
+        merge_pass_v2_kernel<kV2NT, kV2K><<<(unsigned)mt, kV2NT, 0, s>>>(cur, other, P, mp);
       }
       NSB_TRY(check_launch("merge_pass_v2_kernel"));
       std::swap(cur, other);
+      R *= 2;
     }
     return NS_OK;
   }
@@ -187,36 +316,55 @@ int tile_sort_segments(int32_t* d_keys, size_t num_segments, size_t seg_len, int
 // ---------------------------------------------------------------------------
 constexpr int kBaNT = 256, kBaPer = 4, kBaArr = kBaNT * kBaPer;
 
+// Lanes of a warp that sort arrays of different lengths would serialise the
+// seven network paths, so each CTA first counting-sorts its arrays by length
+// (shared-memory histogram + scatter of array ids); thread t then sorts the
+// t-th array of that order and a warp runs one network width almost always.
 __global__ void __launch_bounds__(kBaNT)
     sort_small_batch_kernel(int32_t* __restrict__ keys, const uint32_t* __restrict__ offsets,
                             int64_t num_arrays, int* __restrict__ bad) {
   __shared__ uint32_t so[kBaArr + 1];
   __shared__ int32_t sk[kBaArr * 8];
+  __shared__ uint16_t perm[kBaArr];
+  __shared__ int hist[9], cursor[9];
   __shared__ int s_bad;
   const int tid = threadIdx.x;
   const int64_t first = (int64_t)blockIdx.x * kBaArr;
   const int cnt = (int)min((int64_t)kBaArr, num_arrays - first);
   if (tid == 0) s_bad = 0;
+  if (tid < 9) hist[tid] = 0;
   for (int i = tid; i <= cnt; i += kBaNT) so[i] = __ldg(offsets + first + i);
   __syncthreads();
-  // validate lengths before touching keys (lengths outside [0,8] -> error)
+  // validate (lengths outside [0, 8] -> error, nothing is touched) + histogram
   for (int i = tid; i < cnt; i += kBaNT) {
     const uint32_t len = so[i + 1] - so[i];
     if (so[i + 1] < so[i] || len > 8) s_bad = 1;
+    else atomicAdd(&hist[len], 1);
   }
   __syncthreads();
   if (s_bad) {
     if (tid == 0) atomicExch(bad, 1);
     return;
   }
+  if (tid == 0) {
+    int acc = 0;
+    for (int l = 0; l <= 8; ++l) {
+      cursor[l] = acc;
+      acc += hist[l];
+    }
+  }
   const uint32_t k0 = so[0];
   const int nk = (int)(so[cnt] - k0);
+#pragma unroll 8
   for (int i = tid; i < nk; i += kBaNT) sk[i] = __ldcs(keys + k0 + i);
+  __syncthreads();
+  for (int i = tid; i < cnt; i += kBaNT) perm[atomicAdd(&cursor[so[i + 1] - so[i]], 1)] = (uint16_t)i;
   __syncthreads();
 #pragma unroll
   for (int r = 0; r < kBaPer; ++r) {
-    const int j = r * kBaNT + tid;  // lanes take consecutive arrays
-    if (j < cnt) {
+    const int slot = r * kBaNT + tid;
+    if (slot < cnt) {
+      const int j = perm[slot];
       const int off = (int)(so[j] - k0);
       const int len = (int)(so[j + 1] - so[j]);
       int32_t v[8];
@@ -229,7 +377,32 @@ __global__ void __launch_bounds__(kBaNT)
     }
   }
   __syncthreads();
+#pragma unroll 8
   for (int i = tid; i < nk; i += kBaNT) __stcs(keys + k0 + i, sk[i]);
+}
+
+// Per-device validation flag + pinned host mirror, allocated once.
+struct BatchFlag {
+  int* dev = nullptr;
+  int* host = nullptr;
+};
+static std::mutex g_flag_mu;
+static BatchFlag g_flags[64];
+
+static int batch_flag(BatchFlag** out) {
+  int dev = 0;
+  NSB_TRY(check_cuda(cudaGetDevice(&dev), "cudaGetDevice"));
+  if (dev < 0 || dev >= 64) return NS_ERR_INVALID;
+  std::lock_guard<std::mutex> lk(g_flag_mu);
+  BatchFlag& f = g_flags[dev];
+  if (!f.dev) {
+    NSB_TRY(check_cuda(cudaMalloc(reinterpret_cast<void**>(&f.dev), sizeof(int)), "cudaMalloc"));
+    NSB_TRY(check_cuda(cudaHostAlloc(reinterpret_cast<void**>(&f.host), sizeof(int),
+                                     cudaHostAllocDefault),
+                       "cudaHostAlloc"));
+  }
+  *out = &f;
+  return NS_OK;
 }
 
 // ---------------------------------------------------------------------------
@@ -299,6 +472,13 @@ const char* ns_status_string(int status) {
 
 int ns_version(void) { return 100; }
 
+#ifdef NSB_DEBUG_KWAY
+int ns_debug_read(int* out8) {
+  cudaDeviceSynchronize();
+  return cudaMemcpyFromSymbol(out8, g_dbg, 8 * sizeof(int)) == cudaSuccess ? 0 : 2;
+}
+#endif
+
 int ns_leaf_width(uint32_t width_mask, int varsort_max) { return leaf_of(width_mask, varsort_max); }
 
 int ns_network_comparators(int width, uint8_t* pairs, int cap) {
@@ -336,27 +516,21 @@ int ns_sort_small_batch_i32(int32_t* d_keys, const uint32_t* d_offsets, size_t n
   if (num_arrays == 0) return NS_OK;
   if (!d_keys || !d_offsets) return NS_ERR_INVALID;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  int* bad = nullptr;
-  NSB_TRY(check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&bad), sizeof(int), s),
-                     "cudaMallocAsync"));
-  NSB_TRY(check_cuda(cudaMemsetAsync(bad, 0, sizeof(int), s), "cudaMemsetAsync"));
+  BatchFlag* f = nullptr;
+  NSB_TRY(batch_flag(&f));
+  NSB_TRY(check_cuda(cudaMemsetAsync(f->dev, 0, sizeof(int), s), "cudaMemsetAsync"));
   const int64_t ctas = (int64_t)((num_arrays + kBaArr - 1) / kBaArr);
   {
     Prof prof(PK_BATCH, s);
     sort_small_batch_kernel<<<(unsigned)ctas, kBaNT, 0, s>>>(d_keys, d_offsets,
-                                                              (int64_t)num_arrays, bad);
+                                                              (int64_t)num_arrays, f->dev);
   }
-  int st = check_launch("sort_small_batch_kernel");
-  int h_bad = 0;
-  if (st == NS_OK) {
-    // The length check is the only device->host traffic of this call.
-    st = check_cuda(cudaMemcpyAsync(&h_bad, bad, sizeof(int), cudaMemcpyDeviceToHost, s),
-                    "cudaMemcpyAsync");
-    if (st == NS_OK) st = check_cuda(cudaStreamSynchronize(s), "cudaStreamSynchronize");
-  }
-  cudaFreeAsync(bad, s);
-  if (st != NS_OK) return st;
-  return h_bad ? NS_ERR_INVALID : NS_OK;
+  NSB_TRY(check_launch("sort_small_batch_kernel"));
+  // The length check is the only device->host traffic of this call.
+  NSB_TRY(check_cuda(cudaMemcpyAsync(f->host, f->dev, sizeof(int), cudaMemcpyDeviceToHost, s),
+                     "cudaMemcpyAsync"));
+  NSB_TRY(check_cuda(cudaStreamSynchronize(s), "cudaStreamSynchronize"));
+  return *f->host ? NS_ERR_INVALID : NS_OK;
 }
 
 size_t ns_segmented_sort_temp_bytes(size_t num_segments, size_t seg_len) {

@@ -59,15 +59,54 @@ __device__ __forceinline__ int smem_merge_path(const int32_t* A, int a_len, cons
 // 1 SEL + 2 predicated IADD + 2 predicated MOV.  A is never stepped past its
 // sentinel: when ka == +inf both heads are +inf and so is every remaining
 // output; take_a false implies kb < ka, so B cannot pass its sentinel either.
+#ifdef NSB_DEBUG_KWAY
+__device__ int g_dbg[8];
+__device__ __forceinline__ void dbg_record(int code, int x, int y, int z) {
+  if (atomicCAS(&g_dbg[0], 0, code) == 0) {
+    g_dbg[1] = x;
+    g_dbg[2] = y;
+    g_dbg[3] = z;
+    g_dbg[4] = blockIdx.x;
+    g_dbg[5] = threadIdx.x;
+  }
+}
+#endif
+
 __device__ __forceinline__ void sentinel_merge(const int32_t* A, const int32_t* B, int a, int b,
                                                int32_t* Y, int cnt) {
+#ifdef NSB_DEBUG_KWAY
+  {
+    extern __shared__ int32_t kw_sm[];
+    const int lim = 2 * (7936 + 64 + 16);
+    const int ia = (int)(A + a - kw_sm), ib = (int)(B + b - kw_sm), iy = (int)(Y - kw_sm);
+    if (ia < 0 || ia >= lim || ib < 0 || ib >= lim || iy < 0 || iy + cnt > lim || cnt < 0) {
+      dbg_record(1, ia, ib, iy * 100000 + cnt);
+      return;
+    }
+    const int32_t* pa = A + a;
+    const int32_t* pb = B + b;
+    for (int k = 0; k < cnt; ++k) {
+      const int ja = (int)(pa - kw_sm), jb = (int)(pb - kw_sm);
+      if (ja < 0 || ja >= lim || jb < 0 || jb >= lim) {
+        dbg_record(2, ja, jb, k);
+        return;
+      }
+      const int32_t ka = *pa, kb = *pb;
+      const bool take_a = ka <= kb;
+      Y[k] = take_a ? ka : kb;
+      pa += take_a & (ka != INT_MAX);
+      pb += !take_a;
+    }
+    return;
+  }
+#endif
   uint32_t pa = static_cast<uint32_t>(__cvta_generic_to_shared(A + a));
   uint32_t pb = static_cast<uint32_t>(__cvta_generic_to_shared(B + b));
   uint32_t py = static_cast<uint32_t>(__cvta_generic_to_shared(Y));
   const uint32_t py_end = py + 4u * (uint32_t)cnt;
   int32_t ka, kb;
   asm volatile("ld.shared.b32 %0, [%2];\n ld.shared.b32 %1, [%3];\n"
-               : "=r"(ka), "=r"(kb)
+               : "=&r"(ka), "=&r"(kb)
                : "r"(pa), "r"(pb)
                : "memory");
 #pragma unroll 1

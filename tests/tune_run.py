@@ -22,10 +22,18 @@ def main():
     dev = torch.device("cuda:0")
     L = ns.lib()
     s = torch.cuda.current_stream().cuda_stream
-    a = torch.empty(n, dtype=torch.int32, device=dev)
-    check(L.ns_generate_i32(a.data_ptr(), n, 0, 42, s), "gen")
+    if mode == "batch":
+        from oracle import oracle as O
+        offs, keys = O.generate_batch_i32(n, 42)
+        a = torch.from_numpy(keys).to(dev)
+        o = torch.from_numpy(offs.view("int32")).to(dev)
+    else:
+        a = torch.empty(n, dtype=torch.int32, device=dev)
+        check(L.ns_generate_i32(a.data_ptr(), n, 0, 42, s), "gen")
     w = a.clone()
-    if mode == "merge":
+    if mode == "batch":
+        fn = lambda: ns.sort_small_batch(w, o)  # noqa: E731
+    elif mode == "merge":
         fn = lambda: ns.optimized_merge_sort(w, ns.find_config("6To8"))  # noqa: E731
     elif mode == "quick":
         fn = lambda: ns.optimized_quick_sort(w, ns.find_config("3To5"))  # noqa: E731
@@ -59,7 +67,7 @@ def main():
                                                         round(t.value / c.value, 4)]
     L.ns_profile_enable(0)
     res["prof_ms_launches_avg"] = prof
-    if mode != "segmented":
+    if mode not in ("segmented", "batch"):
         assert ns.count_inversions(w) == 0
     print(json.dumps(res))
 
