@@ -479,6 +479,34 @@ __device__ __forceinline__ TileGeom tile_geom(const PassPlan& P, int64_t c) {
   return g;
 }
 
+// Merge-path split found by a whole warp with a 32-ary search: each round
+// every lane evaluates the predicate A[a] <= B[diag-1-a] at one of 32 evenly
+// spaced candidates and a ballot narrows the range 32x — log32 instead of
+// log2 dependent global loads (used when a merge pass has too few tiles for a
+// separate partition kernel to pay for its launch).  All lanes return the
+// split.
+__device__ __forceinline__ int64_t warp_merge_path(const int32_t* A, int64_t a_len,
+                                                   const int32_t* B, int64_t b_len, int64_t diag) {
+  const int lane = threadIdx.x & 31;
+  int64_t lo = diag > b_len ? diag - b_len : 0;
+  int64_t hi = diag < a_len ? diag : a_len;
+  while (lo < hi) {
+    const int64_t span = hi - lo;
+    const int64_t step = span <= 32 ? 1 : (span + 31) / 32;
+    const int64_t a = lo + lane * step;
+    const bool valid = a < hi;
+    const bool p = valid && (A[a] <= B[diag - 1 - a]);
+    const unsigned m = __ballot_sync(0xffffffffu, p);
+    const int c = __popc(m);  // P holds on a prefix of the candidates
+    if (step == 1) return lo + c;
+    const int64_t new_lo = c == 0 ? lo : lo + (int64_t)(c - 1) * step + 1;
+    const int64_t new_hi = min(hi, lo + (int64_t)c * step);
+    lo = new_lo;
+    hi = new_hi;
+  }
+  return lo;
+}
+
 static __global__ void merge_partition_v2_kernel(const int32_t* __restrict__ src, PassPlan P,
                                           int64_t num_tiles, int64_t* __restrict__ mp) {
   const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -492,7 +520,7 @@ static __global__ void merge_partition_v2_kernel(const int32_t* __restrict__ src
 // alignment slack each, a sentinel after each, 16-byte rounding.
 __host__ __device__ constexpr int v2_smem_words(int TM) { return TM + 16; }
 
-template <int NT, int K>
+template <int NT, int K, bool FUSED = false>
 __global__ void __launch_bounds__(NT)
     merge_pass_v2_kernel(const int32_t* __restrict__ src, int32_t* __restrict__ dst, PassPlan P,
                          const int64_t* __restrict__ mp) {
@@ -504,8 +532,28 @@ __global__ void __launch_bounds__(NT)
   const TileGeom g = tile_geom(P, c);
   if (g.diag0 >= g.diag1) return;  // empty trailing tile of a short last pair
   const bool last_in_pair = g.diag1 == g.a_len + g.b_len;
-  const int64_t a0 = mp[c];
-  const int64_t a1 = last_in_pair ? g.a_len : mp[c + 1];
+  int64_t a0, a1;
+  if constexpr (FUSED) {
+    // splits found here by warps 0 and 1 instead of a partition kernel
+    __shared__ int64_t splits[2];
+    const int warp = tid >> 5;
+    const int32_t* PA = src + g.pair_base;
+    if (warp == 0) {
+      const int64_t v = warp_merge_path(PA, g.a_len, PA + g.a_len, g.b_len, g.diag0);
+      if (tid == 0) splits[0] = v;
+    } else if (warp == 1) {
+      const int64_t v = last_in_pair
+                            ? g.a_len
+                            : warp_merge_path(PA, g.a_len, PA + g.a_len, g.b_len, g.diag1);
+      if (tid == 32) splits[1] = v;
+    }
+    __syncthreads();
+    a0 = splits[0];
+    a1 = splits[1];
+  } else {
+    a0 = mp[c];
+    a1 = last_in_pair ? g.a_len : mp[c + 1];
+  }
   const int la = (int)(a1 - a0);
   const int lb = (int)((g.diag1 - a1) - (g.diag0 - a0));
   const int32_t* A = src + g.pair_base + a0;

@@ -59,7 +59,9 @@ struct MergeTuning {
   int merge_k = 2;
   int kway = 0;  // measured: k-way passes are merge-compute bound, no faster
   int64_t kway_min = int64_t(1) << 22;
+  int64_t fused_max_tiles = 4096;  // passes with fewer tiles search in-kernel (measured crossover)
   MergeTuning() {
+    if (const char* e = getenv("NSB_FUSED_MAX")) fused_max_tiles = atoll(e);
     if (const char* e = getenv("NSB_TILE")) tile = atoi(e) == 16384 ? 16384 : 8192;
     if (const char* e = getenv("NSB_MERGE")) merge_k = atoi(e);
     if (const char* e = getenv("NSB_KWAY")) kway = atoi(e);
@@ -253,6 +255,18 @@ int merge_sort_device(int32_t* d_keys, size_t n, int leaf, void* d_temp, size_t 
       const PassPlan P = plan_pass((int64_t)n, R);
       const int64_t pairs = ((int64_t)n + 2 * R - 1) / (2 * R);
       const int64_t mt = pairs * P.tpp;
+      if (mt <= tu.fused_max_tiles) {
+        // few tiles: every CTA finds its own split (no partition launch)
+        {
+          Prof prof(PK_MERGE_PASS, s);
+          merge_pass_v2_kernel<kV2NT, kV2K, true><<<(unsigned)mt, kV2NT, 0, s>>>(cur, other, P,
+                                                                                 nullptr);
+        }
+        NSB_TRY(check_launch("merge_pass_v2_kernel<fused>"));
+        std::swap(cur, other);
+        R *= 2;
+        continue;
+      }
       {
         Prof prof(PK_PARTITION, s);
         merge_partition_v2_kernel<<<(unsigned)((mt + 255) / 256), 256, 0, s>>>(cur, P, mt, mp);
