@@ -1,0 +1,162 @@
+// C++ host-API test: the reference's own call shapes (hybrid.hpp / config.hpp)
+// against netsort_b200.hpp, mirroring the predicates of the reference's
+// tests/test_hybrid.cpp (restated, not copied).  Exit status = #failures.
+//   argv[1] == "--no-gpu": only the host-side checks (registry, configs).
+#include <algorithm>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+#include <random>
+#include <stdexcept>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "netsort_b200.hpp"
+
+namespace ns = netsort_b200;
+
+static int failures = 0;
+#define CHECK(cond)                                                     \
+  do {                                                                  \
+    if (!(cond)) {                                                      \
+      std::printf("FAIL %s:%d: %s\n", __FILE__, __LINE__, #cond);       \
+      ++failures;                                                       \
+    }                                                                   \
+  } while (0)
+
+static std::vector<int32_t> random_values(size_t n, uint64_t seed) {
+  std::mt19937_64 rng(seed);
+  std::vector<int32_t> v(n);
+  for (auto& x : v) x = static_cast<int32_t>(rng() >> 33);
+  return v;
+}
+
+static void host_side() {
+  // test_hybrid.cpp:48-100 restated: registry, names, width sets
+  const auto& reg = ns::config_registry();
+  CHECK(reg.size() == 12);
+  CHECK(reg.front().name == "Classic" && reg.front().is_classic());
+  CHECK(ns::find_config("9To12") == nullptr);
+  CHECK(ns::find_config("classic") == nullptr);
+  CHECK(ns::bundled_variants().size() == 24);
+  CHECK(ns::base_case_applies(7, *ns::find_config("6To8")));
+  CHECK(!ns::base_case_applies(5, *ns::find_config("6To8")));
+  CHECK(ns::base_case_applies(2, *ns::find_config("VarSort5")));
+  CHECK(!ns::base_case_applies(6, *ns::find_config("VarSort5")));
+  CHECK(ns::base_case_applies(8, *ns::find_config("PowerOf2")));
+  CHECK(!ns::base_case_applies(2, *ns::find_config("3")));
+  for (int s = 0; s <= 10; ++s) CHECK(!ns::base_case_applies(s, ns::classic_config()));
+  bool threw = false;
+  try {
+    ns::make_fixed_config("bad", {2});
+  } catch (const std::invalid_argument&) {
+    threw = true;
+  }
+  CHECK(threw);
+  threw = false;
+  try {
+    ns::make_varsort_config("bad", 6);
+  } catch (const std::invalid_argument&) {
+    threw = true;
+  }
+  CHECK(threw);
+  // C ABI agrees with the C++ registry
+  for (const auto& c : reg) {
+    uint32_t m = 0;
+    int v = 0;
+    CHECK(ns_find_config(c.name.c_str(), &m, &v) == NS_OK);
+    CHECK(m == c.width_mask && v == c.varsort_max);
+  }
+}
+
+static void device_side() {
+  // every variant on random arrays (test_hybrid.cpp:306-318)
+  for (size_t n : {0u, 1u, 2u, 3u, 4u, 7u, 16u, 33u, 64u, 501u, 1000u, 20000u, 300000u}) {
+    const auto input = random_values(n, 3000 + n);
+    auto expect = input;
+    std::sort(expect.begin(), expect.end());
+    for (const auto& var : ns::bundled_variants()) {
+      auto v = input;
+      ns::run_variant(var, std::span<int32_t>(v));
+      CHECK(v == expect);
+    }
+  }
+  // classical sorts (test_hybrid.cpp:102-117)
+  for (size_t n : {0u, 1u, 2u, 3u, 5u, 17u, 64u, 1000u, 10000u}) {
+    auto m = random_values(n, 1000 + n), q = m, e = m;
+    std::sort(e.begin(), e.end());
+    ns::classical_merge_sort(std::span<int32_t>(m));
+    ns::classical_quick_sort(std::span<int32_t>(q));
+    CHECK(m == e && q == e);
+  }
+  // ternary arrays up to length 6 through all 24 variants (test_hybrid.cpp:283-304)
+  for (int len = 0; len <= 6; ++len) {
+    int total = 1;
+    for (int i = 0; i < len; ++i) total *= 3;
+    for (int code = 0; code < total; ++code) {
+      std::vector<int32_t> base(static_cast<size_t>(len));
+      int rest = code;
+      for (int i = 0; i < len; ++i) {
+        base[static_cast<size_t>(i)] = rest % 3;
+        rest /= 3;
+      }
+      auto expect = base;
+      std::sort(expect.begin(), expect.end());
+      for (const auto& var : {ns::SortVariant{ns::Algorithm::merge_sort, *ns::find_config("6To8")},
+                              ns::SortVariant{ns::Algorithm::quick_sort, *ns::find_config("3To5")}}) {
+        auto v = base;
+        ns::run_variant(var, std::span<int32_t>(v));
+        CHECK(v == expect);
+      }
+    }
+  }
+  // range sorts leave the outside untouched; inverted ranges are no-ops
+  // (test_hybrid.cpp:320-354)
+  auto base = random_values(40, 17);
+  for (auto& x : base) x %= 100;
+  std::vector<int32_t> window(base.begin() + 10, base.begin() + 30);
+  std::sort(window.begin(), window.end());
+  for (const char* name : {"Classic", "3To8", "VarSort4"}) {
+    const auto& cfg = *ns::find_config(name);
+    auto m = base, q = base;
+    ns::optimized_merge_sort(std::span<int32_t>(m), 10, 29, cfg);
+    ns::optimized_quick_sort(std::span<int32_t>(q), 10, 29, cfg);
+    for (int k = 0; k < 40; ++k) {
+      if (k >= 10 && k < 30) continue;
+      CHECK(m[static_cast<size_t>(k)] == base[static_cast<size_t>(k)]);
+      CHECK(q[static_cast<size_t>(k)] == base[static_cast<size_t>(k)]);
+    }
+    CHECK(std::equal(window.begin(), window.end(), m.begin() + 10));
+    CHECK(std::equal(window.begin(), window.end(), q.begin() + 10));
+  }
+  std::vector<int32_t> v{3, 1, 2};
+  ns::optimized_merge_sort(std::span<int32_t>(v), 2, 1, *ns::find_config("3To8"));
+  ns::optimized_quick_sort(std::span<int32_t>(v), 2, 1, *ns::find_config("3To8"));
+  CHECK((v == std::vector<int32_t>{3, 1, 2}));
+  // device spans with caller scratch
+  ns::DeviceScratch scratch;
+  const auto big = random_values(1 << 20, 5);
+  int32_t* d = nullptr;
+  CHECK(cudaMalloc(&d, big.size() * 4) == cudaSuccess);
+  cudaMemcpy(d, big.data(), big.size() * 4, cudaMemcpyHostToDevice);
+  ns::device_merge_sort(d, big.size(), *ns::find_config("6To8"), scratch);
+  std::vector<int32_t> back(big.size());
+  cudaMemcpy(back.data(), d, big.size() * 4, cudaMemcpyDeviceToHost);
+  auto e = big;
+  std::sort(e.begin(), e.end());
+  CHECK(back == e);
+  cudaMemcpy(d, big.data(), big.size() * 4, cudaMemcpyHostToDevice);
+  ns::device_quick_sort(d, big.size(), *ns::find_config("3To5"), scratch);
+  cudaMemcpy(back.data(), d, big.size() * 4, cudaMemcpyDeviceToHost);
+  CHECK(back == e);
+  cudaFree(d);
+}
+
+int main(int argc, char** argv) {
+  host_side();
+  if (!(argc > 1 && std::strcmp(argv[1], "--no-gpu") == 0)) device_side();
+  std::printf("%s: %d failure(s)\n", failures ? "FAILED" : "PASSED", failures);
+  return failures;
+}
