@@ -4,6 +4,7 @@
 // DeviceScratch / device_* helpers declared in include/netsort_b200.hpp.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "../../include/netsort_b200.hpp"
@@ -15,22 +16,37 @@ size_t quick_sort_temp(size_t n);
 // Per-thread device staging: keys + scratch, grown on demand, plus one
 // non-blocking stream.  Mirrors the reference's per-call `new T[n]` scratch
 // (hybrid.hpp:163) without paying an allocation on every call.
+constexpr int kMaxChunks = 8;
+
 struct HostCache {
   void* dev = nullptr;
   size_t bytes = 0;
-  cudaStream_t stream = nullptr;
+  cudaStream_t stream = nullptr;  // compute
+  cudaStream_t copy = nullptr;    // host->device chunks
+  cudaEvent_t ev[kMaxChunks] = {};
   ~HostCache() { release(); }
   void release() {
     if (dev) cudaFree(dev);
     if (stream) cudaStreamDestroy(stream);
+    if (copy) cudaStreamDestroy(copy);
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+    for (auto& e : ev) e = nullptr;
     dev = nullptr;
     bytes = 0;
     stream = nullptr;
+    copy = nullptr;
   }
   int ensure(size_t need) {
-    if (!stream)
+    if (!stream) {
       NSB_TRY(check_cuda(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking),
                          "cudaStreamCreate"));
+      NSB_TRY(check_cuda(cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking),
+                         "cudaStreamCreate"));
+      for (auto& e : ev)
+        NSB_TRY(check_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming),
+                           "cudaEventCreate"));
+    }
     if (bytes >= need) return NS_OK;
     if (dev) cudaFree(dev);
     dev = nullptr;
@@ -42,6 +58,12 @@ struct HostCache {
 };
 static thread_local HostCache g_host;
 
+// Host-buffer sort.  Large merge sorts overlap the PCIe upload with compute:
+// the array is cut into up to 8 chunks (multiples of the 8192-key tile); each
+// chunk is merge-sorted on the compute stream as soon as its copy (on the copy
+// stream) lands, so the tile sort and all intra-chunk merge passes hide under
+// the host->device transfer; log2(chunks) pairwise passes then merge the
+// chunks and the result is read back from whichever buffer holds it.
 static int host_sort(int32_t* h_keys, size_t n, uint32_t mask, int vs, int algorithm) {
   if (n <= 1) return NS_OK;
   if (!h_keys) return NS_ERR_INVALID;
@@ -51,15 +73,40 @@ static int host_sort(int32_t* h_keys, size_t n, uint32_t mask, int vs, int algor
   cudaStream_t s = g_host.stream;
   int32_t* d = static_cast<int32_t*>(g_host.dev);
   void* t = static_cast<char*>(g_host.dev) + kb;
-  NSB_TRY(check_cuda(cudaMemcpyAsync(d, h_keys, n * 4, cudaMemcpyHostToDevice, s), "H2D"));
-  const int st = algorithm == NS_MERGE_SORT
-                     ? ns_merge_sort_i32(d, n, mask, vs, t, tb, s)
-                     : ns_quick_sort_i32(d, n, mask, vs, t, tb, s);
-  if (st != NS_OK) {
-    cudaStreamSynchronize(s);
-    return st;
+  const size_t chunk_min = size_t(1) << 22;
+  int32_t* result = d;
+  if (algorithm == NS_MERGE_SORT && n >= 2 * chunk_min) {
+    int chunks = (int)std::min<size_t>(kMaxChunks, n / chunk_min);
+    size_t clen = (n + chunks - 1) / chunks;
+    clen = (clen + 8191) / 8192 * 8192;
+    chunks = (int)((n + clen - 1) / clen);
+    for (int c = 0; c < chunks; ++c) {
+      const size_t off = c * clen, len = std::min(clen, n - off);
+      NSB_TRY(check_cuda(cudaMemcpyAsync(d + off, h_keys + off, len * 4, cudaMemcpyHostToDevice,
+                                         g_host.copy),
+                         "H2D"));
+      NSB_TRY(check_cuda(cudaEventRecord(g_host.ev[c], g_host.copy), "cudaEventRecord"));
+    }
+    for (int c = 0; c < chunks; ++c) {
+      const size_t off = c * clen, len = std::min(clen, n - off);
+      NSB_TRY(check_cuda(cudaStreamWaitEvent(s, g_host.ev[c], 0), "cudaStreamWaitEvent"));
+      const int st = ns_merge_sort_i32(d + off, len, mask, vs, t, tb, s);
+      if (st != NS_OK) {
+        cudaStreamSynchronize(s);
+        return st;
+      }
+    }
+    NSB_TRY(merge_existing_runs(d, static_cast<int32_t*>(t), n, (int64_t)clen, t, s, &result));
+  } else {
+    NSB_TRY(check_cuda(cudaMemcpyAsync(d, h_keys, n * 4, cudaMemcpyHostToDevice, s), "H2D"));
+    const int st = algorithm == NS_MERGE_SORT ? ns_merge_sort_i32(d, n, mask, vs, t, tb, s)
+                                              : ns_quick_sort_i32(d, n, mask, vs, t, tb, s);
+    if (st != NS_OK) {
+      cudaStreamSynchronize(s);
+      return st;
+    }
   }
-  NSB_TRY(check_cuda(cudaMemcpyAsync(h_keys, d, n * 4, cudaMemcpyDeviceToHost, s), "D2H"));
+  NSB_TRY(check_cuda(cudaMemcpyAsync(h_keys, result, n * 4, cudaMemcpyDeviceToHost, s), "D2H"));
   return check_cuda(cudaStreamSynchronize(s), "cudaStreamSynchronize");
 }
 

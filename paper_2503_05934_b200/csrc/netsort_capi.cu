@@ -203,6 +203,50 @@ static PassPlan plan_pass(int64_t n, int64_t R) {
   return P;
 }
 
+// One pairwise merge pass (v2): runs of R in src -> runs of 2R in dst.
+static int v2_pass(const int32_t* src, int32_t* dst, int64_t n, int64_t R, int64_t* mp,
+                   cudaStream_t s) {
+  const MergeTuning& tu = tuning();
+  const PassPlan P = plan_pass(n, R);
+  const int64_t pairs = (n + 2 * R - 1) / (2 * R);
+  const int64_t mt = pairs * P.tpp;
+  if (mt <= tu.fused_max_tiles) {
+    // few tiles: every CTA finds its own split (no partition launch)
+    {
+      Prof prof(PK_MERGE_PASS, s);
+      merge_pass_v2_kernel<kV2NT, kV2K, true><<<(unsigned)mt, kV2NT, 0, s>>>(src, dst, P,
+                                                                             nullptr);
+    }
+    return check_launch("merge_pass_v2_kernel<fused>");
+  }
+  {
+    Prof prof(PK_PARTITION, s);
+    merge_partition_v2_kernel<<<(unsigned)((mt + 255) / 256), 256, 0, s>>>(src, P, mt, mp);
+  }
+  NSB_TRY(check_launch("merge_partition_v2_kernel"));
+  {
+    Prof prof(PK_MERGE_PASS, s);
+    merge_pass_v2_kernel<kV2NT, kV2K><<<(unsigned)mt, kV2NT, 0, s>>>(src, dst, P, mp);
+  }
+  return check_launch("merge_pass_v2_kernel");
+}
+
+// Pairwise passes over existing sorted runs of length R0 (the last may be
+// shorter) until one run remains; *result = the buffer holding it (keys or tmp).
+int merge_existing_runs(int32_t* keys, int32_t* tmp, size_t n, int64_t R0, void* d_temp,
+                        cudaStream_t s, int32_t** result) {
+  int64_t* mp = reinterpret_cast<int64_t*>(static_cast<char*>(d_temp) +
+                                           align_up(n * sizeof(int32_t), 256));
+  int32_t* cur = keys;
+  int32_t* other = tmp;
+  for (int64_t R = R0; R < (int64_t)n; R *= 2) {
+    NSB_TRY(v2_pass(cur, other, (int64_t)n, R, mp, s));
+    std::swap(cur, other);
+  }
+  *result = cur;
+  return NS_OK;
+}
+
 int merge_sort_device(int32_t* d_keys, size_t n, int leaf, void* d_temp, size_t temp_bytes,
                       cudaStream_t s) {
   if (n <= 1) return NS_OK;
@@ -252,31 +296,7 @@ int merge_sort_device(int32_t* d_keys, size_t n, int leaf, void* d_temp, size_t 
         R *= k;
         continue;
       }
-      const PassPlan P = plan_pass((int64_t)n, R);
-      const int64_t pairs = ((int64_t)n + 2 * R - 1) / (2 * R);
-      const int64_t mt = pairs * P.tpp;
-      if (mt <= tu.fused_max_tiles) {
-        // few tiles: every CTA finds its own split (no partition launch)
-        {
-          Prof prof(PK_MERGE_PASS, s);
-          merge_pass_v2_kernel<kV2NT, kV2K, true><<<(unsigned)mt, kV2NT, 0, s>>>(cur, other, P,
-                                                                                 nullptr);
-        }
-        NSB_TRY(check_launch("merge_pass_v2_kernel<fused>"));
-        std::swap(cur, other);
-        R *= 2;
-        continue;
-      }
-      {
-        Prof prof(PK_PARTITION, s);
-        merge_partition_v2_kernel<<<(unsigned)((mt + 255) / 256), 256, 0, s>>>(cur, P, mt, mp);
-      }
-      NSB_TRY(check_launch("merge_partition_v2_kernel"));
-      {
-        Prof prof(PK_MERGE_PASS, s);
-        merge_pass_v2_kernel<kV2NT, kV2K><<<(unsigned)mt, kV2NT, 0, s>>>(cur, other, P, mp);
-      }
-      NSB_TRY(check_launch("merge_pass_v2_kernel"));
+      NSB_TRY(v2_pass(cur, other, (int64_t)n, R, mp, s));
       std::swap(cur, other);
       R *= 2;
     }
