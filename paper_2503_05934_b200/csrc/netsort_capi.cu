@@ -351,55 +351,146 @@ int tile_sort_segments(int32_t* d_keys, size_t num_segments, size_t seg_len, int
 constexpr int kBaNT = 256, kBaPer = 4, kBaArr = kBaNT * kBaPer;
 
 // Lanes of a warp that sort arrays of different lengths would serialise the
-// seven network paths, so each CTA first counting-sorts its arrays by length
-// (shared-memory histogram + scatter of array ids); thread t then sorts the
-// t-th array of that order and a warp runs one network width almost always.
+// seven network paths, so each CTA first splits its arrays by length (a
+// 9-way block multisplit with warp ballots: deterministic and stable, so the
+// arrays one warp receives are same-length neighbours ~6 arrays apart in
+// memory, i.e. on different banks), then thread t sorts the t-th array of
+// that order and a warp runs one network width almost always.  Keys are
+// staged in shared memory at the same 16-byte phase as in HBM so the
+// 128-bit loads and stores of the aligned body are bank-conflict free.
 __global__ void __launch_bounds__(kBaNT)
     sort_small_batch_kernel(int32_t* __restrict__ keys, const uint32_t* __restrict__ offsets,
                             int64_t num_arrays, int* __restrict__ bad) {
+  constexpr int NW = kBaNT / 32;
   __shared__ uint32_t so[kBaArr + 1];
-  __shared__ int32_t sk[kBaArr * 8];
+  __shared__ __align__(16) int32_t sk[kBaArr * 8 + 8];
   __shared__ uint16_t perm[kBaArr];
-  __shared__ int hist[9], cursor[9];
+  __shared__ int wcnt[9][kBaPer][NW];  // per (length, round, warp) counts -> bases
   __shared__ int s_bad;
+  __shared__ uint32_t s_k0, s_k1;
   const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
   const int64_t first = (int64_t)blockIdx.x * kBaArr;
   const int cnt = (int)min((int64_t)kBaArr, num_arrays - first);
-  if (tid == 0) s_bad = 0;
-  if (tid < 9) hist[tid] = 0;
-  for (int i = tid; i <= cnt; i += kBaNT) so[i] = __ldg(offsets + first + i);
+  if (tid == 0) {
+    s_bad = 0;
+    s_k0 = __ldg(offsets + first);
+    s_k1 = __ldg(offsets + first + cnt);
+    if (s_k1 < s_k0 || s_k1 - s_k0 > 8u * (uint32_t)cnt) s_bad = 1;
+  }
   __syncthreads();
-  // validate (lengths outside [0, 8] -> error, nothing is touched) + histogram
-  for (int i = tid; i < cnt; i += kBaNT) {
-    const uint32_t len = so[i + 1] - so[i];
-    if (so[i + 1] < so[i] || len > 8) s_bad = 1;
-    else atomicAdd(&hist[len], 1);
+  const uint32_t k0 = s_k0;
+  const int nk = s_bad ? 0 : (int)(s_k1 - k0);
+  // issue the key loads (128-bit on the aligned body) together with the
+  // offset loads: one DRAM round trip per CTA
+  const int32_t* kp = keys + k0;
+  const int phase = (int)((reinterpret_cast<uintptr_t>(kp) & 15) >> 2);  // key i -> sk[i + phase]
+  const int head = min(nk, (4 - phase) & 3);
+  const int body = (nk - head) >> 2;
+  const int tail = nk - head - 4 * body;
+  const int4* kb4 = reinterpret_cast<const int4*>(kp + head);
+  constexpr int CH = kBaArr * 8 / 4 / kBaNT;
+  int4 x[CH];
+#pragma unroll
+  for (int u = 0; u < CH; ++u) {
+    const int j = u * kBaNT + tid;
+    if (j < body) x[u] = __ldcs(kb4 + j);
+  }
+  int32_t hx = 0, tx = 0;
+  if (tid < head) hx = __ldcs(kp + tid);
+  if (tid < tail) tx = __ldcs(kp + head + 4 * body + tid);
+  for (int i = tid; i <= cnt; i += kBaNT) so[i] = __ldg(offsets + first + i);
+  int4* sk4 = reinterpret_cast<int4*>(sk + phase + head);  // 16-byte aligned
+#pragma unroll
+  for (int u = 0; u < CH; ++u) {
+    const int j = u * kBaNT + tid;
+    if (j < body) sk4[j] = x[u];
+  }
+  if (tid < head) sk[phase + tid] = hx;
+  if (tid < tail) sk[phase + head + 4 * body + tid] = tx;
+  __syncthreads();
+  // validate (lengths outside [0, 8] -> error, nothing is touched) and count
+  // lengths per (round, warp) with ballots
+  int mylen[kBaPer];
+#pragma unroll
+  for (int r = 0; r < kBaPer; ++r) {
+    const int j = r * kBaNT + tid;
+    int len = -1;
+    if (j < cnt) {
+      const uint32_t a = so[j], b = so[j + 1];
+      if (b < a || b - a > 8) s_bad = 1;
+      else len = (int)(b - a);
+    }
+    mylen[r] = len;
+#pragma unroll
+    for (int l = 0; l <= 8; ++l) {
+      const unsigned m = __ballot_sync(0xffffffffu, len == l);
+      if (lane == 0) wcnt[l][r][warp] = __popc(m);
+    }
   }
   __syncthreads();
   if (s_bad) {
     if (tid == 0) atomicExch(bad, 1);
     return;
   }
-  if (tid == 0) {
+  // exclusive scan in (length, round, warp) order (stable): each of the
+  // 9*kBaPer rows of NW counts is scanned by one thread, then one warp scans
+  // the row totals
+  __shared__ int rowtot[9 * kBaPer];
+  if (tid < 9 * kBaPer) {
+    int* row = &wcnt[0][0][0] + tid * NW;
     int acc = 0;
-    for (int l = 0; l <= 8; ++l) {
-      cursor[l] = acc;
-      acc += hist[l];
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+      const int c = row[w];
+      row[w] = acc;
+      acc += c;
     }
+    rowtot[tid] = acc;
   }
-  const uint32_t k0 = so[0];
-  const int nk = (int)(so[cnt] - k0);
-#pragma unroll 8
-  for (int i = tid; i < nk; i += kBaNT) sk[i] = __ldcs(keys + k0 + i);
   __syncthreads();
-  for (int i = tid; i < cnt; i += kBaNT) perm[atomicAdd(&cursor[so[i + 1] - so[i]], 1)] = (uint16_t)i;
+  if (warp == 0) {
+    int v0 = lane < 9 * kBaPer ? rowtot[lane] : 0;
+    int v1 = lane + 32 < 9 * kBaPer ? rowtot[lane + 32] : 0;
+    int x0 = v0, x1 = v1;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y0 = __shfl_up_sync(0xffffffffu, x0, o), y1 = __shfl_up_sync(0xffffffffu, x1, o);
+      if (lane >= o) {
+        x0 += y0;
+        x1 += y1;
+      }
+    }
+    const int tot0 = __shfl_sync(0xffffffffu, x0, 31);
+    if (lane < 9 * kBaPer) rowtot[lane] = x0 - v0;
+    if (lane + 32 < 9 * kBaPer) rowtot[lane + 32] = tot0 + x1 - v1;
+  }
+  __syncthreads();
+  if (tid < 9 * kBaPer) {
+    int* row = &wcnt[0][0][0] + tid * NW;
+    const int base = rowtot[tid];
+#pragma unroll
+    for (int w = 0; w < NW; ++w) row[w] += base;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < kBaPer; ++r) {
+    const int len = mylen[r];
+    int rank = 0;
+#pragma unroll
+    for (int l = 0; l <= 8; ++l) {
+      const unsigned m = __ballot_sync(0xffffffffu, len == l);
+      if (len == l) rank = __popc(m & ((1u << lane) - 1));
+    }
+    if (len >= 0) perm[wcnt[len][r][warp] + rank] = (uint16_t)(r * kBaNT + tid);
+  }
   __syncthreads();
 #pragma unroll
   for (int r = 0; r < kBaPer; ++r) {
     const int slot = r * kBaNT + tid;
     if (slot < cnt) {
       const int j = perm[slot];
-      const int off = (int)(so[j] - k0);
+      const int off = (int)(so[j] - k0) + phase;
       const int len = (int)(so[j + 1] - so[j]);
       int32_t v[8];
 #pragma unroll
@@ -411,8 +502,15 @@ __global__ void __launch_bounds__(kBaNT)
     }
   }
   __syncthreads();
-#pragma unroll 8
-  for (int i = tid; i < nk; i += kBaNT) __stcs(keys + k0 + i, sk[i]);
+  int32_t* kw = keys + k0;
+  int4* kw4 = reinterpret_cast<int4*>(kw + head);
+#pragma unroll
+  for (int u = 0; u < CH; ++u) {
+    const int j = u * kBaNT + tid;
+    if (j < body) __stcs(kw4 + j, sk4[j]);
+  }
+  if (tid < head) kw[tid] = sk[phase + tid];
+  if (tid < tail) kw[head + 4 * body + tid] = sk[phase + head + 4 * body + tid];
 }
 
 // Per-device validation flag + pinned host mirror, allocated once.
