@@ -60,7 +60,9 @@ struct MergeTuning {
   int kway = 0;  // measured: k-way passes are merge-compute bound, no faster
   int64_t kway_min = int64_t(1) << 22;
   int64_t fused_max_tiles = 4096;  // passes with fewer tiles search in-kernel (measured crossover)
+  int v2 = 0;  // NSB_V2: 0 -> <256,31>, 1 -> <512,15>, 2 -> <384,21>
   MergeTuning() {
+    if (const char* e = getenv("NSB_V2")) v2 = atoi(e);
     if (const char* e = getenv("NSB_FUSED_MAX")) fused_max_tiles = atoll(e);
     if (const char* e = getenv("NSB_TILE")) tile = atoi(e) == 16384 ? 16384 : 8192;
     if (const char* e = getenv("NSB_MERGE")) merge_k = atoi(e);
@@ -191,31 +193,32 @@ static int kway_pass(const int32_t* src, int32_t* dst, int64_t n, int64_t R, int
                 : launch_kway_merge<4>(src, dst, P, ks.cuts, s);
 }
 
-static PassPlan plan_pass(int64_t n, int64_t R) {
+static PassPlan plan_pass(int64_t n, int64_t R, int nt = kV2NT, int k = kV2K) {
   PassPlan P;
   P.R = R;
   P.n = n;
   const int64_t two_r = 2 * R;
-  P.tpp = (int)((two_r + kV2T - 1) / kV2T);
+  const int tmax = (nt * k) & ~3;
+  P.tpp = (int)((two_r + tmax - 1) / tmax);
   const int64_t even = (two_r + P.tpp - 1) / P.tpp;
   P.tmp = (int)((even + 3) & ~int64_t(3));
-  P.kp = (P.tmp + kV2NT - 1) / kV2NT;
+  P.kp = (P.tmp + nt - 1) / nt;
   return P;
 }
 
 // One pairwise merge pass (v2): runs of R in src -> runs of 2R in dst.
-static int v2_pass(const int32_t* src, int32_t* dst, int64_t n, int64_t R, int64_t* mp,
-                   cudaStream_t s) {
+template <int NT, int K>
+static int v2_pass_t(const int32_t* src, int32_t* dst, int64_t n, int64_t R, int64_t* mp,
+                     cudaStream_t s) {
   const MergeTuning& tu = tuning();
-  const PassPlan P = plan_pass(n, R);
+  const PassPlan P = plan_pass(n, R, NT, K);
   const int64_t pairs = (n + 2 * R - 1) / (2 * R);
   const int64_t mt = pairs * P.tpp;
   if (mt <= tu.fused_max_tiles) {
     // few tiles: every CTA finds its own split (no partition launch)
     {
       Prof prof(PK_MERGE_PASS, s);
-      merge_pass_v2_kernel<kV2NT, kV2K, true><<<(unsigned)mt, kV2NT, 0, s>>>(src, dst, P,
-                                                                             nullptr);
+      merge_pass_v2_kernel<NT, K, true><<<(unsigned)mt, NT, 0, s>>>(src, dst, P, nullptr);
     }
     return check_launch("merge_pass_v2_kernel<fused>");
   }
@@ -226,9 +229,19 @@ static int v2_pass(const int32_t* src, int32_t* dst, int64_t n, int64_t R, int64
   NSB_TRY(check_launch("merge_partition_v2_kernel"));
   {
     Prof prof(PK_MERGE_PASS, s);
-    merge_pass_v2_kernel<kV2NT, kV2K><<<(unsigned)mt, kV2NT, 0, s>>>(src, dst, P, mp);
+    merge_pass_v2_kernel<NT, K><<<(unsigned)mt, NT, 0, s>>>(src, dst, P, mp);
   }
   return check_launch("merge_pass_v2_kernel");
+}
+
+// One pairwise merge pass (v2): runs of R in src -> runs of 2R in dst.
+static int v2_pass(const int32_t* src, int32_t* dst, int64_t n, int64_t R, int64_t* mp,
+                   cudaStream_t s) {
+  switch (tuning().v2) {
+    case 1: return v2_pass_t<512, 15>(src, dst, n, R, mp, s);
+    case 2: return v2_pass_t<384, 21>(src, dst, n, R, mp, s);
+    default: return v2_pass_t<kV2NT, kV2K>(src, dst, n, R, mp, s);
+  }
 }
 
 // Pairwise passes over existing sorted runs of length R0 (the last may be
