@@ -249,11 +249,20 @@ def run_ours(args, metric):
     d_in = ns.multiset_digest(keys)
     ops = samplesort.DeviceOps(cfg.width_mask, cfg.varsort_max)
 
+    exchange = {"mode": args.exchange}
+
     def step():
         if world == 1:
             ops.local_sort(keys)
             return keys
-        return samplesort.sample_sort(keys, ops=ops)
+        try:
+            return samplesort.sample_sort(keys, ops=ops, exchange=exchange["mode"])
+        except Exception as e:  # p2p needs CUDA IPC between the ranks
+            if exchange["mode"] != "p2p":
+                raise
+            exchange["mode"] = "nccl"
+            exchange["p2p_error"] = str(e)[:200]
+            return samplesort.sample_sort(keys, ops=ops, exchange="nccl")
 
     for _ in range(args.warmup):
         keys.copy_(pristine)
@@ -358,7 +367,7 @@ def run_ours(args, metric):
         dist.barrier()
         e0.record()
         keys.copy_(hs, non_blocking=True)
-        out = samplesort.sample_sort(keys, ops=ops)
+        out = samplesort.sample_sort(keys, ops=ops, exchange=exchange["mode"])
         res = out.cpu()
         e1.record()
         torch.cuda.synchronize()
@@ -383,6 +392,7 @@ def run_ours(args, metric):
                        "parallelism": "replicas/shards over NCCL" if world > 1 else "single GPU",
                        "l2": "input 4 GiB >> 126 MB L2; restored by an untimed D2D copy "
                              "before each step"},
+            "exchange": exchange if world > 1 else None,
             "gpu_launches": int(launches), "wall_ms_timed_region": wall * 1e3,
             "roofline": roofline, "byte_model": model, "kernel_profile": prof,
             "e2e": e2e, "clocks": clk, "verified": bool(ok.item())}
@@ -527,6 +537,8 @@ def main():
     ap.add_argument("--n", type=int, default=N_DEFAULT)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--extra", action="store_true", help="also time the other BASELINE configs")
+    ap.add_argument("--exchange", choices=["p2p", "nccl"], default="p2p",
+                    help="N>1: pull-merge over peer memory (default) or NCCL all-to-all")
     args = ap.parse_args()
     metric = baseline_metric()
     if args.impl == "reference":

@@ -133,6 +133,24 @@ size_t ns_merge_runs_temp_bytes(size_t n, int num_runs);
 int ns_merge_runs_i32(int32_t* d_keys, const int64_t* h_run_offsets, int num_runs,
                       void* d_temp, size_t temp_bytes, void* stream);
 
+/* Merges npairs (<= 32) independent pairs of sorted runs given by POINTERS:
+ * pair p = (a_ptrs[p][0 .. a_lens[p]), b_ptrs[p][0 .. b_lens[p])) goes to
+ * d_out[o_p .. o_p + a_lens[p] + b_lens[p]), o_p = sum of the earlier pairs'
+ * lengths.  a_ptrs / b_ptrs / lengths are HOST arrays; the runs may live on
+ * peer GPUs (pointers from ns_ipc_open_handle, read over NVLink), which fuses
+ * the sample sort's all-to-all into its first merge round. */
+size_t ns_merge_pairs_temp_bytes(int64_t total, int npairs);
+int ns_merge_pairs_i32(const int32_t* const* a_ptrs, const int64_t* a_lens,
+                       const int32_t* const* b_ptrs, const int64_t* b_lens, int npairs,
+                       int32_t* d_out, void* d_temp, size_t temp_bytes, void* stream);
+
+/* CUDA IPC for the pull-based exchange: export the allocation that contains
+ * d_ptr (64-byte handle + byte offset of d_ptr inside it), map a peer's
+ * allocation (lazy peer access), unmap it. */
+int ns_ipc_get_handle(const void* d_ptr, uint8_t* handle64, uint64_t* offset);
+int ns_ipc_open_handle(const uint8_t* handle64, void** d_base);
+int ns_ipc_close(void* d_base);
+
 /* ---- checking helpers (used by tests and bench, not by the sort) ------- */
 
 /* d_out[0] += sum of mix64(key), d_out[1] ^= xor of mix64(key) (uint64);

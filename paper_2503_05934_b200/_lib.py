@@ -44,6 +44,11 @@ SIGNATURES = {
     "ns_bucket_bounds_i32": (_i32, [_vp, _sz, _vp, _i32, _vp, _vp]),
     "ns_merge_runs_temp_bytes": (_sz, [_sz, _i32]),
     "ns_merge_runs_i32": (_i32, [_vp, _vp, _i32, _vp, _sz, _vp]),
+    "ns_merge_pairs_temp_bytes": (_sz, [_i64, _i32]),
+    "ns_merge_pairs_i32": (_i32, [_vp, _vp, _vp, _vp, _i32, _vp, _vp, _sz, _vp]),
+    "ns_ipc_get_handle": (_i32, [_vp, _vp, C.POINTER(C.c_uint64)]),
+    "ns_ipc_open_handle": (_i32, [_vp, C.POINTER(C.c_void_p)]),
+    "ns_ipc_close": (_i32, [_vp]),
     "ns_multiset_digest_i32": (_i32, [_vp, _sz, _vp, _vp]),
     "ns_count_inversions_i32": (_i32, [_vp, _sz, _vp, _vp]),
     "ns_generate_i32": (_i32, [_vp, _sz, _i32, C.c_uint64, _vp]),

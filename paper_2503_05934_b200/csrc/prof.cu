@@ -5,9 +5,11 @@
 // launch duration measured live, with CUDA events recorded on the stream each
 // kernel is launched on (torch.cuda.Event would only see torch's stream).
 // Off by default: one relaxed atomic load per launch.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <cstring>
 #include <cstdint>
 #include <mutex>
 #include <string>
@@ -125,6 +127,47 @@ int ns_profile_read(int kind, double* total_ms, uint64_t* launches) {
   *total_ms = ms;
   *launches = cnt;
   return NS_OK;
+}
+
+int ns_ipc_get_handle(const void* d_ptr, uint8_t* handle64, uint64_t* offset) {
+  if (!d_ptr || !handle64 || !offset) return NS_ERR_INVALID;
+  // cuMemGetAddressRange through the runtime's driver entry point, so the
+  // library does not link libcuda (it must load on GPU-less build hosts)
+  using range_fn = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+  static range_fn get_range = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+    return reinterpret_cast<range_fn>(fn);
+  }();
+  if (!get_range) return NS_ERR_CUDA;
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (get_range(&base, &size, reinterpret_cast<CUdeviceptr>(d_ptr)) != CUDA_SUCCESS)
+    return NS_ERR_CUDA;
+  cudaIpcMemHandle_t h;
+  NSB_TRY(check_cuda(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)),
+                     "cudaIpcGetMemHandle"));
+  static_assert(sizeof(h) == 64, "IPC handle size");
+  memcpy(handle64, &h, 64);
+  *offset = reinterpret_cast<uint64_t>(d_ptr) - static_cast<uint64_t>(base);
+  return NS_OK;
+}
+
+int ns_ipc_open_handle(const uint8_t* handle64, void** d_base) {
+  if (!handle64 || !d_base) return NS_ERR_INVALID;
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle64, 64);
+  return check_cuda(cudaIpcOpenMemHandle(d_base, h, cudaIpcMemLazyEnablePeerAccess),
+                    "cudaIpcOpenMemHandle");
+}
+
+int ns_ipc_close(void* d_base) {
+  if (!d_base) return NS_ERR_INVALID;
+  return check_cuda(cudaIpcCloseMemHandle(d_base), "cudaIpcCloseMemHandle");
 }
 
 int ns_generate_i32(int32_t* d_out, size_t n, int kind, uint64_t seed, void* stream) {

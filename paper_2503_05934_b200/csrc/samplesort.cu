@@ -108,6 +108,92 @@ __global__ void __launch_bounds__(NT)
 
 constexpr int kPmNT = 512, kPmK = 16, kPmT = kPmNT * kPmK;
 
+// ---- merge of pairs of runs given by POINTERS (possibly on peer GPUs) -----
+// Pair p = (A_p[0..la_p), B_p[0..lb_p)) -> dst[out_off_p ..).  A_p/B_p may be
+// peer addresses mapped over NVLink (ns_ipc_open_handle): the partition
+// searches and the staging loads then read the peer's HBM directly, so the
+// sample sort's all-to-all is fused into its first merge round (no receive
+// buffer, no extra HBM pass, transfer overlapped with merging).
+constexpr int kMaxPtrPairs = 32;
+struct PtrPairTable {
+  int npairs;
+  const int32_t* a[kMaxPtrPairs];
+  const int32_t* b[kMaxPtrPairs];
+  int64_t a_len[kMaxPtrPairs], b_len[kMaxPtrPairs], out_off[kMaxPtrPairs];
+  int64_t tile0[kMaxPtrPairs + 1];
+};
+
+__device__ __forceinline__ int ptr_pair_of(const PtrPairTable& t, int64_t tile) {
+  int p = 0;
+  while (p + 1 < t.npairs && t.tile0[p + 1] <= tile) ++p;
+  return p;
+}
+
+template <int TM>
+__global__ void ptr_pairs_partition_kernel(PtrPairTable t, int64_t* __restrict__ mp) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= t.tile0[t.npairs]) return;
+  const int p = ptr_pair_of(t, c);
+  const int64_t diag = (c - t.tile0[p]) * TM;
+  mp[c] = merge_path<int64_t>(t.a[p], t.a_len[p], t.b[p], t.b_len[p], diag);
+}
+
+template <int NT, int K>
+__global__ void __launch_bounds__(NT)
+    ptr_pairs_merge_kernel(int32_t* __restrict__ dst, PtrPairTable t,
+                           const int64_t* __restrict__ mp) {
+  constexpr int TM = NT * K;
+  __shared__ __align__(16) int32_t sm[padded_words(TM)];
+  const int tid = threadIdx.x;
+  const int64_t c = blockIdx.x;
+  const int p = ptr_pair_of(t, c);
+  const int64_t pair_len = t.a_len[p] + t.b_len[p];
+  const int64_t diag0 = (c - t.tile0[p]) * TM;
+  const int64_t diag1 = min(diag0 + TM, pair_len);
+  const int64_t a0 = mp[c];
+  const int64_t a1 = (diag1 == pair_len) ? t.a_len[p] : mp[c + 1];
+  const int la = (int)(a1 - a0);
+  const int lb = (int)((diag1 - a1) - (diag0 - a0));
+  const int32_t* A = t.a[p] + a0;
+  const int32_t* B = t.b[p] + (diag0 - a0);
+  const int total = la + lb;
+#pragma unroll 8
+  for (int i = tid; i < total; i += NT) sm[pad_idx(i)] = i < la ? __ldcs(A + i) : __ldcs(B + (i - la));
+  __syncthreads();
+  const int diag = min(tid * K, total);
+  const SmemRun SA{sm, 0}, SB{sm, la};
+  const int a = merge_path<int>(SA, la, SB, lb, diag);
+  int32_t v[K];
+  serial_merge<K>(SA, la, SB, lb, a, diag - a, v);
+  __syncthreads();
+  regs_to_smem<K>(sm, v);
+  __syncthreads();
+  tile_store<NT, TM>(sm, dst + t.out_off[p] + diag0, total);
+}
+
+// Host side: merges up to kMaxPtrPairs pairs in one partition + one merge launch.
+static int merge_ptr_pairs(const PtrPairTable& t0, int32_t* dst, int64_t* mp, cudaStream_t s) {
+  PtrPairTable t = t0;
+  int64_t tiles = 0;
+  for (int p = 0; p < t.npairs; ++p) {
+    t.tile0[p] = tiles;
+    tiles += (t.a_len[p] + t.b_len[p] + kPmT - 1) / kPmT;
+  }
+  t.tile0[t.npairs] = tiles;
+  if (tiles == 0) return NS_OK;
+  {
+    Prof prof(PK_PARTITION, s);
+    ptr_pairs_partition_kernel<kPmT><<<(unsigned)((tiles + 255) / 256), 256, 0, s>>>(t, mp);
+  }
+  NSB_TRY(check_launch("ptr_pairs_partition_kernel"));
+  {
+    Prof prof(PK_MERGE_PASS, s);
+    ptr_pairs_merge_kernel<kPmNT, kPmK><<<(unsigned)tiles, kPmNT, 0, s>>>(dst, t, mp);
+  }
+  return check_launch("ptr_pairs_merge_kernel");
+}
+
+
 }  // namespace nsb
 
 using namespace nsb;
@@ -142,6 +228,35 @@ int ns_bucket_bounds_i32(const int32_t* d_sorted, size_t n, const int32_t* d_spl
   bucket_bounds_kernel<<<(g + 1 + 127) / 128, 128, 0, static_cast<cudaStream_t>(stream)>>>(
       d_sorted, (int64_t)n, d_splitters, g, d_bounds);
   return check_launch("bucket_bounds_kernel");
+}
+
+size_t ns_merge_pairs_temp_bytes(int64_t total, int npairs) {
+  return align_up((size_t)(total / kPmT + npairs + 2) * 8, 256);
+}
+
+int ns_merge_pairs_i32(const int32_t* const* a_ptrs, const int64_t* a_lens,
+                       const int32_t* const* b_ptrs, const int64_t* b_lens, int npairs,
+                       int32_t* d_out, void* d_temp, size_t temp_bytes, void* stream) {
+  if (npairs < 0 || npairs > kMaxPtrPairs || (npairs && (!a_ptrs || !a_lens || !b_ptrs || !b_lens)))
+    return NS_ERR_INVALID;
+  if (npairs == 0) return NS_OK;
+  PtrPairTable t{};
+  t.npairs = npairs;
+  int64_t off = 0;
+  for (int p = 0; p < npairs; ++p) {
+    if (a_lens[p] < 0 || b_lens[p] < 0) return NS_ERR_INVALID;
+    if ((a_lens[p] && !a_ptrs[p]) || (b_lens[p] && !b_ptrs[p])) return NS_ERR_INVALID;
+    t.a[p] = a_ptrs[p];
+    t.b[p] = b_ptrs[p] ? b_ptrs[p] : a_ptrs[p];
+    t.a_len[p] = a_lens[p];
+    t.b_len[p] = b_lens[p];
+    t.out_off[p] = off;
+    off += a_lens[p] + b_lens[p];
+  }
+  if (off == 0) return NS_OK;
+  if (!d_out || !d_temp || temp_bytes < ns_merge_pairs_temp_bytes(off, npairs)) return NS_ERR_TEMP;
+  return merge_ptr_pairs(t, d_out, static_cast<int64_t*>(d_temp),
+                         static_cast<cudaStream_t>(stream));
 }
 
 size_t ns_merge_runs_temp_bytes(size_t n, int num_runs) {

@@ -14,6 +14,14 @@ NVSwitch in production, gloo in the CPU tests):
   6. all-to-all counts, then all-to-all keys (variable sizes)  torch.distributed
   7. g-way merge of the g received sorted runs                 ns_merge_runs_i32
 
+exchange="p2p" replaces 6-7 by a PULL merge over peer memory (NVLink): every
+rank exports its sorted shard once (CUDA IPC), maps its peers' shards, and
+merges the g runs destined to it straight out of the peers' HBM
+(ns_merge_pairs_i32 reads peer pointers; later rounds are local) — the
+all-to-all is fused into the first merge round, with no receive buffer and
+the NVLink transfer overlapped with merging.  A final barrier keeps every
+shard alive until all peers have finished reading it.
+
 The result is globally sorted across ranks in rank order (rank r holds the
 r-th bucket range) and is a permutation of the input.  The reference has no
 distributed path; its single-array merge sort is the oracle.
@@ -84,6 +92,64 @@ class DeviceOps:
                                           self._s(b)), "bucket bounds")
         return b
 
+    # ---- pull exchange over peer memory (exchange="p2p") ------------------
+    def open_peer_runs(self, shard: torch.Tensor, bounds_all: list, group=None) -> list:
+        """(ptr, len) of the run every rank holds for THIS rank; peers' shards
+        are mapped with CUDA IPC (closed by close_peers)."""
+        me, g = dist.get_rank(group), dist.get_world_size(group)
+        h = (C.c_uint8 * 64)()
+        off = C.c_uint64()
+        check(self.L.ns_ipc_get_handle(shard.data_ptr(), C.cast(h, C.c_void_p), C.byref(off)),
+              "ipc handle")
+        mine = (bytes(h), off.value)
+        allh = [None] * g
+        dist.all_gather_object(allh, mine, group=group)
+        self._mapped = []
+        runs = []
+        for p in range(g):
+            lo, hi = bounds_all[p][me], bounds_all[p][me + 1]
+            if p == me:
+                base = shard.data_ptr()
+            else:
+                hb = (C.c_uint8 * 64).from_buffer_copy(allh[p][0])
+                ptr = C.c_void_p()
+                check(self.L.ns_ipc_open_handle(C.cast(hb, C.c_void_p), C.byref(ptr)), "ipc open")
+                self._mapped.append(ptr.value)
+                base = ptr.value + allh[p][1]
+            runs.append((base + 4 * lo, hi - lo))
+        return runs
+
+    def merge_pull(self, runs: list, device) -> torch.Tensor:
+        total = sum(n for _, n in runs)
+        out = torch.empty(total, dtype=torch.int32, device=device)
+        if total == 0:
+            return out
+        if len(runs) == 1:
+            raise ValueError("merge_pull needs >= 2 runs")
+        pairs = [(runs[i], runs[i + 1] if i + 1 < len(runs) else (0, 0))
+                 for i in range(0, len(runs), 2)]
+        np_ = len(pairs)
+        a_p = (C.c_void_p * np_)(*[a[0] for a, _ in pairs])
+        a_l = (C.c_int64 * np_)(*[a[1] for a, _ in pairs])
+        b_p = (C.c_void_p * np_)(*[b[0] for _, b in pairs])
+        b_l = (C.c_int64 * np_)(*[b[1] for _, b in pairs])
+        tb = self.L.ns_merge_pairs_temp_bytes(total, np_)
+        check(self.L.ns_merge_pairs_i32(C.cast(a_p, C.c_void_p), C.cast(a_l, C.c_void_p),
+                                        C.cast(b_p, C.c_void_p), C.cast(b_l, C.c_void_p), np_,
+                                        out.data_ptr(), self._temp(tb, device), tb,
+                                        self._s(out)), "merge pairs (pull)")
+        if np_ > 1:  # remaining rounds are local
+            offs = [0]
+            for a, b in pairs:
+                offs.append(offs[-1] + a[1] + b[1])
+            self.merge_runs(out, offs)
+        return out
+
+    def close_peers(self) -> None:
+        for p in getattr(self, "_mapped", []):
+            self.L.ns_ipc_close(C.c_void_p(p))
+        self._mapped = []
+
     def merge_runs(self, keys: torch.Tensor, run_offsets: list) -> None:
         nr = len(run_offsets) - 1
         tb = self.L.ns_merge_runs_temp_bytes(keys.numel(), nr)
@@ -103,7 +169,7 @@ class SampleSortTiming:
 
 
 def sample_sort(shard: torch.Tensor, group=None, ops=None, samples_per_rank: int = SAMPLES_PER_RANK,
-                timing: Optional[SampleSortTiming] = None) -> torch.Tensor:
+                timing: Optional[SampleSortTiming] = None, exchange: str = "nccl") -> torch.Tensor:
     """Globally sort the distributed array whose rank-local shard is `shard`.
 
     Returns this rank's slice of the sorted result (a new tensor; `shard` is
@@ -130,6 +196,28 @@ def sample_sort(shard: torch.Tensor, group=None, ops=None, samples_per_rank: int
     dist.all_gather(gathered, smp, group=group)
     spl = ops.splitters(torch.cat(gathered), g)
     bnd = ops.bounds(shard, spl, g)
+    if exchange == "p2p":
+        ball = [torch.empty_like(bnd) for _ in range(g)]
+        dist.all_gather(ball, bnd, group=group)
+        bounds_all = [b.cpu().tolist() for b in ball]
+        runs = ops.open_peer_runs(shard, bounds_all, group)
+        if ev:
+            ev[2].record()
+        out = ops.merge_pull(runs, dev)
+        if dev.type == "cuda":
+            torch.cuda.current_stream(dev).synchronize()
+        dist.barrier(group=group)  # peers are done reading this shard
+        ops.close_peers()
+        if ev:
+            ev[3].record()
+            ev[3].synchronize()
+            timing.local_sort_ms = ev[0].elapsed_time(ev[1])
+            timing.exchange_ms = ev[1].elapsed_time(ev[2])
+            timing.merge_ms = ev[2].elapsed_time(ev[3])
+            me = dist.get_rank(group)
+            timing.send_bytes = 4 * sum(bounds_all[me][p + 1] - bounds_all[me][p]
+                                        for p in range(g) if p != me)
+        return out
     send_counts = (bnd[1:] - bnd[:-1]).to(torch.int64)
     recv_counts = torch.empty_like(send_counts)
     dist.all_to_all_single(recv_counts, send_counts, group=group)

@@ -266,3 +266,41 @@ def test_kway_merge_path(ns, cuda, kway):
                          capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stderr[-2000:]
     assert "BAD []" in out.stdout, out.stdout[-2000:]
+
+
+def test_merge_pairs_from_separate_buffers(ns, cuda, oracle):
+    """ns_merge_pairs_i32 with every run in its own allocation and at odd
+    offsets — the same kernel that, in the p2p sample sort, reads the runs
+    from peer GPUs over NVLink (on one GPU the "peers" are local buffers;
+    nothing waits on another kernel)."""
+    import torch
+    from paper_2503_05934_b200 import samplesort
+    rng = np.random.default_rng(9)
+    ops = samplesort.DeviceOps()
+    for lens in ([5000, 7000], [0, 300000, 1, 77777, 123456, 0, 9, 50000],
+                 [100000] * 8, [3, 0, 0], [250000, 250001, 249999]):
+        bufs, runs, allk = [], [], []
+        for i, ln in enumerate(lens):
+            v = np.sort(rng.integers(-2**31, 2**31 - 1, ln, dtype=np.int64).astype(np.int32))
+            if i % 3 == 0:
+                v[: ln // 2] = 7  # duplicates across runs
+                v = np.sort(v)
+            pad = i % 4  # misaligned start inside its allocation
+            t = torch.zeros(ln + pad + 1, dtype=torch.int32, device=cuda)
+            t[pad:pad + ln] = torch.from_numpy(v).to(cuda)
+            bufs.append(t)
+            runs.append((t.data_ptr() + 4 * pad, ln))
+            allk.append(v)
+        out = ops.merge_pull(runs, cuda)
+        want = np.sort(np.concatenate(allk))
+        assert np.array_equal(out.cpu().numpy(), want), lens
+
+
+def test_ipc_handle_export(ns, cuda):
+    import ctypes as C
+    import torch
+    t = torch.empty(1 << 20, dtype=torch.int32, device=cuda)
+    h = (C.c_uint8 * 64)()
+    off = C.c_uint64()
+    assert ns.lib().ns_ipc_get_handle(t.data_ptr() + 4096, C.cast(h, C.c_void_p), C.byref(off)) == 0
+    assert off.value % 4 == 0 and off.value >= 4096 and any(bytes(h))

@@ -39,6 +39,36 @@ class OracleOps:
         b = [0] + [int(np.searchsorted(a, int(x), side="left")) for x in spl.tolist()] + [len(a)]
         return torch.tensor(b, dtype=torch.int64)
 
+    # pull exchange: "peer memory" is simulated by gathering every shard (the
+    # metadata path — bounds all-gather, run assembly, pairing, barrier — is the
+    # product's own code in samplesort.sample_sort)
+    def open_peer_runs(self, shard, bounds_all, group=None):
+        me, g = dist.get_rank(group), dist.get_world_size(group)
+        shards = [None] * g
+        dist.all_gather_object(shards, shard.numpy(), group=group)
+        return [(shards[p][bounds_all[p][me]:bounds_all[p][me + 1]], bounds_all[p][me + 1] - bounds_all[p][me])
+                for p in range(g)]
+
+    def merge_pull(self, runs, device):
+        pairs = [(runs[i], runs[i + 1] if i + 1 < len(runs) else (np.empty(0, np.int32), 0))
+                 for i in range(0, len(runs), 2)]
+        parts = []
+        for (a, _), (b, _) in pairs:
+            cat = np.concatenate([a, b]).astype(np.int32)
+            if len(a) and len(b):
+                self.O.lib().oracle_merge_i32(cat, 0, len(a) - 1, len(cat) - 1)
+            parts.append(cat)
+        out = torch.from_numpy(np.concatenate(parts).astype(np.int32)) if parts else torch.empty(0, dtype=torch.int32)
+        if len(pairs) > 1:
+            offs = [0]
+            for p_ in parts:
+                offs.append(offs[-1] + len(p_))
+            self.merge_runs(out, offs)
+        return out
+
+    def close_peers(self):
+        pass
+
     def merge_runs(self, keys, offs):
         out = keys.numpy().copy()
         runs = [out[offs[i]:offs[i + 1]] for i in range(len(offs) - 1)]
@@ -60,7 +90,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, n, dist_kind, q):
+def _worker(rank, world, port, n, dist_kind, q, exchange="nccl"):
     import sys
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -73,7 +103,7 @@ def _worker(rank, world, port, n, dist_kind, q):
     lo = rank * m
     hi = n if rank == world - 1 else lo + m
     shard = torch.from_numpy(full[lo:hi].copy())
-    out = samplesort.sample_sort(shard, ops=OracleOps())
+    out = samplesort.sample_sort(shard, ops=OracleOps(), exchange=exchange)
     parts = [None] * world
     dist.all_gather_object(parts, out.numpy().tolist())
     if rank == 0:
@@ -82,13 +112,15 @@ def _worker(rank, world, port, n, dist_kind, q):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,n,dist_kind", [(2, 20000, "random"), (2, 5000, "sorted"),
-                                               (3, 30001, "random"), (2, 3, "random")])
-def test_sample_sort_multi_process(oracle, world, n, dist_kind):
+@pytest.mark.parametrize("world,n,dist_kind,exchange", [
+    (2, 20000, "random", "nccl"), (2, 5000, "sorted", "nccl"), (3, 30001, "random", "nccl"),
+    (2, 3, "random", "nccl"), (2, 20000, "random", "p2p"), (3, 30001, "nearly_sorted", "p2p"),
+    (4, 40000, "random", "p2p")])
+def test_sample_sort_multi_process(oracle, world, n, dist_kind, exchange):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, n, dist_kind, q))
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, dist_kind, q, exchange))
              for r in range(world)]
     for p in procs:
         p.start()
