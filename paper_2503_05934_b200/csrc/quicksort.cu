@@ -36,6 +36,7 @@ constexpr int kQsOversample = 16;    // samples per bucket
 constexpr int kQsTarget = 4096;      // target mean bucket size
 constexpr int kQsNT = 512;
 constexpr int kQsChunk = kQsNT * 32;  // keys per CTA in count / scatter
+constexpr int kQsLut = 4096;          // prefix table slots
 
 struct QsAux {  // carved from the caller's scratch, after the n-key buffer
   int32_t* samples;     // kQsMaxB * kQsOversample
@@ -45,13 +46,14 @@ struct QsAux {  // carved from the caller's scratch, after the n-key buffer
   uint32_t* totals;     // 2*kQsMaxB
   unsigned long long* fill;  // 2*kQsMaxB
   int64_t* jobs;        // 2 * 2*kQsMaxB
+  int16_t* lut;         // kQsLut + 1 entries + {base, shift} header
 };
 
 static size_t qs_aux_bytes() {
   const size_t S = (size_t)kQsMaxB * kQsOversample;
   return align_up(S * 4, 256) + align_up(merge_sort_temp(S), 256) + align_up(kQsMaxB * 4, 256) +
          align_up(2 * kQsMaxB * 4, 256) + align_up(2 * kQsMaxB * 8, 256) +
-         align_up(4 * kQsMaxB * 8, 256);
+         align_up(4 * kQsMaxB * 8, 256) + align_up((kQsLut + 1) * 2 + 16, 256);
 }
 
 static QsAux carve_aux(char* p) {
@@ -69,6 +71,8 @@ static QsAux carve_aux(char* p) {
   a.fill = reinterpret_cast<unsigned long long*>(p);
   p += align_up(2 * kQsMaxB * 8, 256);
   a.jobs = reinterpret_cast<int64_t*>(p);
+  p += align_up(4 * kQsMaxB * 8, 256);
+  a.lut = reinterpret_cast<int16_t*>(p);
   return a;
 }
 
@@ -98,23 +102,84 @@ __global__ void splitter_kernel(const int32_t* __restrict__ samples, int S, int 
   spl[j] = j < B - 1 ? samples[(int64_t)(j + 1) * S / B - 1] : INT_MAX;
 }
 
-// lower_bound over spl[0..B-1) (B a power of two, spl[B-1] = +inf pad), then
-// the equal/between bucket id in [0, 2B-1).
-__device__ __forceinline__ int classify(const int32_t* spl, int B, int32_t key) {
-  int j = 0;
-  for (int step = B >> 1; step >= 1; step >>= 1)
-    if (spl[j + step - 1] < key) j += step;
-  return (j < B - 1 && spl[j] == key) ? 2 * j + 1 : 2 * j;
+// Prefix lookup table that shortcuts the splitter search: keys are bucketed
+// by (key - base) >> shift into kQsLut slots spanning [spl[0], spl[B-2]];
+// lut[p] = number of splitters < base + (p << shift).  A key's lower_bound
+// then lies in [lut[p], lut[p+1]] (p < kQsLut-1) — usually 0..2 candidates —
+// instead of needing log2(B) dependent shared-memory loads.  Layout in global:
+// int32 header {base, shift} then kQsLut+1 int16 entries.
+__global__ void lut_kernel(const int32_t* __restrict__ spl, int B, int16_t* __restrict__ lut) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p > kQsLut) return;
+  const int32_t base = spl[0];
+  const int64_t span = (int64_t)spl[max(B - 2, 0)] - base + 1;
+  int shift = 0;
+  while ((span >> shift) > kQsLut) ++shift;
+  if (p == 0) {
+    int32_t* hdr = reinterpret_cast<int32_t*>(lut);
+    hdr[0] = base;
+    hdr[1] = shift;
+  }
+  const int64_t bound = (int64_t)base + ((int64_t)p << shift);
+  int lo = 0, hi = B - 1;  // lower_bound over the B-1 real splitters
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if ((int64_t)spl[mid] < bound) lo = mid + 1;
+    else hi = mid;
+  }
+  lut[8 + p] = (int16_t)lo;
 }
+
+struct Classifier {
+  const int32_t* spl;  // smem, B entries (spl[B-1] = +inf pad)
+  const int16_t* lut;  // smem, kQsLut+1 entries
+  int B;
+  int32_t base;
+  int shift;
+  // equal/between bucket id in [0, 2B-1)
+  __device__ __forceinline__ int operator()(int32_t key) const {
+    const int64_t d = (int64_t)key - base;
+    int lo, hi;
+    if (d < 0) {
+      lo = hi = 0;
+    } else {
+      const int64_t pp = d >> shift;
+      if (pp >= kQsLut - 1) {
+        lo = lut[kQsLut - 1];
+        hi = B - 1;
+      } else {
+        lo = lut[pp];
+        hi = lut[pp + 1];
+      }
+    }
+    while (lo < hi) {  // lower_bound in spl[lo..hi)
+      const int mid = (lo + hi) >> 1;
+      if (spl[mid] < key) lo = mid + 1;
+      else hi = mid;
+    }
+    return (lo < B - 1 && spl[lo] == key) ? 2 * lo + 1 : 2 * lo;
+  }
+};
+
+__device__ __forceinline__ Classifier load_classifier(int32_t* sm, const int32_t* gspl,
+                                                      const int16_t* glut, int B) {
+  int32_t* spl = sm;
+  int16_t* lut = reinterpret_cast<int16_t*>(sm + B);
+  for (int i = threadIdx.x; i < B; i += blockDim.x) spl[i] = gspl[i];
+  for (int i = threadIdx.x; i <= kQsLut; i += blockDim.x) lut[i] = glut[8 + i];
+  const int32_t* hdr = reinterpret_cast<const int32_t*>(glut);
+  return Classifier{spl, lut, B, hdr[0], hdr[1]};
+}
+
+constexpr int kQsClassifierWords = kQsMaxB + (kQsLut + 2) / 2 + 2;
 
 __global__ void __launch_bounds__(kQsNT)
     count_kernel(const int32_t* __restrict__ keys, int64_t n, const int32_t* __restrict__ gspl,
-                 int B, uint32_t* __restrict__ totals) {
+                 const int16_t* __restrict__ glut, int B, uint32_t* __restrict__ totals) {
   extern __shared__ int32_t qsm[];
-  int32_t* spl = qsm;
-  uint32_t* hist = reinterpret_cast<uint32_t*>(qsm + B);
+  const Classifier cls = load_classifier(qsm, gspl, glut, B);
+  uint32_t* hist = reinterpret_cast<uint32_t*>(qsm + kQsClassifierWords);
   const int NB = 2 * B - 1;
-  for (int i = threadIdx.x; i < B; i += kQsNT) spl[i] = gspl[i];
   for (int i = threadIdx.x; i < NB; i += kQsNT) hist[i] = 0;
   __syncthreads();
   const int64_t c0 = (int64_t)blockIdx.x * kQsChunk;
@@ -122,7 +187,7 @@ __global__ void __launch_bounds__(kQsNT)
   const int lane = threadIdx.x & 31;
   for (int64_t i = c0 + threadIdx.x; i - threadIdx.x < c1; i += kQsNT) {
     const bool live = i < c1;
-    const int b = live ? classify(spl, B, __ldg(keys + i)) : -1;
+    const int b = live ? cls(__ldg(keys + i)) : -1;
     const unsigned peers = __match_any_sync(kFull, b);
     if (live && lane == __ffs(peers) - 1) atomicAdd(&hist[b], (uint32_t)__popc(peers));
   }
@@ -133,10 +198,10 @@ __global__ void __launch_bounds__(kQsNT)
 
 __global__ void __launch_bounds__(kQsNT)
     scatter_kernel(const int32_t* __restrict__ keys, int64_t n, const int32_t* __restrict__ gspl,
-                   int B, unsigned long long* __restrict__ fill, int32_t* __restrict__ out) {
+                   const int16_t* __restrict__ glut, int B, unsigned long long* __restrict__ fill,
+                   int32_t* __restrict__ out) {
   extern __shared__ int32_t qsm[];
-  int32_t* spl = qsm;
-  for (int i = threadIdx.x; i < B; i += kQsNT) spl[i] = gspl[i];
+  const Classifier cls = load_classifier(qsm, gspl, glut, B);
   __syncthreads();
   const int64_t c0 = (int64_t)blockIdx.x * kQsChunk;
   const int64_t c1 = min(n, c0 + kQsChunk);
@@ -144,7 +209,7 @@ __global__ void __launch_bounds__(kQsNT)
   for (int64_t i = c0 + threadIdx.x; i - threadIdx.x < c1; i += kQsNT) {
     const bool live = i < c1;
     const int32_t k = live ? __ldcs(keys + i) : 0;
-    const int b = live ? classify(spl, B, k) : -1;
+    const int b = live ? cls(k) : -1;
     const unsigned peers = __match_any_sync(kFull, b);
     const int leader = __ffs(peers) - 1;
     unsigned long long base = 0;
@@ -211,22 +276,27 @@ static int quick_sort_level(int32_t* keys, int32_t* tmp, size_t n, int leaf, con
     splitter_kernel<<<(B + 255) / 256, 256, 0, s>>>(aux.samples, S, B, aux.splitters);
   }
   NSB_TRY(check_launch("splitter_kernel"));
+  {
+    Prof prof(PK_QS_SAMPLE, s);
+    lut_kernel<<<(kQsLut + 1 + 255) / 256, 256, 0, s>>>(aux.splitters, B, aux.lut);
+  }
+  NSB_TRY(check_launch("lut_kernel"));
 
   NSB_TRY(check_cuda(cudaMemsetAsync(aux.totals, 0, NB * sizeof(uint32_t), s), "memset"));
   const int64_t ctas = (int64_t)((n + kQsChunk - 1) / kQsChunk);
-  const int count_smem = (B + NB) * 4;
+  const int count_smem = (kQsClassifierWords + NB) * 4;
   static bool attr_set = false;
   if (!attr_set) {
     NSB_TRY(check_cuda(cudaFuncSetAttribute(count_kernel,
                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            (kQsMaxB * 3) * 4),
+                                            (kQsClassifierWords + 2 * kQsMaxB) * 4),
                        "cudaFuncSetAttribute(count)"));
     attr_set = true;
   }
   {
     Prof prof(PK_QS_COUNT, s);
-    count_kernel<<<(unsigned)ctas, kQsNT, count_smem, s>>>(keys, (int64_t)n, aux.splitters, B,
-                                                           aux.totals);
+    count_kernel<<<(unsigned)ctas, kQsNT, count_smem, s>>>(keys, (int64_t)n, aux.splitters,
+                                                           aux.lut, B, aux.totals);
   }
   NSB_TRY(check_launch("count_kernel"));
 
@@ -250,8 +320,8 @@ static int quick_sort_level(int32_t* keys, int32_t* tmp, size_t n, int leaf, con
                      "cudaMemcpyAsync(fill)"));
   {
     Prof prof(PK_QS_SCATTER, s);
-    scatter_kernel<<<(unsigned)ctas, kQsNT, B * 4, s>>>(keys, (int64_t)n, aux.splitters, B,
-                                                        aux.fill, tmp);
+    scatter_kernel<<<(unsigned)ctas, kQsNT, kQsClassifierWords * 4, s>>>(
+        keys, (int64_t)n, aux.splitters, aux.lut, B, aux.fill, tmp);
   }
   NSB_TRY(check_launch("scatter_kernel"));
 
