@@ -196,26 +196,55 @@ __global__ void __launch_bounds__(kQsNT)
     if (hist[i]) atomicAdd(&totals[i], hist[i]);
 }
 
+// Scatter with one global reservation per (CTA, bucket): the CTA classifies
+// its chunk once (bucket ids stay in registers), builds a shared-memory
+// histogram, reserves each non-empty bucket's range with ONE global atomic,
+// then places every key at base + warp-aggregated shared-memory rank.
+constexpr int kQsPer = 16;                  // keys per thread in scatter
+constexpr int kQsSChunk = kQsPer * kQsNT;  // keys per CTA in scatter
+
 __global__ void __launch_bounds__(kQsNT)
     scatter_kernel(const int32_t* __restrict__ keys, int64_t n, const int32_t* __restrict__ gspl,
                    const int16_t* __restrict__ glut, int B, unsigned long long* __restrict__ fill,
                    int32_t* __restrict__ out) {
   extern __shared__ int32_t qsm[];
   const Classifier cls = load_classifier(qsm, gspl, glut, B);
+  unsigned long long* pos =
+      reinterpret_cast<unsigned long long*>(qsm + ((kQsClassifierWords + 3) & ~1));  // 8-byte aligned
+  const int NB = 2 * B - 1;
+  for (int i = threadIdx.x; i < NB; i += kQsNT) pos[i] = 0;
   __syncthreads();
-  const int64_t c0 = (int64_t)blockIdx.x * kQsChunk;
-  const int64_t c1 = min(n, c0 + kQsChunk);
+  const int64_t c0 = (int64_t)blockIdx.x * kQsSChunk;
   const int lane = threadIdx.x & 31;
-  for (int64_t i = c0 + threadIdx.x; i - threadIdx.x < c1; i += kQsNT) {
-    const bool live = i < c1;
-    const int32_t k = live ? __ldcs(keys + i) : 0;
-    const int b = live ? cls(k) : -1;
+  int32_t k[kQsPer];
+  int bk[kQsPer];
+#pragma unroll
+  for (int u = 0; u < kQsPer; ++u) {
+    const int64_t i = c0 + u * kQsNT + threadIdx.x;
+    k[u] = i < n ? __ldcs(keys + i) : 0;
+  }
+#pragma unroll
+  for (int u = 0; u < kQsPer; ++u) {
+    const int64_t i = c0 + u * kQsNT + threadIdx.x;
+    bk[u] = i < n ? cls(k[u]) : -1;
+    const unsigned peers = __match_any_sync(kFull, bk[u]);
+    if (bk[u] >= 0 && lane == __ffs(peers) - 1) atomicAdd(&pos[bk[u]], (unsigned long long)__popc(peers));
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < NB; b += kQsNT) {
+    const unsigned long long c = pos[b];
+    if (c) pos[b] = atomicAdd(&fill[b], c);  // one global atomic per (CTA, bucket)
+  }
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < kQsPer; ++u) {
+    const int b = bk[u];
     const unsigned peers = __match_any_sync(kFull, b);
     const int leader = __ffs(peers) - 1;
     unsigned long long base = 0;
-    if (live && lane == leader) base = atomicAdd(&fill[b], (unsigned long long)__popc(peers));
+    if (b >= 0 && lane == leader) base = atomicAdd(&pos[b], (unsigned long long)__popc(peers));
     base = __shfl_sync(kFull, base, leader);
-    if (live) out[base + __popc(peers & ((1u << lane) - 1))] = k;
+    if (b >= 0) out[base + __popc(peers & ((1u << lane) - 1))] = k[u];
   }
 }
 
@@ -285,12 +314,17 @@ static int quick_sort_level(int32_t* keys, int32_t* tmp, size_t n, int leaf, con
   NSB_TRY(check_cuda(cudaMemsetAsync(aux.totals, 0, NB * sizeof(uint32_t), s), "memset"));
   const int64_t ctas = (int64_t)((n + kQsChunk - 1) / kQsChunk);
   const int count_smem = (kQsClassifierWords + NB) * 4;
+  const int scatter_smem = ((kQsClassifierWords + 3) & ~1) * 4 + NB * 8;
   static bool attr_set = false;
   if (!attr_set) {
     NSB_TRY(check_cuda(cudaFuncSetAttribute(count_kernel,
                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             (kQsClassifierWords + 2 * kQsMaxB) * 4),
                        "cudaFuncSetAttribute(count)"));
+    NSB_TRY(check_cuda(cudaFuncSetAttribute(scatter_kernel,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            ((kQsClassifierWords + 3) & ~1) * 4 + 2 * kQsMaxB * 8),
+                       "cudaFuncSetAttribute(scatter)"));
     attr_set = true;
   }
   {
@@ -320,7 +354,7 @@ static int quick_sort_level(int32_t* keys, int32_t* tmp, size_t n, int leaf, con
                      "cudaMemcpyAsync(fill)"));
   {
     Prof prof(PK_QS_SCATTER, s);
-    scatter_kernel<<<(unsigned)ctas, kQsNT, kQsClassifierWords * 4, s>>>(
+    scatter_kernel<<<(unsigned)((n + kQsSChunk - 1) / kQsSChunk), kQsNT, scatter_smem, s>>>(
         keys, (int64_t)n, aux.splitters, aux.lut, B, aux.fill, tmp);
   }
   NSB_TRY(check_launch("scatter_kernel"));
