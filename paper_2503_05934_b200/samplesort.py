@@ -175,6 +175,18 @@ class SampleSortTiming:
     send_bytes: int = 0
 
 
+def _all_gather_cat(t: torch.Tensor, g: int, group) -> torch.Tensor:
+    """all_gather of a small tensor, concatenated.  Metadata collectives go
+    through host memory when the process group is gloo (CPU tests, and the
+    single-GPU multi-process check of the p2p path), device memory otherwise."""
+    host = dist.get_backend(group) == "gloo" and t.is_cuda
+    src = t.cpu() if host else t
+    parts = [torch.empty_like(src) for _ in range(g)]
+    dist.all_gather(parts, src, group=group)
+    out = torch.cat(parts)
+    return out.to(t.device) if host else out
+
+
 def sample_sort(shard: torch.Tensor, group=None, ops=None, samples_per_rank: int = SAMPLES_PER_RANK,
                 timing: Optional[SampleSortTiming] = None, exchange: str = "nccl") -> torch.Tensor:
     """Globally sort the distributed array whose rank-local shard is `shard`.
@@ -199,14 +211,10 @@ def sample_sort(shard: torch.Tensor, group=None, ops=None, samples_per_rank: int
     if ev:
         ev[1].record()
     smp = ops.samples(shard, samples_per_rank)
-    gathered = [torch.empty_like(smp) for _ in range(g)]
-    dist.all_gather(gathered, smp, group=group)
-    spl = ops.splitters(torch.cat(gathered), g)
+    spl = ops.splitters(_all_gather_cat(smp, g, group), g)
     bnd = ops.bounds(shard, spl, g)
     if exchange == "p2p":
-        ball = [torch.empty_like(bnd) for _ in range(g)]
-        dist.all_gather(ball, bnd, group=group)
-        bounds_all = [b.cpu().tolist() for b in ball]
+        bounds_all = _all_gather_cat(bnd, g, group).view(g, g + 1).cpu().tolist()
         runs = ops.open_peer_runs(shard, bounds_all, group)
         if ev:
             ev[2].record()

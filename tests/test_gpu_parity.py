@@ -304,3 +304,19 @@ def test_ipc_handle_export(ns, cuda):
     off = C.c_uint64()
     assert ns.lib().ns_ipc_get_handle(t.data_ptr() + 4096, C.cast(h, C.c_void_p), C.byref(off)) == 0
     assert off.value % 4 == 0 and off.value >= 4096 and any(bytes(h))
+
+
+@pytest.mark.parametrize("world,n,dist_kind", [(2, 3_000_000, "random"), (3, 1_000_003, "sorted"),
+                                               (4, 2_000_000, "nearly_sorted")])
+def test_p2p_sample_sort_processes_one_gpu(ns, cuda, world, n, dist_kind):
+    """The p2p exchange end to end: `world` processes on one GPU, each rank's
+    pull-merge kernel reading the other ranks' shards through CUDA IPC
+    mappings (host-side gloo for the metadata; no kernel waits on another)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(root, "tests", "multiproc_p2p_gpu.py"),
+                          str(world), str(n), dist_kind], cwd=root, capture_output=True,
+                         text=True, timeout=600)
+    assert "P2P_OK" in out.stdout, (out.stdout[-1500:], out.stderr[-3000:])
