@@ -264,9 +264,14 @@ int merge_sort_device(int32_t* d_keys, size_t n, int leaf, void* d_temp, size_t 
                       cudaStream_t s) {
   if (n <= 1) return NS_OK;
   if (n <= (size_t)kSmT) {
+    // one CTA sized to the array: fewer threads and merge levels for small n
     return with_leaf(leaf, [&](auto L) {
-      return launch_blocksort<kSmNT, kSmK, decltype(L)::value>(d_keys, d_keys, (int64_t)n,
-                                                                kSmT, 1, s);
+      constexpr int LF = decltype(L)::value;
+      if (n <= 512) return launch_blocksort<32, 16, LF>(d_keys, d_keys, (int64_t)n, 512, 1, s);
+      if (n <= 2048) return launch_blocksort<128, 16, LF>(d_keys, d_keys, (int64_t)n, 2048, 1, s);
+      if (n <= 4096) return launch_blocksort<256, 16, LF>(d_keys, d_keys, (int64_t)n, 4096, 1, s);
+      if (n <= 8192) return launch_blocksort<512, 16, LF>(d_keys, d_keys, (int64_t)n, 8192, 1, s);
+      return launch_blocksort<kSmNT, kSmK, LF>(d_keys, d_keys, (int64_t)n, kSmT, 1, s);
     });
   }
   if (temp_bytes < merge_sort_temp(n) || d_temp == nullptr) return NS_ERR_TEMP;
