@@ -22,6 +22,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
+#include <utility>
 #include <climits>
 #include <cstdint>
 #include <vector>
@@ -403,9 +405,431 @@ static int quick_sort_level(int32_t* keys, int32_t* tmp, size_t n, int leaf, con
   return NS_OK;
 }
 
+// ===========================================================================
+// Multi-level, multi-segment partition (default).  Every level partitions ALL
+// oversized segments at once with at most 256 splitters per segment, so the
+// count/scatter kernels stay cheap (8-step search, <= 511 buckets, coalesced
+// ~32-key runs per bucket per CTA) and a whole level costs one host read,
+// instead of one per bucket.  Segments ping-pong between the key buffer and
+// tmp at fixed positions; buckets that fit one CTA are sorted straight into
+// the key buffer (jobs), constant "equal" buckets are copied, the rest form
+// the next level's segments.  Random input of 16M keys: 2 levels.
+// ===========================================================================
+constexpr int kMlMaxB = 256;
+
+struct MlSeg {
+  int64_t start, len;
+  int B, spl_off, cnt_off;
+  int64_t chunk0;  // first count/scatter chunk of this segment
+  int64_t smp_off;
+};
+
+struct MlAux {
+  MlSeg* segs;
+  int32_t* samples;
+  int32_t* spl;
+  uint32_t* counts;
+  unsigned long long* fill;
+  int64_t* jobs;
+  size_t max_segs, max_samples, max_spl, max_cnt, max_jobs;
+};
+
+static size_t ml_max_segs(size_t n) { return n / (kSmallTile + 1) + 4; }
+static size_t ml_max_spl(size_t n) { return n / 2048 + 2 * kMlMaxB * ml_max_segs(n) / 64 + 1024; }
+
+static size_t ml_aux_bytes(size_t n) {
+  const size_t segs = ml_max_segs(n), spl = n / 2048 + 512 * segs / 64 + 4096;
+  return align_up(segs * sizeof(MlSeg), 256) + align_up(16 * spl * 4, 256) +
+         align_up(spl * 4, 256) + align_up(2 * spl * 4, 256) + align_up(2 * spl * 8, 256) +
+         align_up(2 * (2 * spl + segs) * 8, 256);
+}
+
+static MlAux carve_ml(char* p, size_t n) {
+  MlAux a;
+  a.max_segs = ml_max_segs(n);
+  a.max_spl = n / 2048 + 512 * a.max_segs / 64 + 4096;
+  a.max_samples = 16 * a.max_spl;
+  a.max_cnt = 2 * a.max_spl;
+  a.max_jobs = 2 * a.max_spl + a.max_segs;
+  a.segs = reinterpret_cast<MlSeg*>(p);
+  p += align_up(a.max_segs * sizeof(MlSeg), 256);
+  a.samples = reinterpret_cast<int32_t*>(p);
+  p += align_up(a.max_samples * 4, 256);
+  a.spl = reinterpret_cast<int32_t*>(p);
+  p += align_up(a.max_spl * 4, 256);
+  a.counts = reinterpret_cast<uint32_t*>(p);
+  p += align_up(a.max_cnt * 4, 256);
+  a.fill = reinterpret_cast<unsigned long long*>(p);
+  p += align_up(a.max_cnt * 8, 256);
+  a.jobs = reinterpret_cast<int64_t*>(p);
+  return a;
+}
+
+__device__ __forceinline__ int seg_of_chunk(const MlSeg* segs, int nseg, int64_t c) {
+  int lo = 0, hi = nseg - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (segs[mid].chunk0 <= c) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ int seg_of_sample(const MlSeg* segs, int nseg, int64_t i) {
+  int lo = 0, hi = nseg - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (segs[mid].smp_off <= i) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+__global__ void ml_sample_kernel(const int32_t* __restrict__ X, const MlSeg* __restrict__ segs,
+                                 int nseg, int64_t total, int32_t* __restrict__ samples) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= total) return;
+  const MlSeg sg = segs[seg_of_sample(segs, nseg, i)];
+  const int S = kQsOversample * sg.B;
+  const int64_t j = i - sg.smp_off;
+  const int64_t stride = sg.len / S;
+  const int64_t pos = j * stride + (stride > 1 ? hash32((uint32_t)j) % stride : 0);
+  samples[i] = X[sg.start + pos];
+}
+
+__global__ void ml_splitter_kernel(const int32_t* __restrict__ samples,
+                                   const MlSeg* __restrict__ segs, int nseg,
+                                   int32_t* __restrict__ spl) {
+  const int sgi = blockIdx.x;
+  if (sgi >= nseg) return;
+  const MlSeg sg = segs[sgi];
+  const int S = kQsOversample * sg.B;
+  for (int j = threadIdx.x; j < sg.B; j += blockDim.x)
+    spl[sg.spl_off + j] =
+        j < sg.B - 1 ? samples[sg.smp_off + (int64_t)(j + 1) * S / sg.B - 1] : INT_MAX;
+}
+
+template <int LOGB>
+__device__ __forceinline__ int ml_classify(const int32_t* spl, int32_t key) {
+  constexpr int B = 1 << LOGB;
+  int j = 0;
+#pragma unroll
+  for (int step = B >> 1; step >= 1; step >>= 1)
+    if (spl[j + step - 1] < key) j += step;
+  return (j < B - 1 && spl[j] == key) ? 2 * j + 1 : 2 * j;
+}
+
+constexpr int kMlNT = 512, kMlPer = 16, kMlChunk = kMlNT * kMlPer;
+
+// Per-warp private histograms: a warp's lanes that share a bucket are
+// combined with __match_any_sync and one lane updates the warp's own row, so
+// no shared-memory atomics contend (with only 2B-1 <= 511 buckets, 16 warps
+// hammering one shared histogram serialised on the atomic unit).
+constexpr int kMlWarps = kMlNT / 32;
+
+// Lanes of the warp holding the same bucket id, from one ballot per id bit
+// (cheaper than __match_any_sync, which measured as the bottleneck of the
+// count/scatter kernels).  Ids are < 2^nbits; an invalid lane passes -1 and
+// lands in the all-ones group, which callers never use as a real id.
+template <int NBITS>
+__device__ __forceinline__ unsigned warp_peers(int b) {
+  unsigned m = kFull;
+#pragma unroll
+  for (int i = 0; i < NBITS; ++i) {
+    const bool bit = (b >> i) & 1;
+    const unsigned bal = __ballot_sync(kFull, bit);
+    m &= bit ? bal : ~bal;
+  }
+  return m;
+}
+
+template <int LOGB>
+__device__ __forceinline__ void ml_warp_hist(const int32_t* spl, const int32_t (&k)[kMlPer],
+                                             int (&bk)[kMlPer], int64_t c0, int64_t c1,
+                                             uint32_t* row) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int u = 0; u < kMlPer; ++u) {
+    const int64_t i = c0 + u * kMlNT + threadIdx.x;
+    bk[u] = i < c1 ? ml_classify<LOGB>(spl, k[u]) : -1;
+    const unsigned peers = warp_peers<LOGB + 1>(bk[u]);
+    if (bk[u] >= 0 && lane == __ffs(peers) - 1) row[bk[u]] += __popc(peers);
+    __syncwarp();
+  }
+}
+
+template <int LOGB>
+__device__ __noinline__ void ml_count_body(const int32_t* __restrict__ X, const MlSeg& sg,
+                                              const int32_t* spl, uint32_t (*wh)[2 * kMlMaxB],
+                                              uint32_t* __restrict__ counts) {
+  const int NB = 2 * sg.B - 1;
+  const int warp = threadIdx.x >> 5;
+  const int64_t c0 = sg.start + (blockIdx.x - sg.chunk0) * (int64_t)kMlChunk;
+  const int64_t c1 = min(sg.start + sg.len, c0 + kMlChunk);
+  int32_t k[kMlPer];
+  int bk[kMlPer];
+#pragma unroll
+  for (int u = 0; u < kMlPer; ++u) {
+    const int64_t i = c0 + u * kMlNT + threadIdx.x;
+    k[u] = i < c1 ? __ldg(X + i) : 0;
+  }
+  ml_warp_hist<LOGB>(spl, k, bk, c0, c1, wh[warp]);
+  __syncthreads();
+  for (int b = threadIdx.x; b < NB; b += kMlNT) {
+    uint32_t t = 0;
+#pragma unroll
+    for (int w = 0; w < kMlWarps; ++w) t += wh[w][b];
+    if (t) atomicAdd(&counts[sg.cnt_off + b], t);
+  }
+}
+
+#define NSB_LOGB_DISPATCH(B, CALL)        \
+  switch (B) {                            \
+    case 2: CALL(1); break;               \
+    case 4: CALL(2); break;               \
+    case 8: CALL(3); break;               \
+    case 16: CALL(4); break;              \
+    case 32: CALL(5); break;              \
+    case 64: CALL(6); break;              \
+    case 128: CALL(7); break;             \
+    default: CALL(8); break;              \
+  }
+
+__global__ void __launch_bounds__(kMlNT)
+    ml_count_kernel(const int32_t* __restrict__ X, const MlSeg* __restrict__ segs, int nseg,
+                    const int32_t* __restrict__ gspl, uint32_t* __restrict__ counts) {
+  __shared__ int32_t spl[kMlMaxB];
+  __shared__ uint32_t wh[kMlWarps][2 * kMlMaxB];
+  const MlSeg sg = segs[seg_of_chunk(segs, nseg, blockIdx.x)];
+  for (int i = threadIdx.x; i < sg.B; i += kMlNT) spl[i] = gspl[sg.spl_off + i];
+  for (int i = threadIdx.x; i < kMlWarps * 2 * kMlMaxB; i += kMlNT) (&wh[0][0])[i] = 0;
+  __syncthreads();
+#define NSB_COUNT_CALL(L) ml_count_body<L>(X, sg, spl, wh, counts)
+  NSB_LOGB_DISPATCH(sg.B, NSB_COUNT_CALL)
+#undef NSB_COUNT_CALL
+}
+
+template <int LOGB>
+__device__ __noinline__ void ml_scatter_body(const int32_t* __restrict__ X, const MlSeg& sg,
+                                                const int32_t* spl,
+                                                uint32_t (*wh)[2 * kMlMaxB],
+                                                unsigned long long* __restrict__ fill,
+                                                int32_t* __restrict__ Y) {
+  const int NB = 2 * sg.B - 1;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t c0 = sg.start + (blockIdx.x - sg.chunk0) * (int64_t)kMlChunk;
+  const int64_t c1 = min(sg.start + sg.len, c0 + kMlChunk);
+  int32_t k[kMlPer];
+  int bk[kMlPer];
+#pragma unroll
+  for (int u = 0; u < kMlPer; ++u) {
+    const int64_t i = c0 + u * kMlNT + threadIdx.x;
+    k[u] = i < c1 ? __ldcs(X + i) : 0;
+  }
+  ml_warp_hist<LOGB>(spl, k, bk, c0, c1, wh[warp]);
+  __syncthreads();
+  // one global reservation per (CTA, bucket); warps get consecutive sub-ranges
+  for (int b = threadIdx.x; b < NB; b += kMlNT) {
+    uint32_t t = 0;
+#pragma unroll
+    for (int w = 0; w < kMlWarps; ++w) t += wh[w][b];
+    if (t) {
+      uint32_t pos = (uint32_t)(atomicAdd(&fill[sg.cnt_off + b], (unsigned long long)t) -
+                                (unsigned long long)sg.start);
+#pragma unroll
+      for (int w = 0; w < kMlWarps; ++w) {
+        const uint32_t c = wh[w][b];
+        wh[w][b] = pos;
+        pos += c;
+      }
+    }
+  }
+  __syncthreads();
+  uint32_t* row = wh[warp];
+  int32_t* Ys = Y + sg.start;
+#pragma unroll
+  for (int u = 0; u < kMlPer; ++u) {
+    const int b = bk[u];
+    const unsigned peers = warp_peers<LOGB + 1>(b);
+    const int leader = __ffs(peers) - 1;
+    uint32_t base = 0;
+    if (b >= 0 && lane == leader) {
+      base = row[b];
+      row[b] = base + __popc(peers);
+    }
+    base = __shfl_sync(kFull, base, leader);
+    if (b >= 0) Ys[base + __popc(peers & ((1u << lane) - 1))] = k[u];
+    __syncwarp();
+  }
+}
+
+__global__ void __launch_bounds__(kMlNT)
+    ml_scatter_kernel(const int32_t* __restrict__ X, const MlSeg* __restrict__ segs, int nseg,
+                      const int32_t* __restrict__ gspl, unsigned long long* __restrict__ fill,
+                      int32_t* __restrict__ Y) {
+  __shared__ int32_t spl[kMlMaxB];
+  __shared__ uint32_t wh[kMlWarps][2 * kMlMaxB];  // counts, then cursors (rel. to seg start)
+  const MlSeg sg = segs[seg_of_chunk(segs, nseg, blockIdx.x)];
+  for (int i = threadIdx.x; i < sg.B; i += kMlNT) spl[i] = gspl[sg.spl_off + i];
+  for (int i = threadIdx.x; i < kMlWarps * 2 * kMlMaxB; i += kMlNT) (&wh[0][0])[i] = 0;
+  __syncthreads();
+#define NSB_SCATTER_CALL(L) ml_scatter_body<L>(X, sg, spl, wh, fill, Y)
+  NSB_LOGB_DISPATCH(sg.B, NSB_SCATTER_CALL)
+#undef NSB_SCATTER_CALL
+}
+
+// Copies jobs (start, len) from src to dst (constant "equal" buckets).
+__global__ void copy_jobs_kernel(const int32_t* __restrict__ src, int32_t* __restrict__ dst,
+                                 const int64_t* __restrict__ jobs) {
+  const int64_t st = jobs[2 * blockIdx.x], len = jobs[2 * blockIdx.x + 1];
+  for (int64_t i = threadIdx.x; i < len; i += blockDim.x) dst[st + i] = src[st + i];
+}
+
+static int ml_quick_sort(int32_t* keys, int32_t* tmp, size_t n, int leaf, const MlAux& ax,
+                         cudaStream_t s) {
+  std::vector<std::pair<int64_t, int64_t>> cur{{0, (int64_t)n}};
+  int32_t* X = keys;
+  int32_t* Y = tmp;
+  std::vector<MlSeg> segs;
+  std::vector<uint32_t> counts;
+  std::vector<unsigned long long> fill;
+  while (!cur.empty()) {
+    // ---- plan the level
+    segs.clear();
+    int spl = 0, cnt = 0;
+    int64_t chunks = 0, smp = 0;
+    for (auto [st, len] : cur) {
+      MlSeg g{};
+      g.start = st;
+      g.len = len;
+      int B = 2;
+      while (B < kMlMaxB && (int64_t)B * kQsTarget < len) B *= 2;
+      g.B = B;
+      g.spl_off = spl;
+      g.cnt_off = cnt;
+      g.chunk0 = chunks;
+      g.smp_off = smp;
+      spl += B;
+      cnt += 2 * B - 1;
+      chunks += (len + kMlChunk - 1) / kMlChunk;
+      smp += kQsOversample * B;
+      segs.push_back(g);
+    }
+    const int nseg = (int)segs.size();
+    if ((size_t)nseg > ax.max_segs || (size_t)spl > ax.max_spl || (size_t)cnt > ax.max_cnt ||
+        (size_t)smp > ax.max_samples)
+      return NS_ERR_TEMP;
+    NSB_TRY(check_cuda(cudaMemcpyAsync(ax.segs, segs.data(), nseg * sizeof(MlSeg),
+                                       cudaMemcpyHostToDevice, s),
+                       "H2D(segs)"));
+    // ---- splitters: sample, sort each segment's samples on chip, pick
+    {
+      Prof prof(PK_QS_SAMPLE, s);
+      ml_sample_kernel<<<(unsigned)((smp + 255) / 256), 256, 0, s>>>(X, ax.segs, nseg, smp,
+                                                                       ax.samples);
+    }
+    NSB_TRY(check_launch("ml_sample_kernel"));
+    std::vector<int64_t> sjobs;
+    for (const auto& g : segs) {
+      sjobs.push_back(g.smp_off);
+      sjobs.push_back(kQsOversample * g.B);
+    }
+    NSB_TRY(check_cuda(cudaMemcpyAsync(ax.jobs, sjobs.data(), sjobs.size() * 8,
+                                       cudaMemcpyHostToDevice, s),
+                       "H2D(sample jobs)"));
+    NSB_TRY((launch_bucket_sort<256, 16, 8>(ax.samples, ax.samples, ax.jobs, nseg, s)));
+    {
+      Prof prof(PK_QS_SAMPLE, s);
+      ml_splitter_kernel<<<nseg, 256, 0, s>>>(ax.samples, ax.segs, nseg, ax.spl);
+    }
+    NSB_TRY(check_launch("ml_splitter_kernel"));
+    // ---- count
+    NSB_TRY(check_cuda(cudaMemsetAsync(ax.counts, 0, cnt * 4, s), "memset"));
+    {
+      Prof prof(PK_QS_COUNT, s);
+      ml_count_kernel<<<(unsigned)chunks, kMlNT, 0, s>>>(X, ax.segs, nseg, ax.spl, ax.counts);
+    }
+    NSB_TRY(check_launch("ml_count_kernel"));
+    // One device->host read per LEVEL: bucket sizes drive the plan, as the
+    // split point drives quick_sort_rec (hybrid.hpp:145-148).
+    counts.resize(cnt);
+    NSB_TRY(check_cuda(cudaMemcpyAsync(counts.data(), ax.counts, cnt * 4, cudaMemcpyDeviceToHost,
+                                       s),
+                       "D2H(counts)"));
+    NSB_TRY(check_cuda(cudaStreamSynchronize(s), "cudaStreamSynchronize"));
+    // ---- plan buckets: fill positions, jobs, next level
+    fill.resize(cnt);
+    std::vector<int64_t> cls[4], copies;
+    std::vector<std::pair<int64_t, int64_t>> next;
+    for (const auto& g : segs) {
+      int64_t acc = g.start;
+      const int NB = 2 * g.B - 1;
+      for (int b = 0; b < NB; ++b) {
+        const int64_t len = counts[g.cnt_off + b];
+        fill[g.cnt_off + b] = (unsigned long long)acc;
+        if (len > 0) {
+          if (b & 1) {  // constant bucket: already sorted
+            if (Y != keys) {
+              copies.push_back(acc);
+              copies.push_back(len);
+            }
+          } else if (len <= kSmallTile) {
+            const int c = len <= 2048 ? 0 : len <= 4096 ? 1 : len <= 8192 ? 2 : 3;
+            cls[c].push_back(acc);
+            cls[c].push_back(len);
+          } else {
+            next.push_back({acc, len});
+          }
+        }
+        acc += len;
+      }
+      if (acc != g.start + g.len) return NS_ERR_CUDA;  // lost keys: a device fault
+    }
+    NSB_TRY(check_cuda(cudaMemcpyAsync(ax.fill, fill.data(), cnt * 8, cudaMemcpyHostToDevice, s),
+                       "H2D(fill)"));
+    {
+      Prof prof(PK_QS_SCATTER, s);
+      ml_scatter_kernel<<<(unsigned)chunks, kMlNT, 0, s>>>(X, ax.segs, nseg, ax.spl, ax.fill, Y);
+    }
+    NSB_TRY(check_launch("ml_scatter_kernel"));
+    // ---- leaf buckets -> key buffer
+    std::vector<int64_t> jobs;
+    int off[6] = {0, 0, 0, 0, 0, 0};
+    for (int c = 0; c < 4; ++c) {
+      off[c] = (int)(jobs.size() / 2);
+      jobs.insert(jobs.end(), cls[c].begin(), cls[c].end());
+    }
+    off[4] = (int)(jobs.size() / 2);
+    jobs.insert(jobs.end(), copies.begin(), copies.end());
+    off[5] = (int)(jobs.size() / 2);
+    if ((size_t)off[5] > ax.max_jobs) return NS_ERR_TEMP;
+    if (!jobs.empty())
+      NSB_TRY(check_cuda(cudaMemcpyAsync(ax.jobs, jobs.data(), jobs.size() * 8,
+                                         cudaMemcpyHostToDevice, s),
+                         "H2D(jobs)"));
+    NSB_TRY(with_leaf(leaf, [&](auto L) {
+      constexpr int LF = decltype(L)::value;
+      NSB_TRY((launch_bucket_sort<128, 16, LF>(Y, keys, ax.jobs + 2 * off[0], off[1] - off[0], s)));
+      NSB_TRY((launch_bucket_sort<256, 16, LF>(Y, keys, ax.jobs + 2 * off[1], off[2] - off[1], s)));
+      NSB_TRY((launch_bucket_sort<512, 16, LF>(Y, keys, ax.jobs + 2 * off[2], off[3] - off[2], s)));
+      return launch_bucket_sort<1024, 16, LF>(Y, keys, ax.jobs + 2 * off[3], off[4] - off[3], s);
+    }));
+    if (off[5] > off[4]) {
+      copy_jobs_kernel<<<off[5] - off[4], 256, 0, s>>>(Y, keys, ax.jobs + 2 * off[4]);
+      NSB_TRY(check_launch("copy_jobs_kernel"));
+    }
+    // the jobs/fill/segs buffers are rewritten by the next level: the stream
+    // orders that after this level's kernels; the host vectors are copied
+    // by value into pageable H2D copies (staged before cudaMemcpyAsync returns)
+    cur.swap(next);
+    std::swap(X, Y);
+  }
+  return NS_OK;
+}
+
 size_t quick_sort_temp(size_t n) {
   if (n <= (size_t)kSmallTile) return 0;
-  return align_up(n * 4, 256) + qs_aux_bytes();
+  return align_up(n * 4, 256) + std::max(qs_aux_bytes(), ml_aux_bytes(n));
 }
 
 }  // namespace nsb
@@ -425,8 +849,18 @@ int ns_quick_sort_i32(int32_t* d_keys, size_t n, uint32_t width_mask, int varsor
   if (n <= (size_t)kSmallTile) return small_sort(d_keys, n, leaf, s);
   if (!d_temp || temp_bytes < quick_sort_temp(n)) return NS_ERR_TEMP;
   int32_t* tmp = static_cast<int32_t*>(d_temp);
-  const QsAux aux = carve_aux(static_cast<char*>(d_temp) + align_up(n * 4, 256));
-  return quick_sort_level(d_keys, tmp, n, leaf, aux, s);
+  char* auxp = static_cast<char*>(d_temp) + align_up(n * 4, 256);
+  // Single level (up to 4096 splitters, measured faster while its buckets
+  // fit one CTA) up to 2^25 keys; the multi-level partition above that,
+  // where a single level would leave thousands of oversized buckets.
+  // NSB_QS=1 / 2 forces one or the other.
+  static const int mode = [] {
+    const char* e = getenv("NSB_QS");
+    return e ? atoi(e) : 0;
+  }();
+  const bool single = mode == 1 || (mode == 0 && n <= (size_t(1) << 25));
+  if (single) return quick_sort_level(d_keys, tmp, n, leaf, carve_aux(auxp), s);
+  return ml_quick_sort(d_keys, tmp, n, leaf, carve_ml(auxp, n), s);
 }
 
 }  // extern "C"
