@@ -320,3 +320,51 @@ def test_p2p_sample_sort_processes_one_gpu(ns, cuda, world, n, dist_kind):
                           str(world), str(n), dist_kind], cwd=root, capture_output=True,
                          text=True, timeout=600)
     assert "P2P_OK" in out.stdout, (out.stdout[-1500:], out.stderr[-3000:])
+
+
+@pytest.mark.slow
+def test_full_batch_matches_reference_digest(ns, cuda, oracle, golden):
+    """BASELINE config 2 at full size: 2^24 ragged arrays, digest of the
+    reference's own output (tests/golden/golden.json)."""
+    import torch
+    b = golden["batch"]
+    offs, keys = oracle.generate_batch_i32(b["num_arrays"], b["seed"])
+    assert sha(offs) == b["offsets_sha256"] and sha(keys) == b["input_sha256"]
+    k = to_dev(keys, cuda)
+    ns.sort_small_batch(k, torch.from_numpy(offs.view(np.int32)).to(cuda))
+    assert sha(from_dev(k)) == b["output_sha256"]
+
+
+@pytest.mark.slow
+def test_full_segmented_batch(ns, cuda, oracle, golden):
+    """BASELINE config 4's segmented batch at full size (65,536 x 16,384):
+    the reference digest of the first 1,024 segments plus sortedness of every
+    segment and the multiset of the whole batch."""
+    import torch
+    g = golden["segmented"]
+    seg, nseg = g["seg_len"], g["full_num_segments"]
+    n = seg * nseg
+    t = torch.empty(n, dtype=torch.int32, device=cuda)
+    from paper_2503_05934_b200._lib import check
+    check(ns.lib().ns_generate_i32(t.data_ptr(), n, 0, g["seed"],
+                                   torch.cuda.current_stream().cuda_stream), "gen")
+    d0 = ns.multiset_digest(t)
+    ns.segmented_sort(t, seg, ns.find_config(g["config"]), ns.Algorithm.quick_sort)
+    prefix = from_dev(t[: g["num_segments_checked"] * seg])
+    assert sha(prefix) == g["output_prefix_sha256"]
+    v = t.view(nseg, seg)
+    assert bool((v[:, 1:] >= v[:, :-1]).all())
+    assert ns.multiset_digest(t) == d0
+
+
+@pytest.mark.slow
+def test_p2p_sample_sort_large(ns, cuda):
+    """Config 5's exchange at scale: 2^27 keys over 2 processes (p2p pull-merge)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(root, "tests", "multiproc_p2p_gpu.py"),
+                          "2", str(1 << 27), "random"], cwd=root, capture_output=True,
+                         text=True, timeout=900)
+    assert "P2P_OK" in out.stdout, (out.stdout[-1500:], out.stderr[-3000:])
