@@ -260,105 +260,6 @@ __device__ __forceinline__ void cta_sort(const int32_t* in, int32_t* out, int va
   tile_store<NT, T>(sm, out, valid);
 }
 
-// ---------------------------------------------------------------------------
-// Tile sort v3: same register phase (networks + warp bitonic -> 32K-key runs
-// per warp), then shared-memory merge levels on sentinel-terminated runs
-// (smem_merge.cuh): no padding words and no bounds tests above level 0.
-//   buffer P (padded, padded_words(T)): tile load, level-0 input
-//   buffer Q (unpadded, T + T/512 + 8): level-0 output; then P and Q
-//   alternate as unpadded ping-pong buffers.
-// ---------------------------------------------------------------------------
-__host__ __device__ constexpr int cta_sort_q_words(int T) { return T + T / 256 + 8; }
-__host__ __device__ constexpr int cta_sort_smem_bytes(int T) {
-  return (padded_words(T) + cta_sort_q_words(T)) * 4;
-}
-
-template <int NT, int T>
-__device__ __forceinline__ void tile_store_flat(const int32_t* sm, int32_t* out, int valid) {
-  const int tid = threadIdx.x;
-  if (valid == T && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
-    const int4* q = reinterpret_cast<const int4*>(sm);
-    int4* p = reinterpret_cast<int4*>(out);
-#pragma unroll
-    for (int i = 0; i < T / 4 / NT; ++i) __stcs(p + i * NT + tid, q[i * NT + tid]);
-  } else {
-    for (int i = tid; i < valid; i += NT) out[i] = sm[i];
-  }
-}
-
-// Debug/tuning knob (NSB_TS_STAGE): 0 full sort, 1 stop after the register
-// phase, 2 stop after the relayout, 3 load+store only.  Output is only a
-// sort for stage 0.
-__device__ int g_ts_stage = 0;
-__device__ int g_ts_kb = 1;
-
-template <int NT, int K, int LEAF>
-__device__ __forceinline__ void cta_sort_v3(const int32_t* in, int32_t* out, int valid,
-                                            int32_t* smem) {
-  constexpr int T = NT * K;
-  constexpr int R0 = 32 * K;  // run length after the warp bitonic stage
-  int32_t* P = smem;
-  int32_t* Q = smem + padded_words(T);
-  const int tid = threadIdx.x;
-  const int lane = tid & 31;
-
-  const int stage = g_ts_stage;
-  const int min_kb = g_ts_kb;
-  tile_load<NT, T>(in, valid, P);
-  __syncthreads();
-  if (stage == 3) {
-    tile_store<NT, T>(P, out, valid);
-    return;
-  }
-  int32_t v[K];
-  smem_to_regs<K>(P, v);
-  thread_sort<LEAF>(v);  // the network base case (try_base_case, hybrid.hpp:48-56)
-  if constexpr (NT >= 32) warp_bitonic<5>(v, lane);
-  if (stage == 1) {
-    __syncthreads();
-    regs_to_smem<K>(P, v);
-    __syncthreads();
-    tile_store<NT, T>(P, out, valid);
-    return;
-  }
-  if constexpr (T == R0) {
-    __syncthreads();
-    regs_to_smem<K>(P, v);
-    __syncthreads();
-    tile_store<NT, T>(P, out, valid);
-    return;
-  } else {
-    __syncthreads();
-    regs_to_smem<K>(P, v);
-    // relayout: padded R0-runs -> Q as sentinel-terminated runs at r*(R0+1)
-    // (coalesced, bank-conflict free on both sides)
-    __syncthreads();
-    for (int i = tid; i < T; i += NT) Q[i + i / R0] = P[pad_idx(i)];
-    if (tid < T / R0) Q[tid * (R0 + 1) + R0] = INT_MAX;
-    if (stage == 2) {
-      __syncthreads();
-      for (int i = tid; i < valid; i += NT) out[i] = Q[i + i / R0];
-      return;
-    }
-    // levels 1..: sentinel runs ping-pong Q <-> P (P reused unpadded)
-    int32_t* X = Q;
-    int32_t* Y = P;
-#pragma unroll 1
-    for (int R = R0; R < T; R *= 2) {
-      const bool last = 2 * R == T;
-      __syncthreads();
-      merge_level<NT>(X, RegularRuns{T / R, R, R + 1}, Y,
-                      RegularRuns{T / (2 * R), 2 * R, last ? 2 * R : 2 * R + 1}, T, !last,
-                      min_kb);
-      int32_t* t = X;
-      X = Y;
-      Y = t;
-    }
-    __syncthreads();
-    tile_store_flat<NT, T>(X, out, valid);
-  }
-}
-
 // CTA b sorts [b*stride, b*stride + min(stride, n - b*stride)), stride <= T
 // (stride == T for plain tiling, the segment length for segmented sorts).
 template <int NT, int K, int LEAF>
@@ -384,54 +285,6 @@ __device__ __forceinline__ PassGeom pass_geom(int64_t pos0, int64_t n, int64_t R
   g.b_len = max((int64_t)0, min(R, n - g.pair_base - R));
   g.diag0 = pos0 - g.pair_base;
   return g;
-}
-
-// One thread per output tile boundary: mp[c] = merge-path split at tile c.
-template <int TM>
-__global__ void merge_partition_kernel(const int32_t* __restrict__ src, int64_t n, int64_t R,
-                                       int64_t num_tiles, int64_t* __restrict__ mp) {
-  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= num_tiles) return;
-  const PassGeom g = pass_geom(c * TM, n, R);
-  const int32_t* A = src + g.pair_base;
-  const int32_t* B = A + g.a_len;
-  mp[c] = merge_path<int64_t>(A, g.a_len, B, g.b_len, g.diag0);
-}
-
-template <int NT, int K>
-__global__ void __launch_bounds__(NT)
-    merge_pass_kernel(const int32_t* __restrict__ src, int32_t* __restrict__ dst, int64_t n,
-                      int64_t R, const int64_t* __restrict__ mp) {
-  constexpr int TM = NT * K;
-  __shared__ __align__(16) int32_t sm[padded_words(TM)];
-  const int tid = threadIdx.x;
-  const int64_t c = blockIdx.x;
-  const PassGeom g = pass_geom(c * TM, n, R);
-  const int64_t pair_len = g.a_len + g.b_len;
-  const int64_t diag1 = min(g.diag0 + TM, pair_len);
-  const int64_t a0 = mp[c];
-  const int64_t a1 = (diag1 == pair_len) ? g.a_len : mp[c + 1];
-  const int la = (int)(a1 - a0);
-  const int lb = (int)((diag1 - a1) - (g.diag0 - a0));
-  const int32_t* A = src + g.pair_base + a0;
-  const int32_t* B = src + g.pair_base + g.a_len + (g.diag0 - a0);
-
-  // stage both input slices in padded smem: [A slice | B slice]
-  const int total = la + lb;
-  stage_slices<NT, TM>(src, src + n, A, la, B, lb, sm);
-  __syncthreads();
-
-  const int diag = min(tid * K, total);
-  const SmemRun SA{sm, 0}, SB{sm, la};
-  const int a = merge_path<int>(SA, la, SB, lb, diag);
-  int32_t v[K];
-  serial_merge<K>(SA, la, SB, lb, a, diag - a, v);
-
-  // restage the merged tile so the HBM stores are coalesced 128-bit writes
-  __syncthreads();
-  regs_to_smem<K>(sm, v);
-  __syncthreads();
-  tile_store<NT, TM>(sm, dst + c * TM, total);
 }
 
 }  // namespace nsb

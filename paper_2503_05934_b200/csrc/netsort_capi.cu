@@ -23,9 +23,6 @@ constexpr int kBsNT = 512, kBsK = 16, kBsT = kBsNT * kBsK;
 // Single-CTA sort for n <= 16384: 1024 threads x 16 keys (64 KiB smem).
 constexpr int kSmNT = 1024, kSmK = 16, kSmT = kSmNT * kSmK;
 static_assert(kSmT == kSmallTile, "small-tile size mismatch");
-// Merge pass: 512 threads x 16 outputs = 8192 keys per CTA.
-constexpr int kMgNT = 512, kMgK = 16, kMgT = kMgNT * kMgK;
-static_assert((2 * kBsT) % kMgT == 0, "merge tiles must not straddle run pairs");
 
 
 template <int NT, int K, int LEAF>
@@ -49,14 +46,11 @@ static int launch_blocksort(const int32_t* src, int32_t* dst, int64_t n, int str
 
 // Tuning knobs (read once; the defaults are the measured best on B200).
 //   NSB_TILE  = 8192 | 16384 : keys per tile-sort CTA
-//   NSB_MERGE = 16 | 32      : outputs per thread in the merge pass (CTA = 8192 keys)
-//   NSB_MERGE = 2 selects the TMA-staged pair-local merge pass (merge_pass_v2)
 constexpr int kV2NT = 256, kV2K = 31, kV2T = kV2NT * kV2K;  // 7936 keys per tile
 //   NSB_KWAY  = 0 | 4 | 8 : widest k-way merge pass (0 = pairwise only, default)
 //   NSB_KWAY_MIN = n below which only pairwise passes are used
 struct MergeTuning {
   int tile = kBsT;
-  int merge_k = 2;
   int kway = 0;  // measured: k-way passes are merge-compute bound, no faster
   int64_t kway_min = int64_t(1) << 22;
   int64_t fused_max_tiles = 4096;  // passes with fewer tiles search in-kernel (measured crossover)
@@ -65,7 +59,6 @@ struct MergeTuning {
     if (const char* e = getenv("NSB_V2")) v2 = atoi(e);
     if (const char* e = getenv("NSB_FUSED_MAX")) fused_max_tiles = atoll(e);
     if (const char* e = getenv("NSB_TILE")) tile = atoi(e) == 16384 ? 16384 : 8192;
-    if (const char* e = getenv("NSB_MERGE")) merge_k = atoi(e);
     if (const char* e = getenv("NSB_KWAY")) kway = atoi(e);
     if (const char* e = getenv("NSB_KWAY_MIN")) kway_min = atoll(e);
   }
@@ -73,20 +66,12 @@ struct MergeTuning {
 static const MergeTuning& tuning() {
   static const MergeTuning t = [] {
     MergeTuning m;
-    if (const char* e = getenv("NSB_TS_STAGE")) {
-      const int st = atoi(e);
-      cudaMemcpyToSymbol(g_ts_stage, &st, sizeof(int));
-    }
-    if (const char* e = getenv("NSB_TS_KB")) {
-      const int kb = atoi(e);
-      cudaMemcpyToSymbol(g_ts_kb, &kb, sizeof(int));
-    }
     return m;
   }();
   return t;
 }
 
-// Upper bound on merge tiles of any pass (v1: n/kMgT; v2: <= 4n/kV2T + n/16384 + 2).
+// Upper bound on merge-path splits of any pass (v2 tiles >= 3968 keys).
 static size_t max_merge_tiles(size_t n) { return n / 1024 + 64; }
 
 // k-way scratch: raw + 2 merged sample buffers (u64), their merge-path splits,
@@ -287,12 +272,12 @@ int merge_sort_device(int32_t* d_keys, size_t n, int leaf, void* d_temp, size_t 
   int npass = 0;
   for (int64_t runs = tiles; runs > 1;) {
     int k = 2;
-    if (tu.merge_k == 2 && tu.kway >= 4 && (int64_t)n >= tu.kway_min && runs >= 3)
+    if (tu.kway >= 4 && (int64_t)n >= tu.kway_min && runs >= 3)
       k = (tu.kway >= 8 && runs >= 5) ? 8 : 4;
     sched[npass++] = k;
     runs = (runs + k - 1) / k;
   }
-  const int passes = tu.merge_k == 2 ? npass : ceil_log2((uint64_t)tiles);
+  const int passes = npass;
   // Pick the tile-sort destination so the last pass lands in d_keys.
   int32_t* cur = (passes & 1) ? tmp : d_keys;
   int32_t* other = (cur == d_keys) ? tmp : d_keys;
@@ -301,7 +286,7 @@ int merge_sort_device(int32_t* d_keys, size_t n, int leaf, void* d_temp, size_t 
     return T == kSmT ? launch_blocksort<kSmNT, kSmK, LF>(d_keys, cur, (int64_t)n, T, tiles, s)
                      : launch_blocksort<kBsNT, kBsK, LF>(d_keys, cur, (int64_t)n, T, tiles, s);
   }));
-  if (tu.merge_k == 2) {
+  {
     const KwScratch ks = carve_kway(reinterpret_cast<char*>(mp) +
                                         align_up((max_merge_tiles(n) + 1) * 8, 256),
                                     n);
@@ -319,26 +304,6 @@ int merge_sort_device(int32_t* d_keys, size_t n, int leaf, void* d_temp, size_t 
       R *= 2;
     }
     return NS_OK;
-  }
-  const int64_t mtiles = (int64_t)((n + kMgT - 1) / kMgT);
-  for (int64_t R = T; R < (int64_t)n; R *= 2) {
-    {
-      Prof prof(PK_PARTITION, s);
-      merge_partition_kernel<kMgT><<<(unsigned)((mtiles + 255) / 256), 256, 0, s>>>(
-          cur, (int64_t)n, R, mtiles, mp);
-    }
-    NSB_TRY(check_launch("merge_partition_kernel"));
-    {
-      Prof prof(PK_MERGE_PASS, s);
-      if (tu.merge_k == 32)
-        merge_pass_kernel<kMgT / 32, 32><<<(unsigned)mtiles, kMgT / 32, 0, s>>>(
-            cur, other, (int64_t)n, R, mp);
-      else
-        merge_pass_kernel<kMgNT, kMgK><<<(unsigned)mtiles, kMgNT, 0, s>>>(cur, other,
-                                                                          (int64_t)n, R, mp);
-    }
-    NSB_TRY(check_launch("merge_pass_kernel"));
-    std::swap(cur, other);
   }
   return NS_OK;
 }

@@ -49,63 +49,6 @@ __global__ void bucket_bounds_kernel(const int32_t* __restrict__ sorted, int64_t
   bounds[k] = lo;
 }
 
-// ---- merge of explicit adjacent run pairs (uneven lengths) ---------------
-constexpr int kMaxPairs = 64;
-struct PairTable {
-  int npairs;
-  int64_t n;  // keys in the buffer (bounds every read)
-  int64_t a_base[kMaxPairs], a_len[kMaxPairs], b_len[kMaxPairs], tile0[kMaxPairs + 1];
-};
-
-__device__ __forceinline__ int pair_of(const PairTable& t, int64_t tile) {
-  int p = 0;
-  while (p + 1 < t.npairs && t.tile0[p + 1] <= tile) ++p;
-  return p;
-}
-
-template <int TM>
-__global__ void pairs_partition_kernel(const int32_t* __restrict__ src, PairTable t,
-                                       int64_t* __restrict__ mp) {
-  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= t.tile0[t.npairs]) return;
-  const int p = pair_of(t, c);
-  const int32_t* A = src + t.a_base[p];
-  const int64_t diag = (c - t.tile0[p]) * TM;
-  mp[c] = merge_path<int64_t>(A, t.a_len[p], A + t.a_len[p], t.b_len[p], diag);
-}
-
-template <int NT, int K>
-__global__ void __launch_bounds__(NT)
-    pairs_merge_kernel(const int32_t* __restrict__ src, int32_t* __restrict__ dst, PairTable t,
-                       const int64_t* __restrict__ mp) {
-  constexpr int TM = NT * K;
-  __shared__ __align__(16) int32_t sm[padded_words(TM)];
-  const int tid = threadIdx.x;
-  const int64_t c = blockIdx.x;
-  const int p = pair_of(t, c);
-  const int64_t pair_len = t.a_len[p] + t.b_len[p];
-  const int64_t diag0 = (c - t.tile0[p]) * TM;
-  const int64_t diag1 = min(diag0 + TM, pair_len);
-  const int64_t a0 = mp[c];
-  const int64_t a1 = (diag1 == pair_len) ? t.a_len[p] : mp[c + 1];
-  const int la = (int)(a1 - a0);
-  const int lb = (int)((diag1 - a1) - (diag0 - a0));
-  const int32_t* A = src + t.a_base[p] + a0;
-  const int32_t* B = src + t.a_base[p] + t.a_len[p] + (diag0 - a0);
-  const int total = la + lb;
-  stage_slices<NT, TM>(src, src + t.n, A, la, B, lb, sm);
-  __syncthreads();
-  const int diag = min(tid * K, total);
-  const SmemRun SA{sm, 0}, SB{sm, la};
-  const int a = merge_path<int>(SA, la, SB, lb, diag);
-  int32_t v[K];
-  serial_merge<K>(SA, la, SB, lb, a, diag - a, v);
-  __syncthreads();
-  regs_to_smem<K>(sm, v);
-  __syncthreads();
-  tile_store<NT, TM>(sm, dst + t.a_base[p] + diag0, total);
-}
-
 constexpr int kPmNT = 512, kPmK = 16, kPmT = kPmNT * kPmK;
 
 // ---- merge of pairs of runs given by POINTERS (possibly on peer GPUs) -----
@@ -117,6 +60,7 @@ constexpr int kPmNT = 512, kPmK = 16, kPmT = kPmNT * kPmK;
 constexpr int kMaxPtrPairs = 32;
 struct PtrPairTable {
   int npairs;
+  int contiguous;  // every B run directly follows its A run in one buffer
   const int32_t* a[kMaxPtrPairs];
   const int32_t* b[kMaxPtrPairs];
   int64_t a_len[kMaxPtrPairs], b_len[kMaxPtrPairs], out_off[kMaxPtrPairs];
@@ -157,8 +101,15 @@ __global__ void __launch_bounds__(NT)
   const int32_t* A = t.a[p] + a0;
   const int32_t* B = t.b[p] + (diag0 - a0);
   const int total = la + lb;
+  if (t.contiguous) {
+    // one allocation: 128-bit staging bounded by the pair's own extent
+    stage_slices<NT, TM>(t.a[p], t.b[p] + t.b_len[p], A, la, B, lb, sm);
+  } else {
+    // runs in different (possibly peer) allocations: scalar coalesced loads
 #pragma unroll 8
-  for (int i = tid; i < total; i += NT) sm[pad_idx(i)] = i < la ? __ldcs(A + i) : __ldcs(B + (i - la));
+    for (int i = tid; i < total; i += NT)
+      sm[pad_idx(i)] = i < la ? __ldcs(A + i) : __ldcs(B + (i - la));
+  }
   __syncthreads();
   const int diag = min(tid * K, total);
   const SmemRun SA{sm, 0}, SB{sm, la};
@@ -261,12 +212,12 @@ int ns_merge_pairs_i32(const int32_t* const* a_ptrs, const int64_t* a_lens,
 
 size_t ns_merge_runs_temp_bytes(size_t n, int num_runs) {
   if (num_runs <= 1) return 0;
-  return align_up(n * 4, 256) + align_up((n / kPmT + 2 * kMaxPairs + 2) * 8, 256);
+  return align_up(n * 4, 256) + align_up((n / kPmT + 2 * kMaxPtrPairs + 2) * 8, 256);
 }
 
 int ns_merge_runs_i32(int32_t* d_keys, const int64_t* h_run_offsets, int num_runs, void* d_temp,
                       size_t temp_bytes, void* stream) {
-  if (num_runs < 1 || num_runs > 2 * kMaxPairs || !h_run_offsets) return NS_ERR_INVALID;
+  if (num_runs < 1 || num_runs > 2 * kMaxPtrPairs || !h_run_offsets) return NS_ERR_INVALID;
   const int64_t n = h_run_offsets[num_runs] - h_run_offsets[0];
   if (num_runs == 1 || n <= 1) return NS_OK;
   for (int r = 0; r < num_runs; ++r)
@@ -292,33 +243,20 @@ int ns_merge_runs_i32(int32_t* d_keys, const int64_t* h_run_offsets, int num_run
   }
   while (runs.size() > 2) {
     const int nr = (int)runs.size() - 1;
-    PairTable t{};
+    PtrPairTable t{};
     t.npairs = (nr + 1) / 2;
-    t.n = n;
-    int64_t tiles = 0;
+    t.contiguous = 1;
     std::vector<int64_t> next{0};
     for (int p = 0; p < t.npairs; ++p) {
       const int ra = 2 * p, rb = 2 * p + 1;
-      t.a_base[p] = runs[ra];
+      t.a[p] = cur + runs[ra];
       t.a_len[p] = runs[ra + 1] - runs[ra];
+      t.b[p] = cur + runs[ra + 1];
       t.b_len[p] = rb < nr ? runs[rb + 1] - runs[rb] : 0;
-      t.tile0[p] = tiles;
-      tiles += (t.a_len[p] + t.b_len[p] + kPmT - 1) / kPmT;
+      t.out_off[p] = runs[ra];
       next.push_back(runs[std::min(rb + 1, nr)]);
     }
-    t.tile0[t.npairs] = tiles;
-    if (tiles > 0) {
-      {
-        Prof prof(PK_PARTITION, s);
-        pairs_partition_kernel<kPmT><<<(unsigned)((tiles + 255) / 256), 256, 0, s>>>(cur, t, mp);
-      }
-      NSB_TRY(check_launch("pairs_partition_kernel"));
-      {
-        Prof prof(PK_MERGE_PASS, s);
-        pairs_merge_kernel<kPmNT, kPmK><<<(unsigned)tiles, kPmNT, 0, s>>>(cur, other, t, mp);
-      }
-      NSB_TRY(check_launch("pairs_merge_kernel"));
-    }
+    NSB_TRY(merge_ptr_pairs(t, other, mp, s));
     std::swap(cur, other);
     runs.swap(next);
   }
