@@ -62,6 +62,11 @@ inline int check_cuda(cudaError_t e, const char* where) {
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
+// Opt a kernel into `bytes` of dynamic shared memory on the CURRENT device,
+// once per (device, kernel): the attribute is per device, so a process that
+// drives several GPUs must set it on each.
+int ensure_smem_attr(const void* kern, int bytes, const char* what);
+
 inline int ceil_log2(uint64_t x) {
   int p = 0;
   while ((uint64_t(1) << p) < x) ++p;

@@ -30,13 +30,8 @@ static int launch_blocksort(const int32_t* src, int32_t* dst, int64_t n, int str
                             int64_t ctas, cudaStream_t s) {
   constexpr int smem = padded_words(NT * K) * 4;
   auto* kern = blocksort_kernel<NT, K, LEAF>;
-  static bool attr_set = false;  // benign race: idempotent attribute write
-  if (!attr_set) {
-    NSB_TRY(check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            smem),
-                       "cudaFuncSetAttribute(blocksort)"));
-    attr_set = true;
-  }
+  NSB_TRY(ensure_smem_attr(reinterpret_cast<const void*>(kern), smem,
+                           "cudaFuncSetAttribute(blocksort)"));
   {
     Prof prof(PK_TILE_SORT, s);
     kern<<<(unsigned)ctas, NT, smem, s>>>(src, dst, n, stride);
@@ -114,13 +109,8 @@ static int launch_kway_merge(const int32_t* src, int32_t* dst, const KwPlan& P,
                              const int32_t* cuts, cudaStream_t s) {
   constexpr int smem = 2 * kway_buf_words(K) * 4;
   auto* kern = kway_merge_kernel<K>;
-  static bool attr = false;
-  if (!attr) {
-    NSB_TRY(check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            smem),
-                       "cudaFuncSetAttribute(kway)"));
-    attr = true;
-  }
+  NSB_TRY(ensure_smem_attr(reinterpret_cast<const void*>(kern), smem,
+                           "cudaFuncSetAttribute(kway)"));
   {
     Prof prof(PK_MERGE_PASS, s);
     kern<<<(unsigned)P.tiles, kKwNT, smem, s>>>(src, dst, P, cuts);

@@ -36,6 +36,20 @@ void set_last_error(const char* where, cudaError_t e) {
 
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
+int ensure_smem_attr(const void* kern, int bytes, const char* what) {
+  static std::mutex mu;
+  static std::vector<std::pair<int, const void*>> done;
+  int dev = 0;
+  NSB_TRY(check_cuda(cudaGetDevice(&dev), "cudaGetDevice"));
+  std::lock_guard<std::mutex> lk(mu);
+  for (const auto& d : done)
+    if (d.first == dev && d.second == kern) return NS_OK;
+  NSB_TRY(check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes),
+                     what));
+  done.emplace_back(dev, kern);
+  return NS_OK;
+}
+
 Prof::Prof(int k, cudaStream_t s) : kind(k), stream(s) {
   if (!g_prof_on.load(std::memory_order_relaxed)) return;
   if (cudaEventCreate(&begin) != cudaSuccess) {

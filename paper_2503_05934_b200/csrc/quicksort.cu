@@ -267,13 +267,8 @@ static int launch_bucket_sort(const int32_t* src, int32_t* dst, const int64_t* j
   if (njobs == 0) return NS_OK;
   constexpr int smem = padded_words(NT * K) * 4;
   auto* kern = bucket_sort_kernel<NT, K, LEAF>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    NSB_TRY(check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            smem),
-                       "cudaFuncSetAttribute(bucket_sort)"));
-    attr_set = true;
-  }
+  NSB_TRY(ensure_smem_attr(reinterpret_cast<const void*>(kern), smem,
+                           "cudaFuncSetAttribute(bucket_sort)"));
   {
     Prof prof(PK_QS_BUCKET, s);
     kern<<<njobs, NT, smem, s>>>(src, dst, jobs);
@@ -317,18 +312,11 @@ static int quick_sort_level(int32_t* keys, int32_t* tmp, size_t n, int leaf, con
   const int64_t ctas = (int64_t)((n + kQsChunk - 1) / kQsChunk);
   const int count_smem = (kQsClassifierWords + NB) * 4;
   const int scatter_smem = ((kQsClassifierWords + 3) & ~1) * 4 + NB * 8;
-  static bool attr_set = false;
-  if (!attr_set) {
-    NSB_TRY(check_cuda(cudaFuncSetAttribute(count_kernel,
-                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            (kQsClassifierWords + 2 * kQsMaxB) * 4),
-                       "cudaFuncSetAttribute(count)"));
-    NSB_TRY(check_cuda(cudaFuncSetAttribute(scatter_kernel,
-                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            ((kQsClassifierWords + 3) & ~1) * 4 + 2 * kQsMaxB * 8),
-                       "cudaFuncSetAttribute(scatter)"));
-    attr_set = true;
-  }
+  NSB_TRY(ensure_smem_attr(reinterpret_cast<const void*>(count_kernel),
+                           (kQsClassifierWords + 2 * kQsMaxB) * 4, "cudaFuncSetAttribute(count)"));
+  NSB_TRY(ensure_smem_attr(reinterpret_cast<const void*>(scatter_kernel),
+                           ((kQsClassifierWords + 3) & ~1) * 4 + 2 * kQsMaxB * 8,
+                           "cudaFuncSetAttribute(scatter)"));
   {
     Prof prof(PK_QS_COUNT, s);
     count_kernel<<<(unsigned)ctas, kQsNT, count_smem, s>>>(keys, (int64_t)n, aux.splitters,
