@@ -12,7 +12,8 @@
  * ctypes / cgo / JNI binding would call them directly.
  *
  * Conventions
- *   - keys are int32_t, sorted ascending, in place;
+ *   - keys are int32_t (the BASELINE configs; *_i32) or int64_t (the
+ *     reference's own benchmark type; *_i64), sorted ascending, in place;
  *   - ranges are half-open (ptr, n); the C++ layer converts the reference's
  *     inclusive [left, right] and keeps its "right < left is a no-op" rule
  *     (hybrid.hpp:160, 201);
@@ -79,6 +80,12 @@ int ns_network_comparators(int width, uint8_t* pairs, int cap);
 size_t ns_merge_sort_temp_bytes(size_t n);
 int ns_merge_sort_i32(int32_t* d_keys, size_t n, uint32_t width_mask, int varsort_max,
                       void* d_temp, size_t temp_bytes, void* stream);
+/* The same for int64 keys, the type the reference's own benchmarks and
+ * generator use (optimized_merge_sort<std::int64_t>, bench.hpp:59-61,
+ * datagen.hpp:47). */
+size_t ns_merge_sort_temp_bytes_i64(size_t n);
+int ns_merge_sort_i64(int64_t* d_keys, size_t n, uint32_t width_mask, int varsort_max,
+                      void* d_temp, size_t temp_bytes, void* stream);
 
 /* optimized_quick_sort — include/netsort/hybrid.hpp:197-216.  GPU form: a
  * sampled-splitter partition (the many-pivot analogue of median_of_three +
@@ -88,6 +95,11 @@ int ns_merge_sort_i32(int32_t* d_keys, size_t n, uint32_t width_mask, int varsor
  * launch plan, as the partition split drives the reference recursion). */
 size_t ns_quick_sort_temp_bytes(size_t n);
 int ns_quick_sort_i32(int32_t* d_keys, size_t n, uint32_t width_mask, int varsort_max,
+                      void* d_temp, size_t temp_bytes, void* stream);
+/* int64 keys (optimized_quick_sort<std::int64_t>): always the multi-level
+ * splitter partition. */
+size_t ns_quick_sort_temp_bytes_i64(size_t n);
+int ns_quick_sort_i64(int64_t* d_keys, size_t n, uint32_t width_mask, int varsort_max,
                       void* d_temp, size_t temp_bytes, void* stream);
 
 /* Base-case batch (BASELINE config 2; no reference batch API — the
@@ -159,6 +171,11 @@ int ns_multiset_digest_i32(const int32_t* d_keys, size_t n, uint64_t* d_out, voi
 /* d_out[0] += number of i with d_keys[i] > d_keys[i+1] (0 == sorted). */
 int ns_count_inversions_i32(const int32_t* d_keys, size_t n, unsigned long long* d_out,
                             void* stream);
+/* int64 forms of the two checking helpers (the digest mixes all 64 bits;
+ * matches oracle_multiset_digest_i64). */
+int ns_multiset_digest_i64(const int64_t* d_keys, size_t n, uint64_t* d_out, void* stream);
+int ns_count_inversions_i64(const int64_t* d_keys, size_t n, unsigned long long* d_out,
+                            void* stream);
 
 /* Device generator for the seeded inputs (bench/tests): kind 0 = uniform
  * random int32 in [0, 2^31) = int32(SplitMix64(seed).next() >> 33) element by
@@ -184,6 +201,8 @@ int ns_profile_read(int kind, double* total_ms, uint64_t* launches);
  * synchronises.  Device buffers are cached per thread (ns_release_cache). */
 int ns_merge_sort_host_i32(int32_t* h_keys, size_t n, uint32_t width_mask, int varsort_max);
 int ns_quick_sort_host_i32(int32_t* h_keys, size_t n, uint32_t width_mask, int varsort_max);
+int ns_merge_sort_host_i64(int64_t* h_keys, size_t n, uint32_t width_mask, int varsort_max);
+int ns_quick_sort_host_i64(int64_t* h_keys, size_t n, uint32_t width_mask, int varsort_max);
 int ns_release_cache(void);
 
 #ifdef __cplusplus

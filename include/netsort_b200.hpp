@@ -1,7 +1,7 @@
 // netsort_b200.hpp — C++20 host API with the reference's entry points.
 //
 // Mirrors /root/reference/proj/include/netsort/{config,hybrid}.hpp for int32
-// keys so that a user of the reference can switch by changing the namespace:
+// and int64 keys so that a user of the reference can switch by changing the namespace:
 //   NetworkConfig, base_case_applies      config.hpp:20-36
 //   config_registry, find_config, ...     src/config.cpp:11-70
 //   optimized_merge_sort (3 overloads)    hybrid.hpp:156-177
@@ -73,43 +73,60 @@ inline void check(int status, const char* what) {
 }  // namespace detail
 
 // ---- host spans (the reference's own call shape) --------------------------
+// Overloads for int32 (the BASELINE configs) and int64 (the reference's own
+// benchmark type: measure_loop's sort_fn takes std::span<std::int64_t>,
+// bench.hpp:58-61, so run_variant below binds to it directly).
 
-inline void optimized_merge_sort(std::span<std::int32_t> a, std::ptrdiff_t left,
-                                 std::ptrdiff_t right, const NetworkConfig& cfg) {
-  if (right < left) return;  // hybrid.hpp:160
-  if (left < 0 || right >= static_cast<std::ptrdiff_t>(a.size()))
-    throw std::invalid_argument("optimized_merge_sort: range outside the span");
-  detail::check(ns_merge_sort_host_i32(a.data() + left, static_cast<size_t>(right - left + 1),
-                                       cfg.width_mask, cfg.varsort_max),
-                "optimized_merge_sort");
+namespace detail {
+inline int host_sort(std::int32_t* p, size_t n, const NetworkConfig& c, Algorithm a) {
+  return a == Algorithm::merge_sort ? ns_merge_sort_host_i32(p, n, c.width_mask, c.varsort_max)
+                                    : ns_quick_sort_host_i32(p, n, c.width_mask, c.varsort_max);
 }
-inline void optimized_merge_sort(std::span<std::int32_t> a, const NetworkConfig& cfg) {
-  optimized_merge_sort(a, 0, static_cast<std::ptrdiff_t>(a.size()) - 1, cfg);
+inline int host_sort(std::int64_t* p, size_t n, const NetworkConfig& c, Algorithm a) {
+  return a == Algorithm::merge_sort ? ns_merge_sort_host_i64(p, n, c.width_mask, c.varsort_max)
+                                    : ns_quick_sort_host_i64(p, n, c.width_mask, c.varsort_max);
 }
-inline void classical_merge_sort(std::span<std::int32_t> a) {
-  optimized_merge_sort(a, classic_config());
+template <class Key>
+void sort_range(std::span<Key> a, std::ptrdiff_t lo, std::ptrdiff_t hi, const NetworkConfig& cfg,
+                Algorithm alg) {
+  const char* what =
+      alg == Algorithm::merge_sort ? "optimized_merge_sort" : "optimized_quick_sort";
+  if (hi < lo) return;  // hybrid.hpp:160, 201
+  if (lo < 0 || hi >= static_cast<std::ptrdiff_t>(a.size()))
+    throw std::invalid_argument(std::string(what) + ": range outside the span");
+  check(host_sort(a.data() + lo, static_cast<size_t>(hi - lo + 1), cfg, alg), what);
 }
+}  // namespace detail
 
-inline void optimized_quick_sort(std::span<std::int32_t> a, std::ptrdiff_t low,
-                                 std::ptrdiff_t high, const NetworkConfig& cfg) {
-  if (high < low) return;  // hybrid.hpp:201
-  if (low < 0 || high >= static_cast<std::ptrdiff_t>(a.size()))
-    throw std::invalid_argument("optimized_quick_sort: range outside the span");
-  detail::check(ns_quick_sort_host_i32(a.data() + low, static_cast<size_t>(high - low + 1),
-                                       cfg.width_mask, cfg.varsort_max),
-                "optimized_quick_sort");
-}
-inline void optimized_quick_sort(std::span<std::int32_t> a, const NetworkConfig& cfg) {
-  optimized_quick_sort(a, 0, static_cast<std::ptrdiff_t>(a.size()) - 1, cfg);
-}
-inline void classical_quick_sort(std::span<std::int32_t> a) {
-  optimized_quick_sort(a, classic_config());
-}
+#define NETSORT_B200_HOST_OVERLOADS(KEY)                                                  \
+  inline void optimized_merge_sort(std::span<KEY> a, std::ptrdiff_t left,                 \
+                                   std::ptrdiff_t right, const NetworkConfig& cfg) {      \
+    detail::sort_range(a, left, right, cfg, Algorithm::merge_sort);                       \
+  }                                                                                       \
+  inline void optimized_merge_sort(std::span<KEY> a, const NetworkConfig& cfg) {          \
+    optimized_merge_sort(a, 0, static_cast<std::ptrdiff_t>(a.size()) - 1, cfg);           \
+  }                                                                                       \
+  inline void classical_merge_sort(std::span<KEY> a) {                                    \
+    optimized_merge_sort(a, classic_config());                                            \
+  }                                                                                       \
+  inline void optimized_quick_sort(std::span<KEY> a, std::ptrdiff_t low,                  \
+                                   std::ptrdiff_t high, const NetworkConfig& cfg) {       \
+    detail::sort_range(a, low, high, cfg, Algorithm::quick_sort);                         \
+  }                                                                                       \
+  inline void optimized_quick_sort(std::span<KEY> a, const NetworkConfig& cfg) {          \
+    optimized_quick_sort(a, 0, static_cast<std::ptrdiff_t>(a.size()) - 1, cfg);           \
+  }                                                                                       \
+  inline void classical_quick_sort(std::span<KEY> a) {                                    \
+    optimized_quick_sort(a, classic_config());                                            \
+  }                                                                                       \
+  inline void run_variant(const SortVariant& v, std::span<KEY> a) {                       \
+    if (v.algorithm == Algorithm::merge_sort) optimized_merge_sort(a, v.config);          \
+    else optimized_quick_sort(a, v.config);                                               \
+  }
 
-inline void run_variant(const SortVariant& v, std::span<std::int32_t> a) {
-  if (v.algorithm == Algorithm::merge_sort) optimized_merge_sort(a, v.config);
-  else optimized_quick_sort(a, v.config);
-}
+NETSORT_B200_HOST_OVERLOADS(std::int32_t)
+NETSORT_B200_HOST_OVERLOADS(std::int64_t)
+#undef NETSORT_B200_HOST_OVERLOADS
 
 // ---- device spans (caller-owned device memory, stream-ordered) ------------
 
@@ -130,6 +147,10 @@ class DeviceScratch {
 void device_merge_sort(std::int32_t* d_keys, size_t n, const NetworkConfig& cfg,
                        DeviceScratch& scratch, void* stream = nullptr);
 void device_quick_sort(std::int32_t* d_keys, size_t n, const NetworkConfig& cfg,
+                       DeviceScratch& scratch, void* stream = nullptr);
+void device_merge_sort(std::int64_t* d_keys, size_t n, const NetworkConfig& cfg,
+                       DeviceScratch& scratch, void* stream = nullptr);
+void device_quick_sort(std::int64_t* d_keys, size_t n, const NetworkConfig& cfg,
                        DeviceScratch& scratch, void* stream = nullptr);
 
 }  // namespace netsort_b200

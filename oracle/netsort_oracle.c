@@ -113,133 +113,30 @@ int oracle_network(int width, uint8_t* pairs, int cap) {
   return count;
 }
 
-/* compare_exchange — networks.hpp:25-32 (select form, no branch on data) */
-static inline void cx(int32_t* a, int32_t* b) {
-  const int32_t x = *a, y = *b;
-  const int ooo = y < x;
-  *a = ooo ? y : x;
-  *b = ooo ? x : y;
-}
-
-/* sort_small — networks.hpp:132-145 */
-void oracle_sort_small_i32(int32_t* v, int size) {
-  int count;
-  const uint8_t(*t)[2] = net_table(size, &count);
-  if (!t) return;
-  for (int i = 0; i < count; ++i) cx(&v[t[i][0]], &v[t[i][1]]);
-}
-
 /* base_case_applies — config.hpp:30-36 (fixed widths first, then varsort) */
 int oracle_base_case_applies(int64_t size, uint32_t width_mask, int varsort_max) {
   if (size >= 2 && size <= 8 && ((width_mask >> size) & 1u)) return 1;
   return varsort_max != 0 && size >= 2 && size <= varsort_max;
 }
 
-/* ---- merge sort -------------------------------------------------------- */
-
 static inline void st_depth(oracle_stats* s, int d) {
   if (s && d > s->max_depth) s->max_depth = d;
 }
 
-/* try_base_case — hybrid.hpp:48-56 */
-static int try_base(int32_t* a, int64_t left, int64_t size, uint32_t mask, int vs,
-                    oracle_stats* st) {
-  if (!oracle_base_case_applies(size, mask, vs)) return 0;
-  if (st) st->network_hits[size]++;
-  oracle_sort_small_i32(a + left, (int)size);
-  return 1;
-}
+#define CAT2_(a, b) a##b
+#define CAT_(a, b) CAT2_(a, b)
 
-/* merge_runs — hybrid.hpp:61-79: left run staged in scratch, left wins ties */
-static void merge_runs(int32_t* a, int64_t left, int64_t mid, int64_t right,
-                       int32_t* scratch) {
-  const int64_t left_len = mid - left + 1;
-  memcpy(scratch, a + left, (size_t)left_len * sizeof(int32_t));
-  int64_t i = 0, j = mid + 1, out = left;
-  while (i < left_len && j <= right) {
-    if (a[j] < scratch[i]) a[out++] = a[j++];
-    else a[out++] = scratch[i++];
-  }
-  while (i < left_len) a[out++] = scratch[i++];
-}
+#define KEY int32_t
+#define NAME(x) CAT_(x, _i32)
+#include "netsort_oracle_sort.inc"
+#undef KEY
+#undef NAME
 
-/* merge_sort_rec — hybrid.hpp:81-95 */
-static void ms_rec(int32_t* a, int64_t left, int64_t right, uint32_t mask, int vs,
-                   int32_t* scratch, oracle_stats* st, int depth) {
-  st_depth(st, depth);
-  const int64_t size = right - left + 1;
-  if (try_base(a, left, size, mask, vs, st)) return;
-  if (left < right) {
-    const int64_t mid = left + (right - left) / 2;
-    ms_rec(a, left, mid, mask, vs, scratch, st, depth + 1);
-    ms_rec(a, mid + 1, right, mask, vs, scratch, st, depth + 1);
-    if (st) st->merges++;
-    merge_runs(a, left, mid, right, scratch);
-  }
-}
-
-/* optimized_merge_sort — hybrid.hpp:156-165 */
-void oracle_merge_sort_i32(int32_t* a, int64_t left, int64_t right, uint32_t mask,
-                           int vs, oracle_stats* st) {
-  if (right < left) return;
-  int32_t* scratch = (int32_t*)malloc((size_t)(right - left + 1) * sizeof(int32_t));
-  ms_rec(a, left, right, mask, vs, scratch, st, 1);
-  free(scratch);
-}
-
-/* merge — hybrid.hpp:186-193 */
-void oracle_merge_i32(int32_t* a, int64_t left, int64_t mid, int64_t right) {
-  int32_t* scratch = (int32_t*)malloc((size_t)(mid - left + 1) * sizeof(int32_t));
-  merge_runs(a, left, mid, right, scratch);
-  free(scratch);
-}
-
-/* ---- quick sort -------------------------------------------------------- */
-
-/* median_of_three — hybrid.hpp:105-114 */
-int32_t oracle_median_of_three_i32(int32_t* a, int64_t low, int64_t high) {
-  if (high - low < 2) return a[low];
-  const int64_t mid = low + (high - low) / 2;
-  cx(&a[low], &a[mid]);
-  cx(&a[low], &a[high]);
-  cx(&a[mid], &a[high]);
-  return a[mid];
-}
-
-/* hoare_partition — hybrid.hpp:121-133 (j == high fix-up at 130) */
-int64_t oracle_hoare_partition_i32(int32_t* a, int64_t low, int64_t high, int32_t pivot) {
-  int64_t i = low - 1, j = high + 1;
-  for (;;) {
-    do { ++i; } while (a[i] < pivot);
-    do { --j; } while (pivot < a[j]);
-    if (i >= j) return j < high ? j : high - 1;
-    const int32_t t = a[i];
-    a[i] = a[j];
-    a[j] = t;
-  }
-}
-
-/* quick_sort_rec — hybrid.hpp:137-150 */
-static void qs_rec(int32_t* a, int64_t low, int64_t high, uint32_t mask, int vs,
-                   oracle_stats* st, int depth) {
-  st_depth(st, depth);
-  const int64_t size = high - low + 1;
-  if (try_base(a, low, size, mask, vs, st)) return;
-  if (low < high) {
-    const int32_t pivot = oracle_median_of_three_i32(a, low, high);
-    if (st) st->partitions++;
-    const int64_t split = oracle_hoare_partition_i32(a, low, high, pivot);
-    qs_rec(a, low, split, mask, vs, st, depth + 1);
-    qs_rec(a, split + 1, high, mask, vs, st, depth + 1);
-  }
-}
-
-/* optimized_quick_sort — hybrid.hpp:197-204 */
-void oracle_quick_sort_i32(int32_t* a, int64_t low, int64_t high, uint32_t mask, int vs,
-                           oracle_stats* st) {
-  if (high < low) return;
-  qs_rec(a, low, high, mask, vs, st, 1);
-}
+#define KEY int64_t
+#define NAME(x) CAT_(x, _i64)
+#include "netsort_oracle_sort.inc"
+#undef KEY
+#undef NAME
 
 /* ---- batch helpers ----------------------------------------------------- */
 
@@ -268,6 +165,17 @@ void oracle_multiset_digest_i32(const int32_t* keys, size_t n, uint64_t out[2]) 
   uint64_t s = 0, x = 0;
   for (size_t i = 0; i < n; ++i) {
     const uint64_t m = mix64((uint64_t)(uint32_t)keys[i] + 0x9E3779B97F4A7C15ull);
+    s += m;
+    x ^= m;
+  }
+  out[0] = s;
+  out[1] = x;
+}
+
+void oracle_multiset_digest_i64(const int64_t* keys, size_t n, uint64_t out[2]) {
+  uint64_t s = 0, x = 0;
+  for (size_t i = 0; i < n; ++i) {
+    const uint64_t m = mix64((uint64_t)keys[i] + 0x9E3779B97F4A7C15ull);
     s += m;
     x ^= m;
   }

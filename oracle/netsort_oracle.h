@@ -80,6 +80,17 @@ int64_t oracle_hoare_partition_i32(int32_t* a, int64_t low, int64_t high, int32_
 void oracle_quick_sort_i32(int32_t* a, int64_t low, int64_t high, uint32_t width_mask,
                            int varsort_max, oracle_stats* stats);
 
+/* int64 keys — the reference's own benchmark type (bench.hpp:59-61); same
+ * functions, same citations (the reference templates them on T). */
+void oracle_sort_small_i64(int64_t* v, int size);
+void oracle_merge_sort_i64(int64_t* a, int64_t left, int64_t right, uint32_t width_mask,
+                           int varsort_max, oracle_stats* stats);
+void oracle_merge_i64(int64_t* a, int64_t left, int64_t mid, int64_t right);
+int64_t oracle_median_of_three_i64(int64_t* a, int64_t low, int64_t high);
+int64_t oracle_hoare_partition_i64(int64_t* a, int64_t low, int64_t high, int64_t pivot);
+void oracle_quick_sort_i64(int64_t* a, int64_t low, int64_t high, uint32_t width_mask,
+                           int varsort_max, oracle_stats* stats);
+
 /* Batch / segmented helpers (no reference symbol):
  * sort_small per array, optimized_quick_sort per fixed-length segment. */
 void oracle_sort_small_batch_i32(int32_t* keys, const uint32_t* offsets, size_t num_arrays);
@@ -89,6 +100,8 @@ void oracle_segmented_quick_sort_i32(int32_t* keys, size_t num_segments, size_t 
 /* Order-independent multiset digest used for the permutation property at
  * full sizes (sum of a 64-bit mix of every key, and xor of the same). */
 void oracle_multiset_digest_i32(const int32_t* keys, size_t n, uint64_t out[2]);
+/* int64: the mix is applied to the key's 64-bit pattern */
+void oracle_multiset_digest_i64(const int64_t* keys, size_t n, uint64_t out[2]);
 
 #ifdef __cplusplus
 }

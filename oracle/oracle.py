@@ -87,6 +87,18 @@ def lib():
         L.oracle_segmented_quick_sort_i32.argtypes = [_i32p, C.c_size_t, C.c_size_t,
                                                       C.c_uint32, C.c_int]
         L.oracle_multiset_digest_i32.argtypes = [_i32p, C.c_size_t, _u64p]
+        # int64 instantiations (netsort_oracle_sort.inc with KEY = int64_t)
+        L.oracle_sort_small_i64.argtypes = [_i64p, C.c_int]
+        L.oracle_merge_sort_i64.argtypes = [_i64p, C.c_int64, C.c_int64, C.c_uint32, C.c_int,
+                                            C.c_void_p]
+        L.oracle_merge_i64.argtypes = [_i64p, C.c_int64, C.c_int64, C.c_int64]
+        L.oracle_median_of_three_i64.argtypes = [_i64p, C.c_int64, C.c_int64]
+        L.oracle_median_of_three_i64.restype = C.c_int64
+        L.oracle_hoare_partition_i64.argtypes = [_i64p, C.c_int64, C.c_int64, C.c_int64]
+        L.oracle_hoare_partition_i64.restype = C.c_int64
+        L.oracle_quick_sort_i64.argtypes = [_i64p, C.c_int64, C.c_int64, C.c_uint32, C.c_int,
+                                            C.c_void_p]
+        L.oracle_multiset_digest_i64.argtypes = [_i64p, C.c_size_t, _u64p]
         _lib = L
     return _lib
 
@@ -121,6 +133,8 @@ def ref():
         R.ref_median_of_three_i32.restype = C.c_int32
         R.ref_hoare_partition_i32.argtypes = [_i32p, C.c_int64, C.c_int64, C.c_int64, C.c_int32]
         R.ref_hoare_partition_i32.restype = C.c_int64
+        R.ref_merge_sort_i64.argtypes = [_i64p, C.c_int64, C.c_uint32, C.c_int, C.c_void_p]
+        R.ref_quick_sort_i64.argtypes = [_i64p, C.c_int64, C.c_uint32, C.c_int, C.c_void_p]
         R.ref_generate_i64.argtypes = [C.c_int, C.c_int64, C.c_uint64, C.c_double, _i64p]
         R.ref_splitmix64_nth.argtypes = [C.c_uint64, C.c_int64]
         R.ref_splitmix64_nth.restype = C.c_uint64
@@ -162,19 +176,29 @@ def network(width: int):
     return [(int(buf[2 * i]), int(buf[2 * i + 1])) for i in range(cnt)]
 
 
+def _keys(a: np.ndarray):
+    """int64 arrays keep their type (the *_i64 instantiation); anything else
+    is taken as int32 (the BASELINE configs)."""
+    if isinstance(a, np.ndarray) and a.dtype == np.int64:
+        return np.ascontiguousarray(a).copy(), "i64"
+    return np.ascontiguousarray(a, np.int32).copy(), "i32"
+
+
 def merge_sort(a: np.ndarray, config: str = "6To8", stats: bool = False):
     mask, vs = CONFIGS[config]
-    a = np.ascontiguousarray(a, np.int32).copy()
+    a, t = _keys(a)
     st = OracleStats()
-    lib().oracle_merge_sort_i32(a, 0, len(a) - 1, mask, vs, C.addressof(st) if stats else None)
+    getattr(lib(), f"oracle_merge_sort_{t}")(a, 0, len(a) - 1, mask, vs,
+                                             C.addressof(st) if stats else None)
     return (a, st) if stats else a
 
 
 def quick_sort(a: np.ndarray, config: str = "3To5", stats: bool = False):
     mask, vs = CONFIGS[config]
-    a = np.ascontiguousarray(a, np.int32).copy()
+    a, t = _keys(a)
     st = OracleStats()
-    lib().oracle_quick_sort_i32(a, 0, len(a) - 1, mask, vs, C.addressof(st) if stats else None)
+    getattr(lib(), f"oracle_quick_sort_{t}")(a, 0, len(a) - 1, mask, vs,
+                                             C.addressof(st) if stats else None)
     return (a, st) if stats else a
 
 
@@ -194,6 +218,6 @@ def segmented_quick_sort(keys: np.ndarray, seg_len: int, config: str = "3To5") -
 
 def multiset_digest(a: np.ndarray):
     out = np.zeros(2, np.uint64)
-    a = np.ascontiguousarray(a, np.int32)
-    lib().oracle_multiset_digest_i32(a, len(a), out)
+    a, t = _keys(a)
+    getattr(lib(), f"oracle_multiset_digest_{t}")(a, len(a), out)
     return int(out[0]), int(out[1])

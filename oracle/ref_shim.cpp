@@ -74,6 +74,29 @@ void ref_quick_sort_i32(int32_t* a, int64_t n, uint32_t mask, int vs, uint64_t* 
   }
 }
 
+// The reference's native benchmark instantiation: T = std::int64_t
+// (bench.hpp:59-61, bench.cpp:94-96).
+void ref_merge_sort_i64(int64_t* a, int64_t n, uint32_t mask, int vs, uint64_t* stats) {
+  std::span<int64_t> s(a, static_cast<size_t>(n));
+  if (stats) {
+    DispatchStats st;
+    optimized_merge_sort(s, 0, static_cast<std::ptrdiff_t>(n) - 1, cfg_of(mask, vs), st);
+    copy_stats(st, stats);
+  } else {
+    optimized_merge_sort(s, cfg_of(mask, vs));
+  }
+}
+void ref_quick_sort_i64(int64_t* a, int64_t n, uint32_t mask, int vs, uint64_t* stats) {
+  std::span<int64_t> s(a, static_cast<size_t>(n));
+  if (stats) {
+    DispatchStats st;
+    optimized_quick_sort(s, 0, static_cast<std::ptrdiff_t>(n) - 1, cfg_of(mask, vs), st);
+    copy_stats(st, stats);
+  } else {
+    optimized_quick_sort(s, cfg_of(mask, vs));
+  }
+}
+
 // Range form with inclusive bounds (hybrid.hpp:156-172, 197-211).
 void ref_merge_sort_range_i32(int32_t* a, int64_t n, int64_t left, int64_t right,
                               uint32_t mask, int vs) {

@@ -1,4 +1,4 @@
-"""netsort-b200: merge sort and quick sort over int32 keys whose recursion
+"""netsort-b200: merge sort and quick sort over int32 and int64 keys whose recursion
 bottoms out in fixed sorting networks (arXiv 2503.05934), rebuilt for B200
 (sm_100a).  The compute lives in lib/libnetsort_b200.so behind the C ABI
 include/netsort_b200.h; this package is the Python host layer over it."""

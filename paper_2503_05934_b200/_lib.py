@@ -34,7 +34,11 @@ SIGNATURES = {
     "ns_network_comparators": (_i32, [_i32, _vp, _i32]),
     "ns_merge_sort_temp_bytes": (_sz, [_sz]),
     "ns_merge_sort_i32": (_i32, [_vp, _sz, _u32, _i32, _vp, _sz, _vp]),
+    "ns_merge_sort_temp_bytes_i64": (_sz, [_sz]),
+    "ns_merge_sort_i64": (_i32, [_vp, _sz, _u32, _i32, _vp, _sz, _vp]),
     "ns_quick_sort_temp_bytes": (_sz, [_sz]),
+    "ns_quick_sort_temp_bytes_i64": (_sz, [_sz]),
+    "ns_quick_sort_i64": (_i32, [_vp, _sz, _u32, _i32, _vp, _sz, _vp]),
     "ns_quick_sort_i32": (_i32, [_vp, _sz, _u32, _i32, _vp, _sz, _vp]),
     "ns_sort_small_batch_i32": (_i32, [_vp, _vp, _sz, _vp]),
     "ns_segmented_sort_temp_bytes": (_sz, [_sz, _sz]),
@@ -51,6 +55,8 @@ SIGNATURES = {
     "ns_ipc_close": (_i32, [_vp]),
     "ns_multiset_digest_i32": (_i32, [_vp, _sz, _vp, _vp]),
     "ns_count_inversions_i32": (_i32, [_vp, _sz, _vp, _vp]),
+    "ns_multiset_digest_i64": (_i32, [_vp, _sz, _vp, _vp]),
+    "ns_count_inversions_i64": (_i32, [_vp, _sz, _vp, _vp]),
     "ns_generate_i32": (_i32, [_vp, _sz, _i32, C.c_uint64, _vp]),
     "ns_launch_count": (C.c_uint64, []),
     "ns_profile_enable": (_i32, [_i32]),
@@ -58,6 +64,8 @@ SIGNATURES = {
     "ns_profile_kind_name": (C.c_char_p, [_i32]),
     "ns_profile_read": (_i32, [_i32, C.POINTER(C.c_double), C.POINTER(C.c_uint64)]),
     "ns_merge_sort_host_i32": (_i32, [_vp, _sz, _u32, _i32]),
+    "ns_merge_sort_host_i64": (_i32, [_vp, _sz, _u32, _i32]),
+    "ns_quick_sort_host_i64": (_i32, [_vp, _sz, _u32, _i32]),
     "ns_quick_sort_host_i32": (_i32, [_vp, _sz, _u32, _i32]),
     "ns_release_cache": (_i32, []),
 }

@@ -8,10 +8,11 @@ Names, argument meaning and error behaviour follow
   optimized_quick_sort(a, [low, high,] cfg)   hybrid.hpp:197-216
   classical_merge_sort / classical_quick_sort hybrid.hpp:180-183, 220-223
   run_variant(variant, a)                     hybrid.hpp:225-232
-Arrays are sorted IN PLACE.  ``a`` may be a CUDA int32 tensor (device path:
-no host copies, stream-ordered on torch's current stream) or a host int32
-numpy array (the reference's call shape: copied to the GPU, sorted, copied
-back).  Everything executes in the sm_100a library through the C ABI; there
+Arrays are sorted IN PLACE.  ``a`` may be a CUDA tensor (device path: no
+host copies, stream-ordered on torch's current stream) or a host numpy array
+(the reference's call shape: copied to the GPU, sorted, copied back); keys
+are int32 (the BASELINE configs) or int64 (the reference's own benchmark
+type, bench.hpp:59-61), dispatched to the *_i32 / *_i64 entry points.  Everything executes in the sm_100a library through the C ABI; there
 is no CPU fallback.  Configuration errors raise ValueError (the reference
 throws std::invalid_argument), device errors raise NetsortError.
 """
@@ -159,18 +160,22 @@ def _is_device(a) -> bool:
     return torch is not None and isinstance(a, torch.Tensor) and a.is_cuda
 
 
-def _check_tensor(a):
-    if a.dtype != torch.int32:
-        raise ValueError(f"keys must be int32, got {a.dtype}")
+def _check_tensor(a, allow_i64: bool = False):
+    ok = (torch.int32, torch.int64) if allow_i64 else (torch.int32,)
+    if a.dtype not in ok:
+        raise ValueError(f"keys must be {' or '.join(str(t) for t in ok)}, got {a.dtype}")
     if not a.is_contiguous():
         raise ValueError("keys must be contiguous")
+    return "i64" if a.dtype == torch.int64 else "i32"
 
 
 def _check_host(a):
-    if not isinstance(a, np.ndarray) or a.dtype != np.int32 or not a.flags.c_contiguous:
-        raise ValueError("host keys must be a C-contiguous int32 numpy array")
+    if not isinstance(a, np.ndarray) or a.dtype not in (np.int32, np.int64) \
+            or not a.flags.c_contiguous:
+        raise ValueError("host keys must be a C-contiguous int32 or int64 numpy array")
     if not a.flags.writeable:
         raise ValueError("host keys must be writeable (sorted in place)")
+    return "i64" if a.dtype == np.int64 else "i32"
 
 
 def _range(a, left, right):
@@ -188,24 +193,21 @@ def _sort(algo: int, a, left, right, cfg: NetworkConfig):
         raise ValueError("range outside the array")
     cnt = right - left + 1
     L = lib()
+    what = "optimized_merge_sort" if algo == _lib.NS_MERGE_SORT else "optimized_quick_sort"
+    alg = "merge" if algo == _lib.NS_MERGE_SORT else "quick"
     if _is_device(a):
-        _check_tensor(a)
-        ptr = a.data_ptr() + 4 * left
-        if algo == _lib.NS_MERGE_SORT:
-            tb = L.ns_merge_sort_temp_bytes(cnt)
-            st = L.ns_merge_sort_i32(ptr, cnt, cfg.width_mask, cfg.varsort_max,
-                                     scratch(tb, a.device), tb, _stream_ptr(a))
-        else:
-            tb = L.ns_quick_sort_temp_bytes(cnt)
-            st = L.ns_quick_sort_i32(ptr, cnt, cfg.width_mask, cfg.varsort_max,
-                                     scratch(tb, a.device), tb, _stream_ptr(a))
-        check(st, "optimized_merge_sort" if algo == 0 else "optimized_quick_sort")
+        t = _check_tensor(a, allow_i64=True)
+        ptr = a.data_ptr() + a.element_size() * left
+        sfx = "" if t == "i32" else "_i64"
+        tb = getattr(L, f"ns_{alg}_sort_temp_bytes{sfx}")(cnt)
+        st = getattr(L, f"ns_{alg}_sort_{t}")(ptr, cnt, cfg.width_mask, cfg.varsort_max,
+                                             scratch(tb, a.device), tb, _stream_ptr(a))
+        check(st, what)
     else:
-        _check_host(a)
-        ptr = a.ctypes.data + 4 * left
-        fn = L.ns_merge_sort_host_i32 if algo == 0 else L.ns_quick_sort_host_i32
-        check(fn(ptr, cnt, cfg.width_mask, cfg.varsort_max),
-              "optimized_merge_sort" if algo == 0 else "optimized_quick_sort")
+        t = _check_host(a)
+        ptr = a.ctypes.data + a.itemsize * left
+        fn = getattr(L, f"ns_{alg}_sort_host_{t}")
+        check(fn(ptr, cnt, cfg.width_mask, cfg.varsort_max), what)
     return a
 
 
@@ -273,18 +275,20 @@ def segmented_sort(keys, seg_len: int, cfg: NetworkConfig,
 
 def multiset_digest(keys) -> tuple:
     """Order-independent (sum, xor) digest of mix64(key) over a CUDA tensor."""
-    _check_tensor(keys)
+    t = _check_tensor(keys, allow_i64=True)
     out = torch.zeros(2, dtype=torch.int64, device=keys.device)
-    check(lib().ns_multiset_digest_i32(keys.data_ptr(), keys.numel(), out.data_ptr(),
-                                       _stream_ptr(keys)), "multiset_digest")
+    check(getattr(lib(), f"ns_multiset_digest_{t}")(keys.data_ptr(), keys.numel(),
+                                                      out.data_ptr(), _stream_ptr(keys)),
+          "multiset_digest")
     s, x = out.cpu().tolist()
     return s & (2**64 - 1), x & (2**64 - 1)
 
 
 def count_inversions(keys) -> int:
     """Number of adjacent descents (0 == sorted)."""
-    _check_tensor(keys)
+    t = _check_tensor(keys, allow_i64=True)
     out = torch.zeros(1, dtype=torch.int64, device=keys.device)
-    check(lib().ns_count_inversions_i32(keys.data_ptr(), keys.numel(), out.data_ptr(),
-                                        _stream_ptr(keys)), "count_inversions")
+    check(getattr(lib(), f"ns_count_inversions_{t}")(keys.data_ptr(), keys.numel(),
+                                                       out.data_ptr(), _stream_ptr(keys)),
+          "count_inversions")
     return int(out.item())

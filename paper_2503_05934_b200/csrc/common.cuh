@@ -89,9 +89,14 @@ int merge_sort_device(int32_t* d_keys, size_t n, int leaf, void* d_temp, size_t 
                       cudaStream_t s);
 int tile_sort_segments(int32_t* d_keys, size_t num_segments, size_t seg_len, int leaf,
                        cudaStream_t s);
+int merge_sort_device(int64_t* d_keys, size_t n, int leaf, void* d_temp, size_t temp_bytes,
+                      cudaStream_t s);
 size_t merge_sort_temp(size_t n);
+size_t merge_sort_temp_i64(size_t n);
 int merge_existing_runs(int32_t* keys, int32_t* tmp, size_t n, int64_t R0, void* d_temp,
                         cudaStream_t s, int32_t** result);
+int merge_existing_runs(int64_t* keys, int64_t* tmp, size_t n, int64_t R0, void* d_temp,
+                        cudaStream_t s, int64_t** result);
 constexpr int kSmallTile = 16384;  // largest array one CTA sorts on chip
 
 }  // namespace nsb

@@ -12,6 +12,7 @@
 
 namespace nsb {
 size_t quick_sort_temp(size_t n);
+size_t quick_sort_temp_i64(size_t n);
 
 // Per-thread device staging: keys + scratch, grown on demand, plus one
 // non-blocking stream.  Mirrors the reference's per-call `new T[n]` scratch
@@ -64,17 +65,36 @@ static thread_local HostCache g_host;
 // stream) lands, so the tile sort and all intra-chunk merge passes hide under
 // the host->device transfer; log2(chunks) pairwise passes then merge the
 // chunks and the result is read back from whichever buffer holds it.
-static int host_sort(int32_t* h_keys, size_t n, uint32_t mask, int vs, int algorithm) {
+static size_t dev_temp(const int32_t*, int algorithm, size_t n) {
+  return algorithm == NS_MERGE_SORT ? merge_sort_temp(n) : quick_sort_temp(n);
+}
+static size_t dev_temp(const int64_t*, int algorithm, size_t n) {
+  return algorithm == NS_MERGE_SORT ? merge_sort_temp_i64(n) : quick_sort_temp_i64(n);
+}
+static int dev_sort(int32_t* d, size_t n, uint32_t mask, int vs, void* t, size_t tb, int algorithm,
+                    cudaStream_t s) {
+  return algorithm == NS_MERGE_SORT ? ns_merge_sort_i32(d, n, mask, vs, t, tb, s)
+                                    : ns_quick_sort_i32(d, n, mask, vs, t, tb, s);
+}
+static int dev_sort(int64_t* d, size_t n, uint32_t mask, int vs, void* t, size_t tb, int algorithm,
+                    cudaStream_t s) {
+  return algorithm == NS_MERGE_SORT ? ns_merge_sort_i64(d, n, mask, vs, t, tb, s)
+                                    : ns_quick_sort_i64(d, n, mask, vs, t, tb, s);
+}
+
+template <class Key>
+static int host_sort(Key* h_keys, size_t n, uint32_t mask, int vs, int algorithm) {
   if (n <= 1) return NS_OK;
   if (!h_keys) return NS_ERR_INVALID;
-  const size_t kb = align_up(n * sizeof(int32_t), 256);
-  const size_t tb = algorithm == NS_MERGE_SORT ? merge_sort_temp(n) : quick_sort_temp(n);
+  constexpr size_t KB = sizeof(Key);
+  const size_t kb = align_up(n * KB, 256);
+  const size_t tb = dev_temp(h_keys, algorithm, n);
   NSB_TRY(g_host.ensure(kb + tb));
   cudaStream_t s = g_host.stream;
-  int32_t* d = static_cast<int32_t*>(g_host.dev);
+  Key* d = static_cast<Key*>(g_host.dev);
   void* t = static_cast<char*>(g_host.dev) + kb;
-  const size_t chunk_min = size_t(1) << 22;
-  int32_t* result = d;
+  const size_t chunk_min = (size_t(1) << 24) / KB;  // 16 MiB
+  Key* result = d;
   if (algorithm == NS_MERGE_SORT && n >= 2 * chunk_min) {
     int chunks = (int)std::min<size_t>(kMaxChunks, n / chunk_min);
     size_t clen = (n + chunks - 1) / chunks;
@@ -82,7 +102,7 @@ static int host_sort(int32_t* h_keys, size_t n, uint32_t mask, int vs, int algor
     chunks = (int)((n + clen - 1) / clen);
     for (int c = 0; c < chunks; ++c) {
       const size_t off = c * clen, len = std::min(clen, n - off);
-      NSB_TRY(check_cuda(cudaMemcpyAsync(d + off, h_keys + off, len * 4, cudaMemcpyHostToDevice,
+      NSB_TRY(check_cuda(cudaMemcpyAsync(d + off, h_keys + off, len * KB, cudaMemcpyHostToDevice,
                                          g_host.copy),
                          "H2D"));
       NSB_TRY(check_cuda(cudaEventRecord(g_host.ev[c], g_host.copy), "cudaEventRecord"));
@@ -90,23 +110,22 @@ static int host_sort(int32_t* h_keys, size_t n, uint32_t mask, int vs, int algor
     for (int c = 0; c < chunks; ++c) {
       const size_t off = c * clen, len = std::min(clen, n - off);
       NSB_TRY(check_cuda(cudaStreamWaitEvent(s, g_host.ev[c], 0), "cudaStreamWaitEvent"));
-      const int st = ns_merge_sort_i32(d + off, len, mask, vs, t, tb, s);
+      const int st = dev_sort(d + off, len, mask, vs, t, tb, NS_MERGE_SORT, s);
       if (st != NS_OK) {
         cudaStreamSynchronize(s);
         return st;
       }
     }
-    NSB_TRY(merge_existing_runs(d, static_cast<int32_t*>(t), n, (int64_t)clen, t, s, &result));
+    NSB_TRY(merge_existing_runs(d, static_cast<Key*>(t), n, (int64_t)clen, t, s, &result));
   } else {
-    NSB_TRY(check_cuda(cudaMemcpyAsync(d, h_keys, n * 4, cudaMemcpyHostToDevice, s), "H2D"));
-    const int st = algorithm == NS_MERGE_SORT ? ns_merge_sort_i32(d, n, mask, vs, t, tb, s)
-                                              : ns_quick_sort_i32(d, n, mask, vs, t, tb, s);
+    NSB_TRY(check_cuda(cudaMemcpyAsync(d, h_keys, n * KB, cudaMemcpyHostToDevice, s), "H2D"));
+    const int st = dev_sort(d, n, mask, vs, t, tb, algorithm, s);
     if (st != NS_OK) {
       cudaStreamSynchronize(s);
       return st;
     }
   }
-  NSB_TRY(check_cuda(cudaMemcpyAsync(h_keys, result, n * 4, cudaMemcpyDeviceToHost, s), "D2H"));
+  NSB_TRY(check_cuda(cudaMemcpyAsync(h_keys, result, n * KB, cudaMemcpyDeviceToHost, s), "D2H"));
   return check_cuda(cudaStreamSynchronize(s), "cudaStreamSynchronize");
 }
 
@@ -119,6 +138,14 @@ int ns_merge_sort_host_i32(int32_t* h_keys, size_t n, uint32_t width_mask, int v
 }
 
 int ns_quick_sort_host_i32(int32_t* h_keys, size_t n, uint32_t width_mask, int varsort_max) {
+  return nsb::host_sort(h_keys, n, width_mask, varsort_max, NS_QUICK_SORT);
+}
+
+int ns_merge_sort_host_i64(int64_t* h_keys, size_t n, uint32_t width_mask, int varsort_max) {
+  return nsb::host_sort(h_keys, n, width_mask, varsort_max, NS_MERGE_SORT);
+}
+
+int ns_quick_sort_host_i64(int64_t* h_keys, size_t n, uint32_t width_mask, int varsort_max) {
   return nsb::host_sort(h_keys, n, width_mask, varsort_max, NS_QUICK_SORT);
 }
 
@@ -159,6 +186,22 @@ void device_quick_sort(std::int32_t* d_keys, size_t n, const NetworkConfig& cfg,
   const size_t tb = ns_quick_sort_temp_bytes(n);
   void* t = scratch.reserve(tb);
   detail::check(ns_quick_sort_i32(d_keys, n, cfg.width_mask, cfg.varsort_max, t, tb, stream),
+                "device_quick_sort");
+}
+
+void device_merge_sort(std::int64_t* d_keys, size_t n, const NetworkConfig& cfg,
+                       DeviceScratch& scratch, void* stream) {
+  const size_t tb = ns_merge_sort_temp_bytes_i64(n);
+  void* t = scratch.reserve(tb);
+  detail::check(ns_merge_sort_i64(d_keys, n, cfg.width_mask, cfg.varsort_max, t, tb, stream),
+                "device_merge_sort");
+}
+
+void device_quick_sort(std::int64_t* d_keys, size_t n, const NetworkConfig& cfg,
+                       DeviceScratch& scratch, void* stream) {
+  const size_t tb = ns_quick_sort_temp_bytes_i64(n);
+  void* t = scratch.reserve(tb);
+  detail::check(ns_quick_sort_i64(d_keys, n, cfg.width_mask, cfg.varsort_max, t, tb, stream),
                 "device_quick_sort");
 }
 

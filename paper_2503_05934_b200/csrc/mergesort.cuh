@@ -19,6 +19,7 @@
 #pragma once
 #include <cstdint>
 #include <climits>
+#include <cstring>
 
 #include "networks.cuh"
 #include "smem_merge.cuh"
@@ -69,14 +70,52 @@ __device__ __forceinline__ void warp_bitonic(T (&v)[K], int lane) {
 // bank every 32/(K/2) lanes without padding; with it every warp-wide blocked
 // access (thread t touching t*K + k) and every coalesced access is bank
 // conflict free, and data-dependent merge cursors spread across banks.
-__host__ __device__ constexpr int pad_idx(int i) { return i + (i >> 5); }
-__host__ __device__ constexpr int padded_words(int T) { return T + (T >> 5) + 8; }
+//
+// Keys are int32 (the BASELINE configs) or int64 (the reference's own
+// benchmark type, datagen.hpp:47).  An int64 key covers two banks, and 64-bit
+// shared accesses are served per half-warp, so its pad is one key per 16.
+template <class Key>
+struct KeyT;
+template <>
+struct KeyT<int32_t> {
+  static constexpr int32_t kMax = INT_MAX;
+  static constexpr int kPadShift = 5;
+};
+template <>
+struct KeyT<int64_t> {
+  static constexpr int64_t kMax = INT64_MAX;
+  static constexpr int kPadShift = 4;
+};
+// keys per 16-byte vector
+template <class Key>
+__host__ __device__ constexpr int kpv() { return 16 / (int)sizeof(Key); }
+
+template <class Key = int32_t>
+__host__ __device__ constexpr int pad_idx(int i) { return i + (i >> KeyT<Key>::kPadShift); }
+template <class Key = int32_t>
+__host__ __device__ constexpr int padded_words(int T) { return T + (T >> KeyT<Key>::kPadShift) + 8; }
+// bytes of dynamic shared memory a padded T-key tile needs
+template <class Key>
+__host__ __device__ constexpr int padded_bytes(int T) { return padded_words<Key>(T) * (int)sizeof(Key); }
+
+// 16 bytes <-> kpv<Key>() keys (register moves only)
+template <class Key>
+__device__ __forceinline__ void unpack16(const int4& x, Key (&e)[kpv<Key>()]) {
+  memcpy(e, &x, 16);
+}
+template <class Key>
+__device__ __forceinline__ int4 pack16(const Key (&e)[kpv<Key>()]) {
+  int4 x;
+  memcpy(&x, e, 16);
+  return x;
+}
 
 // Read-only view of a run that starts at logical index `off` of padded smem.
+template <class Key = int32_t>
 struct SmemRun {
-  const int32_t* s;
+  const Key* s;
   int off;
-  __device__ __forceinline__ int32_t operator[](int i) const { return s[pad_idx(off + i)]; }
+  __device__ __forceinline__ Key operator[](int i) const { return s[pad_idx<Key>(off + i)]; }
 };
 
 // Merge-path split: number of elements taken from A among the first `diag`
@@ -95,14 +134,14 @@ __device__ __forceinline__ IDX merge_path(PA A, IDX a_len, PB B, IDX b_len, IDX 
 }
 
 // Serial merge of K outputs starting at (a, b).
-template <int K, class SA, class SB>
+template <int K, class SA, class SB, class Key>
 __device__ __forceinline__ void serial_merge(SA A, int a_len, SB B, int b_len, int a, int b,
-                                             int32_t (&v)[K]) {
+                                             Key (&v)[K]) {
   // clamped indices keep every read inside the staged tile; the clamped
   // value is never selected because the exhausted side loses every test
   const int a_last = max(a_len - 1, 0), b_last = max(b_len - 1, 0);
-  int32_t ka = A[min(a, a_last)];
-  int32_t kb = B[min(b, b_last)];
+  Key ka = A[min(a, a_last)];
+  Key kb = B[min(b, b_last)];
 #pragma unroll
   for (int k = 0; k < K; ++k) {
     const bool take_a = (b >= b_len) || (a < a_len && ka <= kb);
@@ -118,36 +157,39 @@ __device__ __forceinline__ void serial_merge(SA A, int a_len, SB B, int b_len, i
 }
 
 // Blocked registers <-> padded smem (thread t owns logical [t*K, t*K+K)).
-template <int K>
-__device__ __forceinline__ void regs_to_smem(int32_t* sm, const int32_t (&v)[K]) {
+template <int K, class Key>
+__device__ __forceinline__ void regs_to_smem(Key* sm, const Key (&v)[K]) {
   const int base = threadIdx.x * K;
 #pragma unroll
-  for (int k = 0; k < K; ++k) sm[pad_idx(base + k)] = v[k];
+  for (int k = 0; k < K; ++k) sm[pad_idx<Key>(base + k)] = v[k];
 }
-template <int K>
-__device__ __forceinline__ void smem_to_regs(const int32_t* sm, int32_t (&v)[K]) {
+template <int K, class Key>
+__device__ __forceinline__ void smem_to_regs(const Key* sm, Key (&v)[K]) {
   const int base = threadIdx.x * K;
 #pragma unroll
-  for (int k = 0; k < K; ++k) v[k] = sm[pad_idx(base + k)];
+  for (int k = 0; k < K; ++k) v[k] = sm[pad_idx<Key>(base + k)];
 }
 
 // Coalesced global -> padded smem for a T-key tile (`valid` live keys, the
-// rest padded with INT_MAX, which sorts to the tail).
-template <int NT, int T>
-__device__ __forceinline__ void tile_load(const int32_t* in, int valid, int32_t* sm) {
+// rest padded with the key maximum, which sorts to the tail).
+template <int NT, int T, class Key>
+__device__ __forceinline__ void tile_load(const Key* in, int valid, Key* sm) {
+  constexpr int PV = kpv<Key>();
   const int tid = threadIdx.x;
   if (valid == T && (reinterpret_cast<uintptr_t>(in) & 15) == 0) {
     const int4* p = reinterpret_cast<const int4*>(in);
 #pragma unroll
-    for (int q = 0; q < T / 4 / NT; ++q) {
+    for (int q = 0; q < T / PV / NT; ++q) {
       const int j = q * NT + tid;
-      const int4 x = __ldcs(p + j);  // streamed: every key is read exactly once
-      const int i = pad_idx(4 * j);  // 4 consecutive keys never straddle a pad
-      sm[i] = x.x; sm[i + 1] = x.y; sm[i + 2] = x.z; sm[i + 3] = x.w;
+      Key e[PV];
+      unpack16<Key>(__ldcs(p + j), e);  // streamed: every key is read exactly once
+      const int i = pad_idx<Key>(PV * j);  // one vector never straddles a pad
+#pragma unroll
+      for (int u = 0; u < PV; ++u) sm[i + u] = e[u];
     }
   } else {
 #pragma unroll 4
-    for (int i = tid; i < T; i += NT) sm[pad_idx(i)] = i < valid ? in[i] : INT_MAX;
+    for (int i = tid; i < T; i += NT) sm[pad_idx<Key>(i)] = i < valid ? in[i] : KeyT<Key>::kMax;
   }
 }
 
@@ -203,20 +245,24 @@ __device__ __forceinline__ void stage_slices(const int32_t* lo, const int32_t* h
 }
 
 // Coalesced padded smem -> global for the first `valid` keys of a T-key tile.
-template <int NT, int T>
-__device__ __forceinline__ void tile_store(const int32_t* sm, int32_t* out, int valid) {
+template <int NT, int T, class Key>
+__device__ __forceinline__ void tile_store(const Key* sm, Key* out, int valid) {
+  constexpr int PV = kpv<Key>();
   const int tid = threadIdx.x;
   if (valid == T && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
     int4* p = reinterpret_cast<int4*>(out);
 #pragma unroll
-    for (int q = 0; q < T / 4 / NT; ++q) {
+    for (int q = 0; q < T / PV / NT; ++q) {
       const int j = q * NT + tid;
-      const int i = pad_idx(4 * j);
-      __stcs(p + j, make_int4(sm[i], sm[i + 1], sm[i + 2], sm[i + 3]));
+      const int i = pad_idx<Key>(PV * j);
+      Key e[PV];
+#pragma unroll
+      for (int u = 0; u < PV; ++u) e[u] = sm[i + u];
+      __stcs(p + j, pack16<Key>(e));
     }
   } else {
 #pragma unroll 4
-    for (int i = tid; i < valid; i += NT) out[i] = sm[pad_idx(i)];
+    for (int i = tid; i < valid; i += NT) out[i] = sm[pad_idx<Key>(i)];
   }
 }
 
@@ -225,16 +271,15 @@ __device__ __forceinline__ void tile_store(const int32_t* sm, int32_t* out, int 
 // place allowed) on chip.  Shared by the tiled merge sort, the segmented sort
 // and the quick-sort bucket sort.
 // ---------------------------------------------------------------------------
-template <int NT, int K, int LEAF>
-__device__ __forceinline__ void cta_sort(const int32_t* in, int32_t* out, int valid,
-                                         int32_t* sm) {
+template <int NT, int K, int LEAF, class Key>
+__device__ __forceinline__ void cta_sort(const Key* in, Key* out, int valid, Key* sm) {
   constexpr int T = NT * K;
   const int tid = threadIdx.x;
   const int lane = tid & 31;
 
   tile_load<NT, T>(in, valid, sm);
   __syncthreads();
-  int32_t v[K];
+  Key v[K];
   smem_to_regs<K>(sm, v);
 
   thread_sort<LEAF>(v);  // the network base case (try_base_case, hybrid.hpp:48-56)
@@ -249,7 +294,7 @@ __device__ __forceinline__ void cta_sort(const int32_t* in, int32_t* out, int va
     const int pos = tid * K;
     const int pair = pos & ~(2 * R - 1);
     const int diag = pos - pair;
-    const SmemRun A{sm, pair}, B{sm, pair + R};
+    const SmemRun<Key> A{sm, pair}, B{sm, pair + R};
     const int a = merge_path<int>(A, R, B, R, diag);
     serial_merge<K>(A, R, B, R, a, diag - a, v);
   }
@@ -262,10 +307,11 @@ __device__ __forceinline__ void cta_sort(const int32_t* in, int32_t* out, int va
 
 // CTA b sorts [b*stride, b*stride + min(stride, n - b*stride)), stride <= T
 // (stride == T for plain tiling, the segment length for segmented sorts).
-template <int NT, int K, int LEAF>
+template <int NT, int K, int LEAF, class Key = int32_t>
 __global__ void __launch_bounds__(NT)
-    blocksort_kernel(const int32_t* src, int32_t* dst, int64_t n, int stride) {  // src == dst ok
-  extern __shared__ __align__(16) int32_t sm[];
+    blocksort_kernel(const Key* src, Key* dst, int64_t n, int stride) {  // src == dst ok
+  extern __shared__ __align__(16) unsigned char sm_raw[];
+  Key* sm = reinterpret_cast<Key*>(sm_raw);
   const int64_t base = (int64_t)blockIdx.x * stride;
   const int valid = (int)min((int64_t)stride, n - base);
   cta_sort<NT, K, LEAF>(src + base, dst + base, valid, sm);
@@ -338,8 +384,9 @@ __device__ __forceinline__ TileGeom tile_geom(const PassPlan& P, int64_t c) {
 // log2 dependent global loads (used when a merge pass has too few tiles for a
 // separate partition kernel to pay for its launch).  All lanes return the
 // split.
-__device__ __forceinline__ int64_t warp_merge_path(const int32_t* A, int64_t a_len,
-                                                   const int32_t* B, int64_t b_len, int64_t diag) {
+template <class Key>
+__device__ __forceinline__ int64_t warp_merge_path(const Key* A, int64_t a_len, const Key* B,
+                                                   int64_t b_len, int64_t diag) {
   const int lane = threadIdx.x & 31;
   int64_t lo = diag > b_len ? diag - b_len : 0;
   int64_t hi = diag < a_len ? diag : a_len;
@@ -360,25 +407,28 @@ __device__ __forceinline__ int64_t warp_merge_path(const int32_t* A, int64_t a_l
   return lo;
 }
 
-static __global__ void merge_partition_v2_kernel(const int32_t* __restrict__ src, PassPlan P,
+template <class Key>
+__global__ void merge_partition_v2_kernel(const Key* __restrict__ src, PassPlan P,
                                           int64_t num_tiles, int64_t* __restrict__ mp) {
   const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= num_tiles) return;
   const TileGeom g = tile_geom(P, c);
-  const int32_t* A = src + g.pair_base;
+  const Key* A = src + g.pair_base;
   mp[c] = merge_path<int64_t>(A, g.a_len, A + g.a_len, g.b_len, g.diag0);
 }
 
-// Words of shared memory a v2 tile needs: two slices with up to 3 words of
+// Keys of shared memory a v2 tile needs: two slices with up to 3 keys of
 // alignment slack each, a sentinel after each, 16-byte rounding.
 __host__ __device__ constexpr int v2_smem_words(int TM) { return TM + 16; }
 
-template <int NT, int K, bool FUSED = false>
+template <int NT, int K, bool FUSED = false, class Key = int32_t>
 __global__ void __launch_bounds__(NT, (NT == 256 ? 6 : 1))  // 6 CTAs/SM: measured best (40 regs, no spills)
-    merge_pass_v2_kernel(const int32_t* __restrict__ src, int32_t* __restrict__ dst, PassPlan P,
+    merge_pass_v2_kernel(const Key* __restrict__ src, Key* __restrict__ dst, PassPlan P,
                          const int64_t* __restrict__ mp) {
   constexpr int TM = NT * K;
-  __shared__ __align__(128) int32_t sm[v2_smem_words(TM)];
+  constexpr int PV = kpv<Key>();           // keys per 16 bytes
+  constexpr int KB = (int)sizeof(Key);
+  __shared__ __align__(128) Key sm[v2_smem_words(TM)];
   __shared__ __align__(8) uint64_t bar;
   const int tid = threadIdx.x;
   const int64_t c = blockIdx.x;
@@ -390,7 +440,7 @@ __global__ void __launch_bounds__(NT, (NT == 256 ? 6 : 1))  // 6 CTAs/SM: measur
     // splits found here by warps 0 and 1 instead of a partition kernel
     __shared__ int64_t splits[2];
     const int warp = tid >> 5;
-    const int32_t* PA = src + g.pair_base;
+    const Key* PA = src + g.pair_base;
     if (warp == 0) {
       const int64_t v = warp_merge_path(PA, g.a_len, PA + g.a_len, g.b_len, g.diag0);
       if (tid == 0) splits[0] = v;
@@ -409,20 +459,20 @@ __global__ void __launch_bounds__(NT, (NT == 256 ? 6 : 1))  // 6 CTAs/SM: measur
   }
   const int la = (int)(a1 - a0);
   const int lb = (int)((g.diag1 - a1) - (g.diag0 - a0));
-  const int32_t* A = src + g.pair_base + a0;
-  const int32_t* B = src + g.pair_base + g.a_len + (g.diag0 - a0);
-  const int32_t* lo = src;
-  const int32_t* hi = src + P.n;
+  const Key* A = src + g.pair_base + a0;
+  const Key* B = src + g.pair_base + g.a_len + (g.diag0 - a0);
+  const Key* lo = src;
+  const Key* hi = src + P.n;
 
   // smem placement mirrors global 16-byte alignment so one bulk copy per slice
   const uintptr_t a_addr = reinterpret_cast<uintptr_t>(A), b_addr = reinterpret_cast<uintptr_t>(B);
-  const int a_shift = (int)((a_addr & 15) >> 2), b_shift = (int)((b_addr & 15) >> 2);
-  const int b_off = (a_shift + la + 1 + 3) & ~3;  // B cover starts 16-byte aligned
-  const int32_t* a_cov = A - a_shift;
-  const int32_t* b_cov = B - b_shift;
-  const int a_words = (a_shift + la + 3) & ~3, b_words = (b_shift + lb + 3) & ~3;
-  const bool a_tma = la > 0 && (a_addr & 3) == 0 && a_cov >= lo && a_cov + a_words <= hi;
-  const bool b_tma = lb > 0 && (b_addr & 3) == 0 && b_cov >= lo && b_cov + b_words <= hi;
+  const int a_shift = (int)((a_addr & 15) / KB), b_shift = (int)((b_addr & 15) / KB);
+  const int b_off = (a_shift + la + 1 + PV - 1) & ~(PV - 1);  // B cover starts 16-byte aligned
+  const Key* a_cov = A - a_shift;
+  const Key* b_cov = B - b_shift;
+  const int a_words = (a_shift + la + PV - 1) & ~(PV - 1), b_words = (b_shift + lb + PV - 1) & ~(PV - 1);
+  const bool a_tma = la > 0 && (a_addr % KB) == 0 && a_cov >= lo && a_cov + a_words <= hi;
+  const bool b_tma = lb > 0 && (b_addr % KB) == 0 && b_cov >= lo && b_cov + b_words <= hi;
 
   if (tid == 0) {
     mbar_init(&bar, 1);
@@ -430,10 +480,10 @@ __global__ void __launch_bounds__(NT, (NT == 256 ? 6 : 1))  // 6 CTAs/SM: measur
   }
   __syncthreads();
   if (tid == 0) {
-    const uint32_t bytes = (a_tma ? a_words * 4u : 0u) + (b_tma ? b_words * 4u : 0u);
+    const uint32_t bytes = (a_tma ? a_words * (uint32_t)KB : 0u) + (b_tma ? b_words * (uint32_t)KB : 0u);
     mbar_arrive_expect_tx(&bar, bytes);
-    if (a_tma) tma_load_1d(sm, a_cov, a_words * 4u, &bar);
-    if (b_tma) tma_load_1d(sm + b_off, b_cov, b_words * 4u, &bar);
+    if (a_tma) tma_load_1d(sm, a_cov, a_words * (uint32_t)KB, &bar);
+    if (b_tma) tma_load_1d(sm + b_off, b_cov, b_words * (uint32_t)KB, &bar);
   }
   if (!a_tma)
     for (int i = tid; i < la; i += NT) sm[a_shift + i] = __ldcs(A + i);
@@ -442,21 +492,21 @@ __global__ void __launch_bounds__(NT, (NT == 256 ? 6 : 1))  // 6 CTAs/SM: measur
   mbar_wait(&bar, 0);
   __syncthreads();
   if (tid == 0) {
-    sm[a_shift + la] = INT_MAX;          // sentinels: the merge loop has no bounds tests
-    sm[b_off + b_shift + lb] = INT_MAX;
+    sm[a_shift + la] = KeyT<Key>::kMax;  // sentinels: the merge loop has no bounds tests
+    sm[b_off + b_shift + lb] = KeyT<Key>::kMax;
   }
   __syncthreads();
 
-  const int32_t* SA = sm + a_shift;
-  const int32_t* SB = sm + b_off + b_shift;
+  const Key* SA = sm + a_shift;
+  const Key* SB = sm + b_off + b_shift;
   const int total = la + lb;
   const int kp = P.kp;
   const int d = min(tid * kp, total);
   const int cnt = min(kp, total - d);
   const int a = merge_path<int>(SA, la, SB, lb, d);
   int ia = a, ib = d - a;
-  int32_t ka = SA[ia], kb = SB[ib];
-  int32_t v[K];
+  Key ka = SA[ia], kb = SB[ib];
+  Key v[K];
 #pragma unroll
   for (int k = 0; k < K; ++k) {
     if (k < cnt) {
@@ -476,13 +526,13 @@ __global__ void __launch_bounds__(NT, (NT == 256 ? 6 : 1))  // 6 CTAs/SM: measur
   for (int k = 0; k < K; ++k)
     if (k < cnt) sm[d + k] = v[k];
 
-  int32_t* out = dst + g.pair_base + g.diag0;
-  const bool o_tma = ((reinterpret_cast<uintptr_t>(out) & 15) == 0) && (total & 3) == 0;
+  Key* out = dst + g.pair_base + g.diag0;
+  const bool o_tma = ((reinterpret_cast<uintptr_t>(out) & 15) == 0) && (total % PV) == 0;
   if (o_tma) {
     fence_proxy_async_smem();
     __syncthreads();
     if (tid == 0) {
-      tma_store_1d(out, sm, (uint32_t)total * 4u);
+      tma_store_1d(out, sm, (uint32_t)total * (uint32_t)KB);
       bulk_commit();
       bulk_wait_read_all();
     }

@@ -9,6 +9,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <type_traits>
 
 #include "common.cuh"
 #include "mergesort.cuh"
@@ -25,11 +26,11 @@ constexpr int kSmNT = 1024, kSmK = 16, kSmT = kSmNT * kSmK;
 static_assert(kSmT == kSmallTile, "small-tile size mismatch");
 
 
-template <int NT, int K, int LEAF>
-static int launch_blocksort(const int32_t* src, int32_t* dst, int64_t n, int stride,
-                            int64_t ctas, cudaStream_t s) {
-  constexpr int smem = padded_words(NT * K) * 4;
-  auto* kern = blocksort_kernel<NT, K, LEAF>;
+template <int NT, int K, int LEAF, class Key>
+static int launch_blocksort(const Key* src, Key* dst, int64_t n, int stride, int64_t ctas,
+                            cudaStream_t s) {
+  constexpr int smem = padded_bytes<Key>(NT * K);
+  auto* kern = blocksort_kernel<NT, K, LEAF, Key>;
   NSB_TRY(ensure_smem_attr(reinterpret_cast<const void*>(kern), smem,
                            "cudaFuncSetAttribute(blocksort)"));
   {
@@ -42,6 +43,9 @@ static int launch_blocksort(const int32_t* src, int32_t* dst, int64_t n, int str
 // Tuning knobs (read once; the defaults are the measured best on B200).
 //   NSB_TILE  = 8192 | 16384 : keys per tile-sort CTA
 constexpr int kV2NT = 256, kV2K = 31, kV2T = kV2NT * kV2K;  // 7936 keys per tile
+// int64 keys: 3840 keys (30 KiB) per tile; K odd keeps the half-warp 64-bit
+// cursor accesses on distinct banks
+constexpr int kV2K64 = 15;
 //   NSB_KWAY  = 0 | 4 | 8 : widest k-way merge pass (0 = pairwise only, default)
 //   NSB_KWAY_MIN = n below which only pairwise passes are used
 struct MergeTuning {
@@ -84,6 +88,12 @@ size_t merge_sort_temp(size_t n) {
   if (n <= (size_t)kSmT) return 0;
   return align_up(n * sizeof(int32_t), 256) + align_up((max_merge_tiles(n) + 1) * 8, 256) +
          kway_temp(n);
+}
+
+// int64: ping-pong buffer + merge-path splits (no k-way scratch)
+size_t merge_sort_temp_i64(size_t n) {
+  if (n <= (size_t)kSmT) return 0;
+  return align_up(n * sizeof(int64_t), 256) + align_up((max_merge_tiles(n) + 1) * 8, 256);
 }
 
 struct KwScratch {
@@ -182,8 +192,8 @@ static PassPlan plan_pass(int64_t n, int64_t R, int nt = kV2NT, int k = kV2K) {
 }
 
 // One pairwise merge pass (v2): runs of R in src -> runs of 2R in dst.
-template <int NT, int K>
-static int v2_pass_t(const int32_t* src, int32_t* dst, int64_t n, int64_t R, int64_t* mp,
+template <int NT, int K, class Key>
+static int v2_pass_t(const Key* src, Key* dst, int64_t n, int64_t R, int64_t* mp,
                      cudaStream_t s) {
   const MergeTuning& tu = tuning();
   const PassPlan P = plan_pass(n, R, NT, K);
@@ -193,18 +203,18 @@ static int v2_pass_t(const int32_t* src, int32_t* dst, int64_t n, int64_t R, int
     // few tiles: every CTA finds its own split (no partition launch)
     {
       Prof prof(PK_MERGE_PASS, s);
-      merge_pass_v2_kernel<NT, K, true><<<(unsigned)mt, NT, 0, s>>>(src, dst, P, nullptr);
+      merge_pass_v2_kernel<NT, K, true, Key><<<(unsigned)mt, NT, 0, s>>>(src, dst, P, nullptr);
     }
     return check_launch("merge_pass_v2_kernel<fused>");
   }
   {
     Prof prof(PK_PARTITION, s);
-    merge_partition_v2_kernel<<<(unsigned)((mt + 255) / 256), 256, 0, s>>>(src, P, mt, mp);
+    merge_partition_v2_kernel<Key><<<(unsigned)((mt + 255) / 256), 256, 0, s>>>(src, P, mt, mp);
   }
   NSB_TRY(check_launch("merge_partition_v2_kernel"));
   {
     Prof prof(PK_MERGE_PASS, s);
-    merge_pass_v2_kernel<NT, K><<<(unsigned)mt, NT, 0, s>>>(src, dst, P, mp);
+    merge_pass_v2_kernel<NT, K, false, Key><<<(unsigned)mt, NT, 0, s>>>(src, dst, P, mp);
   }
   return check_launch("merge_pass_v2_kernel");
 }
@@ -218,15 +228,20 @@ static int v2_pass(const int32_t* src, int32_t* dst, int64_t n, int64_t R, int64
     default: return v2_pass_t<kV2NT, kV2K>(src, dst, n, R, mp, s);
   }
 }
+static int v2_pass(const int64_t* src, int64_t* dst, int64_t n, int64_t R, int64_t* mp,
+                   cudaStream_t s) {
+  return v2_pass_t<kV2NT, kV2K64>(src, dst, n, R, mp, s);
+}
 
 // Pairwise passes over existing sorted runs of length R0 (the last may be
 // shorter) until one run remains; *result = the buffer holding it (keys or tmp).
-int merge_existing_runs(int32_t* keys, int32_t* tmp, size_t n, int64_t R0, void* d_temp,
-                        cudaStream_t s, int32_t** result) {
+template <class Key>
+static int merge_existing_runs_t(Key* keys, Key* tmp, size_t n, int64_t R0, void* d_temp,
+                                 cudaStream_t s, Key** result) {
   int64_t* mp = reinterpret_cast<int64_t*>(static_cast<char*>(d_temp) +
-                                           align_up(n * sizeof(int32_t), 256));
-  int32_t* cur = keys;
-  int32_t* other = tmp;
+                                           align_up(n * sizeof(Key), 256));
+  Key* cur = keys;
+  Key* other = tmp;
   for (int64_t R = R0; R < (int64_t)n; R *= 2) {
     NSB_TRY(v2_pass(cur, other, (int64_t)n, R, mp, s));
     std::swap(cur, other);
@@ -234,9 +249,19 @@ int merge_existing_runs(int32_t* keys, int32_t* tmp, size_t n, int64_t R0, void*
   *result = cur;
   return NS_OK;
 }
+int merge_existing_runs(int32_t* keys, int32_t* tmp, size_t n, int64_t R0, void* d_temp,
+                        cudaStream_t s, int32_t** result) {
+  return merge_existing_runs_t(keys, tmp, n, R0, d_temp, s, result);
+}
+int merge_existing_runs(int64_t* keys, int64_t* tmp, size_t n, int64_t R0, void* d_temp,
+                        cudaStream_t s, int64_t** result) {
+  return merge_existing_runs_t(keys, tmp, n, R0, d_temp, s, result);
+}
 
-int merge_sort_device(int32_t* d_keys, size_t n, int leaf, void* d_temp, size_t temp_bytes,
-                      cudaStream_t s) {
+template <class Key>
+static int merge_sort_device_t(Key* d_keys, size_t n, int leaf, void* d_temp, size_t temp_bytes,
+                               cudaStream_t s) {
+  constexpr bool k32 = std::is_same_v<Key, int32_t>;
   if (n <= 1) return NS_OK;
   if (n <= (size_t)kSmT) {
     // one CTA sized to the array: fewer threads and merge levels for small n
@@ -249,53 +274,62 @@ int merge_sort_device(int32_t* d_keys, size_t n, int leaf, void* d_temp, size_t 
       return launch_blocksort<kSmNT, kSmK, LF>(d_keys, d_keys, (int64_t)n, kSmT, 1, s);
     });
   }
-  if (temp_bytes < merge_sort_temp(n) || d_temp == nullptr) return NS_ERR_TEMP;
-  int32_t* tmp = static_cast<int32_t*>(d_temp);
+  const size_t need = k32 ? merge_sort_temp(n) : merge_sort_temp_i64(n);
+  if (temp_bytes < need || d_temp == nullptr) return NS_ERR_TEMP;
+  Key* tmp = static_cast<Key*>(d_temp);
   int64_t* mp = reinterpret_cast<int64_t*>(static_cast<char*>(d_temp) +
-                                           align_up(n * sizeof(int32_t), 256));
+                                           align_up(n * sizeof(Key), 256));
   const MergeTuning& tu = tuning();
-  const int T = tu.tile;
+  const int T = k32 ? tu.tile : kBsT;
   const int64_t tiles = (int64_t)((n + T - 1) / T);
   // pass schedule: k-way passes (k = 8 for 5+ runs, 4 for 3-4) on large
-  // inputs, pairwise v2 passes otherwise
+  // int32 inputs when enabled, pairwise v2 passes otherwise
   int sched[64];
   int npass = 0;
   for (int64_t runs = tiles; runs > 1;) {
     int k = 2;
-    if (tu.kway >= 4 && (int64_t)n >= tu.kway_min && runs >= 3)
+    if (k32 && tu.kway >= 4 && (int64_t)n >= tu.kway_min && runs >= 3)
       k = (tu.kway >= 8 && runs >= 5) ? 8 : 4;
     sched[npass++] = k;
     runs = (runs + k - 1) / k;
   }
   const int passes = npass;
   // Pick the tile-sort destination so the last pass lands in d_keys.
-  int32_t* cur = (passes & 1) ? tmp : d_keys;
-  int32_t* other = (cur == d_keys) ? tmp : d_keys;
+  Key* cur = (passes & 1) ? tmp : d_keys;
+  Key* other = (cur == d_keys) ? tmp : d_keys;
   NSB_TRY(with_leaf(leaf, [&](auto L) {
     constexpr int LF = decltype(L)::value;
     return T == kSmT ? launch_blocksort<kSmNT, kSmK, LF>(d_keys, cur, (int64_t)n, T, tiles, s)
                      : launch_blocksort<kBsNT, kBsK, LF>(d_keys, cur, (int64_t)n, T, tiles, s);
   }));
-  {
-    const KwScratch ks = carve_kway(reinterpret_cast<char*>(mp) +
-                                        align_up((max_merge_tiles(n) + 1) * 8, 256),
-                                    n);
-    int64_t R = T;
-    for (int pi = 0; pi < npass; ++pi) {
-      const int k = sched[pi];
+  int64_t R = T;
+  for (int pi = 0; pi < npass; ++pi) {
+    const int k = sched[pi];
+    if constexpr (k32) {
       if (k > 2) {
+        const KwScratch ks = carve_kway(reinterpret_cast<char*>(mp) +
+                                            align_up((max_merge_tiles(n) + 1) * 8, 256),
+                                        n);
         NSB_TRY(kway_pass(cur, other, (int64_t)n, R, k, ks, s));
         std::swap(cur, other);
         R *= k;
         continue;
       }
-      NSB_TRY(v2_pass(cur, other, (int64_t)n, R, mp, s));
-      std::swap(cur, other);
-      R *= 2;
     }
-    return NS_OK;
+    NSB_TRY(v2_pass(cur, other, (int64_t)n, R, mp, s));
+    std::swap(cur, other);
+    R *= 2;
   }
   return NS_OK;
+}
+
+int merge_sort_device(int32_t* d_keys, size_t n, int leaf, void* d_temp, size_t temp_bytes,
+                      cudaStream_t s) {
+  return merge_sort_device_t(d_keys, n, leaf, d_temp, temp_bytes, s);
+}
+int merge_sort_device(int64_t* d_keys, size_t n, int leaf, void* d_temp, size_t temp_bytes,
+                      cudaStream_t s) {
+  return merge_sort_device_t(d_keys, n, leaf, d_temp, temp_bytes, s);
 }
 
 int tile_sort_segments(int32_t* d_keys, size_t num_segments, size_t seg_len, int leaf,
@@ -519,12 +553,18 @@ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
   return z ^ (z >> 31);
 }
 
-__global__ void digest_kernel(const int32_t* __restrict__ keys, int64_t n,
+// key bit pattern fed to the digest mix: uint32 for int32 (oracle_multiset_
+// digest_i32), the full 64 bits for int64
+__device__ __forceinline__ uint64_t key_bits(int32_t k) { return (uint64_t)(uint32_t)k; }
+__device__ __forceinline__ uint64_t key_bits(int64_t k) { return (uint64_t)k; }
+
+template <class Key>
+__global__ void digest_kernel(const Key* __restrict__ keys, int64_t n,
                               unsigned long long* __restrict__ out) {
   unsigned long long s = 0, x = 0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const uint64_t m = mix64((uint64_t)(uint32_t)keys[i] + 0x9E3779B97F4A7C15ull);
+    const uint64_t m = mix64(key_bits(keys[i]) + 0x9E3779B97F4A7C15ull);
     s += m;
     x ^= m;
   }
@@ -539,7 +579,8 @@ __global__ void digest_kernel(const int32_t* __restrict__ keys, int64_t n,
   }
 }
 
-__global__ void inversions_kernel(const int32_t* __restrict__ keys, int64_t n,
+template <class Key>
+__global__ void inversions_kernel(const Key* __restrict__ keys, int64_t n,
                                   unsigned long long* __restrict__ out) {
   unsigned long long c = 0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i + 1 < n;
@@ -616,6 +657,16 @@ int ns_merge_sort_i32(int32_t* d_keys, size_t n, uint32_t width_mask, int varsor
                            static_cast<cudaStream_t>(stream));
 }
 
+size_t ns_merge_sort_temp_bytes_i64(size_t n) { return merge_sort_temp_i64(n); }
+
+int ns_merge_sort_i64(int64_t* d_keys, size_t n, uint32_t width_mask, int varsort_max,
+                      void* d_temp, size_t temp_bytes, void* stream) {
+  if (n > 0 && d_keys == nullptr) return NS_ERR_INVALID;
+  if (n > (size_t)INT64_MAX / 8) return NS_ERR_INVALID;
+  return merge_sort_device(d_keys, n, leaf_of(width_mask, varsort_max), d_temp, temp_bytes,
+                           static_cast<cudaStream_t>(stream));
+}
+
 int ns_sort_small_batch_i32(int32_t* d_keys, const uint32_t* d_offsets, size_t num_arrays,
                             void* stream) {
   if (num_arrays == 0) return NS_OK;
@@ -675,6 +726,25 @@ int ns_multiset_digest_i32(const int32_t* d_keys, size_t n, uint64_t* d_out, voi
 }
 
 int ns_count_inversions_i32(const int32_t* d_keys, size_t n, unsigned long long* d_out,
+                            void* stream) {
+  if (!d_out || (n && !d_keys)) return NS_ERR_INVALID;
+  if (n < 2) return NS_OK;
+  Prof prof(PK_CHECK, static_cast<cudaStream_t>(stream));
+  inversions_kernel<<<grid_for((int64_t)n, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      d_keys, (int64_t)n, d_out);
+  return check_launch("inversions_kernel");
+}
+
+int ns_multiset_digest_i64(const int64_t* d_keys, size_t n, uint64_t* d_out, void* stream) {
+  if (!d_out || (n && !d_keys)) return NS_ERR_INVALID;
+  if (n == 0) return NS_OK;
+  Prof prof(PK_CHECK, static_cast<cudaStream_t>(stream));
+  digest_kernel<<<grid_for((int64_t)n, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      d_keys, (int64_t)n, reinterpret_cast<unsigned long long*>(d_out));
+  return check_launch("digest_kernel");
+}
+
+int ns_count_inversions_i64(const int64_t* d_keys, size_t n, unsigned long long* d_out,
                             void* stream) {
   if (!d_out || (n && !d_keys)) return NS_ERR_INVALID;
   if (n < 2) return NS_OK;

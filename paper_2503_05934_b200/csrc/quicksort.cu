@@ -251,22 +251,23 @@ __global__ void __launch_bounds__(kQsNT)
 }
 
 // One CTA per job (start, len <= T): sorts src[start..start+len) into dst.
-template <int NT, int K, int LEAF>
+template <int NT, int K, int LEAF, class Key>
 __global__ void __launch_bounds__(NT)
-    bucket_sort_kernel(const int32_t* __restrict__ src, int32_t* __restrict__ dst,
+    bucket_sort_kernel(const Key* __restrict__ src, Key* __restrict__ dst,
                        const int64_t* __restrict__ jobs) {
-  extern __shared__ __align__(16) int32_t sm[];
+  extern __shared__ __align__(16) unsigned char bsm_raw[];
+  Key* sm = reinterpret_cast<Key*>(bsm_raw);
   const int64_t start = jobs[2 * blockIdx.x];
   const int len = (int)jobs[2 * blockIdx.x + 1];
   cta_sort<NT, K, LEAF>(src + start, dst + start, len, sm);
 }
 
-template <int NT, int K, int LEAF>
-static int launch_bucket_sort(const int32_t* src, int32_t* dst, const int64_t* jobs, int njobs,
+template <int NT, int K, int LEAF, class Key>
+static int launch_bucket_sort(const Key* src, Key* dst, const int64_t* jobs, int njobs,
                               cudaStream_t s) {
   if (njobs == 0) return NS_OK;
-  constexpr int smem = padded_words(NT * K) * 4;
-  auto* kern = bucket_sort_kernel<NT, K, LEAF>;
+  constexpr int smem = padded_bytes<Key>(NT * K);
+  auto* kern = bucket_sort_kernel<NT, K, LEAF, Key>;
   NSB_TRY(ensure_smem_attr(reinterpret_cast<const void*>(kern), smem,
                            "cudaFuncSetAttribute(bucket_sort)"));
   {
@@ -276,7 +277,8 @@ static int launch_bucket_sort(const int32_t* src, int32_t* dst, const int64_t* j
   return check_launch("bucket_sort_kernel");
 }
 
-static int small_sort(int32_t* d_keys, size_t n, int leaf, cudaStream_t s) {
+template <class Key>
+static int small_sort(Key* d_keys, size_t n, int leaf, cudaStream_t s) {
   // n <= kSmallTile: one CTA, in place (merge_sort_device's single-CTA path)
   return merge_sort_device(d_keys, n, leaf, nullptr, 0, s);
 }
@@ -412,10 +414,11 @@ struct MlSeg {
   int64_t smp_off;
 };
 
+template <class Key>
 struct MlAux {
   MlSeg* segs;
-  int32_t* samples;
-  int32_t* spl;
+  Key* samples;
+  Key* spl;
   uint32_t* counts;
   unsigned long long* fill;
   int64_t* jobs;
@@ -425,15 +428,16 @@ struct MlAux {
 static size_t ml_max_segs(size_t n) { return n / (kSmallTile + 1) + 4; }
 static size_t ml_max_spl(size_t n) { return n / 2048 + 2 * kMlMaxB * ml_max_segs(n) / 64 + 1024; }
 
-static size_t ml_aux_bytes(size_t n) {
+static size_t ml_aux_bytes(size_t n, size_t kb = 4) {
   const size_t segs = ml_max_segs(n), spl = n / 2048 + 512 * segs / 64 + 4096;
-  return align_up(segs * sizeof(MlSeg), 256) + align_up(16 * spl * 4, 256) +
-         align_up(spl * 4, 256) + align_up(2 * spl * 4, 256) + align_up(2 * spl * 8, 256) +
+  return align_up(segs * sizeof(MlSeg), 256) + align_up(16 * spl * kb, 256) +
+         align_up(spl * kb, 256) + align_up(2 * spl * 4, 256) + align_up(2 * spl * 8, 256) +
          align_up(2 * (2 * spl + segs) * 8, 256);
 }
 
-static MlAux carve_ml(char* p, size_t n) {
-  MlAux a;
+template <class Key>
+static MlAux<Key> carve_ml(char* p, size_t n) {
+  MlAux<Key> a;
   a.max_segs = ml_max_segs(n);
   a.max_spl = n / 2048 + 512 * a.max_segs / 64 + 4096;
   a.max_samples = 16 * a.max_spl;
@@ -441,10 +445,10 @@ static MlAux carve_ml(char* p, size_t n) {
   a.max_jobs = 2 * a.max_spl + a.max_segs;
   a.segs = reinterpret_cast<MlSeg*>(p);
   p += align_up(a.max_segs * sizeof(MlSeg), 256);
-  a.samples = reinterpret_cast<int32_t*>(p);
-  p += align_up(a.max_samples * 4, 256);
-  a.spl = reinterpret_cast<int32_t*>(p);
-  p += align_up(a.max_spl * 4, 256);
+  a.samples = reinterpret_cast<Key*>(p);
+  p += align_up(a.max_samples * sizeof(Key), 256);
+  a.spl = reinterpret_cast<Key*>(p);
+  p += align_up(a.max_spl * sizeof(Key), 256);
   a.counts = reinterpret_cast<uint32_t*>(p);
   p += align_up(a.max_cnt * 4, 256);
   a.fill = reinterpret_cast<unsigned long long*>(p);
@@ -473,8 +477,9 @@ __device__ __forceinline__ int seg_of_sample(const MlSeg* segs, int nseg, int64_
   return lo;
 }
 
-__global__ void ml_sample_kernel(const int32_t* __restrict__ X, const MlSeg* __restrict__ segs,
-                                 int nseg, int64_t total, int32_t* __restrict__ samples) {
+template <class Key>
+__global__ void ml_sample_kernel(const Key* __restrict__ X, const MlSeg* __restrict__ segs,
+                                 int nseg, int64_t total, Key* __restrict__ samples) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= total) return;
   const MlSeg sg = segs[seg_of_sample(segs, nseg, i)];
@@ -485,20 +490,21 @@ __global__ void ml_sample_kernel(const int32_t* __restrict__ X, const MlSeg* __r
   samples[i] = X[sg.start + pos];
 }
 
-__global__ void ml_splitter_kernel(const int32_t* __restrict__ samples,
+template <class Key>
+__global__ void ml_splitter_kernel(const Key* __restrict__ samples,
                                    const MlSeg* __restrict__ segs, int nseg,
-                                   int32_t* __restrict__ spl) {
+                                   Key* __restrict__ spl) {
   const int sgi = blockIdx.x;
   if (sgi >= nseg) return;
   const MlSeg sg = segs[sgi];
   const int S = kQsOversample * sg.B;
   for (int j = threadIdx.x; j < sg.B; j += blockDim.x)
     spl[sg.spl_off + j] =
-        j < sg.B - 1 ? samples[sg.smp_off + (int64_t)(j + 1) * S / sg.B - 1] : INT_MAX;
+        j < sg.B - 1 ? samples[sg.smp_off + (int64_t)(j + 1) * S / sg.B - 1] : KeyT<Key>::kMax;
 }
 
-template <int LOGB>
-__device__ __forceinline__ int ml_classify(const int32_t* spl, int32_t key) {
+template <int LOGB, class Key>
+__device__ __forceinline__ int ml_classify(const Key* spl, Key key) {
   constexpr int B = 1 << LOGB;
   int j = 0;
 #pragma unroll
@@ -531,8 +537,8 @@ __device__ __forceinline__ unsigned warp_peers(int b) {
   return m;
 }
 
-template <int LOGB>
-__device__ __forceinline__ void ml_warp_hist(const int32_t* spl, const int32_t (&k)[kMlPer],
+template <int LOGB, class Key>
+__device__ __forceinline__ void ml_warp_hist(const Key* spl, const Key (&k)[kMlPer],
                                              int (&bk)[kMlPer], int64_t c0, int64_t c1,
                                              uint32_t* row) {
   const int lane = threadIdx.x & 31;
@@ -546,15 +552,15 @@ __device__ __forceinline__ void ml_warp_hist(const int32_t* spl, const int32_t (
   }
 }
 
-template <int LOGB>
-__device__ __noinline__ void ml_count_body(const int32_t* __restrict__ X, const MlSeg& sg,
-                                              const int32_t* spl, uint32_t (*wh)[2 * kMlMaxB],
+template <int LOGB, class Key>
+__device__ __noinline__ void ml_count_body(const Key* __restrict__ X, const MlSeg& sg,
+                                              const Key* spl, uint32_t (*wh)[2 * kMlMaxB],
                                               uint32_t* __restrict__ counts) {
   const int NB = 2 * sg.B - 1;
   const int warp = threadIdx.x >> 5;
   const int64_t c0 = sg.start + (blockIdx.x - sg.chunk0) * (int64_t)kMlChunk;
   const int64_t c1 = min(sg.start + sg.len, c0 + kMlChunk);
-  int32_t k[kMlPer];
+  Key k[kMlPer];
   int bk[kMlPer];
 #pragma unroll
   for (int u = 0; u < kMlPer; ++u) {
@@ -583,10 +589,11 @@ __device__ __noinline__ void ml_count_body(const int32_t* __restrict__ X, const 
     default: CALL(8); break;              \
   }
 
+template <class Key>
 __global__ void __launch_bounds__(kMlNT)
-    ml_count_kernel(const int32_t* __restrict__ X, const MlSeg* __restrict__ segs, int nseg,
-                    const int32_t* __restrict__ gspl, uint32_t* __restrict__ counts) {
-  __shared__ int32_t spl[kMlMaxB];
+    ml_count_kernel(const Key* __restrict__ X, const MlSeg* __restrict__ segs, int nseg,
+                    const Key* __restrict__ gspl, uint32_t* __restrict__ counts) {
+  __shared__ Key spl[kMlMaxB];
   __shared__ uint32_t wh[kMlWarps][2 * kMlMaxB];
   const MlSeg sg = segs[seg_of_chunk(segs, nseg, blockIdx.x)];
   for (int i = threadIdx.x; i < sg.B; i += kMlNT) spl[i] = gspl[sg.spl_off + i];
@@ -597,17 +604,17 @@ __global__ void __launch_bounds__(kMlNT)
 #undef NSB_COUNT_CALL
 }
 
-template <int LOGB>
-__device__ __noinline__ void ml_scatter_body(const int32_t* __restrict__ X, const MlSeg& sg,
-                                                const int32_t* spl,
+template <int LOGB, class Key>
+__device__ __noinline__ void ml_scatter_body(const Key* __restrict__ X, const MlSeg& sg,
+                                                const Key* spl,
                                                 uint32_t (*wh)[2 * kMlMaxB],
                                                 unsigned long long* __restrict__ fill,
-                                                int32_t* __restrict__ Y) {
+                                                Key* __restrict__ Y) {
   const int NB = 2 * sg.B - 1;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t c0 = sg.start + (blockIdx.x - sg.chunk0) * (int64_t)kMlChunk;
   const int64_t c1 = min(sg.start + sg.len, c0 + kMlChunk);
-  int32_t k[kMlPer];
+  Key k[kMlPer];
   int bk[kMlPer];
 #pragma unroll
   for (int u = 0; u < kMlPer; ++u) {
@@ -634,7 +641,7 @@ __device__ __noinline__ void ml_scatter_body(const int32_t* __restrict__ X, cons
   }
   __syncthreads();
   uint32_t* row = wh[warp];
-  int32_t* Ys = Y + sg.start;
+  Key* Ys = Y + sg.start;
 #pragma unroll
   for (int u = 0; u < kMlPer; ++u) {
     const int b = bk[u];
@@ -651,11 +658,12 @@ __device__ __noinline__ void ml_scatter_body(const int32_t* __restrict__ X, cons
   }
 }
 
+template <class Key>
 __global__ void __launch_bounds__(kMlNT)
-    ml_scatter_kernel(const int32_t* __restrict__ X, const MlSeg* __restrict__ segs, int nseg,
-                      const int32_t* __restrict__ gspl, unsigned long long* __restrict__ fill,
-                      int32_t* __restrict__ Y) {
-  __shared__ int32_t spl[kMlMaxB];
+    ml_scatter_kernel(const Key* __restrict__ X, const MlSeg* __restrict__ segs, int nseg,
+                      const Key* __restrict__ gspl, unsigned long long* __restrict__ fill,
+                      Key* __restrict__ Y) {
+  __shared__ Key spl[kMlMaxB];
   __shared__ uint32_t wh[kMlWarps][2 * kMlMaxB];  // counts, then cursors (rel. to seg start)
   const MlSeg sg = segs[seg_of_chunk(segs, nseg, blockIdx.x)];
   for (int i = threadIdx.x; i < sg.B; i += kMlNT) spl[i] = gspl[sg.spl_off + i];
@@ -667,17 +675,19 @@ __global__ void __launch_bounds__(kMlNT)
 }
 
 // Copies jobs (start, len) from src to dst (constant "equal" buckets).
-__global__ void copy_jobs_kernel(const int32_t* __restrict__ src, int32_t* __restrict__ dst,
+template <class Key>
+__global__ void copy_jobs_kernel(const Key* __restrict__ src, Key* __restrict__ dst,
                                  const int64_t* __restrict__ jobs) {
   const int64_t st = jobs[2 * blockIdx.x], len = jobs[2 * blockIdx.x + 1];
   for (int64_t i = threadIdx.x; i < len; i += blockDim.x) dst[st + i] = src[st + i];
 }
 
-static int ml_quick_sort(int32_t* keys, int32_t* tmp, size_t n, int leaf, const MlAux& ax,
+template <class Key>
+static int ml_quick_sort(Key* keys, Key* tmp, size_t n, int leaf, const MlAux<Key>& ax,
                          cudaStream_t s) {
   std::vector<std::pair<int64_t, int64_t>> cur{{0, (int64_t)n}};
-  int32_t* X = keys;
-  int32_t* Y = tmp;
+  Key* X = keys;
+  Key* Y = tmp;
   std::vector<MlSeg> segs;
   std::vector<uint32_t> counts;
   std::vector<unsigned long long> fill;
@@ -713,7 +723,7 @@ static int ml_quick_sort(int32_t* keys, int32_t* tmp, size_t n, int leaf, const 
     // ---- splitters: sample, sort each segment's samples on chip, pick
     {
       Prof prof(PK_QS_SAMPLE, s);
-      ml_sample_kernel<<<(unsigned)((smp + 255) / 256), 256, 0, s>>>(X, ax.segs, nseg, smp,
+      ml_sample_kernel<Key><<<(unsigned)((smp + 255) / 256), 256, 0, s>>>(X, ax.segs, nseg, smp,
                                                                        ax.samples);
     }
     NSB_TRY(check_launch("ml_sample_kernel"));
@@ -728,14 +738,14 @@ static int ml_quick_sort(int32_t* keys, int32_t* tmp, size_t n, int leaf, const 
     NSB_TRY((launch_bucket_sort<256, 16, 8>(ax.samples, ax.samples, ax.jobs, nseg, s)));
     {
       Prof prof(PK_QS_SAMPLE, s);
-      ml_splitter_kernel<<<nseg, 256, 0, s>>>(ax.samples, ax.segs, nseg, ax.spl);
+      ml_splitter_kernel<Key><<<nseg, 256, 0, s>>>(ax.samples, ax.segs, nseg, ax.spl);
     }
     NSB_TRY(check_launch("ml_splitter_kernel"));
     // ---- count
     NSB_TRY(check_cuda(cudaMemsetAsync(ax.counts, 0, cnt * 4, s), "memset"));
     {
       Prof prof(PK_QS_COUNT, s);
-      ml_count_kernel<<<(unsigned)chunks, kMlNT, 0, s>>>(X, ax.segs, nseg, ax.spl, ax.counts);
+      ml_count_kernel<Key><<<(unsigned)chunks, kMlNT, 0, s>>>(X, ax.segs, nseg, ax.spl, ax.counts);
     }
     NSB_TRY(check_launch("ml_count_kernel"));
     // One device->host read per LEVEL: bucket sizes drive the plan, as the
@@ -777,7 +787,7 @@ static int ml_quick_sort(int32_t* keys, int32_t* tmp, size_t n, int leaf, const 
                        "H2D(fill)"));
     {
       Prof prof(PK_QS_SCATTER, s);
-      ml_scatter_kernel<<<(unsigned)chunks, kMlNT, 0, s>>>(X, ax.segs, nseg, ax.spl, ax.fill, Y);
+      ml_scatter_kernel<Key><<<(unsigned)chunks, kMlNT, 0, s>>>(X, ax.segs, nseg, ax.spl, ax.fill, Y);
     }
     NSB_TRY(check_launch("ml_scatter_kernel"));
     // ---- leaf buckets -> key buffer
@@ -803,7 +813,7 @@ static int ml_quick_sort(int32_t* keys, int32_t* tmp, size_t n, int leaf, const 
       return launch_bucket_sort<1024, 16, LF>(Y, keys, ax.jobs + 2 * off[3], off[4] - off[3], s);
     }));
     if (off[5] > off[4]) {
-      copy_jobs_kernel<<<off[5] - off[4], 256, 0, s>>>(Y, keys, ax.jobs + 2 * off[4]);
+      copy_jobs_kernel<Key><<<off[5] - off[4], 256, 0, s>>>(Y, keys, ax.jobs + 2 * off[4]);
       NSB_TRY(check_launch("copy_jobs_kernel"));
     }
     // the jobs/fill/segs buffers are rewritten by the next level: the stream
@@ -818,6 +828,13 @@ static int ml_quick_sort(int32_t* keys, int32_t* tmp, size_t n, int leaf, const 
 size_t quick_sort_temp(size_t n) {
   if (n <= (size_t)kSmallTile) return 0;
   return align_up(n * 4, 256) + std::max(qs_aux_bytes(), ml_aux_bytes(n));
+}
+
+// int64 keys always take the multi-level partition (its classifier is a
+// plain splitter search; the single-level prefix table is int32-specific)
+size_t quick_sort_temp_i64(size_t n) {
+  if (n <= (size_t)kSmallTile) return 0;
+  return align_up(n * 8, 256) + ml_aux_bytes(n, 8);
 }
 
 }  // namespace nsb
@@ -848,7 +865,22 @@ int ns_quick_sort_i32(int32_t* d_keys, size_t n, uint32_t width_mask, int varsor
   }();
   const bool single = mode == 1 || (mode == 0 && n <= (size_t(1) << 25));
   if (single) return quick_sort_level(d_keys, tmp, n, leaf, carve_aux(auxp), s);
-  return ml_quick_sort(d_keys, tmp, n, leaf, carve_ml(auxp, n), s);
+  return ml_quick_sort(d_keys, tmp, n, leaf, carve_ml<int32_t>(auxp, n), s);
+}
+
+size_t ns_quick_sort_temp_bytes_i64(size_t n) { return quick_sort_temp_i64(n); }
+
+int ns_quick_sort_i64(int64_t* d_keys, size_t n, uint32_t width_mask, int varsort_max,
+                      void* d_temp, size_t temp_bytes, void* stream) {
+  if (n > 0 && d_keys == nullptr) return NS_ERR_INVALID;
+  if (n <= 1) return NS_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int leaf = leaf_of(width_mask, varsort_max);
+  if (n <= (size_t)kSmallTile) return small_sort(d_keys, n, leaf, s);
+  if (!d_temp || temp_bytes < quick_sort_temp_i64(n)) return NS_ERR_TEMP;
+  int64_t* tmp = static_cast<int64_t*>(d_temp);
+  char* auxp = static_cast<char*>(d_temp) + align_up(n * 8, 256);
+  return ml_quick_sort(d_keys, tmp, n, leaf, carve_ml<int64_t>(auxp, n), s);
 }
 
 }  // extern "C"

@@ -112,7 +112,7 @@ __global__ void __launch_bounds__(NT)
   }
   __syncthreads();
   const int diag = min(tid * K, total);
-  const SmemRun SA{sm, 0}, SB{sm, la};
+  const SmemRun<int32_t> SA{sm, 0}, SB{sm, la};
   const int a = merge_path<int>(SA, la, SB, lb, diag);
   int32_t v[K];
   serial_merge<K>(SA, la, SB, lb, a, diag - a, v);

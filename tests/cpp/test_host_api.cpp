@@ -6,6 +6,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <numeric>
 #include <random>
 #include <stdexcept>
@@ -152,6 +153,43 @@ static void device_side() {
   cudaMemcpy(back.data(), d, big.size() * 4, cudaMemcpyDeviceToHost);
   CHECK(back == e);
   cudaFree(d);
+
+  // int64: the reference's benchmark type, bound exactly as measure_loop's
+  // sort_fn (std::function<void(std::span<std::int64_t>)>, bench.hpp:58-61;
+  // bench.cpp:94-96 binds it to run_variant)
+  std::mt19937_64 rng64(99);
+  for (size_t n : {0u, 1u, 5u, 8u, 100u, 4097u, 70000u, 300000u}) {
+    std::vector<int64_t> in(n);
+    for (auto& x : in) x = static_cast<int64_t>(rng64());  // full 64-bit range, as datagen.cpp:27-29
+    auto expect = in;
+    std::sort(expect.begin(), expect.end());
+    for (const auto& var : ns::bundled_variants()) {
+      auto v = in;
+      std::function<void(std::span<std::int64_t>)> sort_fn =
+          [&var](std::span<std::int64_t> s) { ns::run_variant(var, s); };
+      sort_fn(std::span<int64_t>(v));
+      CHECK(v == expect);
+    }
+  }
+  {
+    const size_t n = size_t(1) << 21;
+    std::vector<int64_t> h(n);
+    for (auto& x : h) x = static_cast<int64_t>(rng64());
+    auto e64 = h;
+    std::sort(e64.begin(), e64.end());
+    int64_t* d64 = nullptr;
+    CHECK(cudaMalloc(&d64, n * 8) == cudaSuccess);
+    std::vector<int64_t> back64(n);
+    cudaMemcpy(d64, h.data(), n * 8, cudaMemcpyHostToDevice);
+    ns::device_merge_sort(d64, n, *ns::find_config("6To8"), scratch);
+    cudaMemcpy(back64.data(), d64, n * 8, cudaMemcpyDeviceToHost);
+    CHECK(back64 == e64);
+    cudaMemcpy(d64, h.data(), n * 8, cudaMemcpyHostToDevice);
+    ns::device_quick_sort(d64, n, *ns::find_config("3To5"), scratch);
+    cudaMemcpy(back64.data(), d64, n * 8, cudaMemcpyDeviceToHost);
+    CHECK(back64 == e64);
+    cudaFree(d64);
+  }
 }
 
 int main(int argc, char** argv) {

@@ -71,6 +71,36 @@ def main() -> None:
             for n in (0, 1, 2, 3, 5, 7, 8, 13, 33, 64, 501, 1000, 8193, 20000):
                 add(algo, cfg, "random", n, seed=3000 + n)
 
+    # int64: the reference's OWN generator stream
+    # (generate(), datagen.cpp:18-50, full 64-bit values) sorted by the
+    # reference's int64 instantiation — the type its benchmarks use.
+    cases_i64 = []
+
+    def add64(algo, cfg, dist, n, seed=42):
+        a = np.empty(n, np.int64)
+        O.ref().ref_generate_i64(O.KIND[dist], n, seed, 0.01, a)
+        out = a.copy()
+        mask, vs = O.CONFIGS[cfg]
+        (O.ref().ref_merge_sort_i64 if algo == "merge" else O.ref().ref_quick_sort_i64)(
+            out, n, mask, vs, None)
+        rec = {"algo": algo, "config": cfg, "dist": dist, "n": n, "seed": seed,
+               "input_sha256": sha(a), "output_sha256": sha(out)}
+        if n <= 64:
+            rec["input"] = [str(x) for x in a.tolist()]
+            rec["output"] = [str(x) for x in out.tolist()]
+        cases_i64.append(rec)
+
+    for n in (10_000, 25_000, 100_000, 1_000_000, 16_777_216):
+        for d in ("random", "sorted", "nearly_sorted"):
+            add64("merge", "6To8", d, n)
+    for n in (10_000, 1_000_000, 16_777_216):
+        for d in ("sorted", "random"):
+            add64("quick", "3To5", d, n)
+    for cfg, _, _ in O.REGISTRY:
+        for algo in ("merge", "quick"):
+            for n in (0, 1, 2, 5, 8, 33, 1000, 20000):
+                add64(algo, cfg, "random", n, seed=5000 + n)
+
     # BASELINE config 2: base-case batch, 2^24 ragged arrays
     offs, keys = O.generate_batch_i32(1 << 24, 42)
     out = keys.copy()
@@ -102,7 +132,7 @@ def main() -> None:
                           for s in (0, 42)}}
     gold = {"generator": "oracle.generate_i32 (int32(next()>>33) | ramp | ramp+swaps)",
             "reference_build": "oracle/Makefile ref -> oracle/_ref/libnetsort_ref.so",
-            "cases": cases, "batch": batch, "small_batch": small_batch,
+            "cases": cases, "cases_i64": cases_i64, "batch": batch, "small_batch": small_batch,
             "segmented": segmented, "kat": kat}
     path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden.json")
     with open(path, "w") as f:

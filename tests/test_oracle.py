@@ -253,3 +253,54 @@ def test_multiset_digest_is_order_independent(oracle):
     b = a.copy()
     b[0] ^= 1
     assert oracle.multiset_digest(a) != oracle.multiset_digest(b)
+
+
+# ---- int64 keys: the reference's own benchmark type -
+
+def test_golden_i64_reference_outputs(oracle, golden):
+    """The oracle's int64 instantiation reproduces the reference's int64 sorts
+    of the reference's own generate() stream (full 64-bit values)."""
+    for c in golden["cases_i64"]:
+        if c["n"] > 1_000_000:
+            continue
+        a = oracle.generate_i64(c["dist"], c["n"], c["seed"])
+        assert sha(a) == c["input_sha256"], c
+        if "input" in c:
+            assert [str(x) for x in a.tolist()] == c["input"]
+        fn = oracle.merge_sort if c["algo"] == "merge" else oracle.quick_sort
+        out = fn(a, c["config"])
+        assert out.dtype == np.int64
+        assert sha(out) == c["output_sha256"], (c["algo"], c["config"], c["dist"], c["n"])
+        if "output" in c:
+            assert [str(x) for x in out.tolist()] == c["output"]
+
+
+@pytest.mark.skipif("not __import__('oracle.oracle').oracle.ref_available()")
+def test_dispatch_counters_match_reference_i64(oracle):
+    R = oracle.ref()
+    for name, mask, vs in oracle.REGISTRY:
+        for n in (1, 2, 7, 13, 1000, 25000):
+            a = oracle.generate_i64("random", n, 17 + n)
+            for algo in ("merge", "quick"):
+                out, st = (oracle.merge_sort if algo == "merge" else oracle.quick_sort)(
+                    a, name, stats=True)
+                ref_out = a.copy()
+                rs = np.zeros(12, np.uint64)
+                (R.ref_merge_sort_i64 if algo == "merge" else R.ref_quick_sort_i64)(
+                    ref_out, n, mask, vs, rs.ctypes.data)
+                assert np.array_equal(out, ref_out)
+                assert list(st.network_hits) == rs[:9].tolist(), (name, algo, n)
+                assert st.merges == rs[9] and st.partitions == rs[10]
+                assert st.max_depth == rs[11]
+
+
+def test_i64_extremes_and_digest(oracle):
+    ext = np.array([2**63 - 1, -2**63, 0, -1, 1, 2**63 - 1, -2**63, 2**31, -2**31 - 1], np.int64)
+    for fn in (oracle.merge_sort, oracle.quick_sort):
+        assert np.array_equal(fn(ext, "6To8"), np.sort(ext))
+    a = oracle.generate_i64("random", 5000, 9)
+    assert oracle.multiset_digest(a) == oracle.multiset_digest(np.sort(a))
+    # int64 keys that agree in their low 32 bits still digest differently
+    b = a.copy()
+    b[0] ^= 1 << 40
+    assert oracle.multiset_digest(a) != oracle.multiset_digest(b)
