@@ -421,11 +421,27 @@ __global__ void merge_partition_v2_kernel(const Key* __restrict__ src, PassPlan 
 // alignment slack each, a sentinel after each, 16-byte rounding.
 __host__ __device__ constexpr int v2_smem_words(int TM) { return TM + 16; }
 
+// Resident CTAs per SM the launch bounds ask for: as many as shared memory
+// (228 KiB per SM, 1 KiB reserved per CTA), the 2048-thread limit and a
+// register floor allow.  <256,31>: 6 CTAs/SM at 40 registers (measured
+// best; 7 CTAs force 32 registers and spill).
+__host__ __device__ constexpr int v2_min_blocks(int NT, int K, int key_bytes) {
+  const int smem = (NT * K + 16) * key_bytes + 1024;
+  int b = 228 * 1024 / smem;
+  if (b > 2048 / NT) b = 2048 / NT;
+  // the K outputs stay in registers until the store (2 registers per int64)
+  const int regs = key_bytes == 8 ? 2 * K + 17 : (K <= 31 ? 40 : K + 17);
+  if (b > 65536 / (NT * regs)) b = 65536 / (NT * regs);
+  if (b > 32) b = 32;
+  return b < 1 ? 1 : b;
+}
+
 template <int NT, int K, bool FUSED = false, class Key = int32_t>
-__global__ void __launch_bounds__(NT, (NT == 256 ? 6 : 1))  // 6 CTAs/SM: measured best (40 regs, no spills)
+__global__ void __launch_bounds__(NT, v2_min_blocks(NT, K, (int)sizeof(Key)))
     merge_pass_v2_kernel(const Key* __restrict__ src, Key* __restrict__ dst, PassPlan P,
                          const int64_t* __restrict__ mp) {
   constexpr int TM = NT * K;
+  static_assert(TM % 4 == 0, "tiles must start 16-byte aligned");
   constexpr int PV = kpv<Key>();           // keys per 16 bytes
   constexpr int KB = (int)sizeof(Key);
   __shared__ __align__(128) Key sm[v2_smem_words(TM)];
@@ -474,9 +490,13 @@ __global__ void __launch_bounds__(NT, (NT == 256 ? 6 : 1))  // 6 CTAs/SM: measur
   const bool a_tma = la > 0 && (a_addr % KB) == 0 && a_cov >= lo && a_cov + a_words <= hi;
   const bool b_tma = lb > 0 && (b_addr % KB) == 0 && b_cov >= lo && b_cov + b_words <= hi;
 
+  // the output offset crosses the merge loop through shared memory, so no
+  // 64-bit geometry stays live in registers next to the K outputs
+  __shared__ int64_t s_out;
   if (tid == 0) {
     mbar_init(&bar, 1);
     fence_mbar_init();
+    s_out = g.pair_base + g.diag0;
   }
   __syncthreads();
   if (tid == 0) {
@@ -500,33 +520,50 @@ __global__ void __launch_bounds__(NT, (NT == 256 ? 6 : 1))  // 6 CTAs/SM: measur
   const Key* SA = sm + a_shift;
   const Key* SB = sm + b_off + b_shift;
   const int total = la + lb;
-  const int kp = P.kp;
-  const int d = min(tid * kp, total);
-  const int cnt = min(kp, total - d);
+  // full tiles (every tile but the last of a pair) give every thread exactly
+  // K outputs: that path has no per-output guard at all
+  const int d = min(tid * K, total);
+  const int cnt = min(K, total - d);
   const int a = merge_path<int>(SA, la, SB, lb, d);
-  int ia = a, ib = d - a;
-  Key ka = SA[ia], kb = SB[ib];
+  // cursors are byte offsets into shared memory (LDS [reg + base] needs no
+  // index arithmetic), clamped at their slice's +inf sentinel
+  const char* smc = reinterpret_cast<const char*>(sm);
+  uint32_t oa = (uint32_t)(a_shift + a) * KB, ob = (uint32_t)(b_off + b_shift + d - a) * KB;
+  const uint32_t ea = (uint32_t)(a_shift + la) * KB, eb = (uint32_t)(b_off + b_shift + lb) * KB;
+  Key ka = *reinterpret_cast<const Key*>(smc + oa), kb = *reinterpret_cast<const Key*>(smc + ob);
   Key v[K];
-#pragma unroll
-  for (int k = 0; k < K; ++k) {
-    if (k < cnt) {
-      const bool take_a = ka <= kb;  // A wins ties (merge_runs, hybrid.hpp:71-75)
-      v[k] = take_a ? ka : kb;
-      if (take_a) {
-        ia = min(ia + 1, la);  // an exhausted side keeps re-reading its sentinel
-        ka = SA[ia];
-      } else {
-        ib = min(ib + 1, lb);
-        kb = SB[ib];
-      }
+  auto step = [&]() {
+    const bool take_a = ka <= kb;  // A wins ties (merge_runs, hybrid.hpp:71-75)
+    const Key out = take_a ? ka : kb;
+    if (take_a) {
+      oa = min(oa + (uint32_t)KB, ea);  // an exhausted side keeps re-reading its sentinel
+      ka = *reinterpret_cast<const Key*>(smc + oa);
+    } else {
+      ob = min(ob + (uint32_t)KB, eb);
+      kb = *reinterpret_cast<const Key*>(smc + ob);
     }
+    return out;
+  };
+  const bool full = total == TM;
+  if (full) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) v[k] = step();
+  } else {
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      if (k < cnt) v[k] = step();
   }
   __syncthreads();  // every thread is done reading the staged inputs
+  if (full) {
 #pragma unroll
-  for (int k = 0; k < K; ++k)
-    if (k < cnt) sm[d + k] = v[k];
+    for (int k = 0; k < K; ++k) sm[d + k] = v[k];
+  } else {
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      if (k < cnt) sm[d + k] = v[k];
+  }
 
-  Key* out = dst + g.pair_base + g.diag0;
+  Key* out = dst + s_out;
   const bool o_tma = ((reinterpret_cast<uintptr_t>(out) & 15) == 0) && (total % PV) == 0;
   if (o_tma) {
     fence_proxy_async_smem();

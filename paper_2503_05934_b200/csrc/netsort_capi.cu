@@ -43,8 +43,8 @@ static int launch_blocksort(const Key* src, Key* dst, int64_t n, int stride, int
 // Tuning knobs (read once; the defaults are the measured best on B200).
 //   NSB_TILE  = 8192 | 16384 : keys per tile-sort CTA
 constexpr int kV2NT = 256, kV2K = 31, kV2T = kV2NT * kV2K;  // 7936 keys per tile
-// int64 keys: 3840 keys (30 KiB) per tile; K odd keeps the half-warp 64-bit
-// cursor accesses on distinct banks
+// int64 keys (NSB_V2_64=0): 3840 keys (30 KiB) per tile; K odd keeps the
+// half-warp 64-bit cursor accesses on distinct banks
 constexpr int kV2K64 = 15;
 //   NSB_KWAY  = 0 | 4 | 8 : widest k-way merge pass (0 = pairwise only, default)
 //   NSB_KWAY_MIN = n below which only pairwise passes are used
@@ -53,7 +53,7 @@ struct MergeTuning {
   int kway = 0;  // measured: k-way passes are merge-compute bound, no faster
   int64_t kway_min = int64_t(1) << 22;
   int64_t fused_max_tiles = 4096;  // passes with fewer tiles search in-kernel (measured crossover)
-  int v2 = 0;  // NSB_V2: 0 -> <256,31>, 1 -> <512,15>, 2 -> <384,21>
+  int v2 = -1;  // NSB_V2 forces one tile shape (see v2_pass); -1 = by size
   MergeTuning() {
     if (const char* e = getenv("NSB_V2")) v2 = atoi(e);
     if (const char* e = getenv("NSB_FUSED_MAX")) fused_max_tiles = atoll(e);
@@ -178,16 +178,17 @@ static int kway_pass(const int32_t* src, int32_t* dst, int64_t n, int64_t R, int
                 : launch_kway_merge<4>(src, dst, P, ks.cuts, s);
 }
 
+// Tiles of exactly NT*K outputs (a multiple of 4 keys, so every tile starts
+// 16-byte aligned); only the last tile of a run pair is partial.  A full tile
+// gives every thread exactly K outputs, which the merge loop exploits.
 static PassPlan plan_pass(int64_t n, int64_t R, int nt = kV2NT, int k = kV2K) {
   PassPlan P;
   P.R = R;
   P.n = n;
   const int64_t two_r = 2 * R;
-  const int tmax = (nt * k) & ~3;
-  P.tpp = (int)((two_r + tmax - 1) / tmax);
-  const int64_t even = (two_r + P.tpp - 1) / P.tpp;
-  P.tmp = (int)((even + 3) & ~int64_t(3));
-  P.kp = (P.tmp + nt - 1) / nt;
+  P.tmp = nt * k;
+  P.tpp = (int)((two_r + P.tmp - 1) / P.tmp);
+  P.kp = k;
   return P;
 }
 
@@ -220,17 +221,42 @@ static int v2_pass_t(const Key* src, Key* dst, int64_t n, int64_t R, int64_t* mp
 }
 
 // One pairwise merge pass (v2): runs of R in src -> runs of 2R in dst.
+// Tile shape by array size (tests/size_sweep.py, tools/mid_sweep.sh on B200):
+// up to 2^23 keys a pass is latency bound and smaller tiles (<128,23>, 2944
+// keys, 12 CTAs/SM) win by 5-10 %; above, <256,31> (7936 keys, 6 CTAs/SM)
+// is within 0.5 % of the best shape measured.
 static int v2_pass(const int32_t* src, int32_t* dst, int64_t n, int64_t R, int64_t* mp,
                    cudaStream_t s) {
   switch (tuning().v2) {
+    case 0: return v2_pass_t<kV2NT, kV2K>(src, dst, n, R, mp, s);
     case 1: return v2_pass_t<512, 15>(src, dst, n, R, mp, s);
     case 2: return v2_pass_t<384, 21>(src, dst, n, R, mp, s);
-    default: return v2_pass_t<kV2NT, kV2K>(src, dst, n, R, mp, s);
+    case 3: return v2_pass_t<128, 31>(src, dst, n, R, mp, s);
+    case 5: return v2_pass_t<128, 47>(src, dst, n, R, mp, s);
+    case 6: return v2_pass_t<128, 23>(src, dst, n, R, mp, s);
+    case 9: return v2_pass_t<128, 63>(src, dst, n, R, mp, s);
+    case 11: return v2_pass_t<128, 55>(src, dst, n, R, mp, s);
+    default:
+      return n <= (int64_t(1) << 23) ? v2_pass_t<128, 23>(src, dst, n, R, mp, s)
+                                     : v2_pass_t<kV2NT, kV2K>(src, dst, n, R, mp, s);
   }
 }
 static int v2_pass(const int64_t* src, int64_t* dst, int64_t n, int64_t R, int64_t* mp,
                    cudaStream_t s) {
-  return v2_pass_t<kV2NT, kV2K64>(src, dst, n, R, mp, s);
+  static const int shape = [] {
+    const char* e = getenv("NSB_V2_64");
+    return e ? atoi(e) : -1;
+  }();
+  switch (shape) {
+    case 0: return v2_pass_t<kV2NT, kV2K64>(src, dst, n, R, mp, s);
+    case 1: return v2_pass_t<128, 23>(src, dst, n, R, mp, s);
+    case 2: return v2_pass_t<128, 31>(src, dst, n, R, mp, s);
+    case 3: return v2_pass_t<128, 15>(src, dst, n, R, mp, s);
+    default:  // by size (tools/i64_sweep.sh on B200)
+      if (n <= (int64_t(1) << 20)) return v2_pass_t<128, 15>(src, dst, n, R, mp, s);
+      if (n <= (int64_t(1) << 25)) return v2_pass_t<128, 23>(src, dst, n, R, mp, s);
+      return v2_pass_t<128, 31>(src, dst, n, R, mp, s);
+  }
 }
 
 // Pairwise passes over existing sorted runs of length R0 (the last may be
