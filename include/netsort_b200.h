@@ -73,6 +73,12 @@ int ns_leaf_width(uint32_t width_mask, int varsort_max);
  * networks.hpp:89-104): writes `cap` (lo,hi) byte pairs at most and returns
  * the comparator count, or -1 for a width outside [2, 8]. */
 int ns_network_comparators(int width, uint8_t* pairs, int cap);
+/* DispatchStats of the reference's merge sort for n keys (hybrid.hpp:18-34,
+ * recursion 81-95), computed from the recursion shape, which depends on n and
+ * the config only: out12 = network_hits[0..8], merges, partitions (0),
+ * max_depth.  Host-only; no device work. */
+int ns_merge_sort_dispatch_stats(int64_t n, uint32_t width_mask, int varsort_max,
+                                 uint64_t* out12);
 
 /* ---- device entry points (caller-owned device memory) ----------------- */
 
@@ -144,6 +150,9 @@ int ns_bucket_bounds_i32(const int32_t* d_sorted, size_t n, const int32_t* d_spl
 size_t ns_merge_runs_temp_bytes(size_t n, int num_runs);
 int ns_merge_runs_i32(int32_t* d_keys, const int64_t* h_run_offsets, int num_runs,
                       void* d_temp, size_t temp_bytes, void* stream);
+size_t ns_merge_runs_temp_bytes_i64(size_t n, int num_runs);
+int ns_merge_runs_i64(int64_t* d_keys, const int64_t* h_run_offsets, int num_runs,
+                      void* d_temp, size_t temp_bytes, void* stream);
 
 /* Merges npairs (<= 32) independent pairs of sorted runs given by POINTERS:
  * pair p = (a_ptrs[p][0 .. a_lens[p]), b_ptrs[p][0 .. b_lens[p])) goes to
@@ -203,6 +212,11 @@ int ns_merge_sort_host_i32(int32_t* h_keys, size_t n, uint32_t width_mask, int v
 int ns_quick_sort_host_i32(int32_t* h_keys, size_t n, uint32_t width_mask, int varsort_max);
 int ns_merge_sort_host_i64(int64_t* h_keys, size_t n, uint32_t width_mask, int varsort_max);
 int ns_quick_sort_host_i64(int64_t* h_keys, size_t n, uint32_t width_mask, int varsort_max);
+/* merge — hybrid.hpp:186-193: h_keys[0, n_left) and h_keys[n_left, n) are
+ * sorted runs of a HOST array; merges them in place (stable, left run wins
+ * ties).  n_left == 0 or n_left == n is a no-op. */
+int ns_merge_host_i32(int32_t* h_keys, size_t n_left, size_t n);
+int ns_merge_host_i64(int64_t* h_keys, size_t n_left, size_t n);
 int ns_release_cache(void);
 
 #ifdef __cplusplus

@@ -17,6 +17,7 @@
 // std::runtime_error.  There is no CPU fallback.
 #pragma once
 
+#include <array>
 #include <cstddef>
 #include <cstdint>
 #include <initializer_list>
@@ -61,6 +62,30 @@ struct SortVariant {
 };
 std::vector<SortVariant> bundled_variants();
 
+// DispatchStats — hybrid.hpp:18-34 (same fields and helpers).
+struct DispatchStats {
+  std::array<std::uint64_t, kMaxNetworkWidth + 1> network_hits{};  // by width
+  std::uint64_t merges = 0;
+  std::uint64_t partitions = 0;
+  int max_depth = 0;
+  std::uint64_t total_network_hits() const {
+    std::uint64_t t = 0;
+    for (std::uint64_t h : network_hits) t += h;
+    return t;
+  }
+  void network(int width) { ++network_hits[static_cast<std::size_t>(width)]; }
+  void merge() { ++merges; }
+  void partition() { ++partitions; }
+  void depth(int d) { max_depth = d > max_depth ? d : max_depth; }
+};
+
+// The counters the reference's merge sort would record for a range of n keys
+// (its recursion shape depends on n and the config only).  The GPU kernels do
+// not recurse; this reproduces the reference's instrumentation exactly.
+// Quick sort's counters depend on the data's pivot splits and have no GPU
+// equivalent.
+DispatchStats merge_sort_dispatch_stats(std::ptrdiff_t n, const NetworkConfig& cfg);
+
 namespace detail {
 inline void check(int status, const char* what) {
   if (status == NS_OK) return;
@@ -85,6 +110,29 @@ inline int host_sort(std::int32_t* p, size_t n, const NetworkConfig& c, Algorith
 inline int host_sort(std::int64_t* p, size_t n, const NetworkConfig& c, Algorithm a) {
   return a == Algorithm::merge_sort ? ns_merge_sort_host_i64(p, n, c.width_mask, c.varsort_max)
                                     : ns_quick_sort_host_i64(p, n, c.width_mask, c.varsort_max);
+}
+// accumulates like the reference's Stats object across calls
+inline void add_stats(DispatchStats& into, const DispatchStats& s) {
+  for (std::size_t w = 0; w < into.network_hits.size(); ++w) into.network_hits[w] += s.network_hits[w];
+  into.merges += s.merges;
+  into.partitions += s.partitions;
+  into.depth(s.max_depth);
+}
+inline int host_merge(std::int32_t* p, size_t n_left, size_t n) {
+  return ns_merge_host_i32(p, n_left, n);
+}
+inline int host_merge(std::int64_t* p, size_t n_left, size_t n) {
+  return ns_merge_host_i64(p, n_left, n);
+}
+// merge — hybrid.hpp:186-193: left <= mid <= right required (the reference
+// asserts it; here it is std::invalid_argument)
+template <class Key>
+void merge_range(std::span<Key> a, std::ptrdiff_t left, std::ptrdiff_t mid, std::ptrdiff_t right) {
+  if (!(left >= 0 && left <= mid && mid <= right && right < static_cast<std::ptrdiff_t>(a.size())))
+    throw std::invalid_argument("merge: need 0 <= left <= mid <= right < size");
+  check(host_merge(a.data() + left, static_cast<size_t>(mid - left + 1),
+                   static_cast<size_t>(right - left + 1)),
+        "merge");
 }
 template <class Key>
 void sort_range(std::span<Key> a, std::ptrdiff_t lo, std::ptrdiff_t hi, const NetworkConfig& cfg,
@@ -122,6 +170,23 @@ void sort_range(std::span<Key> a, std::ptrdiff_t lo, std::ptrdiff_t hi, const Ne
   inline void run_variant(const SortVariant& v, std::span<KEY> a) {                       \
     if (v.algorithm == Algorithm::merge_sort) optimized_merge_sort(a, v.config);          \
     else optimized_quick_sort(a, v.config);                                               \
+  }                                                                                       \
+  /* stats overloads (hybrid.hpp:158-165, 234-243): merge sort only */                    \
+  inline void optimized_merge_sort(std::span<KEY> a, std::ptrdiff_t left,                 \
+                                   std::ptrdiff_t right, const NetworkConfig& cfg,        \
+                                   DispatchStats& stats) {                                \
+    detail::sort_range(a, left, right, cfg, Algorithm::merge_sort);                       \
+    if (right >= left) detail::add_stats(stats, merge_sort_dispatch_stats(right - left + 1, cfg)); \
+  }                                                                                       \
+  inline void run_variant(const SortVariant& v, std::span<KEY> a, DispatchStats& stats) { \
+    if (a.empty()) return;                                                                \
+    if (v.algorithm != Algorithm::merge_sort)                                             \
+      throw std::invalid_argument("run_variant: dispatch stats are defined for merge sort only"); \
+    optimized_merge_sort(a, 0, static_cast<std::ptrdiff_t>(a.size()) - 1, v.config, stats); \
+  }                                                                                       \
+  inline void merge(std::span<KEY> a, std::ptrdiff_t left, std::ptrdiff_t mid,             \
+                    std::ptrdiff_t right) {                                               \
+    detail::merge_range(a, left, mid, right);                                             \
   }
 
 NETSORT_B200_HOST_OVERLOADS(std::int32_t)

@@ -32,6 +32,7 @@ SIGNATURES = {
     "ns_base_case_applies": (_i32, [_i64, _u32, _i32]),
     "ns_leaf_width": (_i32, [_u32, _i32]),
     "ns_network_comparators": (_i32, [_i32, _vp, _i32]),
+    "ns_merge_sort_dispatch_stats": (_i32, [_i64, _u32, _i32, _vp]),
     "ns_merge_sort_temp_bytes": (_sz, [_sz]),
     "ns_merge_sort_i32": (_i32, [_vp, _sz, _u32, _i32, _vp, _sz, _vp]),
     "ns_merge_sort_temp_bytes_i64": (_sz, [_sz]),
@@ -48,6 +49,8 @@ SIGNATURES = {
     "ns_bucket_bounds_i32": (_i32, [_vp, _sz, _vp, _i32, _vp, _vp]),
     "ns_merge_runs_temp_bytes": (_sz, [_sz, _i32]),
     "ns_merge_runs_i32": (_i32, [_vp, _vp, _i32, _vp, _sz, _vp]),
+    "ns_merge_runs_temp_bytes_i64": (_sz, [_sz, _i32]),
+    "ns_merge_runs_i64": (_i32, [_vp, _vp, _i32, _vp, _sz, _vp]),
     "ns_merge_pairs_temp_bytes": (_sz, [_i64, _i32]),
     "ns_merge_pairs_i32": (_i32, [_vp, _vp, _vp, _vp, _i32, _vp, _vp, _sz, _vp]),
     "ns_ipc_get_handle": (_i32, [_vp, _vp, C.POINTER(C.c_uint64)]),
@@ -65,6 +68,8 @@ SIGNATURES = {
     "ns_profile_read": (_i32, [_i32, C.POINTER(C.c_double), C.POINTER(C.c_uint64)]),
     "ns_merge_sort_host_i32": (_i32, [_vp, _sz, _u32, _i32]),
     "ns_merge_sort_host_i64": (_i32, [_vp, _sz, _u32, _i32]),
+    "ns_merge_host_i32": (_i32, [_vp, _sz, _sz]),
+    "ns_merge_host_i64": (_i32, [_vp, _sz, _sz]),
     "ns_quick_sort_host_i64": (_i32, [_vp, _sz, _u32, _i32]),
     "ns_quick_sort_host_i32": (_i32, [_vp, _sz, _u32, _i32]),
     "ns_release_cache": (_i32, []),

@@ -20,7 +20,7 @@ from __future__ import annotations
 
 import ctypes as C
 import enum
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 from typing import Optional, Sequence
 
 import numpy as np
@@ -60,6 +60,35 @@ class NetworkConfig:
 class SortVariant:
     algorithm: Algorithm
     config: NetworkConfig
+
+
+@dataclass
+class DispatchStats:
+    """hybrid.hpp:18-34 (same fields and helpers)."""
+    network_hits: list = field(default_factory=lambda: [0] * (kMaxNetworkWidth + 1))
+    merges: int = 0
+    partitions: int = 0
+    max_depth: int = 0
+
+    def total_network_hits(self) -> int:
+        return sum(self.network_hits)
+
+    def add(self, other: "DispatchStats") -> None:
+        self.network_hits = [a + b for a, b in zip(self.network_hits, other.network_hits)]
+        self.merges += other.merges
+        self.partitions += other.partitions
+        self.max_depth = max(self.max_depth, other.max_depth)
+
+
+def merge_sort_dispatch_stats(n: int, cfg: "NetworkConfig") -> DispatchStats:
+    """The counters the reference's merge sort records for n keys: its
+    recursion shape (hybrid.hpp:81-95) depends on n and the config only.
+    Quick sort's counters depend on the data's pivot splits and have no GPU
+    equivalent."""
+    out = (C.c_uint64 * 12)()
+    check(lib().ns_merge_sort_dispatch_stats(int(n), cfg.width_mask, cfg.varsort_max,
+                                             C.cast(out, C.c_void_p)), "dispatch stats")
+    return DispatchStats(list(out[:9]), int(out[9]), int(out[10]), int(out[11]))
 
 
 def base_case_applies(size: int, cfg: NetworkConfig) -> bool:
@@ -212,11 +241,44 @@ def _sort(algo: int, a, left, right, cfg: NetworkConfig):
 
 
 def optimized_merge_sort(a, *args):
-    """optimized_merge_sort(a, cfg) or optimized_merge_sort(a, left, right, cfg)."""
+    """optimized_merge_sort(a, cfg), optimized_merge_sort(a, left, right, cfg)
+    or optimized_merge_sort(a, left, right, cfg, stats) (hybrid.hpp:156-177;
+    the stats form also adds the reference's DispatchStats counters)."""
     if len(args) == 1:
         return _sort(_lib.NS_MERGE_SORT, a, None, None, args[0])
+    if len(args) == 4:
+        left, right, cfg, stats = args
+        _sort(_lib.NS_MERGE_SORT, a, left, right, cfg)
+        if int(right) >= int(left):
+            stats.add(merge_sort_dispatch_stats(int(right) - int(left) + 1, cfg))
+        return a
     left, right, cfg = args
     return _sort(_lib.NS_MERGE_SORT, a, left, right, cfg)
+
+
+def merge(a, left: int, mid: int, right: int):
+    """merge — hybrid.hpp:186-193: stable in-place merge of the sorted runs
+    a[left..mid] and a[mid+1..right] (inclusive bounds)."""
+    n = a.numel() if _is_device(a) else len(a)
+    left, mid, right = int(left), int(mid), int(right)
+    if not (0 <= left <= mid <= right < n):
+        raise ValueError("merge: need 0 <= left <= mid <= right < size")
+    L = lib()
+    cnt = right - left + 1
+    if _is_device(a):
+        t = _check_tensor(a, allow_i64=True)
+        offs = (C.c_int64 * 3)(0, mid - left + 1, cnt)
+        sfx = "" if t == "i32" else "_i64"
+        tb = getattr(L, f"ns_merge_runs_temp_bytes{sfx}")(cnt, 2)
+        check(getattr(L, f"ns_merge_runs_{t}")(a.data_ptr() + a.element_size() * left,
+                                               C.cast(offs, C.c_void_p), 2,
+                                               scratch(tb, a.device), tb, _stream_ptr(a)),
+              "merge")
+    else:
+        t = _check_host(a)
+        check(getattr(L, f"ns_merge_host_{t}")(a.ctypes.data + a.itemsize * left,
+                                               mid - left + 1, cnt), "merge")
+    return a
 
 
 def optimized_quick_sort(a, *args):
@@ -235,7 +297,16 @@ def classical_quick_sort(a):
     return optimized_quick_sort(a, classic_config())
 
 
-def run_variant(variant: SortVariant, a):
+def run_variant(variant: SortVariant, a, stats: Optional[DispatchStats] = None):
+    """run_variant (hybrid.hpp:225-243).  With stats: merge sort only (quick
+    sort's counters are data-dependent and have no GPU equivalent)."""
+    if stats is not None:
+        n = a.numel() if _is_device(a) else len(a)
+        if n == 0:  # hybrid.hpp:237
+            return a
+        if variant.algorithm is not Algorithm.merge_sort:
+            raise ValueError("run_variant: dispatch stats are defined for merge sort only")
+        return optimized_merge_sort(a, 0, n - 1, variant.config, stats)
     if variant.algorithm is Algorithm.merge_sort:
         return optimized_merge_sort(a, variant.config)
     return optimized_quick_sort(a, variant.config)

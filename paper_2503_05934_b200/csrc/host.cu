@@ -129,9 +129,51 @@ static int host_sort(Key* h_keys, size_t n, uint32_t mask, int vs, int algorithm
   return check_cuda(cudaStreamSynchronize(s), "cudaStreamSynchronize");
 }
 
+// merge (hybrid.hpp:186-193) on a host array: upload, one two-run merge, read back.
+static size_t merge_temp(const int32_t*, size_t n) { return ns_merge_runs_temp_bytes(n, 2); }
+static size_t merge_temp(const int64_t*, size_t n) { return ns_merge_runs_temp_bytes_i64(n, 2); }
+static int merge_dev(int32_t* d, const int64_t* offs, void* t, size_t tb, cudaStream_t s) {
+  return ns_merge_runs_i32(d, offs, 2, t, tb, s);
+}
+static int merge_dev(int64_t* d, const int64_t* offs, void* t, size_t tb, cudaStream_t s) {
+  return ns_merge_runs_i64(d, offs, 2, t, tb, s);
+}
+
+template <class Key>
+static int host_merge(Key* h_keys, size_t n_left, size_t n) {
+  if (n_left > n) return NS_ERR_INVALID;
+  if (n_left == 0 || n_left == n) return NS_OK;
+  if (!h_keys) return NS_ERR_INVALID;
+  constexpr size_t KB = sizeof(Key);
+  const size_t kb = align_up(n * KB, 256);
+  const size_t tb = merge_temp(h_keys, n);
+  NSB_TRY(g_host.ensure(kb + tb));
+  cudaStream_t s = g_host.stream;
+  Key* d = static_cast<Key*>(g_host.dev);
+  void* t = static_cast<char*>(g_host.dev) + kb;
+  const int64_t offs[3] = {0, (int64_t)n_left, (int64_t)n};
+  NSB_TRY(check_cuda(cudaMemcpyAsync(d, h_keys, n * KB, cudaMemcpyHostToDevice, s), "H2D"));
+  const int st = merge_dev(d, offs, t, tb, s);
+  if (st != NS_OK) {
+    cudaStreamSynchronize(s);
+    return st;
+  }
+  NSB_TRY(check_cuda(cudaMemcpyAsync(h_keys, d, n * KB, cudaMemcpyDeviceToHost, s), "D2H"));
+  return check_cuda(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+}
+
 }  // namespace nsb
 
 extern "C" {
+
+int ns_merge_host_i32(int32_t* h_keys, size_t n_left, size_t n) {
+  return nsb::host_merge(h_keys, n_left, n);
+}
+
+int ns_merge_host_i64(int64_t* h_keys, size_t n_left, size_t n) {
+  return nsb::host_merge(h_keys, n_left, n);
+}
+
 
 int ns_merge_sort_host_i32(int32_t* h_keys, size_t n, uint32_t width_mask, int varsort_max) {
   return nsb::host_sort(h_keys, n, width_mask, varsort_max, NS_MERGE_SORT);

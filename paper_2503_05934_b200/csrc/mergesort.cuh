@@ -417,6 +417,86 @@ __global__ void merge_partition_v2_kernel(const Key* __restrict__ src, PassPlan 
   mp[c] = merge_path<int64_t>(A, g.a_len, A + g.a_len, g.b_len, g.diag0);
 }
 
+// Merge of one staged tile: A = sm[a_pos, a_pos+la), B = sm[b_pos, b_pos+lb)
+// (each with one free slot after it for its +inf sentinel), the la+lb merged
+// keys written to dst + *s_out_off.  Shared by the pairwise passes and the
+// pointer-pair merge (samplesort.cu).  Must be called by all NT threads after
+// the staged slices are visible to the CTA.
+template <int NT, int K, class Key>
+__device__ __forceinline__ void merge_staged_tile(Key* sm, int a_pos, int la, int b_pos, int lb,
+                                                  Key* dst, const int64_t* s_out_off) {
+  constexpr int TM = NT * K;
+  constexpr int PV = kpv<Key>();
+  constexpr int KB = (int)sizeof(Key);
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    sm[a_pos + la] = KeyT<Key>::kMax;  // sentinels: the merge loop has no bounds tests
+    sm[b_pos + lb] = KeyT<Key>::kMax;
+  }
+  __syncthreads();
+
+  const Key* SA = sm + a_pos;
+  const Key* SB = sm + b_pos;
+  const int total = la + lb;
+  // full tiles (every tile but the last of a pair) give every thread exactly
+  // K outputs: that path has no per-output guard at all
+  const int d = min(tid * K, total);
+  const int cnt = min(K, total - d);
+  const int a = merge_path<int>(SA, la, SB, lb, d);
+  // cursors are byte offsets into shared memory (LDS [reg + base] needs no
+  // index arithmetic), clamped at their slice's +inf sentinel
+  const char* smc = reinterpret_cast<const char*>(sm);
+  uint32_t oa = (uint32_t)(a_pos + a) * KB, ob = (uint32_t)(b_pos + d - a) * KB;
+  const uint32_t ea = (uint32_t)(a_pos + la) * KB, eb = (uint32_t)(b_pos + lb) * KB;
+  Key ka = *reinterpret_cast<const Key*>(smc + oa), kb = *reinterpret_cast<const Key*>(smc + ob);
+  Key v[K];
+  auto step = [&]() {
+    const bool take_a = ka <= kb;  // A wins ties (merge_runs, hybrid.hpp:71-75)
+    const Key out = take_a ? ka : kb;
+    if (take_a) {
+      oa = min(oa + (uint32_t)KB, ea);  // an exhausted side keeps re-reading its sentinel
+      ka = *reinterpret_cast<const Key*>(smc + oa);
+    } else {
+      ob = min(ob + (uint32_t)KB, eb);
+      kb = *reinterpret_cast<const Key*>(smc + ob);
+    }
+    return out;
+  };
+  const bool full = total == TM;
+  if (full) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) v[k] = step();
+  } else {
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      if (k < cnt) v[k] = step();
+  }
+  __syncthreads();  // every thread is done reading the staged inputs
+  if (full) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) sm[d + k] = v[k];
+  } else {
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      if (k < cnt) sm[d + k] = v[k];
+  }
+
+  Key* out = dst + *s_out_off;
+  const bool o_tma = ((reinterpret_cast<uintptr_t>(out) & 15) == 0) && (total % PV) == 0;
+  if (o_tma) {
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+      tma_store_1d(out, sm, (uint32_t)total * (uint32_t)KB);
+      bulk_commit();
+      bulk_wait_read_all();
+    }
+  } else {
+    __syncthreads();
+    for (int i = tid; i < total; i += NT) out[i] = sm[i];
+  }
+}
+
 // Keys of shared memory a v2 tile needs: two slices with up to 3 keys of
 // alignment slack each, a sentinel after each, 16-byte rounding.
 __host__ __device__ constexpr int v2_smem_words(int TM) { return TM + 16; }
@@ -511,72 +591,7 @@ __global__ void __launch_bounds__(NT, v2_min_blocks(NT, K, (int)sizeof(Key)))
     for (int i = tid; i < lb; i += NT) sm[b_off + b_shift + i] = __ldcs(B + i);
   mbar_wait(&bar, 0);
   __syncthreads();
-  if (tid == 0) {
-    sm[a_shift + la] = KeyT<Key>::kMax;  // sentinels: the merge loop has no bounds tests
-    sm[b_off + b_shift + lb] = KeyT<Key>::kMax;
-  }
-  __syncthreads();
-
-  const Key* SA = sm + a_shift;
-  const Key* SB = sm + b_off + b_shift;
-  const int total = la + lb;
-  // full tiles (every tile but the last of a pair) give every thread exactly
-  // K outputs: that path has no per-output guard at all
-  const int d = min(tid * K, total);
-  const int cnt = min(K, total - d);
-  const int a = merge_path<int>(SA, la, SB, lb, d);
-  // cursors are byte offsets into shared memory (LDS [reg + base] needs no
-  // index arithmetic), clamped at their slice's +inf sentinel
-  const char* smc = reinterpret_cast<const char*>(sm);
-  uint32_t oa = (uint32_t)(a_shift + a) * KB, ob = (uint32_t)(b_off + b_shift + d - a) * KB;
-  const uint32_t ea = (uint32_t)(a_shift + la) * KB, eb = (uint32_t)(b_off + b_shift + lb) * KB;
-  Key ka = *reinterpret_cast<const Key*>(smc + oa), kb = *reinterpret_cast<const Key*>(smc + ob);
-  Key v[K];
-  auto step = [&]() {
-    const bool take_a = ka <= kb;  // A wins ties (merge_runs, hybrid.hpp:71-75)
-    const Key out = take_a ? ka : kb;
-    if (take_a) {
-      oa = min(oa + (uint32_t)KB, ea);  // an exhausted side keeps re-reading its sentinel
-      ka = *reinterpret_cast<const Key*>(smc + oa);
-    } else {
-      ob = min(ob + (uint32_t)KB, eb);
-      kb = *reinterpret_cast<const Key*>(smc + ob);
-    }
-    return out;
-  };
-  const bool full = total == TM;
-  if (full) {
-#pragma unroll
-    for (int k = 0; k < K; ++k) v[k] = step();
-  } else {
-#pragma unroll
-    for (int k = 0; k < K; ++k)
-      if (k < cnt) v[k] = step();
-  }
-  __syncthreads();  // every thread is done reading the staged inputs
-  if (full) {
-#pragma unroll
-    for (int k = 0; k < K; ++k) sm[d + k] = v[k];
-  } else {
-#pragma unroll
-    for (int k = 0; k < K; ++k)
-      if (k < cnt) sm[d + k] = v[k];
-  }
-
-  Key* out = dst + s_out;
-  const bool o_tma = ((reinterpret_cast<uintptr_t>(out) & 15) == 0) && (total % PV) == 0;
-  if (o_tma) {
-    fence_proxy_async_smem();
-    __syncthreads();
-    if (tid == 0) {
-      tma_store_1d(out, sm, (uint32_t)total * (uint32_t)KB);
-      bulk_commit();
-      bulk_wait_read_all();
-    }
-  } else {
-    __syncthreads();
-    for (int i = tid; i < total; i += NT) out[i] = sm[i];
-  }
+  merge_staged_tile<NT, K>(sm, a_shift, la, b_off + b_shift, lb, dst, &s_out);
 }
 
 }  // namespace nsb

@@ -154,6 +154,32 @@ static void device_side() {
   CHECK(back == e);
   cudaFree(d);
 
+  // DispatchStats overloads (hybrid.hpp:158-165, 234-243) and merge (186-193)
+  {
+    auto v = random_values(100000, 77);
+    ns::DispatchStats st;
+    ns::run_variant(ns::SortVariant{ns::Algorithm::merge_sort, *ns::find_config("6To8")},
+                    std::span<int32_t>(v), st);
+    CHECK(std::is_sorted(v.begin(), v.end()));
+    CHECK(st.merges == 16383 && st.network_hits[6] == 14688 && st.network_hits[7] == 1696);
+    CHECK(st.max_depth == 15);  // SURVEY.md A.2 (100,000 keys, 6To8)
+    bool threw = false;
+    try {
+      ns::run_variant(ns::SortVariant{ns::Algorithm::quick_sort, *ns::find_config("3To5")},
+                      std::span<int32_t>(v), st);
+    } catch (const std::invalid_argument&) {
+      threw = true;
+    }
+    CHECK(threw);
+    auto m = random_values(5000, 78);
+    std::sort(m.begin(), m.begin() + 2000);
+    std::sort(m.begin() + 2000, m.end());
+    auto em = m;
+    std::sort(em.begin(), em.end());
+    ns::merge(std::span<int32_t>(m), 0, 1999, 4999);
+    CHECK(m == em);
+  }
+
   // int64: the reference's benchmark type, bound exactly as measure_loop's
   // sort_fn (std::function<void(std::span<std::int64_t>)>, bench.hpp:58-61;
   // bench.cpp:94-96 binds it to run_variant)

@@ -368,3 +368,71 @@ def test_p2p_sample_sort_large(ns, cuda):
                           "2", str(1 << 27), "random"], cwd=root, capture_output=True,
                          text=True, timeout=900)
     assert "P2P_OK" in out.stdout, (out.stdout[-1500:], out.stderr[-3000:])
+
+
+def test_merge_standalone_matches_oracle(ns, cuda, oracle):
+    """merge (hybrid.hpp:186-193): stable merge of a[left..mid], a[mid+1..right],
+    int32 and int64, device tensors and host arrays, against oracle_merge."""
+    rng = np.random.default_rng(12)
+    for n, left, mid, right in [(10, 0, 4, 9), (1000, 0, 0, 999), (1000, 0, 998, 999),
+                                (50000, 100, 30000, 49000), (1 << 20, 0, 700000, (1 << 20) - 1),
+                                (300001, 5, 5, 300000)]:
+        for dt in (np.int32, np.int64):
+            a = rng.integers(-1000, 1000, n).astype(dt)
+            a[left:mid + 1].sort()
+            a[mid + 1:right + 1].sort()
+            want = a.copy()
+            want[left:right + 1] = np.sort(a[left:right + 1], kind="stable")
+            if dt == np.int32:
+                w32 = a.copy()
+                oracle.lib().oracle_merge_i32(w32, left, mid, right)
+                assert np.array_equal(w32, want)
+            import torch
+            t = torch.from_numpy(a.copy()).to(cuda)
+            ns.merge(t, left, mid, right)
+            assert np.array_equal(t.cpu().numpy(), want), (n, left, mid, right, dt)
+            h = a.copy()
+            ns.merge(h, left, mid, right)
+            assert np.array_equal(h, want), (n, dt, "host")
+    with pytest.raises(ValueError):
+        ns.merge(np.zeros(4, np.int32), 2, 1, 3)
+
+
+def test_run_variant_with_stats(ns, cuda, oracle):
+    import torch
+    st = ns.DispatchStats()
+    a = oracle.generate_i32("random", 100000, 3)
+    t = torch.from_numpy(a).to(cuda)
+    ns.run_variant(ns.SortVariant(ns.Algorithm.merge_sort, ns.find_config("6To8")), t, st)
+    want, ost = oracle.merge_sort(a, "6To8", stats=True)
+    assert np.array_equal(t.cpu().numpy(), want)
+    assert st.network_hits == list(ost.network_hits) and st.merges == ost.merges
+    assert st.max_depth == ost.max_depth
+    with pytest.raises(ValueError):
+        ns.run_variant(ns.SortVariant(ns.Algorithm.quick_sort, ns.find_config("3To5")), t, st)
+
+
+def test_merge_runs_many_runs_both_key_types(ns, cuda):
+    """ns_merge_runs_* (the g-way merge of the sample sort and of the chunked
+    host path): ragged runs, 1..64 of them, int32 and int64."""
+    import ctypes as C
+    import torch
+    L = ns.lib()
+    rng = np.random.default_rng(4)
+    for dt, tt, sfx in ((np.int32, torch.int32, "i32"), (np.int64, torch.int64, "i64")):
+        for nruns in (2, 3, 7, 16, 33, 64):
+            lens = rng.integers(0, 40000, nruns)
+            lens[rng.integers(0, nruns)] = 0
+            runs = [np.sort(rng.integers(-2**31, 2**31, l).astype(dt)) for l in lens]
+            flat = np.concatenate(runs)
+            offs = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+            t = torch.from_numpy(flat.copy()).to(cuda)
+            tb = getattr(L, "ns_merge_runs_temp_bytes" + ("" if sfx == "i32" else "_i64"))(
+                flat.size, nruns)
+            tmp = torch.empty(max(tb, 1), dtype=torch.uint8, device=cuda)
+            o = (C.c_int64 * (nruns + 1))(*offs.tolist())
+            rc = getattr(L, f"ns_merge_runs_{sfx}")(t.data_ptr(), C.cast(o, C.c_void_p), nruns,
+                                                    tmp.data_ptr(), tb,
+                                                    torch.cuda.current_stream().cuda_stream)
+            assert rc == 0
+            assert np.array_equal(t.cpu().numpy(), np.sort(flat)), (sfx, nruns)

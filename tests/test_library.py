@@ -140,3 +140,29 @@ def test_temp_bytes_queries(ns):
     assert L.ns_merge_sort_temp_bytes(1 << 20) >= 4 << 20
     assert L.ns_quick_sort_temp_bytes(1 << 20) >= 4 << 20
     assert L.ns_merge_runs_temp_bytes(1000, 1) == 0
+
+
+def test_merge_sort_dispatch_stats_match_reference(oracle):
+    """DispatchStats (hybrid.hpp:18-34) of the reference's merge sort, from the
+    library's host-side recursion-shape count, equal the counters the
+    reference records (oracle/_ref) and the oracle's own — every config."""
+    import paper_2503_05934_b200 as ns
+    for name, mask, vs in oracle.REGISTRY:
+        cfg = ns.find_config(name)
+        for n in (1, 2, 3, 7, 8, 9, 13, 100, 1000, 25000, 100000, 123457):
+            st = ns.merge_sort_dispatch_stats(n, cfg)
+            _, ost = oracle.merge_sort(oracle.generate_i32("random", n, 5), name, stats=True)
+            assert st.network_hits == list(ost.network_hits), (name, n)
+            assert st.merges == ost.merges and st.max_depth == ost.max_depth
+            assert st.partitions == 0
+            if oracle.ref_available():
+                rs = np.zeros(12, np.uint64)
+                a = oracle.generate_i32("random", n, 5)
+                oracle.ref().ref_merge_sort_i32(a, n, mask, vs, rs.ctypes.data)
+                assert st.network_hits == rs[:9].tolist() and st.merges == rs[9]
+                assert st.max_depth == rs[11]
+    # SURVEY.md A.2: 6To8 fires no network at n = 10,000; w8 x 2^21 at 2^24
+    assert ns.merge_sort_dispatch_stats(10_000, ns.find_config("6To8")).total_network_hits() == 0
+    big = ns.merge_sort_dispatch_stats(1 << 24, ns.find_config("6To8"))
+    assert big.network_hits[8] == 2_097_152 and big.max_depth == 22
+    assert ns.merge_sort_dispatch_stats(0, ns.find_config("6To8")).max_depth == 0
