@@ -50,9 +50,12 @@ class OracleStats(C.Structure):
                 ("partitions", C.c_uint64), ("max_depth", C.c_int32)]
 
 
-def build() -> None:
-    """Build the oracle (and oracle/_ref when /root/reference is present)."""
-    subprocess.run(["make", "-s", "-C", HERE, "all"], check=True)
+def build(harness: bool = False) -> None:
+    """Build the oracle (and oracle/_ref when /root/reference is present);
+    harness=True also links the reference's benchmark harness against the
+    product library (oracle/_ref/harness_gpu, needs the library built)."""
+    subprocess.run(["make", "-s", "-C", HERE, "all"] + (["harness"] if harness else []),
+                   check=True)
 
 
 _lib = None
