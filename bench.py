@@ -516,6 +516,18 @@ def other_configs(ns, L, dev):
     for n in (1_000_000, 16_777_216):
         single(f"qs_3to5_random_i64_{n}", "quick", "3To5", "random", n, key="i64")
     torch.cuda.empty_cache()
+    # stable key-value sort (int32 keys + 4-byte payload), SURVEY.md §8(f) row 4
+    n = 1 << 26
+    kk = torch.from_numpy(O.generate_i32("random", n, SEED)).to(dev)
+    vv = torch.arange(n, dtype=torch.int32, device=dev)
+    wk, wv = kk.clone(), vv.clone()
+    fn = lambda: ns.sort_pairs(wk, wv)  # noqa: E731
+    restore = lambda: (wk.copy_(kk), wv.copy_(vv))  # noqa: E731
+    ms = graph_ms(fn, restore, reps=5)
+    res["sort_pairs_i32_random_2^26"] = {"n": n, "graph_ms": ms,
+                                         "gkeys_per_s": n / (ms * 1e-3) / 1e9}
+    del kk, vv, wk, wv
+    torch.cuda.empty_cache()
     # base-case batch, 2^24 ragged arrays
     offs, keys = O.generate_batch_i32(1 << 24, SEED)
     k = torch.from_numpy(keys).to(dev)

@@ -119,6 +119,20 @@ int ns_quick_sort_i64(int64_t* d_keys, size_t n, uint32_t width_mask, int varsor
 int ns_sort_small_batch_i32(int32_t* d_keys, const uint32_t* d_offsets, size_t num_arrays,
                             void* stream);
 
+/* Stable key-value sort and argsort.  The
+ * reference's classical merge sort is stable (merge_runs keeps the left run
+ * on ties, hybrid.hpp:61-79; test_hybrid.cpp:119-150) but has no payload API.
+ * ns_sort_pairs_i32 sorts d_keys in place and applies the same stable
+ * permutation to the 32-bit payload d_values (may be NULL).  ns_argsort_i32
+ * writes d_perm with d_keys[d_perm[i]] stably ascending; d_keys is not
+ * modified.  n < 2^32. */
+size_t ns_sort_pairs_temp_bytes_i32(size_t n);
+int ns_sort_pairs_i32(int32_t* d_keys, uint32_t* d_values, size_t n, void* d_temp,
+                      size_t temp_bytes, void* stream);
+size_t ns_argsort_temp_bytes_i32(size_t n);
+int ns_argsort_i32(const int32_t* d_keys, uint32_t* d_perm, size_t n, void* d_temp,
+                   size_t temp_bytes, void* stream);
+
 /* Segmented sort of num_segments independent arrays of seg_len keys each,
  * stored back to back (BASELINE config 4's 65,536 x 16,384 batch).  The
  * reference would run `algorithm` once per segment. */

@@ -138,6 +138,39 @@ static inline void st_depth(oracle_stats* s, int d) {
 #undef KEY
 #undef NAME
 
+/* ---- stable key/payload merge sort (classical recursion) ---------------- */
+
+static void merge_runs_pairs(int32_t* k, uint32_t* v, int64_t left, int64_t mid, int64_t right,
+                             int32_t* sk, uint32_t* sv) {
+  const int64_t left_len = mid - left + 1;
+  memcpy(sk, k + left, (size_t)left_len * sizeof(int32_t));
+  memcpy(sv, v + left, (size_t)left_len * sizeof(uint32_t));
+  int64_t i = 0, j = mid + 1, out = left;
+  while (i < left_len && j <= right) {
+    if (k[j] < sk[i]) { k[out] = k[j]; v[out++] = v[j++]; }
+    else { k[out] = sk[i]; v[out++] = sv[i++]; }
+  }
+  while (i < left_len) { k[out] = sk[i]; v[out++] = sv[i++]; }
+}
+
+static void ms_pairs_rec(int32_t* k, uint32_t* v, int64_t left, int64_t right, int32_t* sk,
+                         uint32_t* sv) {
+  if (left >= right) return;
+  const int64_t mid = left + (right - left) / 2;
+  ms_pairs_rec(k, v, left, mid, sk, sv);
+  ms_pairs_rec(k, v, mid + 1, right, sk, sv);
+  merge_runs_pairs(k, v, left, mid, right, sk, sv);
+}
+
+void oracle_stable_sort_pairs_i32(int32_t* keys, uint32_t* vals, int64_t n) {
+  if (n < 2) return;
+  int32_t* sk = (int32_t*)malloc((size_t)n * sizeof(int32_t));
+  uint32_t* sv = (uint32_t*)malloc((size_t)n * sizeof(uint32_t));
+  ms_pairs_rec(keys, vals, 0, n - 1, sk, sv);
+  free(sk);
+  free(sv);
+}
+
 /* ---- batch helpers ----------------------------------------------------- */
 
 void oracle_sort_small_batch_i32(int32_t* keys, const uint32_t* offsets, size_t num_arrays) {

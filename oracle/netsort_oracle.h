@@ -91,6 +91,12 @@ int64_t oracle_hoare_partition_i64(int64_t* a, int64_t low, int64_t high, int64_
 void oracle_quick_sort_i64(int64_t* a, int64_t low, int64_t high, uint32_t width_mask,
                            int varsort_max, oracle_stats* stats);
 
+/* Classical (stable) merge sort of key/payload pairs: merge_sort_rec with the
+ * Classic config (hybrid.hpp:81-95, no networks: they are not stable) and
+ * merge_runs carrying the payload (hybrid.hpp:61-79, left run wins ties).
+ * The oracle for ns_sort_pairs_i32 / ns_argsort_i32. */
+void oracle_stable_sort_pairs_i32(int32_t* keys, uint32_t* vals, int64_t n);
+
 /* Batch / segmented helpers (no reference symbol):
  * sort_small per array, optimized_quick_sort per fixed-length segment. */
 void oracle_sort_small_batch_i32(int32_t* keys, const uint32_t* offsets, size_t num_arrays);

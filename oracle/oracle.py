@@ -90,6 +90,7 @@ def lib():
         L.oracle_segmented_quick_sort_i32.argtypes = [_i32p, C.c_size_t, C.c_size_t,
                                                       C.c_uint32, C.c_int]
         L.oracle_multiset_digest_i32.argtypes = [_i32p, C.c_size_t, _u64p]
+        L.oracle_stable_sort_pairs_i32.argtypes = [_i32p, _u32p, C.c_int64]
         # int64 instantiations (netsort_oracle_sort.inc with KEY = int64_t)
         L.oracle_sort_small_i64.argtypes = [_i64p, C.c_int]
         L.oracle_merge_sort_i64.argtypes = [_i64p, C.c_int64, C.c_int64, C.c_uint32, C.c_int,
@@ -224,3 +225,11 @@ def multiset_digest(a: np.ndarray):
     a, t = _keys(a)
     getattr(lib(), f"oracle_multiset_digest_{t}")(a, len(a), out)
     return int(out[0]), int(out[1])
+
+
+def stable_sort_pairs(keys: np.ndarray, values: np.ndarray):
+    """Classical stable merge sort of (key, payload) pairs (hybrid.hpp:61-95)."""
+    k = np.ascontiguousarray(keys, np.int32).copy()
+    v = np.ascontiguousarray(values, np.uint32).copy()
+    lib().oracle_stable_sort_pairs_i32(k, v, len(k))
+    return k, v

@@ -4,10 +4,10 @@ bottoms out in fixed sorting networks (arXiv 2503.05934), rebuilt for B200
 include/netsort_b200.h; this package is the Python host layer over it."""
 from ._lib import NetsortError, build, lib  # noqa: F401
 from .api import (  # noqa: F401
-    Algorithm, DispatchStats, NetworkConfig, SortVariant, algorithm_name, base_case_applies,
+    Algorithm, DispatchStats, argsort, NetworkConfig, SortVariant, algorithm_name, base_case_applies,
     bundled_variants, classic_config, classical_merge_sort, classical_quick_sort,
     config_registry, count_inversions, find_config, kMaxNetworkWidth, kMinNetworkWidth,
     leaf_width, make_fixed_config, make_varsort_config, merge, merge_sort_dispatch_stats,
     multiset_digest, network,
     optimized_merge_sort, optimized_quick_sort, release_scratch, run_variant,
-    segmented_sort, sort_small_batch)
+    segmented_sort, sort_pairs, sort_small_batch)

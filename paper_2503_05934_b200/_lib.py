@@ -42,6 +42,10 @@ SIGNATURES = {
     "ns_quick_sort_i64": (_i32, [_vp, _sz, _u32, _i32, _vp, _sz, _vp]),
     "ns_quick_sort_i32": (_i32, [_vp, _sz, _u32, _i32, _vp, _sz, _vp]),
     "ns_sort_small_batch_i32": (_i32, [_vp, _vp, _sz, _vp]),
+    "ns_sort_pairs_temp_bytes_i32": (_sz, [_sz]),
+    "ns_sort_pairs_i32": (_i32, [_vp, _vp, _sz, _vp, _sz, _vp]),
+    "ns_argsort_temp_bytes_i32": (_sz, [_sz]),
+    "ns_argsort_i32": (_i32, [_vp, _vp, _sz, _vp, _sz, _vp]),
     "ns_segmented_sort_temp_bytes": (_sz, [_sz, _sz]),
     "ns_segmented_sort_i32": (_i32, [_vp, _sz, _sz, _i32, _u32, _i32, _vp, _sz, _vp]),
     "ns_regular_samples_i32": (_i32, [_vp, _sz, _i32, _vp, _vp]),

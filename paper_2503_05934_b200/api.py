@@ -342,6 +342,39 @@ def segmented_sort(keys, seg_len: int, cfg: NetworkConfig,
     return keys
 
 
+# ---- key-value --------------------------------------
+
+def sort_pairs(keys, values=None):
+    """Stable sort of CUDA int32 keys in place, carrying a 4-byte payload
+    (int32/uint32/float32 CUDA tensor of the same length) through the same
+    permutation: equal keys keep their input order, as the reference's
+    classical merge (hybrid.hpp:61-79) keeps them."""
+    _check_tensor(keys)
+    n = keys.numel()
+    if values is not None:
+        if not values.is_cuda or values.numel() != n or values.element_size() != 4 \
+                or not values.is_contiguous():
+            raise ValueError("values must be a contiguous 4-byte CUDA tensor of len(keys)")
+    L = lib()
+    tb = L.ns_sort_pairs_temp_bytes_i32(n)
+    check(L.ns_sort_pairs_i32(keys.data_ptr(), values.data_ptr() if values is not None else None,
+                              n, scratch(tb, keys.device), tb, _stream_ptr(keys)), "sort_pairs")
+    return keys, values
+
+
+def argsort(keys):
+    """Stable argsort of CUDA int32 keys: returns an int64 tensor perm with
+    keys[perm] ascending and equal keys in input order (keys unchanged)."""
+    _check_tensor(keys)
+    n = keys.numel()
+    perm = torch.empty(n, dtype=torch.int32, device=keys.device)
+    L = lib()
+    tb = L.ns_argsort_temp_bytes_i32(n)
+    check(L.ns_argsort_i32(keys.data_ptr(), perm.data_ptr(), n, scratch(tb, keys.device), tb,
+                           _stream_ptr(keys)), "argsort")
+    return perm.to(torch.int64) if n < 2**31 else perm.view(torch.uint32).to(torch.int64)
+
+
 # ---- checking helpers ------------------------------------------------------
 
 def multiset_digest(keys) -> tuple:

@@ -436,3 +436,26 @@ def test_merge_runs_many_runs_both_key_types(ns, cuda):
                                                     torch.cuda.current_stream().cuda_stream)
             assert rc == 0
             assert np.array_equal(t.cpu().numpy(), np.sort(flat)), (sfx, nruns)
+
+
+@pytest.mark.parametrize("n", [0, 1, 2, 7, 1000, 16384, 16385, 100000, 1 << 20, 3_000_001])
+def test_sort_pairs_and_argsort_stable(ns, cuda, oracle, n):
+    """Stable key-value sort / argsort against the
+    classical stable merge sort oracle, many duplicate keys."""
+    import torch
+    rng = np.random.default_rng(n)
+    keys = rng.integers(-50, 50, n).astype(np.int32)
+    if n > 10:
+        keys[: n // 10] = np.iinfo(np.int32).max   # real keys equal to the sentinel
+        keys[n // 10: n // 5] = np.iinfo(np.int32).min
+    vals = rng.integers(0, 2**32, n, dtype=np.uint64).astype(np.uint32)
+    wk, wv = oracle.stable_sort_pairs(keys, vals)
+    tk = torch.from_numpy(keys.copy()).to(cuda)
+    tv = torch.from_numpy(vals.view(np.int32).copy()).to(cuda)
+    ns.sort_pairs(tk, tv)
+    assert np.array_equal(tk.cpu().numpy(), wk)
+    assert np.array_equal(tv.cpu().numpy().view(np.uint32), wv)
+    tk2 = torch.from_numpy(keys.copy()).to(cuda)
+    perm = ns.argsort(tk2)
+    assert np.array_equal(tk2.cpu().numpy(), keys)  # unchanged
+    assert np.array_equal(perm.cpu().numpy(), np.argsort(keys, kind="stable"))

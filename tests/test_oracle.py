@@ -304,3 +304,18 @@ def test_i64_extremes_and_digest(oracle):
     b = a.copy()
     b[0] ^= 1 << 40
     assert oracle.multiset_digest(a) != oracle.multiset_digest(b)
+
+
+def test_stable_pairs_restatement(oracle):
+    """Classical merge is stable (test_hybrid.cpp:119-150 restated: equal keys
+    keep their tags' input order); the pairs oracle equals a stable argsort."""
+    rng = np.random.default_rng(8)
+    for n in (0, 1, 2, 3, 17, 1000, 65537):
+        k = rng.integers(-3, 3, n).astype(np.int32)
+        tags = np.arange(n, dtype=np.uint32)
+        sk, sv = oracle.stable_sort_pairs(k, tags)
+        p = np.argsort(k, kind="stable")
+        assert np.array_equal(sk, k[p]) and np.array_equal(sv, tags[p])
+        for key in np.unique(k):
+            t = sv[sk == key]
+            assert np.all(t[:-1] < t[1:])  # input order kept among equals
