@@ -175,6 +175,30 @@ __device__ __forceinline__ Classifier load_classifier(int32_t* sm, const int32_t
 
 constexpr int kQsClassifierWords = kQsMaxB + (kQsLut + 2) / 2 + 2;
 
+// Runs of equal bucket ids among consecutive lanes (consecutive keys in
+// memory): one ballot finds the run heads, so a run — one lane for random
+// input, the whole warp for sorted input — is charged with ONE shared-memory
+// atomic by its head lane.  Equal ids in different runs of a warp just issue
+// separate atomics.  (Replaces __match_any_sync, which measured as the
+// bottleneck of these kernels.)  Lanes with b < 0 form their own runs and
+// are skipped by the callers.
+struct WarpRun {
+  int head_lane;  // first lane of my run
+  int len;        // my run's length (valid on every lane of the run)
+  bool head;
+};
+__device__ __forceinline__ WarpRun warp_run(int b) {
+  const int lane = threadIdx.x & 31;
+  const int prev = __shfl_up_sync(kFull, b, 1);
+  const bool head = lane == 0 || b != prev;
+  const unsigned heads = __ballot_sync(kFull, head);
+  const unsigned upto = heads & (0xffffffffu >> (31 - lane));      // heads at lanes <= mine
+  const int hl = 31 - __clz(upto);
+  const unsigned after = heads & ~(0xffffffffu >> (31 - lane));    // heads at lanes > mine
+  const int next = after ? __ffs(after) - 1 : 32;
+  return WarpRun{hl, next - hl, head};
+}
+
 __global__ void __launch_bounds__(kQsNT)
     count_kernel(const int32_t* __restrict__ keys, int64_t n, const int32_t* __restrict__ gspl,
                  const int16_t* __restrict__ glut, int B, uint32_t* __restrict__ totals) {
@@ -186,12 +210,19 @@ __global__ void __launch_bounds__(kQsNT)
   __syncthreads();
   const int64_t c0 = (int64_t)blockIdx.x * kQsChunk;
   const int64_t c1 = min(n, c0 + kQsChunk);
-  const int lane = threadIdx.x & 31;
-  for (int64_t i = c0 + threadIdx.x; i - threadIdx.x < c1; i += kQsNT) {
-    const bool live = i < c1;
-    const int b = live ? cls(__ldg(keys + i)) : -1;
-    const unsigned peers = __match_any_sync(kFull, b);
-    if (live && lane == __ffs(peers) - 1) atomicAdd(&hist[b], (uint32_t)__popc(peers));
+  constexpr int kU = kQsChunk / kQsNT;  // keys per thread, loaded up front
+  int32_t k[kU];
+#pragma unroll
+  for (int u = 0; u < kU; ++u) {
+    const int64_t i = c0 + u * kQsNT + threadIdx.x;
+    k[u] = i < c1 ? __ldg(keys + i) : 0;
+  }
+#pragma unroll
+  for (int u = 0; u < kU; ++u) {
+    const int64_t i = c0 + u * kQsNT + threadIdx.x;
+    const int b = i < c1 ? cls(k[u]) : -1;
+    const WarpRun r = warp_run(b);
+    if (b >= 0 && r.head) atomicAdd(&hist[b], (uint32_t)r.len);
   }
   __syncthreads();
   for (int i = threadIdx.x; i < NB; i += kQsNT)
@@ -229,8 +260,8 @@ __global__ void __launch_bounds__(kQsNT)
   for (int u = 0; u < kQsPer; ++u) {
     const int64_t i = c0 + u * kQsNT + threadIdx.x;
     bk[u] = i < n ? cls(k[u]) : -1;
-    const unsigned peers = __match_any_sync(kFull, bk[u]);
-    if (bk[u] >= 0 && lane == __ffs(peers) - 1) atomicAdd(&pos[bk[u]], (unsigned long long)__popc(peers));
+    const WarpRun r = warp_run(bk[u]);
+    if (bk[u] >= 0 && r.head) atomicAdd(&pos[bk[u]], (unsigned long long)r.len);
   }
   __syncthreads();
   for (int b = threadIdx.x; b < NB; b += kQsNT) {
@@ -241,12 +272,11 @@ __global__ void __launch_bounds__(kQsNT)
 #pragma unroll
   for (int u = 0; u < kQsPer; ++u) {
     const int b = bk[u];
-    const unsigned peers = __match_any_sync(kFull, b);
-    const int leader = __ffs(peers) - 1;
+    const WarpRun r = warp_run(b);
     unsigned long long base = 0;
-    if (b >= 0 && lane == leader) base = atomicAdd(&pos[b], (unsigned long long)__popc(peers));
-    base = __shfl_sync(kFull, base, leader);
-    if (b >= 0) out[base + __popc(peers & ((1u << lane) - 1))] = k[u];
+    if (b >= 0 && r.head) base = atomicAdd(&pos[b], (unsigned long long)r.len);
+    base = __shfl_sync(kFull, base, r.head_lane);
+    if (b >= 0) out[base + (lane - r.head_lane)] = k[u];
   }
 }
 
