@@ -238,12 +238,13 @@ constexpr int kQsSChunk = kQsPer * kQsNT;  // keys per CTA in scatter
 
 __global__ void __launch_bounds__(kQsNT)
     scatter_kernel(const int32_t* __restrict__ keys, int64_t n, const int32_t* __restrict__ gspl,
-                   const int16_t* __restrict__ glut, int B, unsigned long long* __restrict__ fill,
+                   const int16_t* __restrict__ glut, int B, uint32_t* __restrict__ fill,
                    int32_t* __restrict__ out) {
   extern __shared__ int32_t qsm[];
   const Classifier cls = load_classifier(qsm, gspl, glut, B);
-  unsigned long long* pos =
-      reinterpret_cast<unsigned long long*>(qsm + ((kQsClassifierWords + 3) & ~1));  // 8-byte aligned
+  // 32-bit counters and positions: the single-level path sorts < 2^32 keys
+  // (64-bit shared atomics measured as the bottleneck of this kernel)
+  uint32_t* pos = reinterpret_cast<uint32_t*>(qsm + kQsClassifierWords);
   const int NB = 2 * B - 1;
   for (int i = threadIdx.x; i < NB; i += kQsNT) pos[i] = 0;
   __syncthreads();
@@ -261,11 +262,11 @@ __global__ void __launch_bounds__(kQsNT)
     const int64_t i = c0 + u * kQsNT + threadIdx.x;
     bk[u] = i < n ? cls(k[u]) : -1;
     const WarpRun r = warp_run(bk[u]);
-    if (bk[u] >= 0 && r.head) atomicAdd(&pos[bk[u]], (unsigned long long)r.len);
+    if (bk[u] >= 0 && r.head) atomicAdd(&pos[bk[u]], (uint32_t)r.len);
   }
   __syncthreads();
   for (int b = threadIdx.x; b < NB; b += kQsNT) {
-    const unsigned long long c = pos[b];
+    const uint32_t c = pos[b];
     if (c) pos[b] = atomicAdd(&fill[b], c);  // one global atomic per (CTA, bucket)
   }
   __syncthreads();
@@ -273,8 +274,8 @@ __global__ void __launch_bounds__(kQsNT)
   for (int u = 0; u < kQsPer; ++u) {
     const int b = bk[u];
     const WarpRun r = warp_run(b);
-    unsigned long long base = 0;
-    if (b >= 0 && r.head) base = atomicAdd(&pos[b], (unsigned long long)r.len);
+    uint32_t base = 0;
+    if (b >= 0 && r.head) base = atomicAdd(&pos[b], (uint32_t)r.len);
     base = __shfl_sync(kFull, base, r.head_lane);
     if (b >= 0) out[base + (lane - r.head_lane)] = k[u];
   }
@@ -343,11 +344,11 @@ static int quick_sort_level(int32_t* keys, int32_t* tmp, size_t n, int leaf, con
   NSB_TRY(check_cuda(cudaMemsetAsync(aux.totals, 0, NB * sizeof(uint32_t), s), "memset"));
   const int64_t ctas = (int64_t)((n + kQsChunk - 1) / kQsChunk);
   const int count_smem = (kQsClassifierWords + NB) * 4;
-  const int scatter_smem = ((kQsClassifierWords + 3) & ~1) * 4 + NB * 8;
+  const int scatter_smem = (kQsClassifierWords + NB) * 4;
   NSB_TRY(ensure_smem_attr(reinterpret_cast<const void*>(count_kernel),
                            (kQsClassifierWords + 2 * kQsMaxB) * 4, "cudaFuncSetAttribute(count)"));
   NSB_TRY(ensure_smem_attr(reinterpret_cast<const void*>(scatter_kernel),
-                           ((kQsClassifierWords + 3) & ~1) * 4 + 2 * kQsMaxB * 8,
+                           (kQsClassifierWords + 2 * kQsMaxB) * 4,
                            "cudaFuncSetAttribute(scatter)"));
   {
     Prof prof(PK_QS_COUNT, s);
@@ -364,20 +365,20 @@ static int quick_sort_level(int32_t* keys, int32_t* tmp, size_t n, int leaf, con
                      "cudaMemcpyAsync(totals)"));
   NSB_TRY(check_cuda(cudaStreamSynchronize(s), "cudaStreamSynchronize"));
 
-  std::vector<unsigned long long> starts(NB);
-  unsigned long long acc = 0;
+  std::vector<uint32_t> starts(NB);
+  uint64_t acc = 0;
   for (int b = 0; b < NB; ++b) {
-    starts[b] = acc;
+    starts[b] = (uint32_t)acc;
     acc += totals[b];
   }
   if (acc != n) return NS_ERR_CUDA;  // classification lost keys: a device fault
-  NSB_TRY(check_cuda(cudaMemcpyAsync(aux.fill, starts.data(), NB * sizeof(unsigned long long),
+  NSB_TRY(check_cuda(cudaMemcpyAsync(aux.fill, starts.data(), NB * sizeof(uint32_t),
                                      cudaMemcpyHostToDevice, s),
                      "cudaMemcpyAsync(fill)"));
   {
     Prof prof(PK_QS_SCATTER, s);
     scatter_kernel<<<(unsigned)((n + kQsSChunk - 1) / kQsSChunk), kQsNT, scatter_smem, s>>>(
-        keys, (int64_t)n, aux.splitters, aux.lut, B, aux.fill, tmp);
+        keys, (int64_t)n, aux.splitters, aux.lut, B, reinterpret_cast<uint32_t*>(aux.fill), tmp);
   }
   NSB_TRY(check_launch("scatter_kernel"));
 
