@@ -459,3 +459,22 @@ def test_sort_pairs_and_argsort_stable(ns, cuda, oracle, n):
     perm = ns.argsort(tk2)
     assert np.array_equal(tk2.cpu().numpy(), keys)  # unchanged
     assert np.array_equal(perm.cpu().numpy(), np.argsort(keys, kind="stable"))
+
+
+@pytest.mark.slow
+def test_merge_sort_beyond_2_31_keys(ns, cuda):
+    """n = 2^31 + 4099 int32 keys (8.6 GB): indexing past 32 bits in every
+    kernel of the merge sort; sorted and a permutation of the input."""
+    import torch
+    n = (1 << 31) + 4099
+    t = torch.empty(n, dtype=torch.int32, device=cuda)
+    L = ns.lib()
+    from paper_2503_05934_b200._lib import check
+    check(L.ns_generate_i32(t.data_ptr(), n, 0, 99, torch.cuda.current_stream().cuda_stream), "gen")
+    before = ns.multiset_digest(t)
+    ns.optimized_merge_sort(t, ns.find_config("6To8"))
+    assert ns.count_inversions(t) == 0
+    assert ns.multiset_digest(t) == before
+    del t
+    ns.release_scratch()
+    torch.cuda.empty_cache()
