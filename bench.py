@@ -231,10 +231,26 @@ def run_ours(args, metric):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # BENCH_TEST_ONE_GPU=1 (code-path check only, never a bench number): every
+    # rank on cuda:0 with gloo metadata collectives, as tests/multiproc_p2p_gpu.py
+    one_gpu = os.environ.get("BENCH_TEST_ONE_GPU") == "1"
+    if one_gpu:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
+    def all_reduce(t, op):  # gloo (one-GPU code-path check) reduces host tensors
+        if world > 1 and dist.get_backend() == "gloo":
+            c = t.cpu()
+            dist.all_reduce(c, op=op)
+            t.copy_(c)
+        elif world > 1:
+            dist.all_reduce(t, op=op)
+
     L = ns.lib()
     cfg = ns.find_config("6To8")
     n = args.n
@@ -296,7 +312,7 @@ def run_ours(args, metric):
     times = [a.elapsed_time(b) for a, b in ev]
     total_ms = torch.tensor([sum(times)], dtype=torch.float64, device=dev)
     if world > 1:
-        dist.all_reduce(total_ms, op=dist.ReduceOp.MAX)
+        all_reduce(total_ms, dist.ReduceOp.MAX)
     total_ms = float(total_ms.item())
     ms_per_step = total_ms / args.steps
     value = n / (ms_per_step * 1e-3) / 1e9
@@ -372,30 +388,61 @@ def run_ours(args, metric):
         e1.record()
         torch.cuda.synchronize()
         t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        all_reduce(t, dist.ReduceOp.MAX)
         e2e = {"value": n / (float(t.item()) * 1e-3) / 1e9, "unit": "Gkeys/s",
                "h2d_bytes_per_step": 4 * m, "d2h_bytes_per_step": 4 * res.numel(),
                "path": "per-rank pinned shard -> sample_sort -> host", "steps": 1}
 
+    # NVLink roofline of the exchange: one step with the
+    # sample sort's own phase events.  exchange="p2p" fuses the all-to-all into
+    # the first merge round (peer HBM read over NVLink), so the fused phase is
+    # the exchange; "nccl" times the all_to_all itself.  Bytes = keys this rank
+    # pulls from / sends to its peers; time = max over ranks.
+    nvlink = None
+    if world > 1:
+        tm = samplesort.SampleSortTiming()
+        keys.copy_(pristine)
+        torch.cuda.synchronize()
+        dist.barrier()
+        samplesort.sample_sort(keys, ops=ops, exchange=exchange["mode"], timing=tm)
+        phase_ms = tm.merge_ms if exchange["mode"] == "p2p" else tm.exchange_ms
+        v = torch.tensor([phase_ms, tm.local_sort_ms, float(tm.send_bytes)], dtype=torch.float64,
+                         device=dev)
+        vmax = v.clone()
+        all_reduce(vmax, dist.ReduceOp.MAX)
+        peer_gbs = 770.0  # measured peer copy per direction (B200_PROFILING.md)
+        per_rank_bytes = float(vmax[2].item())
+        ach = per_rank_bytes / (float(vmax[0].item()) * 1e-3) / 1e9 if vmax[0] > 0 else None
+        nvlink = {"phase": "pull-merge (fused all-to-all)" if exchange["mode"] == "p2p"
+                  else "nccl all_to_all", "phase_ms_max": float(vmax[0].item()),
+                  "local_sort_ms_max": float(vmax[1].item()),
+                  "bytes_per_rank_max": per_rank_bytes, "achieved_gbs": ach,
+                  "peak_gbs": peer_gbs, "peak_source": "measured peer copy (fallback figure)",
+                  "frac": (ach / peer_gbs) if ach else None}
+
     ok = torch.tensor([1 if local_ok else 0], device=dev)
     if world > 1:
-        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        all_reduce(ok, dist.ReduceOp.MIN)
 
     line = {"metric": metric, "value": value, "unit": "Gkeys/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "int32", "data": "synthetic",
             "config": {"workload": ("merge sort 6To8" if world == 1 else
-                                    "sample sort (local merge sort 6To8 + NCCL all-to-all)") +
+                                    "sample sort (local merge sort 6To8 + " +
+                                    ("pull-merge over NVLink peer memory)"
+                                     if exchange["mode"] == "p2p" else "NCCL all-to-all)")) +
                        f", one uniform-random int32 array, n={n} (BASELINE configs[4])",
                        "n": n, "keys_per_gpu": m, "distribution": "uniform [0, 2^31), seed 42",
                        "parallelism": "replicas/shards over NCCL" if world > 1 else "single GPU",
-                       "l2": "input 4 GiB >> 126 MB L2; restored by an untimed D2D copy "
-                             "before each step"},
+                       "l2": f"input {4 * n / 2**30:.2f} GiB vs 126 MB L2; restored by an "
+                             "untimed D2D copy before each step"},
             "exchange": exchange if world > 1 else None,
             "gpu_launches": int(launches), "wall_ms_timed_region": wall * 1e3,
             "roofline": roofline, "byte_model": model, "kernel_profile": prof,
             "e2e": e2e, "clocks": clk, "verified": bool(ok.item())}
+    if nvlink is not None:
+        line["nvlink"] = nvlink
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline()
     if rank == 0 and world == 1 and args.extra:
@@ -563,7 +610,8 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--n", type=int, default=N_DEFAULT)
+    ap.add_argument("--keys", "--n", dest="n", type=int, default=N_DEFAULT,
+                    help="total keys (--keys under torchrun: its parser claims --n)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--extra", action="store_true", help="also time the other BASELINE configs")
     ap.add_argument("--exchange", choices=["p2p", "nccl"], default="p2p",

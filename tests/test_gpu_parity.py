@@ -478,3 +478,31 @@ def test_merge_sort_beyond_2_31_keys(ns, cuda):
     del t
     ns.release_scratch()
     torch.cuda.empty_cache()
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("exchange", ["p2p", "nccl"])
+def test_bench_multi_rank_code_path_on_one_gpu(exchange):
+    """bench.py's N>1 path (sample sort, max-over-ranks timing, nvlink object)
+    with 2 ranks sharing cuda:0 over gloo (BENCH_TEST_ONE_GPU=1): a code-path
+    check, never a bench number."""
+    import json
+    import os
+    import socket
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    env = dict(os.environ, BENCH_TEST_ONE_GPU="1")
+    r = subprocess.run(["python", "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node",
+                        "2", "--master-addr", "127.0.0.1", "--master-port", str(port),
+                        os.path.join(root, "bench.py"), "--gpus", "2", "--steps", "1",
+                        "--warmup", "1", "--keys", str(1 << 24), "--exchange", exchange],
+                       capture_output=True, text=True, timeout=600, env=env, cwd=root)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["verified"] is True
+    assert line["nvlink"]["bytes_per_rank_max"] > 0
+    assert line["exchange"]["mode"] == exchange
