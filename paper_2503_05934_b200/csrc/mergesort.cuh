@@ -23,6 +23,7 @@
 
 #include "networks.cuh"
 #include "smem_merge.cuh"
+#include "tma.cuh"
 
 namespace nsb {
 
@@ -271,6 +272,17 @@ __device__ __forceinline__ void tile_store(const Key* sm, Key* out, int valid) {
 // place allowed) on chip.  Shared by the tiled merge sort, the segmented sort
 // and the quick-sort bucket sort.
 // ---------------------------------------------------------------------------
+//
+// Merge levels (v5).  After the warp bitonic stage every warp holds one
+// sorted 512-key run (16 keys per lane, blocked).  The runs go to shared
+// memory in a GAP layout — run r at r*(R+4), its +inf sentinel right after
+// it — so each level can use the pass kernel's merge loop: byte-offset
+// cursors clamped at the sentinel, no bounds tests, no index arithmetic.
+// Output diagonals are skewed inside each warp (lane l starts at
+// 16l + ((l>>1)&15) and emits 16 or 17 keys; lane 31 emits the last one), so
+// for any k the 32 lanes' k-th output stores fall on 32 different banks
+// without padding words; every lane runs the same 17 unguarded merge steps
+// and only the stores are predicated.
 template <int NT, int K, int LEAF, class Key>
 __device__ __forceinline__ void cta_sort(const Key* in, Key* out, int valid, Key* sm) {
   constexpr int T = NT * K;
@@ -285,30 +297,94 @@ __device__ __forceinline__ void cta_sort(const Key* in, Key* out, int valid, Key
   thread_sort<LEAF>(v);  // the network base case (try_base_case, hybrid.hpp:48-56)
   if constexpr (NT >= 32) warp_bitonic<5>(v, lane);
 
-  // shared-memory merge-path levels: runs of 32*K up to T
-#pragma unroll 1
-  for (int R = 32 * K; R < T; R *= 2) {
+  if constexpr (NT <= 32) {
     __syncthreads();
     regs_to_smem<K>(sm, v);
     __syncthreads();
-    const int pos = tid * K;
-    const int pair = pos & ~(2 * R - 1);
-    const int diag = pos - pair;
-    const SmemRun<Key> A{sm, pair}, B{sm, pair + R};
-    const int a = merge_path<int>(A, R, B, R, diag);
-    serial_merge<K>(A, R, B, R, a, diag - a, v);
+    tile_store<NT, T>(sm, out, valid);
+  } else {
+    static_assert(K == 16, "the skewed merge levels assume 16 keys per lane");
+    constexpr int W = 32 * K;  // warp run
+    constexpr int GAP = 4;     // keeps every run 16-byte aligned
+    constexpr int PV = kpv<Key>();
+    constexpr int KB = (int)sizeof(Key);
+    constexpr int KM = K + 1;
+    const int warp = tid >> 5;
+    __syncthreads();  // every thread is done reading the padded tile
+    {
+      Key* dst = sm + warp * (W + GAP) + K * lane;
+#pragma unroll
+      for (int q = 0; q < K / PV; ++q) {
+        Key e[PV];
+#pragma unroll
+        for (int u = 0; u < PV; ++u) e[u] = v[q * PV + u];
+        *reinterpret_cast<int4*>(dst + q * PV) = pack16<Key>(e);
+      }
+      if (lane == 0) sm[warp * (W + GAP) + W] = KeyT<Key>::kMax;
+    }
+    __syncthreads();
+    const int skew = (lane >> 1) & 15;
+    const int cnt = lane == 31 ? 1 : K + (lane & 1);
+    const char* smc = reinterpret_cast<const char*>(sm);
+#pragma unroll 1
+    for (int R = W; R < T; R *= 2) {
+      const int S = R + GAP, S2 = 2 * R + GAP;
+      const int wpp = 2 * R / W;  // warps per output run
+      const int p = warp / wpp, wi = warp - p * wpp;
+      const int d = W * wi + K * lane + skew;
+      const int a_pos = 2 * p * S, b_pos = a_pos + S;
+      const int a = merge_path<int>(sm + a_pos, R, sm + b_pos, R, d);
+      uint32_t oa = (uint32_t)(a_pos + a) * KB, ob = (uint32_t)(b_pos + d - a) * KB;
+      const uint32_t ea = (uint32_t)(a_pos + R) * KB, eb = (uint32_t)(b_pos + R) * KB;
+      Key ka = *reinterpret_cast<const Key*>(smc + oa), kb = *reinterpret_cast<const Key*>(smc + ob);
+      Key w[KM];
+#pragma unroll
+      for (int k = 0; k < KM; ++k) {
+        const bool take_a = ka <= kb;  // A wins ties (merge_runs, hybrid.hpp:71-75)
+        w[k] = take_a ? ka : kb;
+        if (take_a) {
+          oa = min(oa + (uint32_t)KB, ea);
+          ka = *reinterpret_cast<const Key*>(smc + oa);
+        } else {
+          ob = min(ob + (uint32_t)KB, eb);
+          kb = *reinterpret_cast<const Key*>(smc + ob);
+        }
+      }
+      __syncthreads();  // every thread is done reading this level's input
+      Key* o = sm + p * S2 + d;
+#pragma unroll
+      for (int k = 0; k < KM; ++k)
+        if (k < cnt) o[k] = w[k];
+      if (wi == 0 && lane == 0) sm[p * S2 + 2 * R] = KeyT<Key>::kMax;
+      __syncthreads();
+    }
+    // the sorted tile is sm[0, T)
+    if (valid == T && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
+      fence_proxy_async_smem();
+      __syncthreads();
+      if (tid == 0) {
+        tma_store_1d(out, sm, (uint32_t)T * (uint32_t)KB);
+        bulk_commit();
+        bulk_wait_read_all();
+      }
+    } else {
+      for (int i = tid; i < valid; i += NT) out[i] = sm[i];
+    }
   }
-
-  __syncthreads();
-  regs_to_smem<K>(sm, v);
-  __syncthreads();
-  tile_store<NT, T>(sm, out, valid);
 }
 
 // CTA b sorts [b*stride, b*stride + min(stride, n - b*stride)), stride <= T
 // (stride == T for plain tiling, the segment length for segmented sorts).
+// Resident CTAs per SM requested for a tile-sort CTA of NT threads.
+#ifndef NSB_BS_THREADS_PER_SM
+#define NSB_BS_THREADS_PER_SM 1536
+#endif
+__host__ __device__ constexpr int bs_min_blocks(int NT) {
+  return NT >= NSB_BS_THREADS_PER_SM ? 1 : NSB_BS_THREADS_PER_SM / NT;
+}
+
 template <int NT, int K, int LEAF, class Key = int32_t>
-__global__ void __launch_bounds__(NT)
+__global__ void __launch_bounds__(NT, bs_min_blocks(NT))
     blocksort_kernel(const Key* src, Key* dst, int64_t n, int stride) {  // src == dst ok
   extern __shared__ __align__(16) unsigned char sm_raw[];
   Key* sm = reinterpret_cast<Key*>(sm_raw);
