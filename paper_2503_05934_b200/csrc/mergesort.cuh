@@ -272,6 +272,46 @@ __device__ __forceinline__ void tile_store(const Key* sm, Key* out, int valid) {
 // place allowed) on chip.  Shared by the tiled merge sort, the segmented sort
 // and the quick-sort bucket sort.
 // ---------------------------------------------------------------------------
+
+// Padded variant (one pad word per 32 keys, serial merge with clamped
+// indices): kept for int64 keys and 1024-thread tiles, where the skewed
+// variant below needs more registers than the occupancy it must keep
+// (measured: 2^28 int64 sort 15.1 vs 16.6 ms, 65,536 x 16,384 segmented
+// 9.8 vs 11.2 ms).
+template <int NT, int K, int LEAF, class Key>
+__device__ __forceinline__ void cta_sort_padded(const Key* in, Key* out, int valid, Key* sm) {
+  constexpr int T = NT * K;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+
+  tile_load<NT, T>(in, valid, sm);
+  __syncthreads();
+  Key v[K];
+  smem_to_regs<K>(sm, v);
+
+  thread_sort<LEAF>(v);  // the network base case (try_base_case, hybrid.hpp:48-56)
+  if constexpr (NT >= 32) warp_bitonic<5>(v, lane);
+
+  // shared-memory merge-path levels: runs of 32*K up to T
+#pragma unroll 1
+  for (int R = 32 * K; R < T; R *= 2) {
+    __syncthreads();
+    regs_to_smem<K>(sm, v);
+    __syncthreads();
+    const int pos = tid * K;
+    const int pair = pos & ~(2 * R - 1);
+    const int diag = pos - pair;
+    const SmemRun<Key> A{sm, pair}, B{sm, pair + R};
+    const int a = merge_path<int>(A, R, B, R, diag);
+    serial_merge<K>(A, R, B, R, a, diag - a, v);
+  }
+
+  __syncthreads();
+  regs_to_smem<K>(sm, v);
+  __syncthreads();
+  tile_store<NT, T>(sm, out, valid);
+}
+
 //
 // Merge levels (v5).  After the warp bitonic stage every warp holds one
 // sorted 512-key run (16 keys per lane, blocked).  The runs go to shared
@@ -283,8 +323,17 @@ __device__ __forceinline__ void tile_store(const Key* sm, Key* out, int valid) {
 // for any k the 32 lanes' k-th output stores fall on 32 different banks
 // without padding words; every lane runs the same 17 unguarded merge steps
 // and only the stores are predicated.
+template <int NT, int K, class Key>
+__host__ __device__ constexpr bool cta_sort_skewed() {
+  return sizeof(Key) == 4 && NT > 32 && NT <= 512;
+}
+
 template <int NT, int K, int LEAF, class Key>
 __device__ __forceinline__ void cta_sort(const Key* in, Key* out, int valid, Key* sm) {
+  if constexpr (!cta_sort_skewed<NT, K, Key>()) {
+    cta_sort_padded<NT, K, LEAF>(in, out, valid, sm);
+    return;
+  }
   constexpr int T = NT * K;
   const int tid = threadIdx.x;
   const int lane = tid & 31;
@@ -379,12 +428,15 @@ __device__ __forceinline__ void cta_sort(const Key* in, Key* out, int valid, Key
 #ifndef NSB_BS_THREADS_PER_SM
 #define NSB_BS_THREADS_PER_SM 1536
 #endif
-__host__ __device__ constexpr int bs_min_blocks(int NT) {
-  return NT >= NSB_BS_THREADS_PER_SM ? 1 : NSB_BS_THREADS_PER_SM / NT;
+template <int NT, int K, class Key>
+__host__ __device__ constexpr int bs_min_blocks() {
+  // 0 = no minimum (the padded variant keeps the compiler's own choice)
+  return !cta_sort_skewed<NT, K, Key>() || NT >= NSB_BS_THREADS_PER_SM
+             ? 0 : NSB_BS_THREADS_PER_SM / NT;
 }
 
 template <int NT, int K, int LEAF, class Key = int32_t>
-__global__ void __launch_bounds__(NT, bs_min_blocks(NT))
+__global__ void __launch_bounds__(NT, (bs_min_blocks<NT, K, Key>()))
     blocksort_kernel(const Key* src, Key* dst, int64_t n, int stride) {  // src == dst ok
   extern __shared__ __align__(16) unsigned char sm_raw[];
   Key* sm = reinterpret_cast<Key*>(sm_raw);
