@@ -273,7 +273,7 @@ def run_ours(args, metric):
             return keys
         try:
             return samplesort.sample_sort(keys, ops=ops, exchange=exchange["mode"])
-        except Exception as e:  # p2p needs CUDA IPC between the ranks
+        except samplesort.P2PUnavailable as e:  # raised on every rank together
             if exchange["mode"] != "p2p":
                 raise
             exchange["mode"] = "nccl"

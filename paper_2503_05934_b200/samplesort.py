@@ -99,11 +99,18 @@ class DeviceOps:
         me, g = dist.get_rank(group), dist.get_world_size(group)
         h = (C.c_uint8 * 64)()
         off = C.c_uint64()
-        check(self.L.ns_ipc_get_handle(shard.data_ptr(), C.cast(h, C.c_void_p), C.byref(off)),
-              "ipc handle")
-        mine = (bytes(h), off.value)
+        # export first, then exchange unconditionally (a failed export travels
+        # as None) so every rank reaches the collective and sees the failure
+        try:
+            check(self.L.ns_ipc_get_handle(shard.data_ptr(), C.cast(h, C.c_void_p),
+                                           C.byref(off)), "ipc handle")
+            mine = (bytes(h), off.value)
+        except Exception:  # noqa: BLE001 - reported on every rank below
+            mine = None
         allh = [None] * g
         dist.all_gather_object(allh, mine, group=group)
+        if any(x is None for x in allh):
+            raise RuntimeError("a rank could not export its shard over CUDA IPC")
         # a peer allocation is mapped once and reused while it stays the same
         # (the bench re-sorts the same shard buffer every step)
         cache = self.__dict__.setdefault("_ipc_cache", {})
@@ -175,6 +182,18 @@ class SampleSortTiming:
     send_bytes: int = 0
 
 
+class P2PUnavailable(RuntimeError):
+    """Raised on EVERY rank when any rank cannot map its peers' shards."""
+
+
+def _all_ranks_ok(ok: bool, dev, group) -> bool:
+    flag = torch.tensor([1 if ok else 0], dtype=torch.int32, device=dev)
+    if dist.get_backend(group) == "gloo" and flag.is_cuda:
+        flag = flag.cpu()
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
+    return bool(flag.item())
+
+
 def _all_gather_cat(t: torch.Tensor, g: int, group) -> torch.Tensor:
     """all_gather of a small tensor, concatenated.  Metadata collectives go
     through host memory when the process group is gloo (CPU tests, and the
@@ -215,7 +234,17 @@ def sample_sort(shard: torch.Tensor, group=None, ops=None, samples_per_rank: int
     bnd = ops.bounds(shard, spl, g)
     if exchange == "p2p":
         bounds_all = _all_gather_cat(bnd, g, group).view(g, g + 1).cpu().tolist()
-        runs = ops.open_peer_runs(shard, bounds_all, group)
+        # every rank must agree before any peer is read: a rank that cannot map
+        # its peers (no CUDA IPC / peer access) makes ALL ranks raise, so a
+        # caller can fall back to exchange="nccl" without mismatched collectives
+        err = None
+        try:
+            runs = ops.open_peer_runs(shard, bounds_all, group)
+        except Exception as e:  # noqa: BLE001 - reported below on every rank
+            runs, err = None, e
+        if not _all_ranks_ok(err is None, dev, group):
+            raise P2PUnavailable(f"peer mapping failed on a rank: {err!r}" if err else
+                                 "peer mapping failed on another rank")
         if ev:
             ev[2].record()
         out = ops.merge_pull(runs, dev)

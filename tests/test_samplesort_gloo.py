@@ -82,6 +82,60 @@ class OracleOps:
         keys.copy_(torch.from_numpy(np.ascontiguousarray(merged, np.int32)))
 
 
+class FailingPeerOps(OracleOps):
+    """Rank 1 cannot map its peers: every rank must see P2PUnavailable (and
+    can then fall back to the NCCL exchange consistently)."""
+
+    def open_peer_runs(self, shard, bounds_all, group=None):
+        # like DeviceOps: the handle exchange (a collective) happens first,
+        # mapping the peers (local, may fail) after it
+        runs = super().open_peer_runs(shard, bounds_all, group)
+        if dist.get_rank(group) == 1:
+            raise RuntimeError("no peer access")
+        return runs
+
+
+def _fallback_worker(rank, world, port, q):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle import oracle as O
+    from paper_2503_05934_b200 import samplesort
+    full = O.generate_i32("random", 9000, 5)
+    m = 9000 // world
+    shard = torch.from_numpy(full[rank * m:(rank + 1) * m].copy())
+    raised = False
+    try:
+        samplesort.sample_sort(shard.clone(), ops=FailingPeerOps(), exchange="p2p")
+    except samplesort.P2PUnavailable:
+        raised = True
+    out = samplesort.sample_sort(shard.clone(), ops=OracleOps(), exchange="nccl")
+    parts = [None] * world
+    dist.all_gather_object(parts, (raised, out.numpy().tolist()))
+    if rank == 0:
+        q.put(parts)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_p2p_failure_is_consistent_across_ranks(oracle):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_fallback_worker, args=(r, 3, port, q)) for r in range(3)]
+    for p in procs:
+        p.start()
+    parts = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(raised for raised, _ in parts)
+    result = np.array([x for _, part in parts for x in part], np.int32)
+    assert np.array_equal(result, np.sort(oracle.generate_i32("random", 9000, 5)))
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
