@@ -21,6 +21,7 @@
 #include <climits>
 #include <cstring>
 
+#include "common.cuh"
 #include "networks.cuh"
 #include "smem_merge.cuh"
 #include "tma.cuh"
@@ -442,6 +443,8 @@ __global__ void __launch_bounds__(NT, (bs_min_blocks<NT, K, Key>()))
   Key* sm = reinterpret_cast<Key*>(sm_raw);
   const int64_t base = (int64_t)blockIdx.x * stride;
   const int valid = (int)min((int64_t)stride, n - base);
+  pdl_wait();     // src may be the previous kernel's output
+  pdl_trigger();
   cta_sort<NT, K, LEAF>(src + base, dst + base, valid, sm);
 }
 
@@ -539,6 +542,8 @@ template <class Key>
 __global__ void merge_partition_v2_kernel(const Key* __restrict__ src, PassPlan P,
                                           int64_t num_tiles, int64_t* __restrict__ mp) {
   const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  pdl_wait();  // src is the previous pass's output
+  pdl_trigger();
   if (c >= num_tiles) return;
   const TileGeom g = tile_geom(P, c);
   const Key* A = src + g.pair_base;
@@ -657,6 +662,8 @@ __global__ void __launch_bounds__(NT, v2_min_blocks(NT, K, (int)sizeof(Key)))
   const int tid = threadIdx.x;
   const int64_t c = blockIdx.x;
   const TileGeom g = tile_geom(P, c);
+  pdl_wait();  // src / mp come from the previous kernels
+  pdl_trigger();
   if (g.diag0 >= g.diag1) return;  // empty trailing tile of a short last pair
   const bool last_in_pair = g.diag1 == g.a_len + g.b_len;
   int64_t a0, a1;

@@ -35,7 +35,8 @@ static int launch_blocksort(const Key* src, Key* dst, int64_t n, int stride, int
                            "cudaFuncSetAttribute(blocksort)"));
   {
     Prof prof(PK_TILE_SORT, s);
-    kern<<<(unsigned)ctas, NT, smem, s>>>(src, dst, n, stride);
+    const cudaError_t e = launch_pdl(n, kern, (unsigned)ctas, NT, smem, s, src, dst, n, stride);
+    if (e != cudaSuccess) return check_cuda(e, "blocksort_kernel");
   }
   return check_launch("blocksort_kernel");
 }
@@ -204,18 +205,24 @@ static int v2_pass_t(const Key* src, Key* dst, int64_t n, int64_t R, int64_t* mp
     // few tiles: every CTA finds its own split (no partition launch)
     {
       Prof prof(PK_MERGE_PASS, s);
-      merge_pass_v2_kernel<NT, K, true, Key><<<(unsigned)mt, NT, 0, s>>>(src, dst, P, nullptr);
+      const cudaError_t e = launch_pdl(n, merge_pass_v2_kernel<NT, K, true, Key>, (unsigned)mt, NT,
+                                       0, s, src, dst, P, (const int64_t*)nullptr);
+      if (e != cudaSuccess) return check_cuda(e, "merge_pass_v2_kernel<fused>");
     }
     return check_launch("merge_pass_v2_kernel<fused>");
   }
   {
     Prof prof(PK_PARTITION, s);
-    merge_partition_v2_kernel<Key><<<(unsigned)((mt + 255) / 256), 256, 0, s>>>(src, P, mt, mp);
+    const cudaError_t e = launch_pdl(n, merge_partition_v2_kernel<Key>, (unsigned)((mt + 255) / 256),
+                                     256, 0, s, src, P, mt, mp);
+    if (e != cudaSuccess) return check_cuda(e, "merge_partition_v2_kernel");
   }
   NSB_TRY(check_launch("merge_partition_v2_kernel"));
   {
     Prof prof(PK_MERGE_PASS, s);
-    merge_pass_v2_kernel<NT, K, false, Key><<<(unsigned)mt, NT, 0, s>>>(src, dst, P, mp);
+    const cudaError_t e = launch_pdl(n, merge_pass_v2_kernel<NT, K, false, Key>, (unsigned)mt, NT, 0,
+                                     s, src, dst, P, (const int64_t*)mp);
+    if (e != cudaSuccess) return check_cuda(e, "merge_pass_v2_kernel");
   }
   return check_launch("merge_pass_v2_kernel");
 }

@@ -10,6 +10,7 @@
 
 #include <atomic>
 #include <cstring>
+#include <cstdlib>
 #include <cstdint>
 #include <mutex>
 #include <string>
@@ -35,6 +36,14 @@ void set_last_error(const char* where, cudaError_t e) {
 }
 
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+bool pdl_enabled(int64_t n) {
+  static const int mode = [] {
+    const char* e = getenv("NSB_PDL");
+    return e ? atoi(e) : 1;
+  }();
+  return mode == 2 || (mode == 1 && n <= kPdlMaxKeys);
+}
 
 int ensure_smem_attr(const void* kern, int bytes, const char* what) {
   static std::mutex mu;
