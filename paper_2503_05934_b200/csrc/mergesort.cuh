@@ -555,9 +555,22 @@ __global__ void merge_partition_v2_kernel(const Key* __restrict__ src, PassPlan 
 // keys written to dst + *s_out_off.  Shared by the pairwise passes and the
 // pointer-pair merge (samplesort.cu).  Must be called by all NT threads after
 // the staged slices are visible to the CTA.
+// Block samples of a pass's output, for the next pass's partition search
+// (merge_partition_v3_kernel): for every 256-key block j of the output,
+// first[j] = out[256j] and last[j] = out[min(256j + 255, n - 1)].  They are
+// 1/128 of the keys and stay L2-resident.
+constexpr int kSmpShift = 8;
+template <class Key>
+struct BlockSamples {
+  Key* first;   // nullptr: not recorded
+  Key* last;
+  int64_t n;    // keys in the whole array
+};
+
 template <int NT, int K, class Key>
 __device__ __forceinline__ void merge_staged_tile(Key* sm, int a_pos, int la, int b_pos, int lb,
-                                                  Key* dst, const int64_t* s_out_off) {
+                                                  Key* dst, const int64_t* s_out_off,
+                                                  BlockSamples<Key> bs = {nullptr, nullptr, 0}) {
   constexpr int TM = NT * K;
   constexpr int PV = kpv<Key>();
   constexpr int KB = (int)sizeof(Key);
@@ -616,6 +629,15 @@ __device__ __forceinline__ void merge_staged_tile(Key* sm, int a_pos, int la, in
 
   Key* out = dst + *s_out_off;
   const bool o_tma = ((reinterpret_cast<uintptr_t>(out) & 15) == 0) && (total % PV) == 0;
+  __syncthreads();
+  if (bs.first) {  // tiles start on 256-key block boundaries (TM and 2R are multiples of 256)
+    const int nb = (total + (1 << kSmpShift) - 1) >> kSmpShift;
+    const int64_t b0 = *s_out_off >> kSmpShift;
+    if (tid < nb) {
+      bs.first[b0 + tid] = sm[tid << kSmpShift];
+      bs.last[b0 + tid] = sm[min((tid << kSmpShift) + (1 << kSmpShift) - 1, total - 1)];
+    }
+  }
   if (o_tma) {
     fence_proxy_async_smem();
     __syncthreads();
@@ -625,9 +647,58 @@ __device__ __forceinline__ void merge_staged_tile(Key* sm, int a_pos, int la, in
       bulk_wait_read_all();
     }
   } else {
-    __syncthreads();
     for (int i = tid; i < total; i += NT) out[i] = sm[i];
   }
+}
+
+// Partition with the previous pass's block samples.  For a pair of two FULL
+// runs (the bulk of every pass) the split a for diagonal d (a multiple of
+// 256) is bracketed on the samples first: the predicate
+// A[mid] <= B[d-1-mid] at mid = 256j reads A's first[] and B's last[] of
+// block (d/256 - j - 1), both L2-resident; then 8 steps on the keys finish
+// inside one 256-key block.  Other pairs (the array's short last pair) use
+// the plain search.  Same result as merge_path, fewer DRAM round trips.
+template <class Key>
+__global__ void merge_partition_v3_kernel(const Key* __restrict__ src, PassPlan P,
+                                          int64_t num_tiles, int64_t* __restrict__ mp,
+                                          BlockSamples<Key> bs) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  pdl_wait();
+  pdl_trigger();
+  if (c >= num_tiles) return;
+  const TileGeom g = tile_geom(P, c);
+  const Key* A = src + g.pair_base;
+  const Key* B = A + g.a_len;
+  const int64_t diag = g.diag0;
+  if (g.a_len != P.R || g.b_len != P.R || (diag & 255) != 0) {
+    mp[c] = merge_path<int64_t>(A, g.a_len, B, g.b_len, diag);
+    return;
+  }
+  const int64_t R = P.R;
+  int64_t lo = diag > R ? diag - R : 0;
+  int64_t hi = diag < R ? diag : R;
+  // coarse: largest j with 256j in [lo, hi) and P(256j) true  (P(lo) may be checked exactly)
+  const int64_t abase = g.pair_base >> kSmpShift, bbase = (g.pair_base + R) >> kSmpShift;
+  const int64_t dblk = diag >> kSmpShift;
+  int64_t jl = (lo + 255) >> kSmpShift, jh = (hi + 255) >> kSmpShift;  // candidates j in [jl, jh)
+  // P(256j): A[256j] <= B[diag - 1 - 256j] = last[bbase + dblk - j - 1]
+  while (jl < jh) {
+    const int64_t jm = (jl + jh) >> 1;
+    const bool p = (jm << kSmpShift) < hi &&
+                   bs.first[abase + jm] <= bs.last[bbase + dblk - jm - 1];
+    if (p) jl = jm + 1;
+    else jh = jm;
+  }
+  // P holds for 256j, j < jl (inside [lo, hi)) and fails from 256*jl: a in (256(jl-1), 256 jl]
+  int64_t flo = jl > 0 ? max(lo, ((jl - 1) << kSmpShift) + 1) : lo;
+  int64_t fhi = min(hi, jl << kSmpShift);
+  if (flo > fhi) flo = fhi;
+  while (flo < fhi) {
+    const int64_t mid = (flo + fhi) >> 1;
+    if (A[mid] <= B[diag - 1 - mid]) flo = mid + 1;
+    else fhi = mid;
+  }
+  mp[c] = flo;
 }
 
 // Keys of shared memory a v2 tile needs: two slices with up to 3 keys of
@@ -652,7 +723,7 @@ __host__ __device__ constexpr int v2_min_blocks(int NT, int K, int key_bytes) {
 template <int NT, int K, bool FUSED = false, class Key = int32_t>
 __global__ void __launch_bounds__(NT, v2_min_blocks(NT, K, (int)sizeof(Key)))
     merge_pass_v2_kernel(const Key* __restrict__ src, Key* __restrict__ dst, PassPlan P,
-                         const int64_t* __restrict__ mp) {
+                         const int64_t* __restrict__ mp, BlockSamples<Key> bs) {
   constexpr int TM = NT * K;
   static_assert(TM % 4 == 0, "tiles must start 16-byte aligned");
   constexpr int PV = kpv<Key>();           // keys per 16 bytes
@@ -726,7 +797,7 @@ __global__ void __launch_bounds__(NT, v2_min_blocks(NT, K, (int)sizeof(Key)))
     for (int i = tid; i < lb; i += NT) sm[b_off + b_shift + i] = __ldcs(B + i);
   mbar_wait(&bar, 0);
   __syncthreads();
-  merge_staged_tile<NT, K>(sm, a_shift, la, b_off + b_shift, lb, dst, &s_out);
+  merge_staged_tile<NT, K>(sm, a_shift, la, b_off + b_shift, lb, dst, &s_out, bs);
 }
 
 }  // namespace nsb

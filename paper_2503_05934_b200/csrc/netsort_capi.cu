@@ -55,8 +55,10 @@ struct MergeTuning {
   int64_t kway_min = int64_t(1) << 22;
   int64_t fused_max_tiles = 4096;  // passes with fewer tiles search in-kernel (measured crossover)
   int v2 = -1;  // NSB_V2 forces one tile shape (see v2_pass); -1 = by size
+  int samples = 1;  // NSB_SAMPLES=0: plain partition search on every pass
   MergeTuning() {
     if (const char* e = getenv("NSB_V2")) v2 = atoi(e);
+    if (const char* e = getenv("NSB_SAMPLES")) samples = atoi(e);
     if (const char* e = getenv("NSB_FUSED_MAX")) fused_max_tiles = atoll(e);
     if (const char* e = getenv("NSB_TILE")) tile = atoi(e) == 16384 ? 16384 : 8192;
     if (const char* e = getenv("NSB_KWAY")) kway = atoi(e);
@@ -85,17 +87,40 @@ static size_t kway_temp(size_t n) {
          align_up(kway_max_cuts(n) * 4, 256);
 }
 
+// block samples (first/last key of every 256-key block) for the partition
+static size_t samples_bytes(size_t n, size_t kb) {
+  return 2 * align_up(((n >> kSmpShift) + 2) * kb, 256);
+}
+
 size_t merge_sort_temp(size_t n) {
   if (n <= (size_t)kSmT) return 0;
   return align_up(n * sizeof(int32_t), 256) + align_up((max_merge_tiles(n) + 1) * 8, 256) +
-         kway_temp(n);
+         kway_temp(n) + samples_bytes(n, 4);
 }
 
-// int64: ping-pong buffer + merge-path splits (no k-way scratch)
+// int64: ping-pong buffer + merge-path splits + block samples (no k-way scratch)
 size_t merge_sort_temp_i64(size_t n) {
   if (n <= (size_t)kSmT) return 0;
-  return align_up(n * sizeof(int64_t), 256) + align_up((max_merge_tiles(n) + 1) * 8, 256);
+  return align_up(n * sizeof(int64_t), 256) + align_up((max_merge_tiles(n) + 1) * 8, 256) +
+         samples_bytes(n, 8);
 }
+
+// Block samples of the pass outputs of one sort: recorded by every merge
+// pass, used by the next pass's partition when `have` (the array's previous
+// pass recorded them for the same n).
+struct SmpCtx {
+  void* base = nullptr;  // first[] then last[]
+  int64_t n = 0;
+  bool have = false;
+  template <class Key>
+  BlockSamples<Key> get() const {
+    if (!base) return BlockSamples<Key>{nullptr, nullptr, 0};
+    Key* f = static_cast<Key*>(base);
+    Key* l = reinterpret_cast<Key*>(static_cast<char*>(base) +
+                                    align_up((((size_t)n >> kSmpShift) + 2) * sizeof(Key), 256));
+    return BlockSamples<Key>{f, l, n};
+  }
+};
 
 struct KwScratch {
   uint64_t *raw, *m1, *m2;
@@ -196,34 +221,45 @@ static PassPlan plan_pass(int64_t n, int64_t R, int nt = kV2NT, int k = kV2K) {
 // One pairwise merge pass (v2): runs of R in src -> runs of 2R in dst.
 template <int NT, int K, class Key>
 static int v2_pass_t(const Key* src, Key* dst, int64_t n, int64_t R, int64_t* mp,
-                     cudaStream_t s) {
+                     cudaStream_t s, SmpCtx* sc = nullptr) {
   const MergeTuning& tu = tuning();
   const PassPlan P = plan_pass(n, R, NT, K);
   const int64_t pairs = (n + 2 * R - 1) / (2 * R);
   const int64_t mt = pairs * P.tpp;
+  // samples: only for the whole array of a sort (sc->n == n); tiles must be
+  // whole 256-key blocks (NT*K a multiple of 256)
+  const bool rec = sc && sc->base && sc->n == n && ((NT * K) & 255) == 0;
+  const BlockSamples<Key> bs = rec ? sc->get<Key>() : BlockSamples<Key>{nullptr, nullptr, 0};
   if (mt <= tu.fused_max_tiles) {
     // few tiles: every CTA finds its own split (no partition launch)
     {
       Prof prof(PK_MERGE_PASS, s);
       const cudaError_t e = launch_pdl(n, merge_pass_v2_kernel<NT, K, true, Key>, (unsigned)mt, NT,
-                                       0, s, src, dst, P, (const int64_t*)nullptr);
+                                       0, s, src, dst, P, (const int64_t*)nullptr, bs);
       if (e != cudaSuccess) return check_cuda(e, "merge_pass_v2_kernel<fused>");
     }
+    if (sc) sc->have = rec;
     return check_launch("merge_pass_v2_kernel<fused>");
   }
   {
     Prof prof(PK_PARTITION, s);
-    const cudaError_t e = launch_pdl(n, merge_partition_v2_kernel<Key>, (unsigned)((mt + 255) / 256),
-                                     256, 0, s, src, P, mt, mp);
-    if (e != cudaSuccess) return check_cuda(e, "merge_partition_v2_kernel");
+    cudaError_t e;
+    if (sc && sc->have && rec && tu.samples)
+      e = launch_pdl(n, merge_partition_v3_kernel<Key>, (unsigned)((mt + 255) / 256), 256, 0, s,
+                     src, P, mt, mp, bs);
+    else
+      e = launch_pdl(n, merge_partition_v2_kernel<Key>, (unsigned)((mt + 255) / 256), 256, 0, s,
+                     src, P, mt, mp);
+    if (e != cudaSuccess) return check_cuda(e, "merge_partition_kernel");
   }
-  NSB_TRY(check_launch("merge_partition_v2_kernel"));
+  NSB_TRY(check_launch("merge_partition_kernel"));
   {
     Prof prof(PK_MERGE_PASS, s);
     const cudaError_t e = launch_pdl(n, merge_pass_v2_kernel<NT, K, false, Key>, (unsigned)mt, NT, 0,
-                                     s, src, dst, P, (const int64_t*)mp);
+                                     s, src, dst, P, (const int64_t*)mp, bs);
     if (e != cudaSuccess) return check_cuda(e, "merge_pass_v2_kernel");
   }
+  if (sc) sc->have = rec;
   return check_launch("merge_pass_v2_kernel");
 }
 
@@ -233,36 +269,36 @@ static int v2_pass_t(const Key* src, Key* dst, int64_t n, int64_t R, int64_t* mp
 // keys, 12 CTAs/SM) win by 5-10 %; above, <256,31> (7936 keys, 6 CTAs/SM)
 // is within 0.5 % of the best shape measured.
 static int v2_pass(const int32_t* src, int32_t* dst, int64_t n, int64_t R, int64_t* mp,
-                   cudaStream_t s) {
+                   cudaStream_t s, SmpCtx* sc = nullptr) {
   switch (tuning().v2) {
-    case 0: return v2_pass_t<kV2NT, kV2K>(src, dst, n, R, mp, s);
-    case 1: return v2_pass_t<512, 15>(src, dst, n, R, mp, s);
-    case 2: return v2_pass_t<384, 21>(src, dst, n, R, mp, s);
-    case 3: return v2_pass_t<128, 31>(src, dst, n, R, mp, s);
-    case 5: return v2_pass_t<128, 47>(src, dst, n, R, mp, s);
-    case 6: return v2_pass_t<128, 23>(src, dst, n, R, mp, s);
-    case 9: return v2_pass_t<128, 63>(src, dst, n, R, mp, s);
-    case 11: return v2_pass_t<128, 55>(src, dst, n, R, mp, s);
+    case 0: return v2_pass_t<kV2NT, kV2K>(src, dst, n, R, mp, s, sc);
+    case 1: return v2_pass_t<512, 15>(src, dst, n, R, mp, s, sc);
+    case 2: return v2_pass_t<384, 21>(src, dst, n, R, mp, s, sc);
+    case 3: return v2_pass_t<128, 31>(src, dst, n, R, mp, s, sc);
+    case 5: return v2_pass_t<128, 47>(src, dst, n, R, mp, s, sc);
+    case 6: return v2_pass_t<128, 23>(src, dst, n, R, mp, s, sc);
+    case 9: return v2_pass_t<128, 63>(src, dst, n, R, mp, s, sc);
+    case 11: return v2_pass_t<128, 55>(src, dst, n, R, mp, s, sc);
     default:
-      return n <= (int64_t(1) << 23) ? v2_pass_t<128, 23>(src, dst, n, R, mp, s)
-                                     : v2_pass_t<kV2NT, kV2K>(src, dst, n, R, mp, s);
+      return n <= (int64_t(1) << 23) ? v2_pass_t<128, 23>(src, dst, n, R, mp, s, sc)
+                                     : v2_pass_t<kV2NT, kV2K>(src, dst, n, R, mp, s, sc);
   }
 }
 static int v2_pass(const int64_t* src, int64_t* dst, int64_t n, int64_t R, int64_t* mp,
-                   cudaStream_t s) {
+                   cudaStream_t s, SmpCtx* sc = nullptr) {
   static const int shape = [] {
     const char* e = getenv("NSB_V2_64");
     return e ? atoi(e) : -1;
   }();
   switch (shape) {
-    case 0: return v2_pass_t<kV2NT, kV2K64>(src, dst, n, R, mp, s);
-    case 1: return v2_pass_t<128, 23>(src, dst, n, R, mp, s);
-    case 2: return v2_pass_t<128, 31>(src, dst, n, R, mp, s);
-    case 3: return v2_pass_t<128, 15>(src, dst, n, R, mp, s);
+    case 0: return v2_pass_t<kV2NT, kV2K64>(src, dst, n, R, mp, s, sc);
+    case 1: return v2_pass_t<128, 23>(src, dst, n, R, mp, s, sc);
+    case 2: return v2_pass_t<128, 31>(src, dst, n, R, mp, s, sc);
+    case 3: return v2_pass_t<128, 15>(src, dst, n, R, mp, s, sc);
     default:  // by size (tools/i64_sweep.sh on B200)
-      if (n <= (int64_t(1) << 20)) return v2_pass_t<128, 15>(src, dst, n, R, mp, s);
-      if (n <= (int64_t(1) << 25)) return v2_pass_t<128, 23>(src, dst, n, R, mp, s);
-      return v2_pass_t<128, 31>(src, dst, n, R, mp, s);
+      if (n <= (int64_t(1) << 20)) return v2_pass_t<128, 15>(src, dst, n, R, mp, s, sc);
+      if (n <= (int64_t(1) << 25)) return v2_pass_t<128, 23>(src, dst, n, R, mp, s, sc);
+      return v2_pass_t<128, 31>(src, dst, n, R, mp, s, sc);
   }
 }
 
@@ -335,6 +371,13 @@ static int merge_sort_device_t(Key* d_keys, size_t n, int leaf, void* d_temp, si
     return T == kSmT ? launch_blocksort<kSmNT, kSmK, LF>(d_keys, cur, (int64_t)n, T, tiles, s)
                      : launch_blocksort<kBsNT, kBsK, LF>(d_keys, cur, (int64_t)n, T, tiles, s);
   }));
+  SmpCtx sc;
+  {
+    size_t off = align_up(n * sizeof(Key), 256) + align_up((max_merge_tiles(n) + 1) * 8, 256);
+    if constexpr (k32) off += kway_temp(n);
+    sc.base = static_cast<char*>(d_temp) + off;
+    sc.n = (int64_t)n;
+  }
   int64_t R = T;
   for (int pi = 0; pi < npass; ++pi) {
     const int k = sched[pi];
@@ -344,12 +387,13 @@ static int merge_sort_device_t(Key* d_keys, size_t n, int leaf, void* d_temp, si
                                             align_up((max_merge_tiles(n) + 1) * 8, 256),
                                         n);
         NSB_TRY(kway_pass(cur, other, (int64_t)n, R, k, ks, s));
+        sc.have = false;  // the k-way kernel records no block samples
         std::swap(cur, other);
         R *= k;
         continue;
       }
     }
-    NSB_TRY(v2_pass(cur, other, (int64_t)n, R, mp, s));
+    NSB_TRY(v2_pass(cur, other, (int64_t)n, R, mp, s, &sc));
     std::swap(cur, other);
     R *= 2;
   }
