@@ -392,6 +392,16 @@ __device__ __forceinline__ void cta_sort(const Key* in, Key* out, int valid, Key
       for (int k = 0; k < KM; ++k) {
         const bool take_a = ka <= kb;  // A wins ties (merge_runs, hybrid.hpp:71-75)
         w[k] = take_a ? ka : kb;
+#ifndef NSB_TS_SPLIT_LDS
+        // one 32-lane shared load per step (address selected per lane): this
+        // kernel is LSU-bound, and one random 32-lane access costs fewer
+        // wavefronts than two predicated 16-lane ones
+        if (take_a) oa = min(oa + (uint32_t)KB, ea);
+        else ob = min(ob + (uint32_t)KB, eb);
+        const Key x = *reinterpret_cast<const Key*>(smc + (take_a ? oa : ob));
+        if (take_a) ka = x;
+        else kb = x;
+#else
         if (take_a) {
           oa = min(oa + (uint32_t)KB, ea);
           ka = *reinterpret_cast<const Key*>(smc + oa);
@@ -399,6 +409,7 @@ __device__ __forceinline__ void cta_sort(const Key* in, Key* out, int valid, Key
           ob = min(ob + (uint32_t)KB, eb);
           kb = *reinterpret_cast<const Key*>(smc + ob);
         }
+#endif
       }
       __syncthreads();  // every thread is done reading this level's input
       Key* o = sm + p * S2 + d;
