@@ -314,6 +314,40 @@ static int small_sort(Key* d_keys, size_t n, int leaf, cudaStream_t s) {
   return merge_sort_device(d_keys, n, leaf, nullptr, 0, s);
 }
 
+// Leaf jobs of a partition level.  Consecutive buckets hold disjoint,
+// ascending key ranges, so a run of NEIGHBOURING buckets sorted as one tile
+// is each bucket sorted: small buckets are packed greedily into tiles of up
+// to kPackKeys keys, which removes the per-bucket tile padding (buckets of
+// ~4 K keys in 4 K/8 K tiles wasted about a third of the bucket-sort work).
+// Jobs are grouped by tile size class: <=2048, <=4096, <=8192, <=16384 keys.
+constexpr int64_t kPackKeys = 8192;
+struct JobPacker {
+  std::vector<int64_t> cls[4];
+  int64_t js = 0, jl = 0;
+  static int class_of(int64_t len) { return len <= 2048 ? 0 : len <= 4096 ? 1 : len <= 8192 ? 2 : 3; }
+  void flush() {
+    if (jl > 0) {
+      auto& c = cls[class_of(jl)];
+      c.push_back(js);
+      c.push_back(jl);
+    }
+    jl = 0;
+  }
+  // bucket [st, st+len), len <= kSmallTile
+  void add(int64_t st, int64_t len) {
+    if (len == 0) return;
+    if (len > kPackKeys) {  // alone in the 16 K class
+      flush();
+      cls[3].push_back(st);
+      cls[3].push_back(len);
+      return;
+    }
+    if (jl > 0 && (js + jl != st || jl + len > kPackKeys)) flush();
+    if (jl == 0) js = st;
+    jl += len;
+  }
+};
+
 // Sorts keys[0..n) in place; tmp holds n keys of scratch; aux is reused by
 // recursive calls only after this level has enqueued all its work.
 static int quick_sort_level(int32_t* keys, int32_t* tmp, size_t n, int leaf, const QsAux& aux,
@@ -384,19 +418,20 @@ static int quick_sort_level(int32_t* keys, int32_t* tmp, size_t n, int leaf, con
 
   // Size classes: one CTA shape per class so small buckets do not pay for a
   // 16K-key tile.  Classes: <=2048, <=4096, <=8192, <=16384, larger.
-  std::vector<int64_t> cls[4];
+  JobPacker pk;
   std::vector<int> big;
   for (int b = 0; b < NB; ++b) {
     const int64_t len = totals[b];
     if (len == 0) continue;
-    const int c = len <= 2048 ? 0 : len <= 4096 ? 1 : len <= 8192 ? 2 : len <= 16384 ? 3 : 4;
-    if (c < 4) {
-      cls[c].push_back((int64_t)starts[b]);
-      cls[c].push_back(len);
+    if (len <= kSmallTile) {
+      pk.add((int64_t)starts[b], len);
     } else {
+      pk.flush();
       big.push_back(b);
     }
   }
+  pk.flush();
+  auto& cls = pk.cls;
   std::vector<int64_t> jobs;
   int off[5] = {0, 0, 0, 0, 0};
   for (int c = 0; c < 4; ++c) {
@@ -788,7 +823,8 @@ static int ml_quick_sort(Key* keys, Key* tmp, size_t n, int leaf, const MlAux<Ke
     NSB_TRY(check_cuda(cudaStreamSynchronize(s), "cudaStreamSynchronize"));
     // ---- plan buckets: fill positions, jobs, next level
     fill.resize(cnt);
-    std::vector<int64_t> cls[4], copies;
+    JobPacker pk;
+    std::vector<int64_t> copies;
     std::vector<std::pair<int64_t, int64_t>> next;
     for (const auto& g : segs) {
       int64_t acc = g.start;
@@ -797,16 +833,17 @@ static int ml_quick_sort(Key* keys, Key* tmp, size_t n, int leaf, const MlAux<Ke
         const int64_t len = counts[g.cnt_off + b];
         fill[g.cnt_off + b] = (unsigned long long)acc;
         if (len > 0) {
-          if (b & 1) {  // constant bucket: already sorted
+          if (len <= kSmallTile) {
+            // leaf (a constant bucket too: sorting it from Y is its copy)
+            pk.add(acc, len);
+          } else if (b & 1) {  // large constant bucket: already sorted
+            pk.flush();
             if (Y != keys) {
               copies.push_back(acc);
               copies.push_back(len);
             }
-          } else if (len <= kSmallTile) {
-            const int c = len <= 2048 ? 0 : len <= 4096 ? 1 : len <= 8192 ? 2 : 3;
-            cls[c].push_back(acc);
-            cls[c].push_back(len);
           } else {
+            pk.flush();
             next.push_back({acc, len});
           }
         }
@@ -821,6 +858,8 @@ static int ml_quick_sort(Key* keys, Key* tmp, size_t n, int leaf, const MlAux<Ke
       ml_scatter_kernel<Key><<<(unsigned)chunks, kMlNT, 0, s>>>(X, ax.segs, nseg, ax.spl, ax.fill, Y);
     }
     NSB_TRY(check_launch("ml_scatter_kernel"));
+    pk.flush();
+    auto& cls = pk.cls;
     // ---- leaf buckets -> key buffer
     std::vector<int64_t> jobs;
     int off[6] = {0, 0, 0, 0, 0, 0};
