@@ -506,3 +506,35 @@ def test_bench_multi_rank_code_path_on_one_gpu(exchange):
     assert line["n_gpus"] == 2 and line["verified"] is True
     assert line["nvlink"]["bytes_per_rank_max"] > 0
     assert line["exchange"]["mode"] == exchange
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("kind", ["all_equal", "three_values", "reverse", "sawtooth", "int_max_heavy"])
+def test_adversarial_inputs_large(ns, cuda, kind):
+    """2^26 keys of adversarial shapes through both algorithms: ties everywhere
+    (merge-path ties, constant quick-sort buckets), reverse order, periodic
+    runs, and heavy use of INT_MAX (the kernels' sentinel/pad value)."""
+    import torch
+    n = 1 << 26
+    g = torch.Generator(device=cuda)
+    g.manual_seed(7)
+    if kind == "all_equal":
+        base = torch.full((n,), 12345, dtype=torch.int32, device=cuda)
+    elif kind == "three_values":
+        base = torch.randint(0, 3, (n,), dtype=torch.int32, device=cuda, generator=g)
+    elif kind == "reverse":
+        base = torch.arange(n, 0, -1, dtype=torch.int32, device=cuda)
+    elif kind == "sawtooth":
+        base = (torch.arange(n, dtype=torch.int32, device=cuda) % 4099) * 3
+    else:
+        base = torch.randint(0, 2**31 - 1, (n,), dtype=torch.int32, device=cuda, generator=g)
+        base[torch.rand(n, device=cuda, generator=g) < 0.3] = 2**31 - 1
+    want_digest = ns.multiset_digest(base)
+    for fn, cfg in ((ns.optimized_merge_sort, "6To8"), (ns.optimized_quick_sort, "3To5")):
+        t = base.clone()
+        fn(t, ns.find_config(cfg))
+        assert ns.count_inversions(t) == 0, (kind, fn.__name__)
+        assert ns.multiset_digest(t) == want_digest, (kind, fn.__name__)
+    del base, t
+    ns.release_scratch()
+    torch.cuda.empty_cache()
