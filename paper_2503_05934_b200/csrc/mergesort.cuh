@@ -275,10 +275,11 @@ __device__ __forceinline__ void tile_store(const Key* sm, Key* out, int valid) {
 // ---------------------------------------------------------------------------
 
 // Padded variant (one pad word per 32 keys, serial merge with clamped
-// indices): kept for int64 keys and 1024-thread tiles, where the skewed
-// variant below needs more registers than the occupancy it must keep
-// (measured: 2^28 int64 sort 15.1 vs 16.6 ms, 65,536 x 16,384 segmented
-// 9.8 vs 11.2 ms).
+// indices): kept for int64 keys, where the skewed variant below needs more
+// registers than the occupancy it must keep (measured: 2^28 int64 sort 15.1
+// vs 16.6 ms).  int32 tiles of up to 1024 threads use the skewed variant at
+// 2048 threads/SM (32 registers, no spills): 65,536 x 16,384 segmented
+// 9.8 -> 9.3 ms.
 template <int NT, int K, int LEAF, class Key>
 __device__ __forceinline__ void cta_sort_padded(const Key* in, Key* out, int valid, Key* sm) {
   constexpr int T = NT * K;
@@ -324,9 +325,12 @@ __device__ __forceinline__ void cta_sort_padded(const Key* in, Key* out, int val
 // for any k the 32 lanes' k-th output stores fall on 32 different banks
 // without padding words; every lane runs the same 17 unguarded merge steps
 // and only the stores are predicated.
+#ifndef NSB_SKEW_MAX_NT
+#define NSB_SKEW_MAX_NT 1024
+#endif
 template <int NT, int K, class Key>
 __host__ __device__ constexpr bool cta_sort_skewed() {
-  return sizeof(Key) == 4 && NT > 32 && NT <= 512;
+  return sizeof(Key) == 4 && NT > 32 && NT <= NSB_SKEW_MAX_NT;
 }
 
 template <int NT, int K, int LEAF, class Key>
@@ -438,7 +442,7 @@ __device__ __forceinline__ void cta_sort(const Key* in, Key* out, int valid, Key
 // (stride == T for plain tiling, the segment length for segmented sorts).
 // Resident CTAs per SM requested for a tile-sort CTA of NT threads.
 #ifndef NSB_BS_THREADS_PER_SM
-#define NSB_BS_THREADS_PER_SM 1536
+#define NSB_BS_THREADS_PER_SM 2048
 #endif
 template <int NT, int K, class Key>
 __host__ __device__ constexpr int bs_min_blocks() {
