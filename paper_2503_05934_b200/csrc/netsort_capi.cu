@@ -62,7 +62,7 @@ struct MergeTuning {
     if (const char* e = getenv("NSB_FUSED_MAX")) fused_max_tiles = atoll(e);
     if (const char* e = getenv("NSB_TILE")) {
       const int t = atoi(e);
-      tile = (t == 16384 || t == 4096 || t == 2048) ? t : 8192;
+      tile = (t == 16384 || t == 4096 || t == 2048 || t == 1024) ? t : 8192;
     }
     if (const char* e = getenv("NSB_KWAY")) kway = atoi(e);
     if (const char* e = getenv("NSB_KWAY_MIN")) kway_min = atoll(e);
@@ -373,6 +373,7 @@ static int merge_sort_device_t(Key* d_keys, size_t n, int leaf, void* d_temp, si
     constexpr int LF = decltype(L)::value;
     if (T == 4096) return launch_blocksort<256, 16, LF>(d_keys, cur, (int64_t)n, T, tiles, s);
     if (T == 2048) return launch_blocksort<128, 16, LF>(d_keys, cur, (int64_t)n, T, tiles, s);
+    if (T == 1024) return launch_blocksort<64, 16, LF>(d_keys, cur, (int64_t)n, T, tiles, s);
     return T == kSmT ? launch_blocksort<kSmNT, kSmK, LF>(d_keys, cur, (int64_t)n, T, tiles, s)
                      : launch_blocksort<kBsNT, kBsK, LF>(d_keys, cur, (int64_t)n, T, tiles, s);
   }));
