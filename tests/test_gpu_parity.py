@@ -538,3 +538,83 @@ def test_adversarial_inputs_large(ns, cuda, kind):
     del base, t
     ns.release_scratch()
     torch.cuda.empty_cache()
+
+
+def test_c_abi_status_codes_on_device(ns, cuda):
+    """The C ABI never throws; bad arguments / short scratch return statuses
+    and leave the keys untouched (include/netsort_b200.h conventions)."""
+    import ctypes as C
+    import torch
+    from paper_2503_05934_b200 import _lib
+    L = ns.lib()
+    s = torch.cuda.current_stream().cuda_stream
+    n = 100_000
+    a = torch.randint(0, 1000, (n,), dtype=torch.int32, device=cuda)
+    before = a.clone()
+    need = L.ns_merge_sort_temp_bytes(n)
+    assert need > 0
+    small = torch.empty(need // 2, dtype=torch.uint8, device=cuda)
+    # scratch too small -> NS_ERR_TEMP, nothing launched on the keys
+    assert L.ns_merge_sort_i32(a.data_ptr(), n, 1 << 8, 0, small.data_ptr(), need // 2, s) == \
+        _lib.NS_ERR_TEMP
+    assert L.ns_merge_sort_i32(a.data_ptr(), n, 1 << 8, 0, None, 0, s) == _lib.NS_ERR_TEMP
+    torch.cuda.synchronize()
+    assert torch.equal(a, before)
+    # null keys with n > 0 -> NS_ERR_INVALID; n == 0 is a no-op on null
+    assert L.ns_merge_sort_i32(None, n, 1 << 8, 0, None, 0, s) == _lib.NS_ERR_INVALID
+    assert L.ns_quick_sort_i32(None, 10, 1 << 3, 0, None, 0, s) == _lib.NS_ERR_INVALID
+    assert L.ns_quick_sort_i64(None, 1, 1 << 3, 0, None, 0, s) == _lib.NS_ERR_INVALID
+    assert L.ns_merge_sort_i32(None, 0, 1 << 8, 0, None, 0, s) == _lib.NS_OK
+    assert L.ns_quick_sort_i64(None, 0, 1 << 3, 0, None, 0, s) == _lib.NS_OK
+    qneed = L.ns_quick_sort_temp_bytes(n)
+    assert L.ns_quick_sort_i32(a.data_ptr(), n, 1 << 3, 0, small.data_ptr(), 16, s) == \
+        _lib.NS_ERR_TEMP
+    # merge runs: bad run count / decreasing offsets
+    offs = (C.c_int64 * 3)(0, 60_000, 50_000)
+    tb = L.ns_merge_runs_temp_bytes(n, 2)
+    big = torch.empty(max(tb, qneed, 1), dtype=torch.uint8, device=cuda)
+    assert L.ns_merge_runs_i32(a.data_ptr(), C.cast(offs, C.c_void_p), 2, big.data_ptr(), tb,
+                               s) == _lib.NS_ERR_INVALID
+    assert L.ns_merge_runs_i32(a.data_ptr(), C.cast(offs, C.c_void_p), 0, big.data_ptr(), tb,
+                               s) == _lib.NS_ERR_INVALID
+    # batch with an array longer than 8 -> NS_ERR_INVALID, keys untouched
+    keys = torch.arange(20, 0, -1, dtype=torch.int32, device=cuda)
+    koffs = torch.tensor([0, 4, 16, 20], dtype=torch.int32, device=cuda)
+    kb = keys.clone()
+    assert L.ns_sort_small_batch_i32(keys.data_ptr(), koffs.data_ptr(), 3, s) == _lib.NS_ERR_INVALID
+    assert torch.equal(keys, kb)
+    # key-value: n >= 2^32 rejected without touching memory
+    assert L.ns_sort_pairs_i32(a.data_ptr(), None, 1 << 33, big.data_ptr(), tb, s) == \
+        _lib.NS_ERR_INVALID
+    # the status strings are never NULL
+    for st in range(-1, 6):
+        assert L.ns_status_string(st)
+    torch.cuda.synchronize()
+    assert torch.equal(a, before)
+
+
+def test_two_streams_concurrently(ns, cuda, oracle):
+    """Stream-ordered and reentrant on disjoint buffers: two sorts on two
+    streams, each with its own scratch, overlap without interference."""
+    import torch
+    from paper_2503_05934_b200._lib import check
+    L = ns.lib()
+    n = 1 << 22
+    a = oracle.generate_i32("random", n, 1)
+    b = oracle.generate_i32("nearly_sorted", n, 2)
+    ta, tb_ = torch.from_numpy(a).to(cuda), torch.from_numpy(b).to(cuda)
+    need = L.ns_merge_sort_temp_bytes(n)
+    sa, sb = torch.cuda.Stream(), torch.cuda.Stream()
+    xa = torch.empty(need, dtype=torch.uint8, device=cuda)
+    xb = torch.empty(need, dtype=torch.uint8, device=cuda)
+    torch.cuda.synchronize()
+    for _ in range(3):
+        ta.copy_(torch.from_numpy(a))
+        tb_.copy_(torch.from_numpy(b))
+        torch.cuda.synchronize()
+        check(L.ns_merge_sort_i32(ta.data_ptr(), n, 1 << 8, 0, xa.data_ptr(), need, sa.cuda_stream), "a")
+        check(L.ns_merge_sort_i32(tb_.data_ptr(), n, 1 << 8, 0, xb.data_ptr(), need,
+                                  sb.cuda_stream), "b")
+        torch.cuda.synchronize()
+        assert np.array_equal(ta.cpu().numpy(), np.sort(a))
+        assert np.array_equal(tb_.cpu().numpy(), np.sort(b))
