@@ -574,18 +574,20 @@ __global__ void merge_partition_v2_kernel(const Key* __restrict__ src, PassPlan 
 // (merge_partition_v3_kernel): for every 256-key block j of the output,
 // first[j] = out[256j] and last[j] = out[min(256j + 255, n - 1)].  They are
 // 1/128 of the keys and stay L2-resident.
-constexpr int kSmpShift = 8;
+constexpr int kSmpShift = 8;     // 256-key blocks when the tile size allows
+constexpr int kSmpShiftMin = 7;  // 128-key blocks otherwise (sizes the buffer)
 template <class Key>
 struct BlockSamples {
   Key* first;   // nullptr: not recorded
   Key* last;
   int64_t n;    // keys in the whole array
+  int shift;    // log2 of the block size
 };
 
 template <int NT, int K, class Key>
 __device__ __forceinline__ void merge_staged_tile(Key* sm, int a_pos, int la, int b_pos, int lb,
                                                   Key* dst, const int64_t* s_out_off,
-                                                  BlockSamples<Key> bs = {nullptr, nullptr, 0}) {
+                                                  BlockSamples<Key> bs = {nullptr, nullptr, 0, kSmpShift}) {
   constexpr int TM = NT * K;
   constexpr int PV = kpv<Key>();
   constexpr int KB = (int)sizeof(Key);
@@ -645,12 +647,13 @@ __device__ __forceinline__ void merge_staged_tile(Key* sm, int a_pos, int la, in
   Key* out = dst + *s_out_off;
   const bool o_tma = ((reinterpret_cast<uintptr_t>(out) & 15) == 0) && (total % PV) == 0;
   __syncthreads();
-  if (bs.first) {  // tiles start on 256-key block boundaries (TM and 2R are multiples of 256)
-    const int nb = (total + (1 << kSmpShift) - 1) >> kSmpShift;
-    const int64_t b0 = *s_out_off >> kSmpShift;
-    if (tid < nb) {
-      bs.first[b0 + tid] = sm[tid << kSmpShift];
-      bs.last[b0 + tid] = sm[min((tid << kSmpShift) + (1 << kSmpShift) - 1, total - 1)];
+  if (bs.first) {  // tiles start on block boundaries (TM and 2R are multiples of the block)
+    const int sh = bs.shift;
+    const int nb = (total + (1 << sh) - 1) >> sh;
+    const int64_t b0 = *s_out_off >> sh;
+    for (int t = tid; t < nb; t += NT) {
+      bs.first[b0 + t] = sm[t << sh];
+      bs.last[b0 + t] = sm[min((t << sh) + (1 << sh) - 1, total - 1)];
     }
   }
   if (o_tma) {
@@ -685,28 +688,30 @@ __global__ void merge_partition_v3_kernel(const Key* __restrict__ src, PassPlan 
   const Key* A = src + g.pair_base;
   const Key* B = A + g.a_len;
   const int64_t diag = g.diag0;
-  if (g.a_len != P.R || g.b_len != P.R || (diag & 255) != 0) {
+  const int sh = bs.shift;
+  const int64_t bm = (int64_t(1) << sh) - 1;
+  if (g.a_len != P.R || g.b_len != P.R || (diag & bm) != 0) {
     mp[c] = merge_path<int64_t>(A, g.a_len, B, g.b_len, diag);
     return;
   }
   const int64_t R = P.R;
   int64_t lo = diag > R ? diag - R : 0;
   int64_t hi = diag < R ? diag : R;
-  // coarse: largest j with 256j in [lo, hi) and P(256j) true  (P(lo) may be checked exactly)
-  const int64_t abase = g.pair_base >> kSmpShift, bbase = (g.pair_base + R) >> kSmpShift;
-  const int64_t dblk = diag >> kSmpShift;
-  int64_t jl = (lo + 255) >> kSmpShift, jh = (hi + 255) >> kSmpShift;  // candidates j in [jl, jh)
-  // P(256j): A[256j] <= B[diag - 1 - 256j] = last[bbase + dblk - j - 1]
+  // coarse over block starts mid = j*blk in [lo, hi): find the first j where
+  // P(mid) = A[mid] <= B[diag - 1 - mid] fails; B's element is the LAST key
+  // of block (diag/blk - j - 1) because diag is a block multiple
+  const int64_t abase = g.pair_base >> sh, bbase = (g.pair_base + R) >> sh;
+  const int64_t dblk = diag >> sh;
+  int64_t jl = (lo + bm) >> sh, jh = (hi + bm) >> sh;  // candidates j in [jl, jh)
   while (jl < jh) {
     const int64_t jm = (jl + jh) >> 1;
-    const bool p = (jm << kSmpShift) < hi &&
-                   bs.first[abase + jm] <= bs.last[bbase + dblk - jm - 1];
+    const bool p = (jm << sh) < hi && bs.first[abase + jm] <= bs.last[bbase + dblk - jm - 1];
     if (p) jl = jm + 1;
     else jh = jm;
   }
-  // P holds for 256j, j < jl (inside [lo, hi)) and fails from 256*jl: a in (256(jl-1), 256 jl]
-  int64_t flo = jl > 0 ? max(lo, ((jl - 1) << kSmpShift) + 1) : lo;
-  int64_t fhi = min(hi, jl << kSmpShift);
+  // P holds at block starts j < jl and fails from jl: a in (blk(jl-1), blk*jl]
+  int64_t flo = jl > 0 ? max(lo, ((jl - 1) << sh) + 1) : lo;
+  int64_t fhi = min(hi, jl << sh);
   if (flo > fhi) flo = fhi;
   while (flo < fhi) {
     const int64_t mid = (flo + fhi) >> 1;

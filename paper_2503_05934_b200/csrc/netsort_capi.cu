@@ -92,7 +92,7 @@ static size_t kway_temp(size_t n) {
 
 // block samples (first/last key of every 256-key block) for the partition
 static size_t samples_bytes(size_t n, size_t kb) {
-  return 2 * align_up(((n >> kSmpShift) + 2) * kb, 256);
+  return 2 * align_up(((n >> kSmpShiftMin) + 2) * kb, 256);
 }
 
 size_t merge_sort_temp(size_t n) {
@@ -115,13 +115,14 @@ struct SmpCtx {
   void* base = nullptr;  // first[] then last[]
   int64_t n = 0;
   bool have = false;
+  int shift = kSmpShift;  // block size the last recording pass used
   template <class Key>
-  BlockSamples<Key> get() const {
-    if (!base) return BlockSamples<Key>{nullptr, nullptr, 0};
+  BlockSamples<Key> get(int sh) const {
+    if (!base) return BlockSamples<Key>{nullptr, nullptr, 0, sh};
     Key* f = static_cast<Key*>(base);
     Key* l = reinterpret_cast<Key*>(static_cast<char*>(base) +
-                                    align_up((((size_t)n >> kSmpShift) + 2) * sizeof(Key), 256));
-    return BlockSamples<Key>{f, l, n};
+                                    align_up((((size_t)n >> kSmpShiftMin) + 2) * sizeof(Key), 256));
+    return BlockSamples<Key>{f, l, n, sh};
   }
 };
 
@@ -231,8 +232,12 @@ static int v2_pass_t(const Key* src, Key* dst, int64_t n, int64_t R, int64_t* mp
   const int64_t mt = pairs * P.tpp;
   // samples: only for the whole array of a sort (sc->n == n); tiles must be
   // whole 256-key blocks (NT*K a multiple of 256)
-  const bool rec = sc && sc->base && sc->n == n && ((NT * K) & 255) == 0;
-  const BlockSamples<Key> bs = rec ? sc->get<Key>() : BlockSamples<Key>{nullptr, nullptr, 0};
+  // block = 256 keys when the tile is a multiple of it, else 128 (every
+  // shape's NT is a multiple of 128)
+  constexpr int kShift = ((NT * K) % 256 == 0) ? kSmpShift : kSmpShiftMin;
+  const bool rec = sc && sc->base && sc->n == n && ((NT * K) % (1 << kShift)) == 0;
+  const BlockSamples<Key> bs =
+      rec ? sc->get<Key>(kShift) : BlockSamples<Key>{nullptr, nullptr, 0, kShift};
   if (mt <= tu.fused_max_tiles) {
     // few tiles: every CTA finds its own split (no partition launch)
     {
@@ -241,7 +246,10 @@ static int v2_pass_t(const Key* src, Key* dst, int64_t n, int64_t R, int64_t* mp
                                        0, s, src, dst, P, (const int64_t*)nullptr, bs);
       if (e != cudaSuccess) return check_cuda(e, "merge_pass_v2_kernel<fused>");
     }
-    if (sc) sc->have = rec;
+    if (sc) {
+      sc->have = rec;
+      sc->shift = kShift;
+    }
     return check_launch("merge_pass_v2_kernel<fused>");
   }
   {
@@ -249,7 +257,7 @@ static int v2_pass_t(const Key* src, Key* dst, int64_t n, int64_t R, int64_t* mp
     cudaError_t e;
     if (sc && sc->have && rec && tu.samples)
       e = launch_pdl(n, merge_partition_v3_kernel<Key>, (unsigned)((mt + 255) / 256), 256, 0, s,
-                     src, P, mt, mp, bs);
+                     src, P, mt, mp, sc->get<Key>(sc->shift));
     else
       e = launch_pdl(n, merge_partition_v2_kernel<Key>, (unsigned)((mt + 255) / 256), 256, 0, s,
                      src, P, mt, mp);
@@ -262,7 +270,10 @@ static int v2_pass_t(const Key* src, Key* dst, int64_t n, int64_t R, int64_t* mp
                                      s, src, dst, P, (const int64_t*)mp, bs);
     if (e != cudaSuccess) return check_cuda(e, "merge_pass_v2_kernel");
   }
-  if (sc) sc->have = rec;
+  if (sc) {
+    sc->have = rec;
+    sc->shift = kShift;
+  }
   return check_launch("merge_pass_v2_kernel");
 }
 
