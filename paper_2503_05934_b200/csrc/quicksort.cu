@@ -233,10 +233,14 @@ __global__ void __launch_bounds__(kQsNT)
 // its chunk once (bucket ids stay in registers), builds a shared-memory
 // histogram, reserves each non-empty bucket's range with ONE global atomic,
 // then places every key at base + warp-aggregated shared-memory rank.
+#ifndef NSB_QS_SNT
+#define NSB_QS_SNT 512
+#endif
+constexpr int kQsSNT = NSB_QS_SNT;          // scatter threads (1024 measured no faster)
 constexpr int kQsPer = 16;                  // keys per thread in scatter
-constexpr int kQsSChunk = kQsPer * kQsNT;  // keys per CTA in scatter
+constexpr int kQsSChunk = kQsPer * kQsSNT;  // keys per CTA in scatter
 
-__global__ void __launch_bounds__(kQsNT)
+__global__ void __launch_bounds__(kQsSNT)
     scatter_kernel(const int32_t* __restrict__ keys, int64_t n, const int32_t* __restrict__ gspl,
                    const int16_t* __restrict__ glut, int B, uint32_t* __restrict__ fill,
                    int32_t* __restrict__ out) {
@@ -246,7 +250,7 @@ __global__ void __launch_bounds__(kQsNT)
   // (64-bit shared atomics measured as the bottleneck of this kernel)
   uint32_t* pos = reinterpret_cast<uint32_t*>(qsm + kQsClassifierWords);
   const int NB = 2 * B - 1;
-  for (int i = threadIdx.x; i < NB; i += kQsNT) pos[i] = 0;
+  for (int i = threadIdx.x; i < NB; i += kQsSNT) pos[i] = 0;
   __syncthreads();
   const int64_t c0 = (int64_t)blockIdx.x * kQsSChunk;
   const int lane = threadIdx.x & 31;
@@ -254,18 +258,18 @@ __global__ void __launch_bounds__(kQsNT)
   int bk[kQsPer];
 #pragma unroll
   for (int u = 0; u < kQsPer; ++u) {
-    const int64_t i = c0 + u * kQsNT + threadIdx.x;
+    const int64_t i = c0 + u * kQsSNT + threadIdx.x;
     k[u] = i < n ? __ldcs(keys + i) : 0;
   }
 #pragma unroll
   for (int u = 0; u < kQsPer; ++u) {
-    const int64_t i = c0 + u * kQsNT + threadIdx.x;
+    const int64_t i = c0 + u * kQsSNT + threadIdx.x;
     bk[u] = i < n ? cls(k[u]) : -1;
     const WarpRun r = warp_run(bk[u]);
     if (bk[u] >= 0 && r.head) atomicAdd(&pos[bk[u]], (uint32_t)r.len);
   }
   __syncthreads();
-  for (int b = threadIdx.x; b < NB; b += kQsNT) {
+  for (int b = threadIdx.x; b < NB; b += kQsSNT) {
     const uint32_t c = pos[b];
     if (c) pos[b] = atomicAdd(&fill[b], c);  // one global atomic per (CTA, bucket)
   }
@@ -411,7 +415,7 @@ static int quick_sort_level(int32_t* keys, int32_t* tmp, size_t n, int leaf, con
                      "cudaMemcpyAsync(fill)"));
   {
     Prof prof(PK_QS_SCATTER, s);
-    scatter_kernel<<<(unsigned)((n + kQsSChunk - 1) / kQsSChunk), kQsNT, scatter_smem, s>>>(
+    scatter_kernel<<<(unsigned)((n + kQsSChunk - 1) / kQsSChunk), kQsSNT, scatter_smem, s>>>(
         keys, (int64_t)n, aux.splitters, aux.lut, B, reinterpret_cast<uint32_t*>(aux.fill), tmp);
   }
   NSB_TRY(check_launch("scatter_kernel"));
