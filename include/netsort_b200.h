@@ -140,6 +140,10 @@ size_t ns_segmented_sort_temp_bytes(size_t num_segments, size_t seg_len);
 int ns_segmented_sort_i32(int32_t* d_keys, size_t num_segments, size_t seg_len,
                           int algorithm, uint32_t width_mask, int varsort_max, void* d_temp,
                           size_t temp_bytes, void* stream);
+size_t ns_segmented_sort_temp_bytes_i64(size_t num_segments, size_t seg_len);
+int ns_segmented_sort_i64(int64_t* d_keys, size_t num_segments, size_t seg_len,
+                          int algorithm, uint32_t width_mask, int varsort_max, void* d_temp,
+                          size_t temp_bytes, void* stream);
 
 /* ---- sample-sort building blocks (multi-GPU layer, BASELINE config 5) ---
  * The exchange itself is an NCCL all-to-all issued by the host layer; these

@@ -48,6 +48,8 @@ SIGNATURES = {
     "ns_argsort_i32": (_i32, [_vp, _vp, _sz, _vp, _sz, _vp]),
     "ns_segmented_sort_temp_bytes": (_sz, [_sz, _sz]),
     "ns_segmented_sort_i32": (_i32, [_vp, _sz, _sz, _i32, _u32, _i32, _vp, _sz, _vp]),
+    "ns_segmented_sort_temp_bytes_i64": (_sz, [_sz, _sz]),
+    "ns_segmented_sort_i64": (_i32, [_vp, _sz, _sz, _i32, _u32, _i32, _vp, _sz, _vp]),
     "ns_regular_samples_i32": (_i32, [_vp, _sz, _i32, _vp, _vp]),
     "ns_select_splitters_i32": (_i32, [_vp, _i32, _i32, _vp, _vp]),
     "ns_bucket_bounds_i32": (_i32, [_vp, _sz, _vp, _i32, _vp, _vp]),

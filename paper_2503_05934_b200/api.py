@@ -330,15 +330,17 @@ def sort_small_batch(keys, offsets):
 def segmented_sort(keys, seg_len: int, cfg: NetworkConfig,
                    algorithm: Algorithm = Algorithm.quick_sort):
     """Sort keys.numel() // seg_len back-to-back segments independently."""
-    _check_tensor(keys)
+    t = _check_tensor(keys, allow_i64=True)
     if seg_len <= 0 or keys.numel() % seg_len:
         raise ValueError("keys must hold a whole number of segments")
     nseg = keys.numel() // seg_len
     L = lib()
-    tb = L.ns_segmented_sort_temp_bytes(nseg, seg_len)
-    check(L.ns_segmented_sort_i32(keys.data_ptr(), nseg, seg_len, algorithm.value,
-                                  cfg.width_mask, cfg.varsort_max, scratch(tb, keys.device),
-                                  tb, _stream_ptr(keys)), "segmented_sort")
+    sfx = "" if t == "i32" else "_i64"
+    tb = getattr(L, f"ns_segmented_sort_temp_bytes{sfx}")(nseg, seg_len)
+    check(getattr(L, f"ns_segmented_sort_{t}")(keys.data_ptr(), nseg, seg_len, algorithm.value,
+                                               cfg.width_mask, cfg.varsort_max,
+                                               scratch(tb, keys.device), tb, _stream_ptr(keys)),
+          "segmented_sort")
     return keys
 
 

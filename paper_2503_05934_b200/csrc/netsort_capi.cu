@@ -426,21 +426,28 @@ int merge_sort_device(int64_t* d_keys, size_t n, int leaf, void* d_temp, size_t 
   return merge_sort_device_t(d_keys, n, leaf, d_temp, temp_bytes, s);
 }
 
-int tile_sort_segments(int32_t* d_keys, size_t num_segments, size_t seg_len, int leaf,
-                       cudaStream_t s) {
+// One CTA per segment, the tile sized to the segment (a 100-key segment does
+// not pay for an 8192-key tile).
+template <class Key>
+static int tile_sort_segments_t(Key* d_keys, size_t num_segments, size_t seg_len, int leaf,
+                                cudaStream_t s) {
   if (seg_len > (size_t)kSmT) return NS_ERR_INVALID;
   (void)tuning();
   const int64_t n = (int64_t)(num_segments * seg_len);
-  if (seg_len <= (size_t)kBsT) {
-    return with_leaf(leaf, [&](auto L) {
-      return launch_blocksort<kBsNT, kBsK, decltype(L)::value>(d_keys, d_keys, n, (int)seg_len,
-                                                                (int64_t)num_segments, s);
-    });
-  }
+  const int st = (int)seg_len;
+  const int64_t g = (int64_t)num_segments;
   return with_leaf(leaf, [&](auto L) {
-    return launch_blocksort<kSmNT, kSmK, decltype(L)::value>(d_keys, d_keys, n, (int)seg_len,
-                                                              (int64_t)num_segments, s);
+    constexpr int LF = decltype(L)::value;
+    if (seg_len <= 512) return launch_blocksort<32, 16, LF>(d_keys, d_keys, n, st, g, s);
+    if (seg_len <= 2048) return launch_blocksort<128, 16, LF>(d_keys, d_keys, n, st, g, s);
+    if (seg_len <= 4096) return launch_blocksort<256, 16, LF>(d_keys, d_keys, n, st, g, s);
+    if (seg_len <= (size_t)kBsT) return launch_blocksort<kBsNT, kBsK, LF>(d_keys, d_keys, n, st, g, s);
+    return launch_blocksort<kSmNT, kSmK, LF>(d_keys, d_keys, n, st, g, s);
   });
+}
+int tile_sort_segments(int32_t* d_keys, size_t num_segments, size_t seg_len, int leaf,
+                       cudaStream_t s) {
+  return tile_sort_segments_t(d_keys, num_segments, seg_len, leaf, s);
 }
 
 // ---------------------------------------------------------------------------
@@ -804,6 +811,32 @@ int ns_segmented_sort_i32(int32_t* d_keys, size_t num_segments, size_t seg_len, 
     const int st = algorithm == NS_MERGE_SORT
                        ? merge_sort_device(seg, seg_len, leaf, d_temp, temp_bytes, s)
                        : ns_quick_sort_i32(seg, seg_len, width_mask, varsort_max, d_temp,
+                                           temp_bytes, stream);
+    if (st != NS_OK) return st;
+  }
+  return NS_OK;
+}
+
+size_t ns_segmented_sort_temp_bytes_i64(size_t num_segments, size_t seg_len) {
+  (void)num_segments;
+  if (seg_len <= (size_t)kSmT) return 0;
+  return std::max(merge_sort_temp_i64(seg_len), ns_quick_sort_temp_bytes_i64(seg_len));
+}
+
+int ns_segmented_sort_i64(int64_t* d_keys, size_t num_segments, size_t seg_len, int algorithm,
+                          uint32_t width_mask, int varsort_max, void* d_temp,
+                          size_t temp_bytes, void* stream) {
+  if (algorithm != NS_MERGE_SORT && algorithm != NS_QUICK_SORT) return NS_ERR_INVALID;
+  if (num_segments == 0 || seg_len <= 1) return NS_OK;
+  if (!d_keys) return NS_ERR_INVALID;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int leaf = leaf_of(width_mask, varsort_max);
+  if (seg_len <= (size_t)kSmT) return tile_sort_segments_t(d_keys, num_segments, seg_len, leaf, s);
+  for (size_t g = 0; g < num_segments; ++g) {
+    int64_t* seg = d_keys + g * seg_len;
+    const int st = algorithm == NS_MERGE_SORT
+                       ? merge_sort_device(seg, seg_len, leaf, d_temp, temp_bytes, s)
+                       : ns_quick_sort_i64(seg, seg_len, width_mask, varsort_max, d_temp,
                                            temp_bytes, stream);
     if (st != NS_OK) return st;
   }

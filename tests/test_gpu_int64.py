@@ -123,3 +123,15 @@ def test_i64_full_size_properties(ns, cuda, algo, n):
     del t
     ns.release_scratch()
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("seg_len", [2, 7, 100, 513, 4096, 9000, 16384, 20000])
+def test_i64_segmented(ns, cuda, oracle, seg_len):
+    import torch
+    nseg = max(1, (1 << 18) // seg_len)
+    a = oracle.generate_i64("random", nseg * seg_len, 31 + seg_len)
+    for algo in (ns.Algorithm.merge_sort, ns.Algorithm.quick_sort):
+        t = to_dev(a, cuda)
+        ns.segmented_sort(t, seg_len, ns.find_config("3To5"), algo)
+        assert np.array_equal(t.cpu().numpy().reshape(nseg, seg_len),
+                              np.sort(a.reshape(nseg, seg_len), axis=1)), (seg_len, algo)
