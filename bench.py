@@ -445,12 +445,66 @@ def run_ours(args, metric):
         line["nvlink"] = nvlink
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline()
+    if rank == 0 and world == 1 and not args.no_size_sweep:
+        line["size_sweep"] = size_sweep(ns, L, dev, peak)
     if rank == 0 and world == 1 and args.extra:
         line["other_configs"] = other_configs(ns, L, dev)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def size_sweep(ns, L, dev, peak):
+    """The metric across the range BASELINE.json names (n = 10K..1G): merge
+    sort 6To8 of uniform-random keys at each n, device time by CUDA-graph
+    replay (sort + an untimed-by-subtraction input restore), with the byte
+    model's fraction (8n bytes per pass, 1 tile pass + ceil(log2(n/8192))
+    merge passes) of the measured HBM bandwidth.  Below ~2^24 keys the data
+    is L2-resident and the sort is latency-bound: the fraction is reported,
+    not a bandwidth statement.  2^30 is the headline line itself."""
+    import torch
+    from paper_2503_05934_b200._lib import check
+    out = {}
+    s = torch.cuda.current_stream().cuda_stream
+    cfg = ns.find_config("6To8")
+    for n in (10_000, 100_000, 1_000_000, 1 << 22, 1 << 24, 1 << 26, 1 << 28):
+        src = torch.empty(n, dtype=torch.int32, device=dev)
+        check(L.ns_generate_i32(src.data_ptr(), n, 0, SEED, s), "generate")
+        w = src.clone()
+        fn = lambda: ns.optimized_merge_sort(w, cfg)  # noqa: E731
+        restore = lambda: w.copy_(src)  # noqa: E731
+        reps = max(3, min(50, (1 << 26) // n))
+        for _ in range(3):
+            restore()
+            fn()
+        torch.cuda.synchronize()
+        times = []
+        for body in ((restore, fn), (restore,)):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                for f in body:
+                    f()
+            g.replay()
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            for _ in range(reps):
+                g.replay()
+            b.record()
+            torch.cuda.synchronize()
+            times.append(a.elapsed_time(b) / reps)
+        ms = max(times[0] - times[1], 1e-6)
+        restore()
+        fn()
+        passes = 1 + max(0, (n - 1).bit_length() - 13)
+        out[str(n)] = {"ms": ms, "gkeys_per_s": n / (ms * 1e-3) / 1e9,
+                       "frac_all_passes": 8 * n * passes / (ms * 1e-3) / 1e9 / peak,
+                       "sorted": ns.count_inversions(w) == 0}
+        del src, w
+    ns.release_scratch()
+    torch.cuda.empty_cache()
+    return out
 
 
 def other_configs(ns, L, dev):
@@ -614,6 +668,8 @@ def main():
                     help="total keys (--keys under torchrun: its parser claims --n)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--extra", action="store_true", help="also time the other BASELINE configs")
+    ap.add_argument("--no-size-sweep", action="store_true",
+                    help="skip the n = 10K..256M merge-sort sweep (N=1 only)")
     ap.add_argument("--exchange", choices=["p2p", "nccl"], default="p2p",
                     help="N>1: pull-merge over peer memory (default) or NCCL all-to-all")
     args = ap.parse_args()
