@@ -616,9 +616,17 @@ __device__ __forceinline__ void ml_warp_hist(const Key* spl, const Key (&k)[kMlP
   for (int u = 0; u < kMlPer; ++u) {
     const int64_t i = c0 + u * kMlNT + threadIdx.x;
     bk[u] = i < c1 ? ml_classify<LOGB>(spl, k[u]) : -1;
+#ifndef NSB_ML_PEERS
+    // runs of equal ids among consecutive lanes (one ballot); equal ids in
+    // different runs of the warp add with separate (warp-private) atomics
+    const WarpRun r = warp_run(bk[u]);
+    if (bk[u] >= 0 && r.head) atomicAdd(&row[bk[u]], (uint32_t)r.len);
+    (void)lane;
+#else
     const unsigned peers = warp_peers<LOGB + 1>(bk[u]);
     if (bk[u] >= 0 && lane == __ffs(peers) - 1) row[bk[u]] += __popc(peers);
     __syncwarp();
+#endif
   }
 }
 
@@ -715,6 +723,13 @@ __device__ __noinline__ void ml_scatter_body(const Key* __restrict__ X, const Ml
 #pragma unroll
   for (int u = 0; u < kMlPer; ++u) {
     const int b = bk[u];
+#ifndef NSB_ML_PEERS
+    const WarpRun r = warp_run(b);
+    uint32_t base = 0;
+    if (b >= 0 && r.head) base = atomicAdd(&row[b], (uint32_t)r.len);
+    base = __shfl_sync(kFull, base, r.head_lane);
+    if (b >= 0) Ys[base + (lane - r.head_lane)] = k[u];
+#else
     const unsigned peers = warp_peers<LOGB + 1>(b);
     const int leader = __ffs(peers) - 1;
     uint32_t base = 0;
@@ -725,6 +740,7 @@ __device__ __noinline__ void ml_scatter_body(const Key* __restrict__ X, const Ml
     base = __shfl_sync(kFull, base, leader);
     if (b >= 0) Ys[base + __popc(peers & ((1u << lane) - 1))] = k[u];
     __syncwarp();
+#endif
   }
 }
 
