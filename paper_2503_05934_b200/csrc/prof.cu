@@ -55,6 +55,12 @@ int ensure_smem_attr(const void* kern, int bytes, const char* what) {
     if (d.first == dev && d.second == kern) return NS_OK;
   NSB_TRY(check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes),
                      what));
+  // prefer the largest shared-memory carveout: these kernels are sized by
+  // their shared memory, and a small default carveout can cap residency at
+  // one CTA per SM
+  NSB_TRY(check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                          (int)cudaSharedmemCarveoutMaxShared),
+                     what));
   done.emplace_back(dev, kern);
   return NS_OK;
 }

@@ -199,7 +199,10 @@ __device__ __forceinline__ WarpRun warp_run(int b) {
   return WarpRun{hl, next - hl, head};
 }
 
-__global__ void __launch_bounds__(kQsNT)
+// 2 CTAs/SM (<= 64 registers; the classifier + histogram take 57 KiB of
+// shared memory each): measured at 112 registers and ONE CTA/SM the kernel
+// ran at 25 % occupancy and 0.6 TB/s.
+__global__ void __launch_bounds__(kQsNT, 2)
     count_kernel(const int32_t* __restrict__ keys, int64_t n, const int32_t* __restrict__ gspl,
                  const int16_t* __restrict__ glut, int B, uint32_t* __restrict__ totals) {
   extern __shared__ int32_t qsm[];
@@ -210,19 +213,23 @@ __global__ void __launch_bounds__(kQsNT)
   __syncthreads();
   const int64_t c0 = (int64_t)blockIdx.x * kQsChunk;
   const int64_t c1 = min(n, c0 + kQsChunk);
-  constexpr int kU = kQsChunk / kQsNT;  // keys per thread, loaded up front
-  int32_t k[kU];
+  constexpr int kU = kQsChunk / kQsNT;  // keys per thread
+  constexpr int kG = 8;                 // loaded in groups of 8
+#pragma unroll 1
+  for (int g0 = 0; g0 < kU; g0 += kG) {
+    int32_t k[kG];
 #pragma unroll
-  for (int u = 0; u < kU; ++u) {
-    const int64_t i = c0 + u * kQsNT + threadIdx.x;
-    k[u] = i < c1 ? __ldg(keys + i) : 0;
-  }
+    for (int u = 0; u < kG; ++u) {
+      const int64_t i = c0 + (g0 + u) * kQsNT + threadIdx.x;
+      k[u] = i < c1 ? __ldg(keys + i) : 0;
+    }
 #pragma unroll
-  for (int u = 0; u < kU; ++u) {
-    const int64_t i = c0 + u * kQsNT + threadIdx.x;
-    const int b = i < c1 ? cls(k[u]) : -1;
-    const WarpRun r = warp_run(b);
-    if (b >= 0 && r.head) atomicAdd(&hist[b], (uint32_t)r.len);
+    for (int u = 0; u < kG; ++u) {
+      const int64_t i = c0 + (g0 + u) * kQsNT + threadIdx.x;
+      const int b = i < c1 ? cls(k[u]) : -1;
+      const WarpRun r = warp_run(b);
+      if (b >= 0 && r.head) atomicAdd(&hist[b], (uint32_t)r.len);
+    }
   }
   __syncthreads();
   for (int i = threadIdx.x; i < NB; i += kQsNT)
@@ -240,7 +247,7 @@ constexpr int kQsSNT = NSB_QS_SNT;          // scatter threads (1024 measured no
 constexpr int kQsPer = 16;                  // keys per thread in scatter
 constexpr int kQsSChunk = kQsPer * kQsSNT;  // keys per CTA in scatter
 
-__global__ void __launch_bounds__(kQsSNT)
+__global__ void __launch_bounds__(kQsSNT, 2)
     scatter_kernel(const int32_t* __restrict__ keys, int64_t n, const int32_t* __restrict__ gspl,
                    const int16_t* __restrict__ glut, int B, uint32_t* __restrict__ fill,
                    int32_t* __restrict__ out) {
