@@ -614,35 +614,27 @@ __device__ __forceinline__ unsigned warp_peers(int b) {
   return m;
 }
 
+// Per-CTA bucket histogram: runs of equal ids among consecutive lanes are
+// found with one ballot (warp_run) and charged with ONE shared atomic by the
+// run's head lane; equal ids in different runs just add separately.
 template <int LOGB, class Key>
-__device__ __forceinline__ void ml_warp_hist(const Key* spl, const Key (&k)[kMlPer],
-                                             int (&bk)[kMlPer], int64_t c0, int64_t c1,
-                                             uint32_t* row) {
-  const int lane = threadIdx.x & 31;
+__device__ __forceinline__ void ml_hist(const Key* spl, const Key (&k)[kMlPer],
+                                        int (&bk)[kMlPer], int64_t c0, int64_t c1,
+                                        uint32_t* hist) {
 #pragma unroll
   for (int u = 0; u < kMlPer; ++u) {
     const int64_t i = c0 + u * kMlNT + threadIdx.x;
     bk[u] = i < c1 ? ml_classify<LOGB>(spl, k[u]) : -1;
-#ifndef NSB_ML_PEERS
-    // runs of equal ids among consecutive lanes (one ballot); equal ids in
-    // different runs of the warp add with separate (warp-private) atomics
     const WarpRun r = warp_run(bk[u]);
-    if (bk[u] >= 0 && r.head) atomicAdd(&row[bk[u]], (uint32_t)r.len);
-    (void)lane;
-#else
-    const unsigned peers = warp_peers<LOGB + 1>(bk[u]);
-    if (bk[u] >= 0 && lane == __ffs(peers) - 1) row[bk[u]] += __popc(peers);
-    __syncwarp();
-#endif
+    if (bk[u] >= 0 && r.head) atomicAdd(&hist[bk[u]], (uint32_t)r.len);
   }
 }
 
 template <int LOGB, class Key>
 __device__ __noinline__ void ml_count_body(const Key* __restrict__ X, const MlSeg& sg,
-                                              const Key* spl, uint32_t (*wh)[2 * kMlMaxB],
+                                              const Key* spl, uint32_t* hist,
                                               uint32_t* __restrict__ counts) {
   const int NB = 2 * sg.B - 1;
-  const int warp = threadIdx.x >> 5;
   const int64_t c0 = sg.start + (blockIdx.x - sg.chunk0) * (int64_t)kMlChunk;
   const int64_t c1 = min(sg.start + sg.len, c0 + kMlChunk);
   Key k[kMlPer];
@@ -652,12 +644,10 @@ __device__ __noinline__ void ml_count_body(const Key* __restrict__ X, const MlSe
     const int64_t i = c0 + u * kMlNT + threadIdx.x;
     k[u] = i < c1 ? __ldg(X + i) : 0;
   }
-  ml_warp_hist<LOGB>(spl, k, bk, c0, c1, wh[warp]);
+  ml_hist<LOGB>(spl, k, bk, c0, c1, hist);
   __syncthreads();
   for (int b = threadIdx.x; b < NB; b += kMlNT) {
-    uint32_t t = 0;
-#pragma unroll
-    for (int w = 0; w < kMlWarps; ++w) t += wh[w][b];
+    const uint32_t t = hist[b];
     if (t) atomicAdd(&counts[sg.cnt_off + b], t);
   }
 }
@@ -675,28 +665,27 @@ __device__ __noinline__ void ml_count_body(const Key* __restrict__ X, const MlSe
   }
 
 template <class Key>
-__global__ void __launch_bounds__(kMlNT)
+__global__ void __launch_bounds__(kMlNT, 2)
     ml_count_kernel(const Key* __restrict__ X, const MlSeg* __restrict__ segs, int nseg,
                     const Key* __restrict__ gspl, uint32_t* __restrict__ counts) {
   __shared__ Key spl[kMlMaxB];
-  __shared__ uint32_t wh[kMlWarps][2 * kMlMaxB];
+  __shared__ uint32_t hist[2 * kMlMaxB];
   const MlSeg sg = segs[seg_of_chunk(segs, nseg, blockIdx.x)];
   for (int i = threadIdx.x; i < sg.B; i += kMlNT) spl[i] = gspl[sg.spl_off + i];
-  for (int i = threadIdx.x; i < kMlWarps * 2 * kMlMaxB; i += kMlNT) (&wh[0][0])[i] = 0;
+  for (int i = threadIdx.x; i < 2 * sg.B - 1; i += kMlNT) hist[i] = 0;
   __syncthreads();
-#define NSB_COUNT_CALL(L) ml_count_body<L>(X, sg, spl, wh, counts)
+#define NSB_COUNT_CALL(L) ml_count_body<L>(X, sg, spl, hist, counts)
   NSB_LOGB_DISPATCH(sg.B, NSB_COUNT_CALL)
 #undef NSB_COUNT_CALL
 }
 
 template <int LOGB, class Key>
 __device__ __noinline__ void ml_scatter_body(const Key* __restrict__ X, const MlSeg& sg,
-                                                const Key* spl,
-                                                uint32_t (*wh)[2 * kMlMaxB],
+                                                const Key* spl, uint32_t* hist,
                                                 unsigned long long* __restrict__ fill,
                                                 Key* __restrict__ Y) {
   const int NB = 2 * sg.B - 1;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31;
   const int64_t c0 = sg.start + (blockIdx.x - sg.chunk0) * (int64_t)kMlChunk;
   const int64_t c1 = min(sg.start + sg.len, c0 + kMlChunk);
   Key k[kMlPer];
@@ -706,63 +695,40 @@ __device__ __noinline__ void ml_scatter_body(const Key* __restrict__ X, const Ml
     const int64_t i = c0 + u * kMlNT + threadIdx.x;
     k[u] = i < c1 ? __ldcs(X + i) : 0;
   }
-  ml_warp_hist<LOGB>(spl, k, bk, c0, c1, wh[warp]);
+  ml_hist<LOGB>(spl, k, bk, c0, c1, hist);
   __syncthreads();
-  // one global reservation per (CTA, bucket); warps get consecutive sub-ranges
+  // one global reservation per (CTA, bucket); cursors relative to the segment
   for (int b = threadIdx.x; b < NB; b += kMlNT) {
-    uint32_t t = 0;
-#pragma unroll
-    for (int w = 0; w < kMlWarps; ++w) t += wh[w][b];
-    if (t) {
-      uint32_t pos = (uint32_t)(atomicAdd(&fill[sg.cnt_off + b], (unsigned long long)t) -
-                                (unsigned long long)sg.start);
-#pragma unroll
-      for (int w = 0; w < kMlWarps; ++w) {
-        const uint32_t c = wh[w][b];
-        wh[w][b] = pos;
-        pos += c;
-      }
-    }
+    const uint32_t t = hist[b];
+    if (t)
+      hist[b] = (uint32_t)(atomicAdd(&fill[sg.cnt_off + b], (unsigned long long)t) -
+                           (unsigned long long)sg.start);
   }
   __syncthreads();
-  uint32_t* row = wh[warp];
   Key* Ys = Y + sg.start;
 #pragma unroll
   for (int u = 0; u < kMlPer; ++u) {
     const int b = bk[u];
-#ifndef NSB_ML_PEERS
     const WarpRun r = warp_run(b);
     uint32_t base = 0;
-    if (b >= 0 && r.head) base = atomicAdd(&row[b], (uint32_t)r.len);
+    if (b >= 0 && r.head) base = atomicAdd(&hist[b], (uint32_t)r.len);
     base = __shfl_sync(kFull, base, r.head_lane);
     if (b >= 0) Ys[base + (lane - r.head_lane)] = k[u];
-#else
-    const unsigned peers = warp_peers<LOGB + 1>(b);
-    const int leader = __ffs(peers) - 1;
-    uint32_t base = 0;
-    if (b >= 0 && lane == leader) {
-      base = row[b];
-      row[b] = base + __popc(peers);
-    }
-    base = __shfl_sync(kFull, base, leader);
-    if (b >= 0) Ys[base + __popc(peers & ((1u << lane) - 1))] = k[u];
-    __syncwarp();
-#endif
   }
 }
 
 template <class Key>
-__global__ void __launch_bounds__(kMlNT)
+__global__ void __launch_bounds__(kMlNT, 2)
     ml_scatter_kernel(const Key* __restrict__ X, const MlSeg* __restrict__ segs, int nseg,
                       const Key* __restrict__ gspl, unsigned long long* __restrict__ fill,
                       Key* __restrict__ Y) {
   __shared__ Key spl[kMlMaxB];
-  __shared__ uint32_t wh[kMlWarps][2 * kMlMaxB];  // counts, then cursors (rel. to seg start)
+  __shared__ uint32_t hist[2 * kMlMaxB];  // counts, then cursors (relative to the segment)
   const MlSeg sg = segs[seg_of_chunk(segs, nseg, blockIdx.x)];
   for (int i = threadIdx.x; i < sg.B; i += kMlNT) spl[i] = gspl[sg.spl_off + i];
-  for (int i = threadIdx.x; i < kMlWarps * 2 * kMlMaxB; i += kMlNT) (&wh[0][0])[i] = 0;
+  for (int i = threadIdx.x; i < 2 * sg.B - 1; i += kMlNT) hist[i] = 0;
   __syncthreads();
-#define NSB_SCATTER_CALL(L) ml_scatter_body<L>(X, sg, spl, wh, fill, Y)
+#define NSB_SCATTER_CALL(L) ml_scatter_body<L>(X, sg, spl, hist, fill, Y)
   NSB_LOGB_DISPATCH(sg.B, NSB_SCATTER_CALL)
 #undef NSB_SCATTER_CALL
 }
