@@ -276,9 +276,22 @@ __global__ void __launch_bounds__(kQsSNT, 2)
     if (bk[u] >= 0 && r.head) atomicAdd(&pos[bk[u]], (uint32_t)r.len);
   }
   __syncthreads();
-  for (int b = threadIdx.x; b < NB; b += kQsSNT) {
-    const uint32_t c = pos[b];
-    if (c) pos[b] = atomicAdd(&fill[b], c);  // one global atomic per (CTA, bucket)
+  {
+    // one global reservation per (CTA, bucket); a thread's atomics are all
+    // issued before any result is used, so their L2 round trips overlap
+    // (one after another they were the kernel's critical path)
+    constexpr int kR = (2 * kQsMaxB + kQsSNT - 1) / kQsSNT;
+    uint32_t c[kR], r[kR];
+#pragma unroll
+    for (int q = 0; q < kR; ++q) {
+      const int b = threadIdx.x + q * kQsSNT;
+      c[q] = b < NB ? pos[b] : 0u;
+    }
+#pragma unroll
+    for (int q = 0; q < kR; ++q) r[q] = c[q] ? atomicAdd(&fill[threadIdx.x + q * kQsSNT], c[q]) : 0u;
+#pragma unroll
+    for (int q = 0; q < kR; ++q)
+      if (c[q]) pos[threadIdx.x + q * kQsSNT] = r[q];
   }
   __syncthreads();
 #pragma unroll
