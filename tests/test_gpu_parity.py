@@ -618,3 +618,51 @@ def test_two_streams_concurrently(ns, cuda, oracle):
         torch.cuda.synchronize()
         assert np.array_equal(ta.cpu().numpy(), np.sort(a))
         assert np.array_equal(tb_.cpu().numpy(), np.sort(b))
+
+
+_PARTITION_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import paper_2503_05934_b200 as ns
+from oracle import oracle as O
+for n in (16385, 20000, 65537, 100003, 1000001, 3 * 8192 * 37 + 5):
+    for dist in ("random", "sorted", "nearly_sorted"):
+        a = O.generate_i32(dist, n, n)
+        t = torch.from_numpy(a).cuda()
+        ns.optimized_merge_sort(t, ns.find_config("6To8"))
+        assert np.array_equal(t.cpu().numpy(), np.sort(a)), (n, dist)
+        a64 = O.generate_i64(dist, n, n)
+        t = torch.from_numpy(a64).cuda()
+        ns.optimized_merge_sort(t, ns.find_config("6To8"))
+        assert np.array_equal(t.cpu().numpy(), np.sort(a64)), (n, dist, "i64")
+print("ok")
+"""
+
+
+@pytest.mark.parametrize("env", [{"NSB_FUSED_MAX": "0"},
+                                 {"NSB_FUSED_MAX": "0", "NSB_SAMPLES": "0"}])
+def test_partition_kernels_at_small_sizes(env):
+    """The separate partition kernels (block-sample bracketed v3, plain v2)
+    normally run only for passes of > 4096 tiles (~32 M keys); forcing them
+    at odd small sizes checks partial last blocks and pairs against numpy."""
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run(["python", "-c", _PARTITION_SCRIPT, root], capture_output=True, text=True,
+                       timeout=600, env=dict(os.environ, **env), cwd=root)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-3000:]
+
+
+@pytest.mark.slow
+def test_merge_sort_odd_size_above_fused_threshold(ns, cuda):
+    """n = 2^25 + 12345: passes with separate partitions and block samples,
+    ragged last pairs and a partial last sample block."""
+    import torch
+    from paper_2503_05934_b200._lib import check
+    n = (1 << 25) + 12345
+    t = torch.empty(n, dtype=torch.int32, device=cuda)
+    check(ns.lib().ns_generate_i32(t.data_ptr(), n, 0, 5, torch.cuda.current_stream().cuda_stream),
+          "gen")
+    before = ns.multiset_digest(t)
+    ns.optimized_merge_sort(t, ns.find_config("6To8"))
+    assert ns.count_inversions(t) == 0 and ns.multiset_digest(t) == before
