@@ -23,7 +23,6 @@
 
 #include "common.cuh"
 #include "networks.cuh"
-#include "smem_merge.cuh"
 #include "tma.cuh"
 
 namespace nsb {

@@ -13,7 +13,6 @@
 
 #include "common.cuh"
 #include "mergesort.cuh"
-#include "kway.cuh"
 #include "networks.cuh"
 
 namespace nsb {
@@ -47,12 +46,8 @@ constexpr int kV2NT = 256, kV2K = 31, kV2T = kV2NT * kV2K;  // 7936 keys per til
 // int64 keys (NSB_V2_64=0): 3840 keys (30 KiB) per tile; K odd keeps the
 // half-warp 64-bit cursor accesses on distinct banks
 constexpr int kV2K64 = 15;
-//   NSB_KWAY  = 0 | 4 | 8 : widest k-way merge pass (0 = pairwise only, default)
-//   NSB_KWAY_MIN = n below which only pairwise passes are used
 struct MergeTuning {
   int tile = kBsT;
-  int kway = 0;  // measured: k-way passes are merge-compute bound, no faster
-  int64_t kway_min = int64_t(1) << 22;
   int64_t fused_max_tiles = 4096;  // passes with fewer tiles search in-kernel (measured crossover)
   int v2 = -1;  // NSB_V2 forces one tile shape (see v2_pass); -1 = by size
   int samples = 1;  // NSB_SAMPLES=0: plain partition search on every pass
@@ -64,8 +59,6 @@ struct MergeTuning {
       const int t = atoi(e);
       tile = (t == 16384 || t == 4096 || t == 2048 || t == 1024) ? t : 8192;
     }
-    if (const char* e = getenv("NSB_KWAY")) kway = atoi(e);
-    if (const char* e = getenv("NSB_KWAY_MIN")) kway_min = atoll(e);
   }
 };
 static const MergeTuning& tuning() {
@@ -79,17 +72,6 @@ static const MergeTuning& tuning() {
 // Upper bound on merge-path splits of any pass (v2 tiles >= 3968 keys).
 static size_t max_merge_tiles(size_t n) { return n / 1024 + 64; }
 
-// k-way scratch: raw + 2 merged sample buffers (u64), their merge-path splits,
-// and the tile cuts (int32 per run per tile).
-static size_t kway_max_samples(size_t n) { return n / kKwS + 1024; }
-// sample-merge splits: tiles of >= 128 samples (2 * Ls, Ls = R / 128 >= 64)
-static size_t kway_max_cuts(size_t n) { return (n / 4096 + 1024) * 8; }
-static size_t kway_temp(size_t n) {
-  return 3 * align_up(kway_max_samples(n) * 8, 256) +
-         align_up((kway_max_samples(n) / 128 + 64) * 8, 256) +
-         align_up(kway_max_cuts(n) * 4, 256);
-}
-
 // block samples (first/last key of every 256-key block) for the partition
 static size_t samples_bytes(size_t n, size_t kb) {
   return 2 * align_up(((n >> kSmpShiftMin) + 2) * kb, 256);
@@ -98,7 +80,7 @@ static size_t samples_bytes(size_t n, size_t kb) {
 size_t merge_sort_temp(size_t n) {
   if (n <= (size_t)kSmT) return 0;
   return align_up(n * sizeof(int32_t), 256) + align_up((max_merge_tiles(n) + 1) * 8, 256) +
-         kway_temp(n) + samples_bytes(n, 4);
+         samples_bytes(n, 4);
 }
 
 // int64: ping-pong buffer + merge-path splits + block samples (no k-way scratch)
@@ -125,88 +107,6 @@ struct SmpCtx {
     return BlockSamples<Key>{f, l, n, sh};
   }
 };
-
-struct KwScratch {
-  uint64_t *raw, *m1, *m2;
-  int64_t* smp;
-  int32_t* cuts;
-};
-
-static KwScratch carve_kway(char* p, size_t n) {
-  KwScratch k;
-  const size_t sb = align_up(kway_max_samples(n) * 8, 256);
-  k.raw = reinterpret_cast<uint64_t*>(p);
-  k.m1 = reinterpret_cast<uint64_t*>(p + sb);
-  k.m2 = reinterpret_cast<uint64_t*>(p + 2 * sb);
-  k.smp = reinterpret_cast<int64_t*>(p + 3 * sb);
-  k.cuts = reinterpret_cast<int32_t*>(p + 3 * sb +
-                                      align_up((kway_max_samples(n) / 128 + 64) * 8, 256));
-  return k;
-}
-
-template <int K>
-static int launch_kway_merge(const int32_t* src, int32_t* dst, const KwPlan& P,
-                             const int32_t* cuts, cudaStream_t s) {
-  constexpr int smem = 2 * kway_buf_words(K) * 4;
-  auto* kern = kway_merge_kernel<K>;
-  NSB_TRY(ensure_smem_attr(reinterpret_cast<const void*>(kern), smem,
-                           "cudaFuncSetAttribute(kway)"));
-  {
-    Prof prof(PK_MERGE_PASS, s);
-    kern<<<(unsigned)P.tiles, kKwNT, smem, s>>>(src, dst, P, cuts);
-  }
-  return check_launch("kway_merge_kernel");
-}
-
-// One k-way pass: runs of R in src -> runs of k*R in dst.
-static int kway_pass(const int32_t* src, int32_t* dst, int64_t n, int64_t R, int k,
-                     const KwScratch& ks, cudaStream_t s) {
-  KwPlan P;
-  P.n = n;
-  P.R = R;
-  P.k = k;
-  P.Ls = R / kKwS;
-  const int64_t nruns = (n + R - 1) / R;
-  const int64_t last_len = n - (nruns - 1) * R;
-  P.S = (nruns - 1) * P.Ls + (last_len + kKwS - 1) / kKwS;
-  const int m = kway_m(k);
-  P.tiles_full = (int)((k * P.Ls + m - 1) / m);
-  P.groups = (nruns + k - 1) / k;
-  P.tiles = P.groups * P.tiles_full;
-  {
-    Prof prof(PK_PARTITION, s);
-    kway_sample_kernel<<<(unsigned)((P.S + 255) / 256), 256, 0, s>>>(src, P, ks.raw);
-  }
-  NSB_TRY(check_launch("kway_sample_kernel"));
-  // merge the k sample sub-runs of every group: log2(k) pairwise rounds
-  const uint64_t* cur = ks.raw;
-  uint64_t* bufs[2] = {ks.m1, ks.m2};
-  int bi = 0;
-  constexpr int SNT = 256, SK = 8, STM = SNT * SK;
-  for (int64_t r = P.Ls; r < (int64_t)k * P.Ls; r *= 2) {
-    const int tm = (int)std::min<int64_t>(STM, 2 * r);  // divides 2r: no tile straddles pairs
-    const int64_t tiles = (P.S + tm - 1) / tm;
-    {
-      Prof prof(PK_PARTITION, s);
-      simple_partition_kernel<uint64_t><<<(unsigned)((tiles + 255) / 256), 256, 0, s>>>(
-          cur, P.S, r, tm, tiles, ks.smp);
-      simple_merge_pass_kernel<uint64_t, SNT, SK><<<(unsigned)tiles, SNT, 0, s>>>(
-          cur, bufs[bi], P.S, r, tm, ks.smp);
-    }
-    NSB_TRY(check_launch("simple_merge_pass_kernel"));
-    cur = bufs[bi];
-    bi ^= 1;
-  }
-  {
-    Prof prof(PK_PARTITION, s);
-    const int64_t threads = P.tiles * k;
-    kway_boundary_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(src, ks.raw, cur, P,
-                                                                           m, ks.cuts);
-  }
-  NSB_TRY(check_launch("kway_boundary_kernel"));
-  return k == 8 ? launch_kway_merge<8>(src, dst, P, ks.cuts, s)
-                : launch_kway_merge<4>(src, dst, P, ks.cuts, s);
-}
 
 // Tiles of exactly NT*K outputs (a multiple of 4 keys, so every tile starts
 // 16-byte aligned); only the last tile of a run pair is partial.  A full tile
@@ -365,18 +265,9 @@ static int merge_sort_device_t(Key* d_keys, size_t n, int leaf, void* d_temp, si
   const MergeTuning& tu = tuning();
   const int T = k32 ? tu.tile : kBsT;
   const int64_t tiles = (int64_t)((n + T - 1) / T);
-  // pass schedule: k-way passes (k = 8 for 5+ runs, 4 for 3-4) on large
-  // int32 inputs when enabled, pairwise v2 passes otherwise
-  int sched[64];
-  int npass = 0;
-  for (int64_t runs = tiles; runs > 1;) {
-    int k = 2;
-    if (k32 && tu.kway >= 4 && (int64_t)n >= tu.kway_min && runs >= 3)
-      k = (tu.kway >= 8 && runs >= 5) ? 8 : 4;
-    sched[npass++] = k;
-    runs = (runs + k - 1) / k;
-  }
-  const int passes = npass;
+  // pairwise passes until one run remains
+  int passes = 0;
+  for (int64_t runs = tiles; runs > 1; runs = (runs + 1) / 2) ++passes;
   // Pick the tile-sort destination so the last pass lands in d_keys.
   Key* cur = (passes & 1) ? tmp : d_keys;
   Key* other = (cur == d_keys) ? tmp : d_keys;
@@ -390,26 +281,13 @@ static int merge_sort_device_t(Key* d_keys, size_t n, int leaf, void* d_temp, si
   }));
   SmpCtx sc;
   {
-    size_t off = align_up(n * sizeof(Key), 256) + align_up((max_merge_tiles(n) + 1) * 8, 256);
-    if constexpr (k32) off += kway_temp(n);
+    const size_t off =
+        align_up(n * sizeof(Key), 256) + align_up((max_merge_tiles(n) + 1) * 8, 256);
     sc.base = static_cast<char*>(d_temp) + off;
     sc.n = (int64_t)n;
   }
   int64_t R = T;
-  for (int pi = 0; pi < npass; ++pi) {
-    const int k = sched[pi];
-    if constexpr (k32) {
-      if (k > 2) {
-        const KwScratch ks = carve_kway(reinterpret_cast<char*>(mp) +
-                                            align_up((max_merge_tiles(n) + 1) * 8, 256),
-                                        n);
-        NSB_TRY(kway_pass(cur, other, (int64_t)n, R, k, ks, s));
-        sc.have = false;  // the k-way kernel records no block samples
-        std::swap(cur, other);
-        R *= k;
-        continue;
-      }
-    }
+  for (int pi = 0; pi < passes; ++pi) {
     NSB_TRY(v2_pass(cur, other, (int64_t)n, R, mp, s, &sc));
     std::swap(cur, other);
     R *= 2;
@@ -719,12 +597,6 @@ const char* ns_status_string(int status) {
 
 int ns_version(void) { return 100; }
 
-#ifdef NSB_DEBUG_KWAY
-int ns_debug_read(int* out8) {
-  cudaDeviceSynchronize();
-  return cudaMemcpyFromSymbol(out8, g_dbg, 8 * sizeof(int)) == cudaSuccess ? 0 : 2;
-}
-#endif
 
 int ns_leaf_width(uint32_t width_mask, int varsort_max) { return leaf_of(width_mask, varsort_max); }
 

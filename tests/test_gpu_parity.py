@@ -228,46 +228,6 @@ def test_full_size_properties(ns, cuda, oracle, algo):
     torch.cuda.empty_cache()
 
 
-KWAY_SCRIPT = r"""
-import os, sys, hashlib
-import numpy as np, torch
-sys.path.insert(0, os.getcwd())
-import paper_2503_05934_b200 as ns
-from oracle import oracle as O
-bad = []
-for n in (16385, 20000, 65537, 100000, 300001, 1000000):
-    for dist in ("random", "sorted", "nearly_sorted"):
-        a = O.generate_i32(dist, n, 7 + n)
-        t = torch.from_numpy(a).cuda()
-        ns.optimized_merge_sort(t, ns.find_config("6To8"))
-        if not np.array_equal(t.cpu().numpy(), np.sort(a)):
-            bad.append((n, dist))
-rng = np.random.default_rng(3)
-for a in (np.full(200000, 7, np.int32), rng.integers(0, 3, 500000).astype(np.int32),
-          np.full(100000, np.iinfo(np.int32).max, np.int32),
-          np.concatenate([np.full(300000, 5, np.int32), rng.integers(0, 9, 100000).astype(np.int32)])):
-    t = torch.from_numpy(a).cuda()
-    ns.optimized_merge_sort(t, ns.find_config("6To8"))
-    if not np.array_equal(t.cpu().numpy(), np.sort(a)):
-        bad.append(("dup", a[:3].tolist()))
-print("BAD", bad)
-"""
-
-
-@pytest.mark.parametrize("kway", ["4", "8"])
-def test_kway_merge_path(ns, cuda, kway):
-    """The k-way pass (sample-cut tiles) forced on for every n > 16384."""
-    import os
-    import subprocess
-    import sys
-    env = dict(os.environ, NSB_KWAY=kway, NSB_KWAY_MIN="16385")
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    out = subprocess.run([sys.executable, "-c", KWAY_SCRIPT], env=env, cwd=root,
-                         capture_output=True, text=True, timeout=600)
-    assert out.returncode == 0, out.stderr[-2000:]
-    assert "BAD []" in out.stdout, out.stdout[-2000:]
-
-
 def test_merge_pairs_from_separate_buffers(ns, cuda, oracle):
     """ns_merge_pairs_i32 with every run in its own allocation and at odd
     offsets — the same kernel that, in the p2p sample sort, reads the runs
