@@ -351,7 +351,9 @@ __global__ void __launch_bounds__(kBaNT)
   __shared__ uint32_t so[kBaArr + 1];
   __shared__ __align__(16) int32_t sk[kBaArr * 8 + 8];
   __shared__ uint16_t perm[kBaArr];
-  __shared__ int wcnt[9][kBaPer][NW];  // per (length, round, warp) counts -> bases
+  // per (warp, length, round) counts -> bases; warp-major so the scan rows
+  // (one per (length, round), across warps) are read conflict-free
+  __shared__ int wcnt[NW][9][kBaPer];
   __shared__ int s_bad;
   __shared__ uint32_t s_k0, s_k1;
   const int tid = threadIdx.x;
@@ -408,11 +410,13 @@ __global__ void __launch_bounds__(kBaNT)
       else len = (int)(b - a);
     }
     mylen[r] = len;
+    int my_cnt = 0;  // lane l (<= 8) keeps the count of length l
 #pragma unroll
     for (int l = 0; l <= 8; ++l) {
       const unsigned m = __ballot_sync(0xffffffffu, len == l);
-      if (lane == 0) wcnt[l][r][warp] = __popc(m);
+      if (lane == l) my_cnt = __popc(m);
     }
+    if (lane <= 8) wcnt[warp][lane][r] = my_cnt;  // one 9-lane store, not nine
   }
   __syncthreads();
   if (s_bad) {
@@ -423,13 +427,13 @@ __global__ void __launch_bounds__(kBaNT)
   // 9*kBaPer rows of NW counts is scanned by one thread, then one warp scans
   // the row totals
   __shared__ int rowtot[9 * kBaPer];
-  if (tid < 9 * kBaPer) {
-    int* row = &wcnt[0][0][0] + tid * NW;
+  if (tid < 9 * kBaPer) {  // row tid = (length, round), stride 9*kBaPer across warps
+    int* row = &wcnt[0][0][0] + tid;
     int acc = 0;
 #pragma unroll
     for (int w = 0; w < NW; ++w) {
-      const int c = row[w];
-      row[w] = acc;
+      const int c = row[w * 9 * kBaPer];
+      row[w * 9 * kBaPer] = acc;
       acc += c;
     }
     rowtot[tid] = acc;
@@ -453,10 +457,10 @@ __global__ void __launch_bounds__(kBaNT)
   }
   __syncthreads();
   if (tid < 9 * kBaPer) {
-    int* row = &wcnt[0][0][0] + tid * NW;
+    int* row = &wcnt[0][0][0] + tid;
     const int base = rowtot[tid];
 #pragma unroll
-    for (int w = 0; w < NW; ++w) row[w] += base;
+    for (int w = 0; w < NW; ++w) row[w * 9 * kBaPer] += base;
   }
   __syncthreads();
 #pragma unroll
@@ -468,7 +472,7 @@ __global__ void __launch_bounds__(kBaNT)
       const unsigned m = __ballot_sync(0xffffffffu, len == l);
       if (len == l) rank = __popc(m & ((1u << lane) - 1));
     }
-    if (len >= 0) perm[wcnt[len][r][warp] + rank] = (uint16_t)(r * kBaNT + tid);
+    if (len >= 0) perm[wcnt[warp][len][r] + rank] = (uint16_t)(r * kBaNT + tid);
   }
   __syncthreads();
 #pragma unroll
