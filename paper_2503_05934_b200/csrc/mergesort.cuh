@@ -329,15 +329,24 @@ __device__ __forceinline__ void cta_sort_padded(const Key* in, Key* out, int val
 #endif
 template <int NT, int K, class Key>
 __host__ __device__ constexpr bool cta_sort_skewed() {
-  return sizeof(Key) == 4 && NT > 32 && NT <= NSB_SKEW_MAX_NT;
+  return ((sizeof(Key) == 4 && K == 16) || (sizeof(Key) == 8 && K == 8)) && NT > 32 &&
+         NT <= NSB_SKEW_MAX_NT;
 }
+
+template <int NT, int K, int LEAF, class Key>
+__device__ __forceinline__ void cta_sort_skewed_body(const Key* in, Key* out, int valid, Key* sm);
 
 template <int NT, int K, int LEAF, class Key>
 __device__ __forceinline__ void cta_sort(const Key* in, Key* out, int valid, Key* sm) {
   if constexpr (!cta_sort_skewed<NT, K, Key>()) {
     cta_sort_padded<NT, K, LEAF>(in, out, valid, sm);
-    return;
+  } else {
+    cta_sort_skewed_body<NT, K, LEAF>(in, out, valid, sm);
   }
+}
+
+template <int NT, int K, int LEAF, class Key>
+__device__ __forceinline__ void cta_sort_skewed_body(const Key* in, Key* out, int valid, Key* sm) {
   constexpr int T = NT * K;
   const int tid = threadIdx.x;
   const int lane = tid & 31;
@@ -356,7 +365,9 @@ __device__ __forceinline__ void cta_sort(const Key* in, Key* out, int valid, Key
     __syncthreads();
     tile_store<NT, T>(sm, out, valid);
   } else {
-    static_assert(K == 16, "the skewed merge levels assume 16 keys per lane");
+    // a bank row holds 128/KB keys; lanes whose diagonals are K apart hit
+    // two residues per row, and the (l>>1) skew spreads them over all of it
+    static_assert(128 / (int)sizeof(Key) == 2 * K, "skew pattern needs 128/sizeof(Key) == 2K");
     constexpr int W = 32 * K;  // warp run
     constexpr int GAP = 4;     // keeps every run 16-byte aligned
     constexpr int PV = kpv<Key>();
@@ -376,8 +387,9 @@ __device__ __forceinline__ void cta_sort(const Key* in, Key* out, int valid, Key
       if (lane == 0) sm[warp * (W + GAP) + W] = KeyT<Key>::kMax;
     }
     __syncthreads();
-    const int skew = (lane >> 1) & 15;
-    const int cnt = lane == 31 ? 1 : K + (lane & 1);
+    const int skew = (lane >> 1) & (K - 1);
+    const int cnt = lane == 31 ? W - (K * 31 + ((31 >> 1) & (K - 1)))
+                               : K + (((lane + 1) >> 1) & (K - 1)) - skew;
     const char* smc = reinterpret_cast<const char*>(sm);
 #pragma unroll 1
     for (int R = W; R < T; R *= 2) {
@@ -443,11 +455,14 @@ __device__ __forceinline__ void cta_sort(const Key* in, Key* out, int valid, Key
 #ifndef NSB_BS_THREADS_PER_SM
 #define NSB_BS_THREADS_PER_SM 2048
 #endif
+#ifndef NSB_BS_THREADS_PER_SM_64
+#define NSB_BS_THREADS_PER_SM_64 1024  // int64: 64 registers per thread
+#endif
 template <int NT, int K, class Key>
 __host__ __device__ constexpr int bs_min_blocks() {
   // 0 = no minimum (the padded variant keeps the compiler's own choice)
-  return !cta_sort_skewed<NT, K, Key>() || NT >= NSB_BS_THREADS_PER_SM
-             ? 0 : NSB_BS_THREADS_PER_SM / NT;
+  constexpr int tps = sizeof(Key) == 8 ? NSB_BS_THREADS_PER_SM_64 : NSB_BS_THREADS_PER_SM;
+  return !cta_sort_skewed<NT, K, Key>() || NT >= tps ? 0 : tps / NT;
 }
 
 template <int NT, int K, int LEAF, class Key = int32_t>

@@ -51,9 +51,14 @@ struct MergeTuning {
   int64_t fused_max_tiles = 4096;  // passes with fewer tiles search in-kernel (measured crossover)
   int v2 = -1;  // NSB_V2 forces one tile shape (see v2_pass); -1 = by size
   int samples = 1;  // NSB_SAMPLES=0: plain partition search on every pass
+  // NSB_TILE64: int64 tile sort 1 = <1024,8> skewed, 2 = <512,16> padded
+  // (measured at 2^28: 7.5 vs 5.1 ms -- the 256-key warp runs need a fifth
+  // shared-memory level and the CTA fits once per SM)
+  int tile64 = 2;
   MergeTuning() {
     if (const char* e = getenv("NSB_V2")) v2 = atoi(e);
     if (const char* e = getenv("NSB_SAMPLES")) samples = atoi(e);
+    if (const char* e = getenv("NSB_TILE64")) tile64 = atoi(e);
     if (const char* e = getenv("NSB_FUSED_MAX")) fused_max_tiles = atoll(e);
     if (const char* e = getenv("NSB_TILE")) {
       const int t = atoi(e);
@@ -273,6 +278,10 @@ static int merge_sort_device_t(Key* d_keys, size_t n, int leaf, void* d_temp, si
   Key* other = (cur == d_keys) ? tmp : d_keys;
   NSB_TRY(with_leaf(leaf, [&](auto L) {
     constexpr int LF = decltype(L)::value;
+    if constexpr (!k32) {
+      if (tu.tile64 == 1) return launch_blocksort<1024, 8, LF>(d_keys, cur, (int64_t)n, T, tiles, s);
+      if (tu.tile64 == 2) return launch_blocksort<512, 16, LF>(d_keys, cur, (int64_t)n, T, tiles, s);
+    }
     if (T == 4096) return launch_blocksort<256, 16, LF>(d_keys, cur, (int64_t)n, T, tiles, s);
     if (T == 2048) return launch_blocksort<128, 16, LF>(d_keys, cur, (int64_t)n, T, tiles, s);
     if (T == 1024) return launch_blocksort<64, 16, LF>(d_keys, cur, (int64_t)n, T, tiles, s);
