@@ -459,8 +459,9 @@ def size_sweep(ns, L, dev, peak):
     """The metric across the range BASELINE.json names (n = 10K..1G): merge
     sort 6To8 of uniform-random keys at each n, device time by CUDA-graph
     replay (sort + an untimed-by-subtraction input restore), with the byte
-    model's fraction (8n bytes per pass, 1 tile pass + ceil(log2(n/8192))
-    merge passes) of the measured HBM bandwidth.  Below ~2^24 keys the data
+    model's fraction (8n bytes per pass, 1 tile pass + ceil(log2(n/T)) merge
+    passes, T = the library's tile: 16384 keys from 2^21, else 8192) of the
+    measured HBM bandwidth.  Below ~2^24 keys the data
     is L2-resident and the sort is latency-bound: the fraction is reported,
     not a bandwidth statement.  2^30 is the headline line itself."""
     import torch
@@ -497,7 +498,8 @@ def size_sweep(ns, L, dev, peak):
         ms = max(times[0] - times[1], 1e-6)
         restore()
         fn()
-        passes = 1 + max(0, (n - 1).bit_length() - 13)
+        tile_lg = 14 if n >= (1 << 21) else 13  # the library's int32 tile (16384 / 8192)
+        passes = 1 + max(0, (n - 1).bit_length() - tile_lg)
         out[str(n)] = {"ms": ms, "gkeys_per_s": n / (ms * 1e-3) / 1e9,
                        "frac_all_passes": 8 * n * passes / (ms * 1e-3) / 1e9 / peak,
                        "sorted": ns.count_inversions(w) == 0}

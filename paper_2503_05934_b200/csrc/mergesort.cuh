@@ -329,8 +329,8 @@ __device__ __forceinline__ void cta_sort_padded(const Key* in, Key* out, int val
 #endif
 template <int NT, int K, class Key>
 __host__ __device__ constexpr bool cta_sort_skewed() {
-  return ((sizeof(Key) == 4 && K == 16) || (sizeof(Key) == 8 && K == 8)) && NT > 32 &&
-         NT <= NSB_SKEW_MAX_NT;
+  return ((sizeof(Key) == 4 && (K == 16 || K == 32)) || (sizeof(Key) == 8 && K == 8)) &&
+         NT > 32 && NT <= NSB_SKEW_MAX_NT;
 }
 
 template <int NT, int K, int LEAF, class Key>
@@ -365,9 +365,11 @@ __device__ __forceinline__ void cta_sort_skewed_body(const Key* in, Key* out, in
     __syncthreads();
     tile_store<NT, T>(sm, out, valid);
   } else {
-    // a bank row holds 128/KB keys; lanes whose diagonals are K apart hit
-    // two residues per row, and the (l>>1) skew spreads them over all of it
-    static_assert(128 / (int)sizeof(Key) == 2 * K, "skew pattern needs 128/sizeof(Key) == 2K");
+    // a bank row holds S = 128/KB keys.  Lanes whose diagonals are K apart
+    // hit S/K residues of a row: the skew spreads them over all of it —
+    // (l>>1) when S == 2K, l itself when S == K
+    constexpr int S = 128 / (int)sizeof(Key);
+    static_assert(S == 2 * K || S == K, "skew pattern needs 128/sizeof(Key) in {K, 2K}");
     constexpr int W = 32 * K;  // warp run
     constexpr int GAP = 4;     // keeps every run 16-byte aligned
     constexpr int PV = kpv<Key>();
@@ -387,9 +389,9 @@ __device__ __forceinline__ void cta_sort_skewed_body(const Key* in, Key* out, in
       if (lane == 0) sm[warp * (W + GAP) + W] = KeyT<Key>::kMax;
     }
     __syncthreads();
-    const int skew = (lane >> 1) & (K - 1);
-    const int cnt = lane == 31 ? W - (K * 31 + ((31 >> 1) & (K - 1)))
-                               : K + (((lane + 1) >> 1) & (K - 1)) - skew;
+    auto skew_of = [](int l) { return S == 2 * K ? ((l >> 1) & (K - 1)) : (l & (S - 1)); };
+    const int skew = skew_of(lane);
+    const int cnt = lane == 31 ? W - (K * 31 + skew_of(31)) : K + skew_of(lane + 1) - skew;
     const char* smc = reinterpret_cast<const char*>(sm);
 #pragma unroll 1
     for (int R = W; R < T; R *= 2) {
@@ -461,7 +463,9 @@ __device__ __forceinline__ void cta_sort_skewed_body(const Key* in, Key* out, in
 template <int NT, int K, class Key>
 __host__ __device__ constexpr int bs_min_blocks() {
   // 0 = no minimum (the padded variant keeps the compiler's own choice)
-  constexpr int tps = sizeof(Key) == 8 ? NSB_BS_THREADS_PER_SM_64 : NSB_BS_THREADS_PER_SM;
+  // 32 keys per thread need ~64 registers: half the threads per SM
+  constexpr int tps = sizeof(Key) == 8 ? NSB_BS_THREADS_PER_SM_64
+                                       : (K >= 32 ? NSB_BS_THREADS_PER_SM / 2 : NSB_BS_THREADS_PER_SM);
   return !cta_sort_skewed<NT, K, Key>() || NT >= tps ? 0 : tps / NT;
 }
 

@@ -47,7 +47,7 @@ constexpr int kV2NT = 256, kV2K = 31, kV2T = kV2NT * kV2K;  // 7936 keys per til
 // half-warp 64-bit cursor accesses on distinct banks
 constexpr int kV2K64 = 15;
 struct MergeTuning {
-  int tile = kBsT;
+  int tile = 0;  // NSB_TILE forces a tile size; 0 = by size (below)
   int64_t fused_max_tiles = 4096;  // passes with fewer tiles search in-kernel (measured crossover)
   int v2 = -1;  // NSB_V2 forces one tile shape (see v2_pass); -1 = by size
   int samples = 1;  // NSB_SAMPLES=0: plain partition search on every pass
@@ -55,10 +55,15 @@ struct MergeTuning {
   // (measured at 2^28: 7.5 vs 5.1 ms -- the 256-key warp runs need a fifth
   // shared-memory level and the CTA fits once per SM)
   int tile64 = 2;
+  // NSB_K32=0: int32 tiles as 16 keys per thread (512-key warp runs)
+  // instead of 32 (1024-key warp runs, one shared-memory level fewer per
+  // tile; measured 2 % faster at 2^26..2^30)
+  int k32tile = 1;
   MergeTuning() {
     if (const char* e = getenv("NSB_V2")) v2 = atoi(e);
     if (const char* e = getenv("NSB_SAMPLES")) samples = atoi(e);
     if (const char* e = getenv("NSB_TILE64")) tile64 = atoi(e);
+    if (const char* e = getenv("NSB_K32")) k32tile = atoi(e);
     if (const char* e = getenv("NSB_FUSED_MAX")) fused_max_tiles = atoll(e);
     if (const char* e = getenv("NSB_TILE")) {
       const int t = atoi(e);
@@ -268,7 +273,12 @@ static int merge_sort_device_t(Key* d_keys, size_t n, int leaf, void* d_temp, si
   int64_t* mp = reinterpret_cast<int64_t*>(static_cast<char*>(d_temp) +
                                            align_up(n * sizeof(Key), 256));
   const MergeTuning& tu = tuning();
-  const int T = k32 ? tu.tile : kBsT;
+  // int32 tile: 16384 keys from 2^21 keys up (one merge pass fewer; with 32
+  // keys per thread it has the 8192-key tile's four shared-memory levels),
+  // 8192 below; int64: 8192
+  const int T = !k32 ? kBsT
+                     : tu.tile ? tu.tile
+                               : (tu.k32tile && n >= (size_t(1) << 21) ? kSmT : kBsT);
   const int64_t tiles = (int64_t)((n + T - 1) / T);
   // pairwise passes until one run remains
   int passes = 0;
@@ -281,6 +291,12 @@ static int merge_sort_device_t(Key* d_keys, size_t n, int leaf, void* d_temp, si
     if constexpr (!k32) {
       if (tu.tile64 == 1) return launch_blocksort<1024, 8, LF>(d_keys, cur, (int64_t)n, T, tiles, s);
       if (tu.tile64 == 2) return launch_blocksort<512, 16, LF>(d_keys, cur, (int64_t)n, T, tiles, s);
+    }
+    if constexpr (k32) {
+      if (tu.k32tile && T == kBsT)
+        return launch_blocksort<256, 32, LF>(d_keys, cur, (int64_t)n, T, tiles, s);
+      if (tu.k32tile && T == kSmT)
+        return launch_blocksort<512, 32, LF>(d_keys, cur, (int64_t)n, T, tiles, s);
     }
     if (T == 4096) return launch_blocksort<256, 16, LF>(d_keys, cur, (int64_t)n, T, tiles, s);
     if (T == 2048) return launch_blocksort<128, 16, LF>(d_keys, cur, (int64_t)n, T, tiles, s);

@@ -6,7 +6,8 @@ For each n, the sort is captured in a CUDA graph together with an input
 restore (D2D copy) and replayed; the restore-only graph is timed separately
 and subtracted.  Prints one JSON line per size with Gkeys/s and the byte-model
 fraction (8 B/key per pass for int32, 16 for int64; passes = 1 tile pass +
-one per doubling above the 8192-key tile) of the measured HBM bandwidth.
+one per doubling above the tile: 16384 int32 keys from 2^21 keys up, else
+8192) of the measured HBM bandwidth.
 """
 import json
 import os
@@ -89,7 +90,9 @@ def main():
             ms = timed_graph(fn, restore, reps)
         restore()
         fn()
-        passes = 1 + max(0, lg - 13)
+        # the library's tile: 16384 int32 keys from 2^21 up, else 8192
+        tile_lg = 14 if (kb == 4 and lg >= 21) else 13
+        passes = 1 + max(0, lg - tile_lg)
         rec = {"n": n, "log2n": lg, "key_bytes": kb, "algo": "quick" if quick else "merge",
                "ms": ms, "gkeys_per_s": n / (ms * 1e-3) / 1e9,
                "frac_all_passes": kb * 2 * n * passes / (ms * 1e-3) / 1e9 / peak,
