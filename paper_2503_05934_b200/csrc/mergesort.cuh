@@ -333,6 +333,22 @@ __host__ __device__ constexpr bool cta_sort_skewed() {
          NT > 32 && NT <= NSB_SKEW_MAX_NT;
 }
 
+// Sentinel pad after every run of the skewed layout: a lane's producer
+// cursor can run at most K+1 keys past its run's end (all-key-maximum
+// tail, see the merge loop), so K+4 sentinels (16-byte multiple) keep every
+// read inside sentinels without a clamp.
+template <int K>
+__host__ __device__ constexpr int skew_pad() { return K + 4; }
+
+// Dynamic shared memory of a tile-sort CTA (either layout).
+template <int NT, int K, class Key>
+__host__ __device__ constexpr int tile_smem_bytes() {
+  constexpr int T = NT * K;
+  constexpr int pw = padded_words<Key>(T);
+  constexpr int sw = T + (NT > 32 ? NT / 32 : 1) * skew_pad<K>() + 8;
+  return (cta_sort_skewed<NT, K, Key>() && sw > pw ? sw : pw) * (int)sizeof(Key);
+}
+
 template <int NT, int K, int LEAF, class Key>
 __device__ __forceinline__ void cta_sort_skewed_body(const Key* in, Key* out, int valid, Key* sm);
 
@@ -371,7 +387,7 @@ __device__ __forceinline__ void cta_sort_skewed_body(const Key* in, Key* out, in
     constexpr int S = 128 / (int)sizeof(Key);
     static_assert(S == 2 * K || S == K, "skew pattern needs 128/sizeof(Key) in {K, 2K}");
     constexpr int W = 32 * K;  // warp run
-    constexpr int GAP = 4;     // keeps every run 16-byte aligned
+    constexpr int GAP = skew_pad<K>();  // sentinels; keeps every run 16-byte aligned
     constexpr int PV = kpv<Key>();
     constexpr int KB = (int)sizeof(Key);
     constexpr int KM = K + 1;
@@ -386,7 +402,7 @@ __device__ __forceinline__ void cta_sort_skewed_body(const Key* in, Key* out, in
         for (int u = 0; u < PV; ++u) e[u] = v[q * PV + u];
         *reinterpret_cast<int4*>(dst + q * PV) = pack16<Key>(e);
       }
-      if (lane == 0) sm[warp * (W + GAP) + W] = KeyT<Key>::kMax;
+      for (int i = lane; i < GAP; i += 32) sm[warp * (W + GAP) + W + i] = KeyT<Key>::kMax;
     }
     __syncthreads();
     auto skew_of = [](int l) { return S == 2 * K ? ((l >> 1) & (K - 1)) : (l & (S - 1)); };
@@ -401,39 +417,35 @@ __device__ __forceinline__ void cta_sort_skewed_body(const Key* in, Key* out, in
       const int d = W * wi + K * lane + skew;
       const int a_pos = 2 * p * S, b_pos = a_pos + S;
       const int a = merge_path<int>(sm + a_pos, R, sm + b_pos, R, d);
-      uint32_t oa = (uint32_t)(a_pos + a) * KB, ob = (uint32_t)(b_pos + d - a) * KB;
-      const uint32_t ea = (uint32_t)(a_pos + R) * KB, eb = (uint32_t)(b_pos + R) * KB;
-      Key ka = *reinterpret_cast<const Key*>(smc + oa), kb = *reinterpret_cast<const Key*>(smc + ob);
+      // Producer/loser form of the merge: m is the head of the run that did
+      // not emit the last key, ptr the next key of the run that did, mnext
+      // the key after m.  Per output: one LDS, a compare, min/max and two
+      // cursor selects — no per-side bookkeeping and no clamp (an exhausted
+      // run is followed by GAP sentinels; a cursor only passes its first
+      // sentinel once m is the key maximum too, i.e. every key left is the
+      // maximum).  Ties may come from either run: for keys alone any greedy
+      // merge from a merge-path split emits the same values.
+      uint32_t ptr = (uint32_t)(a_pos + a) * KB;
+      uint32_t mnext = (uint32_t)(b_pos + d - a + 1) * KB;
+      Key m = sm[b_pos + d - a];
       Key w[KM];
 #pragma unroll
       for (int k = 0; k < KM; ++k) {
-        const bool take_a = ka <= kb;  // A wins ties (merge_runs, hybrid.hpp:71-75)
-        w[k] = take_a ? ka : kb;
-#ifndef NSB_TS_SPLIT_LDS
-        // one 32-lane shared load per step (address selected per lane): this
-        // kernel is LSU-bound, and one random 32-lane access costs fewer
-        // wavefronts than two predicated 16-lane ones
-        if (take_a) oa = min(oa + (uint32_t)KB, ea);
-        else ob = min(ob + (uint32_t)KB, eb);
-        const Key x = *reinterpret_cast<const Key*>(smc + (take_a ? oa : ob));
-        if (take_a) ka = x;
-        else kb = x;
-#else
-        if (take_a) {
-          oa = min(oa + (uint32_t)KB, ea);
-          ka = *reinterpret_cast<const Key*>(smc + oa);
-        } else {
-          ob = min(ob + (uint32_t)KB, eb);
-          kb = *reinterpret_cast<const Key*>(smc + ob);
-        }
-#endif
+        const Key x = *reinterpret_cast<const Key*>(smc + ptr);
+        const bool t = x <= m;
+        w[k] = t ? x : m;
+        const uint32_t q = ptr + (uint32_t)KB;
+        ptr = t ? q : mnext;
+        mnext = t ? mnext : q;
+        m = t ? m : x;
       }
       __syncthreads();  // every thread is done reading this level's input
       Key* o = sm + p * S2 + d;
 #pragma unroll
       for (int k = 0; k < KM; ++k)
         if (k < cnt) o[k] = w[k];
-      if (wi == 0 && lane == 0) sm[p * S2 + 2 * R] = KeyT<Key>::kMax;
+      if (wi == 0)
+        for (int i = lane; i < GAP; i += 32) sm[p * S2 + 2 * R + i] = KeyT<Key>::kMax;
       __syncthreads();
     }
     // the sorted tile is sm[0, T)

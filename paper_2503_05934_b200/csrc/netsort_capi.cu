@@ -28,7 +28,7 @@ static_assert(kSmT == kSmallTile, "small-tile size mismatch");
 template <int NT, int K, int LEAF, class Key>
 static int launch_blocksort(const Key* src, Key* dst, int64_t n, int stride, int64_t ctas,
                             cudaStream_t s) {
-  constexpr int smem = padded_bytes<Key>(NT * K);
+  constexpr int smem = tile_smem_bytes<NT, K, Key>();
   auto* kern = blocksort_kernel<NT, K, LEAF, Key>;
   NSB_TRY(ensure_smem_attr(reinterpret_cast<const void*>(kern), smem,
                            "cudaFuncSetAttribute(blocksort)"));

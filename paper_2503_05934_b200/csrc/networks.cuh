@@ -105,11 +105,41 @@ NSB_HD void windows(T (&v)[K]) {
   }
 }
 
+// Batcher's odd-even merge of the two sorted halves of v[LO..HI] (HI
+// inclusive; R is the recursion's comparator distance, 1 at the top): 9, 25
+// and 65 comparators for 2 x 4, 2 x 8 and 2 x 16 keys, against 12, 32 and 80
+// for a bitonic flip + half-cleaner merge.
+template <int LO, int HI, int R, class T, int K>
+NSB_HD void oe_merge(T (&v)[K]) {
+  constexpr int STEP = 2 * R;
+  if constexpr (STEP < HI - LO) {
+    oe_merge<LO, HI, STEP>(v);
+    oe_merge<LO + R, HI, STEP>(v);
+#pragma unroll
+    for (int i = LO + R; i < HI - R; i += STEP) cx(v[i], v[i + R]);
+  } else {
+    cx(v[LO], v[LO + R]);
+  }
+}
+
+// Merges sorted runs of H keys pairwise up to one sorted run of K.
+template <int H, class T, int K, int... B>
+NSB_HD void merge_level(T (&v)[K], std::integer_sequence<int, B...>) {
+  (oe_merge<B * 2 * H, B * 2 * H + 2 * H - 1, 1>(v), ...);
+}
+template <int H, int K, class T>
+NSB_HD void thread_merges(T (&v)[K]) {
+  if constexpr (H < K) {
+    merge_level<H>(v, std::make_integer_sequence<int, K / (2 * H)>{});
+    thread_merges<2 * H, K>(v);
+  }
+}
+
 // Per-thread sort of K (power of two, >= 8) register-resident keys: each
 // 8-key window is sorted by the config-shaped base case, then the windows are
 // merged in registers.
 template <int LEAF, int K, class T>
-__device__ __forceinline__ void thread_sort(T (&v)[K]) {
+NSB_HD void thread_sort(T (&v)[K]) {
   static_assert(K >= 8 && (K & (K - 1)) == 0, "K must be a power of two >= 8");
   if constexpr (LEAF == 8 || LEAF == 4) windows<LEAF, 0>(v);
   if constexpr (LEAF == 2) {
@@ -117,21 +147,7 @@ __device__ __forceinline__ void thread_sort(T (&v)[K]) {
     for (int i = 0; i < K; i += 2) cx(v[i], v[i + 1]);
   }
   // merges from LEAF up to K (LEAF==1 starts from single elements)
-#pragma unroll
-  for (int h = (LEAF < 1 ? 1 : LEAF); h < K; h *= 2) {
-#pragma unroll
-    for (int base = 0; base < K; base += 2 * h) {
-      // flip + half-cleaners on v[base .. base+2h)
-#pragma unroll
-      for (int i = 0; i < h; ++i) cx(v[base + i], v[base + 2 * h - 1 - i]);
-#pragma unroll
-      for (int s = h / 2; s >= 1; s >>= 1) {
-#pragma unroll
-        for (int i = 0; i < 2 * h; ++i)
-          if ((i & s) == 0) cx(v[base + i], v[base + i + s]);
-      }
-    }
-  }
+  thread_merges<(LEAF < 1 ? 1 : LEAF), K>(v);
   static_assert(K <= 32, "thread_sort supports up to 32 keys per thread");
 }
 

@@ -321,7 +321,7 @@ template <int NT, int K, int LEAF, class Key>
 static int launch_bucket_sort(const Key* src, Key* dst, const int64_t* jobs, int njobs,
                               cudaStream_t s) {
   if (njobs == 0) return NS_OK;
-  constexpr int smem = padded_bytes<Key>(NT * K);
+  constexpr int smem = tile_smem_bytes<NT, K, Key>();
   auto* kern = bucket_sort_kernel<NT, K, LEAF, Key>;
   NSB_TRY(ensure_smem_attr(reinterpret_cast<const void*>(kern), smem,
                            "cudaFuncSetAttribute(bucket_sort)"));

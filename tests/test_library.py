@@ -93,6 +93,20 @@ def test_network_tables_zero_one(ns):
             ns.network(bad)
 
 
+def test_thread_sort_networks_host_compiled(tmp_path):
+    """The per-thread base case of the tile sort (networks.cuh: LEAF-wide
+    networks, then Batcher odd-even merges up to K) compiled for the host and
+    checked by the zero-one principle (tests/cpp/thread_sort_check.cpp)."""
+    exe = tmp_path / "thread_sort_check"
+    subprocess.run(["g++", "-std=c++20", "-O2", "-D__host__=", "-D__device__=",
+                    "-D__forceinline__=inline", "-Wno-unknown-pragmas",
+                    "-I" + os.path.join(ROOT, "paper_2503_05934_b200", "csrc"),
+                    os.path.join(ROOT, "tests", "cpp", "thread_sort_check.cpp"), "-o", str(exe)],
+                   check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert out.returncode == 0 and "thread_sort ok" in out.stdout, out.stdout + out.stderr
+
+
 def test_leaf_width_follows_reference_recursion_on_8(ns, oracle):
     """The per-thread base case equals the reference recursion's leaves on an
     8-key window: largest of 8/4/2 the config sends to a network, else 1."""
