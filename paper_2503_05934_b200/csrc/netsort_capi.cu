@@ -41,7 +41,7 @@ static int launch_blocksort(const Key* src, Key* dst, int64_t n, int stride, int
 }
 
 // Tuning knobs (read once; the defaults are the measured best on B200).
-//   NSB_TILE  = 8192 | 16384 : keys per tile-sort CTA
+//   NSB_TILE  = 8192 | 16384 | 32768 : keys per tile-sort CTA
 constexpr int kV2NT = 256, kV2K = 31, kV2T = kV2NT * kV2K;  // 7936 keys per tile
 // int64 keys (NSB_V2_64=0): 3840 keys (30 KiB) per tile; K odd keeps the
 // half-warp 64-bit cursor accesses on distinct banks
@@ -67,7 +67,7 @@ struct MergeTuning {
     if (const char* e = getenv("NSB_FUSED_MAX")) fused_max_tiles = atoll(e);
     if (const char* e = getenv("NSB_TILE")) {
       const int t = atoi(e);
-      tile = (t == 16384 || t == 4096 || t == 2048 || t == 1024) ? t : 8192;
+      tile = (t == 32768 || t == 16384 || t == 4096 || t == 2048 || t == 1024) ? t : 8192;
     }
   }
 };
@@ -297,6 +297,8 @@ static int merge_sort_device_t(Key* d_keys, size_t n, int leaf, void* d_temp, si
         return launch_blocksort<256, 32, LF>(d_keys, cur, (int64_t)n, T, tiles, s);
       if (tu.k32tile && T == kSmT)
         return launch_blocksort<512, 32, LF>(d_keys, cur, (int64_t)n, T, tiles, s);
+      if (T == 2 * kSmT)
+        return launch_blocksort<1024, 32, LF>(d_keys, cur, (int64_t)n, T, tiles, s);
     }
     if (T == 4096) return launch_blocksort<256, 16, LF>(d_keys, cur, (int64_t)n, T, tiles, s);
     if (T == 2048) return launch_blocksort<128, 16, LF>(d_keys, cur, (int64_t)n, T, tiles, s);
