@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <string>
 
 #include "../../include/netsort_b200.h"
@@ -61,6 +62,17 @@ inline int check_cuda(cudaError_t e, const char* where) {
   } while (0)
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// int32 segment / bucket tiles of 4097..16384 keys as 32 keys per thread
+// (<128,32>, <256,32>, <512,32>: 1024-key warp runs, one shared-memory merge
+// level fewer than 16 keys per thread).  NSB_SEG_K32=0 restores <.., 16>.
+inline bool seg_k32_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("NSB_SEG_K32");
+    return e ? atoi(e) != 0 : true;
+  }();
+  return on;
+}
 
 // Programmatic dependent launch (sm_90+): kernels of one sort are launched
 // with programmatic stream serialization, so the next kernel's CTAs can be

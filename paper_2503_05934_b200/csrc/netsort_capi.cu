@@ -345,6 +345,11 @@ static int tile_sort_segments_t(Key* d_keys, size_t num_segments, size_t seg_len
     constexpr int LF = decltype(L)::value;
     if (seg_len <= 512) return launch_blocksort<32, 16, LF>(d_keys, d_keys, n, st, g, s);
     if (seg_len <= 2048) return launch_blocksort<128, 16, LF>(d_keys, d_keys, n, st, g, s);
+    if (std::is_same_v<Key, int32_t> && seg_k32_enabled()) {
+      if (seg_len <= 4096) return launch_blocksort<128, 32, LF>(d_keys, d_keys, n, st, g, s);
+      if (seg_len <= (size_t)kBsT) return launch_blocksort<256, 32, LF>(d_keys, d_keys, n, st, g, s);
+      return launch_blocksort<512, 32, LF>(d_keys, d_keys, n, st, g, s);
+    }
     if (seg_len <= 4096) return launch_blocksort<256, 16, LF>(d_keys, d_keys, n, st, g, s);
     if (seg_len <= (size_t)kBsT) return launch_blocksort<kBsNT, kBsK, LF>(d_keys, d_keys, n, st, g, s);
     return launch_blocksort<kSmNT, kSmK, LF>(d_keys, d_keys, n, st, g, s);

@@ -26,6 +26,7 @@
 #include <utility>
 #include <climits>
 #include <cstdint>
+#include <type_traits>
 #include <vector>
 
 #include "common.cuh"
@@ -332,6 +333,22 @@ static int launch_bucket_sort(const Key* src, Key* dst, const int64_t* jobs, int
   return check_launch("bucket_sort_kernel");
 }
 
+// Job classes 1..3 (buckets of <= 4096, 8192, 16384 keys; class 0 is launched
+// by the caller with <128,16>): int32 tiles as 32 keys per thread when
+// seg_k32_enabled(), else 16.
+template <int LF, class Key>
+static int bucket_sort_classes(const Key* src, Key* dst, const int64_t* jobs, const int* off,
+                               cudaStream_t s) {
+  if (std::is_same_v<Key, int32_t> && seg_k32_enabled()) {
+    NSB_TRY((launch_bucket_sort<128, 32, LF>(src, dst, jobs + 2 * off[1], off[2] - off[1], s)));
+    NSB_TRY((launch_bucket_sort<256, 32, LF>(src, dst, jobs + 2 * off[2], off[3] - off[2], s)));
+    return launch_bucket_sort<512, 32, LF>(src, dst, jobs + 2 * off[3], off[4] - off[3], s);
+  }
+  NSB_TRY((launch_bucket_sort<256, 16, LF>(src, dst, jobs + 2 * off[1], off[2] - off[1], s)));
+  NSB_TRY((launch_bucket_sort<512, 16, LF>(src, dst, jobs + 2 * off[2], off[3] - off[2], s)));
+  return launch_bucket_sort<1024, 16, LF>(src, dst, jobs + 2 * off[3], off[4] - off[3], s);
+}
+
 template <class Key>
 static int small_sort(Key* d_keys, size_t n, int leaf, cudaStream_t s) {
   // n <= kSmallTile: one CTA, in place (merge_sort_device's single-CTA path)
@@ -470,9 +487,7 @@ static int quick_sort_level(int32_t* keys, int32_t* tmp, size_t n, int leaf, con
   NSB_TRY(with_leaf(leaf, [&](auto L) {
     constexpr int LF = decltype(L)::value;
     NSB_TRY((launch_bucket_sort<128, 16, LF>(tmp, keys, aux.jobs + 2 * off[0], off[1] - off[0], s)));
-    NSB_TRY((launch_bucket_sort<256, 16, LF>(tmp, keys, aux.jobs + 2 * off[1], off[2] - off[1], s)));
-    NSB_TRY((launch_bucket_sort<512, 16, LF>(tmp, keys, aux.jobs + 2 * off[2], off[3] - off[2], s)));
-    return launch_bucket_sort<1024, 16, LF>(tmp, keys, aux.jobs + 2 * off[3], off[4] - off[3], s);
+    return bucket_sort_classes<LF>(tmp, keys, aux.jobs, off, s);
   }));
   // Oversized buckets: equal buckets are already sorted (constant); between
   // buckets recurse, using their own slice of tmp as scratch.
@@ -884,9 +899,7 @@ static int ml_quick_sort(Key* keys, Key* tmp, size_t n, int leaf, const MlAux<Ke
     NSB_TRY(with_leaf(leaf, [&](auto L) {
       constexpr int LF = decltype(L)::value;
       NSB_TRY((launch_bucket_sort<128, 16, LF>(Y, keys, ax.jobs + 2 * off[0], off[1] - off[0], s)));
-      NSB_TRY((launch_bucket_sort<256, 16, LF>(Y, keys, ax.jobs + 2 * off[1], off[2] - off[1], s)));
-      NSB_TRY((launch_bucket_sort<512, 16, LF>(Y, keys, ax.jobs + 2 * off[2], off[3] - off[2], s)));
-      return launch_bucket_sort<1024, 16, LF>(Y, keys, ax.jobs + 2 * off[3], off[4] - off[3], s);
+      return bucket_sort_classes<LF>(Y, keys, ax.jobs, off, s);
     }));
     if (off[5] > off[4]) {
       copy_jobs_kernel<Key><<<off[5] - off[4], 256, 0, s>>>(Y, keys, ax.jobs + 2 * off[4]);
