@@ -376,6 +376,31 @@ constexpr int kBaNT = 256, kBaPer = 4, kBaArr = kBaNT * kBaPer;
 // that order and a warp runs one network width almost always.  Keys are
 // staged in shared memory at the same 16-byte phase as in HBM so the
 // 128-bit loads and stores of the aligned body are bank-conflict free.
+// Lanes of the warp whose len equals this lane's (len in -1..8; -1 = no
+// array): one ballot per bit of the 4-bit length.
+__device__ __forceinline__ unsigned match_len4(int len) {
+  const unsigned u = (unsigned)len & 15u;
+  unsigned eq = 0xffffffffu;
+#pragma unroll
+  for (int b = 0; b < 4; ++b) {
+    const unsigned m = __ballot_sync(0xffffffffu, (u >> b) & 1u);
+    eq &= ((u >> b) & 1u) ? m : ~m;
+  }
+  return eq;
+}
+
+// The width-L network (sort_exact<L>, networks.hpp:122-128) on L keys of
+// shared memory: L loads, the network in registers, L stores.
+template <int L>
+__device__ __forceinline__ void sort_in_place(int32_t* p) {
+  int32_t v[L];
+#pragma unroll
+  for (int k = 0; k < L; ++k) v[k] = p[k];
+  sort_net<L>(v);
+#pragma unroll
+  for (int k = 0; k < L; ++k) p[k] = v[k];
+}
+
 __global__ void __launch_bounds__(kBaNT)
     sort_small_batch_kernel(int32_t* __restrict__ keys, const uint32_t* __restrict__ offsets,
                             int64_t num_arrays, int* __restrict__ bad) {
@@ -432,6 +457,7 @@ __global__ void __launch_bounds__(kBaNT)
   // validate (lengths outside [0, 8] -> error, nothing is touched) and count
   // lengths per (round, warp) with ballots
   int mylen[kBaPer];
+  unsigned myeq[kBaPer];
 #pragma unroll
   for (int r = 0; r < kBaPer; ++r) {
     const int j = r * kBaNT + tid;
@@ -442,13 +468,13 @@ __global__ void __launch_bounds__(kBaNT)
       else len = (int)(b - a);
     }
     mylen[r] = len;
-    int my_cnt = 0;  // lane l (<= 8) keeps the count of length l
-#pragma unroll
-    for (int l = 0; l <= 8; ++l) {
-      const unsigned m = __ballot_sync(0xffffffffu, len == l);
-      if (lane == l) my_cnt = __popc(m);
-    }
-    if (lane <= 8) wcnt[warp][lane][r] = my_cnt;  // one 9-lane store, not nine
+    // lanes with this lane's length (4 ballots on the length bits instead of
+    // one per length); the group's lowest lane records the group's size
+    const unsigned eq = match_len4(len);
+    myeq[r] = eq;
+    if (lane <= 8) wcnt[warp][lane][r] = 0;
+    __syncwarp();
+    if (len >= 0 && (eq & ((1u << lane) - 1u)) == 0) wcnt[warp][len][r] = __popc(eq);
   }
   __syncthreads();
   if (s_bad) {
@@ -498,12 +524,7 @@ __global__ void __launch_bounds__(kBaNT)
 #pragma unroll
   for (int r = 0; r < kBaPer; ++r) {
     const int len = mylen[r];
-    int rank = 0;
-#pragma unroll
-    for (int l = 0; l <= 8; ++l) {
-      const unsigned m = __ballot_sync(0xffffffffu, len == l);
-      if (len == l) rank = __popc(m & ((1u << lane) - 1));
-    }
+    const int rank = __popc(myeq[r] & ((1u << lane) - 1u));
     if (len >= 0) perm[wcnt[warp][len][r] + rank] = (uint16_t)(r * kBaNT + tid);
   }
   __syncthreads();
@@ -514,13 +535,16 @@ __global__ void __launch_bounds__(kBaNT)
       const int j = perm[slot];
       const int off = (int)(so[j] - k0) + phase;
       const int len = (int)(so[j + 1] - so[j]);
-      int32_t v[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) v[k] = k < len ? sk[off + k] : 0;
-      sort_small_switch(v, len);
-#pragma unroll
-      for (int k = 0; k < 8; ++k)
-        if (k < len) sk[off + k] = v[k];
+      switch (len) {  // warp-uniform almost always (arrays are grouped by length)
+        case 2: sort_in_place<2>(sk + off); break;
+        case 3: sort_in_place<3>(sk + off); break;
+        case 4: sort_in_place<4>(sk + off); break;
+        case 5: sort_in_place<5>(sk + off); break;
+        case 6: sort_in_place<6>(sk + off); break;
+        case 7: sort_in_place<7>(sk + off); break;
+        case 8: sort_in_place<8>(sk + off); break;
+        default: break;
+      }
     }
   }
   __syncthreads();
