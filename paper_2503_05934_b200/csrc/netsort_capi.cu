@@ -412,7 +412,8 @@ __global__ void __launch_bounds__(kBaNT)
   // (one per (length, round), across warps) are read conflict-free
   __shared__ int wcnt[NW][9][kBaPer];
   __shared__ int s_bad;
-  __shared__ uint32_t s_k0, s_k1;
+  __shared__ uint32_t s_k0, s_k1, s_kt;
+  __shared__ __align__(8) uint64_t bar;
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   const int64_t first = (int64_t)blockIdx.x * kBaArr;
@@ -421,38 +422,37 @@ __global__ void __launch_bounds__(kBaNT)
     s_bad = 0;
     s_k0 = __ldg(offsets + first);
     s_k1 = __ldg(offsets + first + cnt);
+    s_kt = __ldg(offsets + num_arrays);  // end of the key array
     if (s_k1 < s_k0 || s_k1 - s_k0 > 8u * (uint32_t)cnt) s_bad = 1;
+    mbar_init(&bar, 1);
+    fence_mbar_init();
   }
   __syncthreads();
   const uint32_t k0 = s_k0;
   const int nk = s_bad ? 0 : (int)(s_k1 - k0);
-  // issue the key loads (128-bit on the aligned body) together with the
-  // offset loads: one DRAM round trip per CTA
+  // The keys are staged by one bulk copy (TMA) of their 16-byte-aligned
+  // cover, placed in shared memory at the same 16-byte phase as in HBM; the
+  // neighbours' keys it drags in are never written back.  A cover that would
+  // leave the key array falls back to per-thread loads.
   const int32_t* kp = keys + k0;
   const int phase = (int)((reinterpret_cast<uintptr_t>(kp) & 15) >> 2);  // key i -> sk[i + phase]
   const int head = min(nk, (4 - phase) & 3);
   const int body = (nk - head) >> 2;
   const int tail = nk - head - 4 * body;
-  const int4* kb4 = reinterpret_cast<const int4*>(kp + head);
-  constexpr int CH = kBaArr * 8 / 4 / kBaNT;
-  int4 x[CH];
-#pragma unroll
-  for (int u = 0; u < CH; ++u) {
-    const int j = u * kBaNT + tid;
-    if (j < body) x[u] = __ldcs(kb4 + j);
+  const int32_t* cov = kp - phase;
+  const int cov_words = (phase + nk + 3) & ~3;
+  const bool use_tma = nk > 0 && cov >= keys && cov + cov_words <= keys + s_kt;
+  if (use_tma) {
+    if (tid == 0) {
+      mbar_arrive_expect_tx(&bar, (uint32_t)cov_words * 4u);
+      tma_load_1d(sk, cov, (uint32_t)cov_words * 4u, &bar);
+    }
+  } else {
+    for (int i = tid; i < nk; i += kBaNT) sk[phase + i] = __ldcs(kp + i);
   }
-  int32_t hx = 0, tx = 0;
-  if (tid < head) hx = __ldcs(kp + tid);
-  if (tid < tail) tx = __ldcs(kp + head + 4 * body + tid);
   for (int i = tid; i <= cnt; i += kBaNT) so[i] = __ldg(offsets + first + i);
   int4* sk4 = reinterpret_cast<int4*>(sk + phase + head);  // 16-byte aligned
-#pragma unroll
-  for (int u = 0; u < CH; ++u) {
-    const int j = u * kBaNT + tid;
-    if (j < body) sk4[j] = x[u];
-  }
-  if (tid < head) sk[phase + tid] = hx;
-  if (tid < tail) sk[phase + head + 4 * body + tid] = tx;
+  if (use_tma) mbar_wait(&bar, 0);
   __syncthreads();
   // validate (lengths outside [0, 8] -> error, nothing is touched) and count
   // lengths per (round, warp) with ballots
@@ -549,11 +549,14 @@ __global__ void __launch_bounds__(kBaNT)
   }
   __syncthreads();
   int32_t* kw = keys + k0;
-  int4* kw4 = reinterpret_cast<int4*>(kw + head);
-#pragma unroll
-  for (int u = 0; u < CH; ++u) {
-    const int j = u * kBaNT + tid;
-    if (j < body) __stcs(kw4 + j, sk4[j]);
+  if (body > 0) {  // aligned interior: one bulk store; head/tail keys one by one
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+      tma_store_1d(kw + head, sk4, (uint32_t)body * 16u);
+      bulk_commit();
+      bulk_wait_read_all();
+    }
   }
   if (tid < head) kw[tid] = sk[phase + tid];
   if (tid < tail) kw[head + 4 * body + tid] = sk[phase + head + 4 * body + tid];
