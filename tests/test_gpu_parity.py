@@ -127,6 +127,31 @@ def test_sort_small_batch_edge_cases(ns, cuda):
     assert from_dev(k9).tolist() == list(range(9, 0, -1))
 
 
+def test_sort_small_batch_unaligned_views_keep_neighbours(ns, cuda, oracle):
+    """Key arrays starting 0..3 keys past a 16-byte boundary, totals that are
+    not multiples of 4, and CTAs whose arrays end in empty ones: the batch
+    kernel stages each CTA's 16-byte cover with one bulk copy but must write
+    back exactly its own keys — the guard keys around the view stay put."""
+    import torch
+    for shift in range(4):
+        for narr, seed in ((1, 1), (7, 2), (1023, 3), (1025, 4), (5000, 5), (70001, 6)):
+            o, k = oracle.generate_batch_i32(narr, seed)
+            if narr > 2:  # a run of empty arrays at the end of the first CTA
+                lens = np.diff(o.astype(np.int64))
+                lens[min(1020, narr - 1):min(1024, narr)] = 0
+                o = np.concatenate([[0], np.cumsum(lens)]).astype(np.uint32)
+                k = k[:int(o[-1])]
+            want = oracle.sort_small_batch(k, o)
+            buf = np.full(len(k) + shift + 7, -12345, np.int32)
+            buf[shift:shift + len(k)] = k
+            t = to_dev(buf, cuda)
+            view = t[shift:shift + len(k)]
+            ns.sort_small_batch(view, torch.from_numpy(o.view(np.int32)).to(cuda))
+            got = from_dev(t)
+            assert np.array_equal(got[shift:shift + len(k)], want), (shift, narr)
+            assert (got[:shift] == -12345).all() and (got[shift + len(k):] == -12345).all()
+
+
 def test_segmented_matches_reference_prefix(ns, cuda, oracle, golden):
     g = golden["segmented"]
     nseg, seg = g["num_segments_checked"], g["seg_len"]
