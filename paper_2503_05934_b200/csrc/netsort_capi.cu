@@ -59,7 +59,15 @@ struct MergeTuning {
   // instead of 32 (1024-key warp runs, one shared-memory level fewer per
   // tile; measured 2 % faster at 2^26..2^30)
   int k32tile = 1;
+  // NSB_SINGLE_MAX: largest n sorted by one CTA (<= 16384); above it the
+  // tiled path (measured, tools/small_ab.sh: 10,000 keys 22.9 us in one
+  // 1024-thread CTA, 15.9 us as two 8192-key tiles and one merge pass).
+  // NSB_SMALL_K32=1: single-CTA int32 shapes at 32 keys/thread (slower).
+  int64_t single_max = kBsT;
+  int small_k32 = 0;
   MergeTuning() {
+    if (const char* e = getenv("NSB_SINGLE_MAX")) single_max = std::min<int64_t>(atoll(e), kSmT);
+    if (const char* e = getenv("NSB_SMALL_K32")) small_k32 = atoi(e);
     if (const char* e = getenv("NSB_V2")) v2 = atoi(e);
     if (const char* e = getenv("NSB_SAMPLES")) samples = atoi(e);
     if (const char* e = getenv("NSB_TILE64")) tile64 = atoi(e);
@@ -88,14 +96,14 @@ static size_t samples_bytes(size_t n, size_t kb) {
 }
 
 size_t merge_sort_temp(size_t n) {
-  if (n <= (size_t)kSmT) return 0;
+  if (n <= (size_t)tuning().single_max) return 0;
   return align_up(n * sizeof(int32_t), 256) + align_up((max_merge_tiles(n) + 1) * 8, 256) +
          samples_bytes(n, 4);
 }
 
 // int64: ping-pong buffer + merge-path splits + block samples (no k-way scratch)
 size_t merge_sort_temp_i64(size_t n) {
-  if (n <= (size_t)kSmT) return 0;
+  if (n <= (size_t)tuning().single_max) return 0;
   return align_up(n * sizeof(int64_t), 256) + align_up((max_merge_tiles(n) + 1) * 8, 256) +
          samples_bytes(n, 8);
 }
@@ -256,10 +264,18 @@ static int merge_sort_device_t(Key* d_keys, size_t n, int leaf, void* d_temp, si
                                cudaStream_t s) {
   constexpr bool k32 = std::is_same_v<Key, int32_t>;
   if (n <= 1) return NS_OK;
-  if (n <= (size_t)kSmT) {
+  if (n <= (size_t)kSmT && (n <= (size_t)tuning().single_max || d_temp == nullptr)) {
     // one CTA sized to the array: fewer threads and merge levels for small n
+    // (also up to 16384 keys when the caller passes no scratch)
     return with_leaf(leaf, [&](auto L) {
       constexpr int LF = decltype(L)::value;
+      if constexpr (k32) {
+        if (tuning().small_k32 && n > 2048) {
+          if (n <= 4096) return launch_blocksort<128, 32, LF>(d_keys, d_keys, (int64_t)n, 4096, 1, s);
+          if (n <= 8192) return launch_blocksort<256, 32, LF>(d_keys, d_keys, (int64_t)n, 8192, 1, s);
+          return launch_blocksort<512, 32, LF>(d_keys, d_keys, (int64_t)n, kSmT, 1, s);
+        }
+      }
       if (n <= 512) return launch_blocksort<32, 16, LF>(d_keys, d_keys, (int64_t)n, 512, 1, s);
       if (n <= 2048) return launch_blocksort<128, 16, LF>(d_keys, d_keys, (int64_t)n, 2048, 1, s);
       if (n <= 4096) return launch_blocksort<256, 16, LF>(d_keys, d_keys, (int64_t)n, 4096, 1, s);

@@ -349,10 +349,13 @@ static int bucket_sort_classes(const Key* src, Key* dst, const int64_t* jobs, co
   return launch_bucket_sort<1024, 16, LF>(src, dst, jobs + 2 * off[3], off[4] - off[3], s);
 }
 
+// n <= kSmallTile at the top level: the merge sort (one CTA up to 8192
+// keys, else two tiles and a merge pass in the caller's scratch, which
+// quick_sort_temp sizes for it).
 template <class Key>
-static int small_sort(Key* d_keys, size_t n, int leaf, cudaStream_t s) {
-  // n <= kSmallTile: one CTA, in place (merge_sort_device's single-CTA path)
-  return merge_sort_device(d_keys, n, leaf, nullptr, 0, s);
+static int small_sort(Key* d_keys, size_t n, int leaf, void* d_temp, size_t temp_bytes,
+                      cudaStream_t s) {
+  return merge_sort_device(d_keys, n, leaf, d_temp, temp_bytes, s);
 }
 
 // Leaf jobs of a partition level.  Consecutive buckets hold disjoint,
@@ -393,7 +396,7 @@ struct JobPacker {
 // recursive calls only after this level has enqueued all its work.
 static int quick_sort_level(int32_t* keys, int32_t* tmp, size_t n, int leaf, const QsAux& aux,
                             cudaStream_t s) {
-  if (n <= (size_t)kSmallTile) return small_sort(keys, n, leaf, s);
+  if (n <= (size_t)kSmallTile) return merge_sort_device(keys, n, leaf, nullptr, 0, s);  // one CTA
   int B = 2;
   while (B < kQsMaxB && (size_t)B * kQsTarget < n) B *= 2;
   const int S = B * kQsOversample;
@@ -915,14 +918,14 @@ static int ml_quick_sort(Key* keys, Key* tmp, size_t n, int leaf, const MlAux<Ke
 }
 
 size_t quick_sort_temp(size_t n) {
-  if (n <= (size_t)kSmallTile) return 0;
+  if (n <= (size_t)kSmallTile) return merge_sort_temp(n);
   return align_up(n * 4, 256) + std::max(qs_aux_bytes(), ml_aux_bytes(n));
 }
 
 // int64 keys always take the multi-level partition (its classifier is a
 // plain splitter search; the single-level prefix table is int32-specific)
 size_t quick_sort_temp_i64(size_t n) {
-  if (n <= (size_t)kSmallTile) return 0;
+  if (n <= (size_t)kSmallTile) return merge_sort_temp_i64(n);
   return align_up(n * 8, 256) + ml_aux_bytes(n, 8);
 }
 
@@ -940,7 +943,7 @@ int ns_quick_sort_i32(int32_t* d_keys, size_t n, uint32_t width_mask, int varsor
   if (n <= 1) return NS_OK;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int leaf = leaf_of(width_mask, varsort_max);
-  if (n <= (size_t)kSmallTile) return small_sort(d_keys, n, leaf, s);
+  if (n <= (size_t)kSmallTile) return small_sort(d_keys, n, leaf, d_temp, temp_bytes, s);
   if (!d_temp || temp_bytes < quick_sort_temp(n)) return NS_ERR_TEMP;
   int32_t* tmp = static_cast<int32_t*>(d_temp);
   char* auxp = static_cast<char*>(d_temp) + align_up(n * 4, 256);
@@ -965,7 +968,7 @@ int ns_quick_sort_i64(int64_t* d_keys, size_t n, uint32_t width_mask, int varsor
   if (n <= 1) return NS_OK;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int leaf = leaf_of(width_mask, varsort_max);
-  if (n <= (size_t)kSmallTile) return small_sort(d_keys, n, leaf, s);
+  if (n <= (size_t)kSmallTile) return small_sort(d_keys, n, leaf, d_temp, temp_bytes, s);
   if (!d_temp || temp_bytes < quick_sort_temp_i64(n)) return NS_ERR_TEMP;
   int64_t* tmp = static_cast<int64_t*>(d_temp);
   char* auxp = static_cast<char*>(d_temp) + align_up(n * 8, 256);
