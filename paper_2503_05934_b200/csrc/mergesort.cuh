@@ -274,11 +274,10 @@ __device__ __forceinline__ void tile_store(const Key* sm, Key* out, int valid) {
 // ---------------------------------------------------------------------------
 
 // Padded variant (one pad word per 32 keys, serial merge with clamped
-// indices): kept for int64 keys, where the skewed variant below needs more
-// registers than the occupancy it must keep (measured: 2^28 int64 sort 15.1
-// vs 16.6 ms).  int32 tiles of up to 1024 threads use the skewed variant at
-// 2048 threads/SM (32 registers, no spills): 65,536 x 16,384 segmented
-// 9.8 -> 9.3 ms.
+// indices): the fallback for shapes the skewed variant below does not cover
+// (32-thread tiles, int64 tiles other than 8 or 16 keys per thread).  int32
+// tiles of up to 1024 threads and int64 tiles of 8 / 16 keys per thread use
+// the skewed variant.
 template <int NT, int K, int LEAF, class Key>
 __device__ __forceinline__ void cta_sort_padded(const Key* in, Key* out, int valid, Key* sm) {
   constexpr int T = NT * K;
@@ -327,9 +326,16 @@ __device__ __forceinline__ void cta_sort_padded(const Key* in, Key* out, int val
 #ifndef NSB_SKEW_MAX_NT
 #define NSB_SKEW_MAX_NT 1024
 #endif
+// int64 tiles of 16 keys per thread (<512,16>) in the skewed layout: with
+// the producer/loser loop they fit 64 registers without spills; measured
+// equal for the merge-sort tile and 8 % faster for the 16 M int64 quick-sort
+// bucket tiles (tools/i64_ab.sh)
+#ifndef NSB_SKEW64_K16
+#define NSB_SKEW64_K16 1
+#endif
 template <int NT, int K, class Key>
 __host__ __device__ constexpr bool cta_sort_skewed() {
-  return ((sizeof(Key) == 4 && (K == 16 || K == 32)) || (sizeof(Key) == 8 && K == 8)) &&
+  return ((sizeof(Key) == 4 && (K == 16 || K == 32)) || (sizeof(Key) == 8 && (K == 8 || (NSB_SKEW64_K16 && K == 16)))) &&
          NT > 32 && NT <= NSB_SKEW_MAX_NT;
 }
 
