@@ -51,7 +51,9 @@ struct MergeTuning {
   int64_t fused_max_tiles = 4096;  // passes with fewer tiles search in-kernel (measured crossover)
   int v2 = -1;  // NSB_V2 forces one tile shape (see v2_pass); -1 = by size
   int samples = 1;  // NSB_SAMPLES=0: plain partition search on every pass
-  // NSB_TILE64: int64 tile sort 1 = <1024,8> skewed, 2 = <512,16> padded
+  // NSB_TILE64: int64 tile sort 1 = <1024,8>, 2 = <512,16> (16384-key
+  // <1024,16> tiles measured slower: 2^28 tile sort 5.05 -> 6.92 ms for one
+  // pass fewer, sort 14.8 -> 16.0 ms; tools/tile64_ab.sh)
   // (measured at 2^28: 7.5 vs 5.1 ms -- the 256-key warp runs need a fifth
   // shared-memory level and the CTA fits once per SM)
   int tile64 = 2;
@@ -156,7 +158,11 @@ static int v2_pass_t(const Key* src, Key* dst, int64_t n, int64_t R, int64_t* mp
   const bool rec = sc && sc->base && sc->n == n && ((NT * K) % (1 << kShift)) == 0;
   const BlockSamples<Key> bs =
       rec ? sc->get<Key>(kShift) : BlockSamples<Key>{nullptr, nullptr, 0, kShift};
-  if (mt <= tu.fused_max_tiles) {
+  // in-kernel search up to 4096 tiles of <= 4096 keys, 2048 larger tiles
+  // (tools/fused_ab.sh: 2^24 keys in 2114 <256,31> tiles 480 -> 473 us with
+  // the partition kernel; 2^23 in 2850 <128,23> tiles 235 vs 261 us fused)
+  const int64_t fused_max = NT * K > 4096 ? tu.fused_max_tiles / 2 : tu.fused_max_tiles;
+  if (mt <= fused_max) {
     // few tiles: every CTA finds its own split (no partition launch)
     {
       Prof prof(PK_MERGE_PASS, s);
