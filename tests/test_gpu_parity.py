@@ -163,7 +163,10 @@ def test_segmented_matches_reference_prefix(ns, cuda, oracle, golden):
 
 
 def test_segmented_odd_lengths(ns, cuda, oracle):
-    for seg in (1, 2, 3, 5, 100, 4097, 8192, 12345, 16384, 20000):
+    # every tile shape of the segmented path: <32,16> .. <128,16>, then
+    # 32 keys per thread <128,32> (2049..4096), <256,32> (..8192), <512,32>
+    # (..16384), and whole-array sorts above
+    for seg in (1, 2, 3, 5, 100, 2049, 3000, 4096, 4097, 6000, 8192, 12345, 16384, 20000):
         nseg = max(1, 200000 // seg)
         a = oracle.generate_i32("random", nseg * seg, seed=seg)
         want = np.sort(a.reshape(nseg, seg), axis=1).reshape(-1)
@@ -171,6 +174,15 @@ def test_segmented_odd_lengths(ns, cuda, oracle):
             t = to_dev(a, cuda)
             ns.segmented_sort(t, seg, ns.find_config("3To5"), algo)
             assert np.array_equal(from_dev(t), want), (seg, algo)
+    # every leaf shape (LEAF 1 / 2 / 8) through the 32-keys-per-thread tiles
+    for cfg in ("Classic", "VarSort3", "6To8"):
+        for seg in (3000, 6000, 16384):
+            nseg = max(1, 100000 // seg)
+            a = oracle.generate_i32("random", nseg * seg, seed=seg + 1)
+            want = np.sort(a.reshape(nseg, seg), axis=1).reshape(-1)
+            t = to_dev(a, cuda)
+            ns.segmented_sort(t, seg, ns.find_config(cfg), ns.Algorithm.merge_sort)
+            assert np.array_equal(from_dev(t), want), (seg, cfg)
 
 
 def test_range_sorts_leave_outside_untouched(ns, cuda, oracle):
