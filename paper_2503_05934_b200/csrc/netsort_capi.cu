@@ -584,20 +584,29 @@ __global__ void __launch_bounds__(kBaNT)
   if (tid < tail) kw[head + 4 * body + tid] = sk[phase + head + 4 * body + tid];
 }
 
-// Per-device validation flag + pinned host mirror, allocated once.
+// Validation flag + pinned host mirror per (host thread, device), allocated
+// once: concurrent calls from different host threads never share a flag, and
+// one thread's calls are serialised by the read-back that ends each call.
 struct BatchFlag {
   int* dev = nullptr;
   int* host = nullptr;
 };
-static std::mutex g_flag_mu;
-static BatchFlag g_flags[64];
+struct BatchFlags {
+  BatchFlag f[64];
+  ~BatchFlags() {
+    for (auto& x : f) {
+      if (x.dev) cudaFree(x.dev);
+      if (x.host) cudaFreeHost(x.host);
+    }
+  }
+};
+static thread_local BatchFlags t_flags;
 
 static int batch_flag(BatchFlag** out) {
   int dev = 0;
   NSB_TRY(check_cuda(cudaGetDevice(&dev), "cudaGetDevice"));
   if (dev < 0 || dev >= 64) return NS_ERR_INVALID;
-  std::lock_guard<std::mutex> lk(g_flag_mu);
-  BatchFlag& f = g_flags[dev];
+  BatchFlag& f = t_flags.f[dev];
   if (!f.dev) {
     NSB_TRY(check_cuda(cudaMalloc(reinterpret_cast<void**>(&f.dev), sizeof(int)), "cudaMalloc"));
     NSB_TRY(check_cuda(cudaHostAlloc(reinterpret_cast<void**>(&f.host), sizeof(int),

@@ -617,6 +617,42 @@ def test_two_streams_concurrently(ns, cuda, oracle):
         assert np.array_equal(tb_.cpu().numpy(), np.sort(b))
 
 
+def test_batch_from_two_host_threads(ns, cuda, oracle):
+    """The batch call validates lengths through a device flag read back at
+    the end of the call: calls from two host threads (one with a bad length,
+    one good, each on its own stream) must not see each other's flag."""
+    import threading
+    import torch
+    o, k = oracle.generate_batch_i32(1 << 16, 5)
+    want = oracle.sort_small_batch(k, o)
+    bad_o = o.copy()
+    bad_o[1:] += 9  # the first array has 9 + len keys: invalid (> 8)
+    kb = np.concatenate([k, np.zeros(9, np.int32)])
+    errors = {}
+
+    def run(tag, keys, offs, reps):
+        torch.cuda.set_device(cuda)
+        st = torch.cuda.Stream()
+        with torch.cuda.stream(st):
+            tk = torch.from_numpy(keys).to(cuda)
+            to = torch.from_numpy(offs.view(np.int32)).to(cuda)
+            res = []
+            for _ in range(reps):
+                w = tk.clone()
+                try:
+                    ns.sort_small_batch(w, to)
+                    res.append(("ok", w.cpu().numpy()))
+                except ValueError:
+                    res.append(("bad", None))
+            errors[tag] = res
+
+    ta = threading.Thread(target=run, args=("good", k, o, 20))
+    tb = threading.Thread(target=run, args=("bad", kb, bad_o, 20))
+    ta.start(); tb.start(); ta.join(); tb.join()
+    assert all(r == "ok" and np.array_equal(v, want) for r, v in errors["good"])
+    assert all(r == "bad" for r, _ in errors["bad"])
+
+
 _PARTITION_SCRIPT = r"""
 import sys, numpy as np, torch
 sys.path.insert(0, sys.argv[1])
