@@ -67,7 +67,12 @@ struct MergeTuning {
   // NSB_SMALL_K32=1: single-CTA int32 shapes at 32 keys/thread (slower).
   int64_t single_max = kBsT;
   int small_k32 = 0;
+  // NSB_PART_WARP_MAX: passes of at most this many tiles find their splits
+  // with one warp per tile (merge_partition_v4_kernel), larger ones with one
+  // thread per tile (v3 / v2)
+  int64_t part_warp_max = 16384;
   MergeTuning() {
+    if (const char* e = getenv("NSB_PART_WARP_MAX")) part_warp_max = atoll(e);
     if (const char* e = getenv("NSB_SINGLE_MAX")) single_max = std::min<int64_t>(atoll(e), kSmT);
     if (const char* e = getenv("NSB_SMALL_K32")) small_k32 = atoi(e);
     if (const char* e = getenv("NSB_V2")) v2 = atoi(e);
@@ -179,7 +184,12 @@ static int v2_pass_t(const Key* src, Key* dst, int64_t n, int64_t R, int64_t* mp
   {
     Prof prof(PK_PARTITION, s);
     cudaError_t e;
-    if (sc && sc->have && rec && tu.samples)
+    const bool smp = sc && sc->have && rec && tu.samples;
+    if (mt <= tu.part_warp_max)  // few tiles: latency-bound, one warp per search
+      e = launch_pdl(n, merge_partition_v4_kernel<Key>, (unsigned)((mt + 7) / 8), 256, 0, s,
+                     src, P, mt, mp,
+                     smp ? sc->get<Key>(sc->shift) : BlockSamples<Key>{nullptr, nullptr, 0, kShift});
+    else if (smp)
       e = launch_pdl(n, merge_partition_v3_kernel<Key>, (unsigned)((mt + 255) / 256), 256, 0, s,
                      src, P, mt, mp, sc->get<Key>(sc->shift));
     else
