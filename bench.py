@@ -447,12 +447,56 @@ def run_ours(args, metric):
         line["cpu_baseline"] = cpu_baseline()
     if rank == 0 and world == 1 and not args.no_size_sweep:
         line["size_sweep"] = size_sweep(ns, L, dev, peak)
+    if rank == 0 and world == 1 and not args.no_batch:
+        line["base_case_batch"] = base_case_batch(ns, L, dev, peak)
     if rank == 0 and world == 1 and args.extra:
         line["other_configs"] = other_configs(ns, L, dev)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def base_case_batch(ns, L, dev, peak):
+    """BASELINE configs[1], the base-case kernel alone: 2^24 independent int32
+    arrays, lengths uniform in {3..8}, packed with a uint32 offsets array,
+    each sorted by its size-specific network.  Kernel time from the library's
+    own launch events (median of 7; the call adds one 4-byte validation
+    read-back), algorithmic bytes 8 per key + 4 per offset, checked against
+    the oracle (the checker only)."""
+    import ctypes as C
+    import numpy as np
+    import torch
+    from paper_2503_05934_b200._lib import check
+    from oracle import oracle as O
+    offs, keys = O.generate_batch_i32(1 << 24, SEED)
+    k = torch.from_numpy(keys).to(dev)
+    o = torch.from_numpy(offs.view("int32")).to(dev)
+    w = k.clone()
+    ns.sort_small_batch(w, o)
+    ok = bool(np.array_equal(w.cpu().numpy(), O.sort_small_batch(keys, offs)))
+    ts = []
+    for _ in range(7):
+        w.copy_(k)
+        torch.cuda.synchronize()
+        check(L.ns_profile_enable(1), "profile")
+        ns.sort_small_batch(w, o)
+        torch.cuda.synchronize()
+        tot = 0.0
+        for kind in range(L.ns_profile_kinds()):
+            t, c = C.c_double(), C.c_uint64()
+            check(L.ns_profile_read(kind, C.byref(t), C.byref(c)), "profile read")
+            tot += t.value
+        check(L.ns_profile_enable(0), "profile")
+        ts.append(tot)
+    ms = statistics.median(ts)
+    nbytes = 8 * len(keys) + 4 * len(offs)
+    gbs = nbytes / (ms * 1e-3) / 1e9
+    return {"workload": "BASELINE configs[1]: 2^24 ragged int32 arrays, lengths U{3..8}, "
+                        "uint32 offsets, size-specific networks",
+            "num_arrays": 1 << 24, "num_keys": int(len(keys)), "kernel_ms": ms,
+            "gkeys_per_s": len(keys) / (ms * 1e-3) / 1e9, "bytes": nbytes,
+            "achieved_gbs": gbs, "peak_gbs": peak, "frac": gbs / peak, "verified": ok}
 
 
 def size_sweep(ns, L, dev, peak):
@@ -670,6 +714,8 @@ def main():
                     help="total keys (--keys under torchrun: its parser claims --n)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--extra", action="store_true", help="also time the other BASELINE configs")
+    ap.add_argument("--no-batch", action="store_true",
+                    help="skip the base-case batch kernel (BASELINE configs[1]) object")
     ap.add_argument("--no-size-sweep", action="store_true",
                     help="skip the n = 10K..256M merge-sort sweep (N=1 only)")
     ap.add_argument("--exchange", choices=["p2p", "nccl"], default="p2p",
