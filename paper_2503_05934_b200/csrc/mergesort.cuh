@@ -620,6 +620,14 @@ struct BlockSamples {
   int shift;    // log2 of the block size
 };
 
+// NSB_PASS_PL=1: the pass merge loop in producer/loser form over K-sentinel
+// pads (one LDS per output, no clamps), as in the tile sort.
+#ifndef NSB_PASS_PL
+#define NSB_PASS_PL 1
+#endif
+// sentinel words after each staged slice of a K-output-per-thread merge
+__host__ __device__ constexpr int v2_pad(int K) { return NSB_PASS_PL ? K : 1; }
+
 template <int NT, int K, class Key>
 __device__ __forceinline__ void merge_staged_tile(Key* sm, int a_pos, int la, int b_pos, int lb,
                                                   Key* dst, const int64_t* s_out_off,
@@ -628,9 +636,10 @@ __device__ __forceinline__ void merge_staged_tile(Key* sm, int a_pos, int la, in
   constexpr int PV = kpv<Key>();
   constexpr int KB = (int)sizeof(Key);
   const int tid = threadIdx.x;
-  if (tid == 0) {
-    sm[a_pos + la] = KeyT<Key>::kMax;  // sentinels: the merge loop has no bounds tests
-    sm[b_pos + lb] = KeyT<Key>::kMax;
+  constexpr int PAD = v2_pad(K);
+  for (int q = tid; q < PAD; q += NT) {
+    sm[a_pos + la + q] = KeyT<Key>::kMax;  // sentinels: the merge loop has no bounds tests
+    sm[b_pos + lb + q] = KeyT<Key>::kMax;
   }
   __syncthreads();
 
@@ -642,13 +651,30 @@ __device__ __forceinline__ void merge_staged_tile(Key* sm, int a_pos, int la, in
   const int d = min(tid * K, total);
   const int cnt = min(K, total - d);
   const int a = merge_path<int>(SA, la, SB, lb, d);
+  const char* smc = reinterpret_cast<const char*>(sm);
+  Key v[K];
+#if NSB_PASS_PL
+  // producer/loser form (see cta_sort_skewed_body): one LDS per output; a
+  // cursor runs at most K keys into its slice's K sentinels
+  uint32_t ptr = (uint32_t)(a_pos + a) * KB;
+  uint32_t mnext = (uint32_t)(b_pos + d - a + 1) * KB;
+  Key m = *reinterpret_cast<const Key*>(smc + mnext - KB);
+  auto step = [&]() {
+    const Key x = *reinterpret_cast<const Key*>(smc + ptr);
+    const bool t = x <= m;
+    const Key out = t ? x : m;
+    const uint32_t q = ptr + (uint32_t)KB;
+    ptr = t ? q : mnext;
+    mnext = t ? mnext : q;
+    m = t ? m : x;
+    return out;
+  };
+#else
   // cursors are byte offsets into shared memory (LDS [reg + base] needs no
   // index arithmetic), clamped at their slice's +inf sentinel
-  const char* smc = reinterpret_cast<const char*>(sm);
   uint32_t oa = (uint32_t)(a_pos + a) * KB, ob = (uint32_t)(b_pos + d - a) * KB;
   const uint32_t ea = (uint32_t)(a_pos + la) * KB, eb = (uint32_t)(b_pos + lb) * KB;
   Key ka = *reinterpret_cast<const Key*>(smc + oa), kb = *reinterpret_cast<const Key*>(smc + ob);
-  Key v[K];
   auto step = [&]() {
     const bool take_a = ka <= kb;  // A wins ties (merge_runs, hybrid.hpp:71-75)
     const Key out = take_a ? ka : kb;
@@ -661,6 +687,7 @@ __device__ __forceinline__ void merge_staged_tile(Key* sm, int a_pos, int la, in
     }
     return out;
   };
+#endif
   const bool full = total == TM;
   if (full) {
 #pragma unroll
@@ -821,14 +848,14 @@ __global__ void merge_partition_v4_kernel(const Key* __restrict__ src, PassPlan 
 
 // Keys of shared memory a v2 tile needs: two slices with up to 3 keys of
 // alignment slack each, a sentinel after each, 16-byte rounding.
-__host__ __device__ constexpr int v2_smem_words(int TM) { return TM + 16; }
+__host__ __device__ constexpr int v2_smem_words(int TM, int K = 0) { return TM + 16 + 2 * v2_pad(K); }
 
 // Resident CTAs per SM the launch bounds ask for: as many as shared memory
 // (228 KiB per SM, 1 KiB reserved per CTA), the 2048-thread limit and a
 // register floor allow.  <256,31>: 6 CTAs/SM at 40 registers (measured
 // best; 7 CTAs force 32 registers and spill).
 __host__ __device__ constexpr int v2_min_blocks(int NT, int K, int key_bytes) {
-  const int smem = (NT * K + 16) * key_bytes + 1024;
+  const int smem = v2_smem_words(NT * K, K) * key_bytes + 1024;
   int b = 228 * 1024 / smem;
   if (b > 2048 / NT) b = 2048 / NT;
   // the K outputs stay in registers until the store (2 registers per int64)
@@ -846,7 +873,7 @@ __global__ void __launch_bounds__(NT, v2_min_blocks(NT, K, (int)sizeof(Key)))
   static_assert(TM % 4 == 0, "tiles must start 16-byte aligned");
   constexpr int PV = kpv<Key>();           // keys per 16 bytes
   constexpr int KB = (int)sizeof(Key);
-  __shared__ __align__(128) Key sm[v2_smem_words(TM)];
+  __shared__ __align__(128) Key sm[v2_smem_words(TM, K)];
   __shared__ __align__(8) uint64_t bar;
   const int tid = threadIdx.x;
   const int64_t c = blockIdx.x;
@@ -887,7 +914,7 @@ __global__ void __launch_bounds__(NT, v2_min_blocks(NT, K, (int)sizeof(Key)))
   // smem placement mirrors global 16-byte alignment so one bulk copy per slice
   const uintptr_t a_addr = reinterpret_cast<uintptr_t>(A), b_addr = reinterpret_cast<uintptr_t>(B);
   const int a_shift = (int)((a_addr & 15) / KB), b_shift = (int)((b_addr & 15) / KB);
-  const int b_off = (a_shift + la + 1 + PV - 1) & ~(PV - 1);  // B cover starts 16-byte aligned
+  const int b_off = (a_shift + la + v2_pad(K) + PV - 1) & ~(PV - 1);  // B cover starts 16-byte aligned
   const Key* a_cov = A - a_shift;
   const Key* b_cov = B - b_shift;
   const int a_words = (a_shift + la + PV - 1) & ~(PV - 1), b_words = (b_shift + lb + PV - 1) & ~(PV - 1);

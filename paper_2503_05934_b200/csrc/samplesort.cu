@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(PmShape<Key>::NT, v2_min_blocks(PmShape<Key>::
   constexpr int NT = PmShape<Key>::NT, K = PmShape<Key>::K, TM = NT * K;
   constexpr int PV = kpv<Key>();
   constexpr int KB = (int)sizeof(Key);
-  __shared__ __align__(128) Key sm[v2_smem_words(TM)];
+  __shared__ __align__(128) Key sm[v2_smem_words(TM, K)];
   __shared__ __align__(8) uint64_t bar;
   __shared__ int64_t s_out;
   const int tid = threadIdx.x;
@@ -117,7 +117,7 @@ __global__ void __launch_bounds__(PmShape<Key>::NT, v2_min_blocks(PmShape<Key>::
   // smem placement mirrors global 16-byte alignment (bulk copies need it)
   const uintptr_t a_addr = reinterpret_cast<uintptr_t>(A), b_addr = reinterpret_cast<uintptr_t>(B);
   const int a_shift = (int)((a_addr & 15) / KB), b_shift = (int)((b_addr & 15) / KB);
-  const int b_off = (a_shift + la + 1 + PV - 1) & ~(PV - 1);
+  const int b_off = (a_shift + la + v2_pad(K) + PV - 1) & ~(PV - 1);
   const Key* a_cov = A - a_shift;
   const Key* b_cov = B - b_shift;
   const int a_words = (a_shift + la + PV - 1) & ~(PV - 1), b_words = (b_shift + lb + PV - 1) & ~(PV - 1);
