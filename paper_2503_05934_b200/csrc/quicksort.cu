@@ -35,7 +35,10 @@
 namespace nsb {
 
 constexpr int kQsMaxB = 4096;        // splitter slots (B-1 used, last is +inf pad)
-constexpr int kQsOversample = 16;    // samples per bucket
+#ifndef NSB_QS_OVERSAMPLE
+#define NSB_QS_OVERSAMPLE 16
+#endif
+constexpr int kQsOversample = NSB_QS_OVERSAMPLE;  // samples per bucket
 constexpr int kQsTarget = 4096;      // target mean bucket size
 constexpr int kQsNT = 512;
 constexpr int kQsChunk = kQsNT * 32;  // keys per CTA in count / scatter
