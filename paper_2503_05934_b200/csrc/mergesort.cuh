@@ -475,15 +475,28 @@ __device__ __forceinline__ void cta_sort_skewed_body(const Key* in, Key* out, in
 #ifndef NSB_BS_THREADS_PER_SM
 #define NSB_BS_THREADS_PER_SM 2048
 #endif
+// 32 keys per thread: 512-thread tiles (16384 keys) at 3 CTAs per SM (40
+// registers; measured 2^30 tile sort 8.02 -> 7.60 ms, segmented 65,536 x
+// 16,384 8.07 -> 7.61 ms), smaller tiles at 1024 threads per SM (64
+// registers: the latency-bound sorts of < 2^21 keys run them, and 40
+// registers measured slower there, 2^20 49 -> 53 us)
+#ifndef NSB_BS_THREADS_PER_SM_K32
+#define NSB_BS_THREADS_PER_SM_K32 1536
+#endif
+#ifndef NSB_BS_THREADS_PER_SM_K32_SMALL
+#define NSB_BS_THREADS_PER_SM_K32_SMALL 1024
+#endif
 #ifndef NSB_BS_THREADS_PER_SM_64
 #define NSB_BS_THREADS_PER_SM_64 1024  // int64: 64 registers per thread
 #endif
 template <int NT, int K, class Key>
 __host__ __device__ constexpr int bs_min_blocks() {
   // 0 = no minimum (the padded variant keeps the compiler's own choice)
-  // 32 keys per thread need ~64 registers: half the threads per SM
+  // threads per SM by key size and keys per thread (the macros above)
   constexpr int tps = sizeof(Key) == 8 ? NSB_BS_THREADS_PER_SM_64
-                                       : (K >= 32 ? NSB_BS_THREADS_PER_SM / 2 : NSB_BS_THREADS_PER_SM);
+                                       : (K >= 32 ? (NT >= 512 ? NSB_BS_THREADS_PER_SM_K32
+                                                               : NSB_BS_THREADS_PER_SM_K32_SMALL)
+                                                  : NSB_BS_THREADS_PER_SM);
   return !cta_sort_skewed<NT, K, Key>() || NT >= tps ? 0 : tps / NT;
 }
 
