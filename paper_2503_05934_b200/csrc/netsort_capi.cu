@@ -398,7 +398,13 @@ int tile_sort_segments(int32_t* d_keys, size_t num_segments, size_t seg_len, int
 // in shared memory with coalesced loads, each thread sorts its arrays in
 // registers with the size-specific network, and the CTA stores them back.
 // ---------------------------------------------------------------------------
-constexpr int kBaNT = 256, kBaPer = 4, kBaArr = kBaNT * kBaPer;
+#ifndef NSB_BATCH_PER
+#define NSB_BATCH_PER 4
+#endif
+#ifndef NSB_BATCH_MINB
+#define NSB_BATCH_MINB 1
+#endif
+constexpr int kBaNT = 256, kBaPer = NSB_BATCH_PER, kBaArr = kBaNT * kBaPer;
 
 // Lanes of a warp that sort arrays of different lengths would serialise the
 // seven network paths, so each CTA first splits its arrays by length (a
@@ -433,7 +439,7 @@ __device__ __forceinline__ void sort_in_place(int32_t* p) {
   for (int k = 0; k < L; ++k) p[k] = v[k];
 }
 
-__global__ void __launch_bounds__(kBaNT)
+__global__ void __launch_bounds__(kBaNT, NSB_BATCH_MINB)
     sort_small_batch_kernel(int32_t* __restrict__ keys, const uint32_t* __restrict__ offsets,
                             int64_t num_arrays, int* __restrict__ bad) {
   constexpr int NW = kBaNT / 32;
