@@ -206,7 +206,10 @@ __device__ __forceinline__ WarpRun warp_run(int b) {
 // 2 CTAs/SM (<= 64 registers; the classifier + histogram take 57 KiB of
 // shared memory each): measured at 112 registers and ONE CTA/SM the kernel
 // ran at 25 % occupancy and 0.6 TB/s.
-__global__ void __launch_bounds__(kQsNT, 2)
+#ifndef NSB_QS_COUNT_MINB
+#define NSB_QS_COUNT_MINB 2
+#endif
+__global__ void __launch_bounds__(kQsNT, NSB_QS_COUNT_MINB)
     count_kernel(const int32_t* __restrict__ keys, int64_t n, const int32_t* __restrict__ gspl,
                  const int16_t* __restrict__ glut, int B, uint32_t* __restrict__ totals) {
   extern __shared__ int32_t qsm[];
