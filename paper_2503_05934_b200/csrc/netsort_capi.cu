@@ -427,18 +427,6 @@ __device__ __forceinline__ unsigned match_len4(int len) {
   return eq;
 }
 
-// The width-L network (sort_exact<L>, networks.hpp:122-128) on L keys of
-// shared memory: L loads, the network in registers, L stores.
-template <int L>
-__device__ __forceinline__ void sort_in_place(int32_t* p) {
-  int32_t v[L];
-#pragma unroll
-  for (int k = 0; k < L; ++k) v[k] = p[k];
-  sort_net<L>(v);
-#pragma unroll
-  for (int k = 0; k < L; ++k) p[k] = v[k];
-}
-
 __global__ void __launch_bounds__(kBaNT, NSB_BATCH_MINB)
     sort_small_batch_kernel(int32_t* __restrict__ keys, const uint32_t* __restrict__ offsets,
                             int64_t num_arrays, int* __restrict__ bad) {
@@ -573,16 +561,7 @@ __global__ void __launch_bounds__(kBaNT, NSB_BATCH_MINB)
       const int j = perm[slot];
       const int off = (int)(so[j] - k0) + phase;
       const int len = (int)(so[j + 1] - so[j]);
-      switch (len) {  // warp-uniform almost always (arrays are grouped by length)
-        case 2: sort_in_place<2>(sk + off); break;
-        case 3: sort_in_place<3>(sk + off); break;
-        case 4: sort_in_place<4>(sk + off); break;
-        case 5: sort_in_place<5>(sk + off); break;
-        case 6: sort_in_place<6>(sk + off); break;
-        case 7: sort_in_place<7>(sk + off); break;
-        case 8: sort_in_place<8>(sk + off); break;
-        default: break;
-      }
+      sort_small_in_place(sk + off, len);  // warp-uniform almost always (grouped by length)
     }
   }
   __syncthreads();

@@ -151,18 +151,31 @@ NSB_HD void thread_sort(T (&v)[K]) {
   static_assert(K <= 32, "thread_sort supports up to 32 keys per thread");
 }
 
-// Runtime-width network for one ragged array (the reference's sort_small
-// switch): v holds up to 8 keys, `len` of them live.
+// The width-L network (sort_exact<L>, networks.hpp:122-128) on L keys in
+// memory: L loads, the network in registers, L stores.
+template <int L, class T>
+__device__ __forceinline__ void sort_in_place(T* p) {
+  T v[L];
+#pragma unroll
+  for (int k = 0; k < L; ++k) v[k] = p[k];
+  sort_net<L>(v);
+#pragma unroll
+  for (int k = 0; k < L; ++k) p[k] = v[k];
+}
+
+// Runtime-width network for one ragged array of `len` keys at p (the
+// reference's sort_small switch, networks.hpp:132-145; lengths 0 and 1 are
+// no-ops).  Exactly `len` loads and stores.
 template <class T>
-__device__ __forceinline__ void sort_small_switch(T (&v)[8], int len) {
+__device__ __forceinline__ void sort_small_in_place(T* p, int len) {
   switch (len) {
-    case 2: sort_net<2>(v); break;
-    case 3: sort_net<3>(v); break;
-    case 4: sort_net<4>(v); break;
-    case 5: sort_net<5>(v); break;
-    case 6: sort_net<6>(v); break;
-    case 7: sort_net<7>(v); break;
-    case 8: sort_net<8>(v); break;
+    case 2: sort_in_place<2>(p); break;
+    case 3: sort_in_place<3>(p); break;
+    case 4: sort_in_place<4>(p); break;
+    case 5: sort_in_place<5>(p); break;
+    case 6: sort_in_place<6>(p); break;
+    case 7: sort_in_place<7>(p); break;
+    case 8: sort_in_place<8>(p); break;
     default: break;
   }
 }
