@@ -865,7 +865,7 @@ __host__ __device__ constexpr int v2_smem_words(int TM, int K = 0) { return TM +
 
 // Resident CTAs per SM the launch bounds ask for: as many as shared memory
 // (228 KiB per SM, 1 KiB reserved per CTA), the 2048-thread limit and a
-// register floor allow.  <256,31>: 6 CTAs/SM at 40 registers (measured
+// register floor allow.  <256,29> / <256,31>: 6 CTAs/SM at 40 registers (measured
 // best; 7 CTAs force 32 registers and spill).
 __host__ __device__ constexpr int v2_min_blocks(int NT, int K, int key_bytes) {
   const int smem = v2_smem_words(NT * K, K) * key_bytes + 1024;

@@ -42,7 +42,7 @@ static int launch_blocksort(const Key* src, Key* dst, int64_t n, int stride, int
 
 // Tuning knobs (read once; the defaults are the measured best on B200).
 //   NSB_TILE  = 8192 | 16384 | 32768 : keys per tile-sort CTA
-constexpr int kV2NT = 256, kV2K = 31, kV2T = kV2NT * kV2K;  // 7936 keys per tile
+constexpr int kV2NT = 256, kV2K = 29, kV2T = kV2NT * kV2K;  // 7424 keys per tile (<256,29> measured 0.5-4 % faster than <256,31> from 2^24 to 2^30: tools/shape_ab2.sh)
 // int64 keys (NSB_V2_64=0): 3840 keys (30 KiB) per tile; K odd keeps the
 // half-warp 64-bit cursor accesses on distinct banks
 constexpr int kV2K64 = 15;
@@ -214,8 +214,9 @@ static int v2_pass_t(const Key* src, Key* dst, int64_t n, int64_t R, int64_t* mp
 // One pairwise merge pass (v2): runs of R in src -> runs of 2R in dst.
 // Tile shape by array size (tests/size_sweep.py, tools/mid_sweep.sh on B200):
 // up to 2^23 keys a pass is latency bound and smaller tiles (<128,23>, 2944
-// keys, 12 CTAs/SM) win by 5-10 %; above, <256,31> (7936 keys, 6 CTAs/SM)
-// is within 0.5 % of the best shape measured.
+// keys, 12 CTAs/SM) win by 5-10 %; above, <256,29> (7424 keys, 6 CTAs/SM;
+// tools/shape_ab2.sh: 2^24 411 -> 396 us, 2^30 28.10 -> 27.97 ms against
+// <256,31>, the previous default, now NSB_V2=14).
 static int v2_pass(const int32_t* src, int32_t* dst, int64_t n, int64_t R, int64_t* mp,
                    cudaStream_t s, SmpCtx* sc = nullptr) {
   switch (tuning().v2) {
@@ -227,6 +228,8 @@ static int v2_pass(const int32_t* src, int32_t* dst, int64_t n, int64_t R, int64
     case 6: return v2_pass_t<128, 23>(src, dst, n, R, mp, s, sc);
     case 9: return v2_pass_t<128, 63>(src, dst, n, R, mp, s, sc);
     case 11: return v2_pass_t<128, 55>(src, dst, n, R, mp, s, sc);
+    case 13: return v2_pass_t<256, 27>(src, dst, n, R, mp, s, sc);
+    case 14: return v2_pass_t<256, 31>(src, dst, n, R, mp, s, sc);
     default:
       return n <= (int64_t(1) << 23) ? v2_pass_t<128, 23>(src, dst, n, R, mp, s, sc)
                                      : v2_pass_t<kV2NT, kV2K>(src, dst, n, R, mp, s, sc);

@@ -68,9 +68,9 @@ struct PtrPairTable {
   int64_t tile0[kMaxPtrPairs + 1];
 };
 
-// tile shapes: int32 <256,31> (7936 keys), int64 <256,15> (3840 keys)
+// tile shapes: int32 <256,29> (7424 keys, the pass default), int64 <256,15> (3840 keys)
 template <class Key> struct PmShape;
-template <> struct PmShape<int32_t> { static constexpr int NT = 256, K = 31; };
+template <> struct PmShape<int32_t> { static constexpr int NT = 256, K = 29; };
 template <> struct PmShape<int64_t> { static constexpr int NT = 256, K = 15; };
 template <class Key>
 constexpr int pm_tile() { return PmShape<Key>::NT * PmShape<Key>::K; }
