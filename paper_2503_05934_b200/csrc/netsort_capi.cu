@@ -436,7 +436,8 @@ __global__ void __launch_bounds__(kBaNT, NSB_BATCH_MINB)
   constexpr int NW = kBaNT / 32;
   __shared__ uint32_t so[kBaArr + 1];
   __shared__ __align__(16) int32_t sk[kBaArr * 8 + 8];
-  __shared__ uint16_t perm[kBaArr];
+  // length-grouped order: (shared-memory key offset << 4) | length per slot
+  __shared__ uint32_t perm[kBaArr];
   // per (warp, length, round) counts -> bases; warp-major so the scan rows
   // (one per (length, round), across warps) are read conflict-free
   __shared__ int wcnt[NW][9][kBaPer];
@@ -486,15 +487,18 @@ __global__ void __launch_bounds__(kBaNT, NSB_BATCH_MINB)
   // validate (lengths outside [0, 8] -> error, nothing is touched) and count
   // lengths per (round, warp) with ballots
   int mylen[kBaPer];
+  uint32_t myoff[kBaPer];
   unsigned myeq[kBaPer];
 #pragma unroll
   for (int r = 0; r < kBaPer; ++r) {
     const int j = r * kBaNT + tid;
     int len = -1;
+    myoff[r] = 0;
     if (j < cnt) {
       const uint32_t a = so[j], b = so[j + 1];
       if (b < a || b - a > 8) s_bad = 1;
       else len = (int)(b - a);
+      myoff[r] = a - k0 + (uint32_t)phase;  // < 2^14 when the CTA's range is valid
     }
     mylen[r] = len;
     // lanes with this lane's length (4 ballots on the length bits instead of
@@ -554,16 +558,16 @@ __global__ void __launch_bounds__(kBaNT, NSB_BATCH_MINB)
   for (int r = 0; r < kBaPer; ++r) {
     const int len = mylen[r];
     const int rank = __popc(myeq[r] & ((1u << lane) - 1u));
-    if (len >= 0) perm[wcnt[warp][len][r] + rank] = (uint16_t)(r * kBaNT + tid);
+    if (len >= 0) perm[wcnt[warp][len][r] + rank] = (myoff[r] << 4) | (uint32_t)len;
   }
   __syncthreads();
 #pragma unroll
   for (int r = 0; r < kBaPer; ++r) {
     const int slot = r * kBaNT + tid;
     if (slot < cnt) {
-      const int j = perm[slot];
-      const int off = (int)(so[j] - k0) + phase;
-      const int len = (int)(so[j + 1] - so[j]);
+      const uint32_t pk = perm[slot];  // one load: no second look at the offsets
+      const int off = (int)(pk >> 4);
+      const int len = (int)(pk & 15u);
       sort_small_in_place(sk + off, len);  // warp-uniform almost always (grouped by length)
     }
   }
