@@ -434,7 +434,6 @@ __global__ void __launch_bounds__(kBaNT, NSB_BATCH_MINB)
     sort_small_batch_kernel(int32_t* __restrict__ keys, const uint32_t* __restrict__ offsets,
                             int64_t num_arrays, int* __restrict__ bad) {
   constexpr int NW = kBaNT / 32;
-  __shared__ uint32_t so[kBaArr + 1];
   __shared__ __align__(16) int32_t sk[kBaArr * 8 + 8];
   // length-grouped order: (shared-memory key offset << 4) | length per slot
   __shared__ uint32_t perm[kBaArr];
@@ -480,7 +479,20 @@ __global__ void __launch_bounds__(kBaNT, NSB_BATCH_MINB)
   } else {
     for (int i = tid; i < nk; i += kBaNT) sk[phase + i] = __ldcs(kp + i);
   }
-  for (int i = tid; i <= cnt; i += kBaNT) so[i] = __ldg(offsets + first + i);
+  // this thread's array starts (coalesced; each array's end is the next
+  // lane's start, lane 31 loads its own)
+  uint32_t ofa[kBaPer], ofb[kBaPer];
+#pragma unroll
+  for (int r = 0; r < kBaPer; ++r) {
+    const int j = r * kBaNT + tid;
+    ofa[r] = j <= cnt ? __ldg(offsets + first + j) : 0u;
+    ofb[r] = (lane == 31 && j + 1 <= cnt) ? __ldg(offsets + first + j + 1) : 0u;
+  }
+#pragma unroll
+  for (int r = 0; r < kBaPer; ++r) {
+    const uint32_t nx = __shfl_down_sync(0xffffffffu, ofa[r], 1);
+    if (lane != 31) ofb[r] = nx;
+  }
   int4* sk4 = reinterpret_cast<int4*>(sk + phase + head);  // 16-byte aligned
   if (use_tma) mbar_wait(&bar, 0);
   __syncthreads();
@@ -495,7 +507,7 @@ __global__ void __launch_bounds__(kBaNT, NSB_BATCH_MINB)
     int len = -1;
     myoff[r] = 0;
     if (j < cnt) {
-      const uint32_t a = so[j], b = so[j + 1];
+      const uint32_t a = ofa[r], b = ofb[r];
       if (b < a || b - a > 8) s_bad = 1;
       else len = (int)(b - a);
       myoff[r] = a - k0 + (uint32_t)phase;  // < 2^14 when the CTA's range is valid
