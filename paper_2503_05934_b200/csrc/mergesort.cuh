@@ -867,12 +867,15 @@ __host__ __device__ constexpr int v2_smem_words(int TM, int K = 0) { return TM +
 // (228 KiB per SM, 1 KiB reserved per CTA), the 2048-thread limit and a
 // register floor allow.  <256,29> / <256,31>: 6 CTAs/SM at 40 registers (measured
 // best; 7 CTAs force 32 registers and spill).
+#ifndef NSB_V2_REGS
+#define NSB_V2_REGS 40  // register budget per thread assumed for int32 tiles of <= 31 keys
+#endif
 __host__ __device__ constexpr int v2_min_blocks(int NT, int K, int key_bytes) {
   const int smem = v2_smem_words(NT * K, K) * key_bytes + 1024;
   int b = 228 * 1024 / smem;
   if (b > 2048 / NT) b = 2048 / NT;
   // the K outputs stay in registers until the store (2 registers per int64)
-  const int regs = key_bytes == 8 ? 2 * K + 17 : (K <= 31 ? 40 : K + 17);
+  const int regs = key_bytes == 8 ? 2 * K + 17 : (K <= 31 ? NSB_V2_REGS : K + 17);
   if (b > 65536 / (NT * regs)) b = 65536 / (NT * regs);
   if (b > 32) b = 32;
   return b < 1 ? 1 : b;
