@@ -500,6 +500,19 @@ __host__ __device__ constexpr int bs_min_blocks() {
   return !cta_sort_skewed<NT, K, Key>() || NT >= tps ? 0 : tps / NT;
 }
 
+// Throughput-bound tile sorts (quick-sort buckets: many CTAs, no latency
+// floor): 32-key int32 tiles of every size at NSB_BS_THREADS_PER_SM_K32.
+#ifndef NSB_BUCKET_TPUT
+#define NSB_BUCKET_TPUT 0  // measured: 16M bucket sorts 207 -> 205 us, 1M quick sort 155 -> 164 us
+#endif
+template <int NT, int K, class Key>
+__host__ __device__ constexpr int bs_min_blocks_tput() {
+  if constexpr (NSB_BUCKET_TPUT && sizeof(Key) == 4 && K >= 32 && cta_sort_skewed<NT, K, Key>() &&
+                NT < NSB_BS_THREADS_PER_SM_K32)
+    return NSB_BS_THREADS_PER_SM_K32 / NT;
+  return bs_min_blocks<NT, K, Key>();
+}
+
 template <int NT, int K, int LEAF, class Key = int32_t>
 __global__ void __launch_bounds__(NT, (bs_min_blocks<NT, K, Key>()))
     blocksort_kernel(const Key* src, Key* dst, int64_t n, int stride) {  // src == dst ok

@@ -314,7 +314,7 @@ __global__ void __launch_bounds__(kQsSNT, 2)
 
 // One CTA per job (start, len <= T): sorts src[start..start+len) into dst.
 template <int NT, int K, int LEAF, class Key>
-__global__ void __launch_bounds__(NT, (bs_min_blocks<NT, K, Key>()))
+__global__ void __launch_bounds__(NT, (bs_min_blocks_tput<NT, K, Key>()))
     bucket_sort_kernel(const Key* __restrict__ src, Key* __restrict__ dst,
                        const int64_t* __restrict__ jobs) {
   extern __shared__ __align__(16) unsigned char bsm_raw[];
