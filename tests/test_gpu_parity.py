@@ -236,6 +236,58 @@ def test_duplicates_and_extremes(ns, cuda):
             assert np.array_equal(from_dev(t), np.sort(a)), (fn.__name__, a[:5])
 
 
+def test_sentinel_valued_keys_through_every_path(ns, cuda):
+    """The merge loops run over +inf-sentinel-padded runs (K or K+4 key-maximum
+    sentinels after every run, no cursor clamps): real keys equal to the
+    sentinel must come out right through every path that uses them — the
+    one-CTA and two-tile small sorts, the tiled merge sort, the segmented
+    tiles (16 and 32 keys per thread), the quick-sort buckets, merge() and
+    the int64 twins."""
+    import torch
+    rng = np.random.default_rng(11)
+    imax, imin = np.iinfo(np.int32).max, np.iinfo(np.int32).min
+
+    def heavy(n, dtype=np.int32):
+        info = np.iinfo(dtype)
+        a = rng.integers(-1000, 1000, n).astype(dtype)
+        a[rng.random(n) < 0.4] = info.max
+        a[rng.random(n) < 0.05] = info.min
+        return a
+
+    for n in (5000, 8192, 10000, 16384, 20000, 100003, (1 << 21) + 5):
+        a = heavy(n)
+        for fn, cfg in ((ns.optimized_merge_sort, "6To8"), (ns.optimized_quick_sort, "3To5")):
+            t = to_dev(a, cuda)
+            fn(t, ns.find_config(cfg))
+            assert np.array_equal(from_dev(t), np.sort(a)), (fn.__name__, n)
+    for seg in (3000, 6000, 12000, 16384):
+        nseg = 40
+        a = heavy(nseg * seg)
+        want = np.sort(a.reshape(nseg, seg), axis=1).reshape(-1)
+        for algo in (ns.Algorithm.merge_sort, ns.Algorithm.quick_sort):
+            t = to_dev(a, cuda)
+            ns.segmented_sort(t, seg, ns.find_config("3To5"), algo)
+            assert np.array_equal(from_dev(t), want), (seg, algo)
+    # merge(): two sorted runs whose tails are all INT_MAX
+    left = np.sort(heavy(70001))
+    right = np.sort(heavy(50003))
+    a = np.concatenate([left, right])
+    t = to_dev(a, cuda)
+    ns.merge(t, 0, len(left) - 1, len(a) - 1)
+    assert np.array_equal(from_dev(t), np.sort(a))
+    # int64 keys equal to INT64_MAX through the tiled and segmented paths
+    for n in (20000, (1 << 20) + 3):
+        a = heavy(n, np.int64)
+        t = torch.from_numpy(a).to(cuda)
+        ns.optimized_merge_sort(t, ns.find_config("6To8"))
+        assert np.array_equal(t.cpu().numpy(), np.sort(a)), n
+    a = heavy(30 * 16384, np.int64)
+    t = torch.from_numpy(a).to(cuda)
+    ns.segmented_sort(t, 16384, ns.find_config("3To5"), ns.Algorithm.merge_sort)
+    assert np.array_equal(t.cpu().numpy(), np.sort(a.reshape(30, 16384), axis=1).reshape(-1))
+    assert imax > imin
+
+
 def test_checking_helpers(ns, cuda, oracle):
     a = oracle.generate_i32("random", 123457, 9)
     t = to_dev(a, cuda)
