@@ -558,6 +558,34 @@ def test_bench_multi_rank_code_path_on_one_gpu(exchange):
 
 
 @pytest.mark.slow
+def test_bench_single_gpu_line_contract():
+    """bench.py at N=1 on a small array: one JSON line with the keys the
+    driver reads (value, timing, roofline, byte model, e2e with its copy
+    bytes, launches, clocks, the base-case batch object) and a verified sort."""
+    import json
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run(["python", os.path.join(root, "bench.py"), "--steps", "2", "--warmup", "3",
+                        "--keys", str(1 << 24), "--no-cpu-baseline", "--no-size-sweep"],
+                       capture_output=True, text=True, timeout=600, cwd=root)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    line = json.loads(lines[0])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+              "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config",
+              "roofline", "byte_model", "e2e", "gpu_launches", "clocks", "base_case_batch"):
+        assert k in line, k
+    assert line["n_gpus"] == 1 and line["steps"] == 2 and line["warmup"] == 3
+    assert line["verified"] is True and line["value"] > 0 and line["gpu_launches"] > 0
+    assert line["roofline"]["bound"] == "hbm" and 0 < line["roofline"]["frac"] < 2
+    assert line["e2e"]["h2d_bytes_per_step"] == 4 << 24 == line["e2e"]["d2h_bytes_per_step"]
+    assert line["base_case_batch"]["verified"] is True
+    assert "workload" in line["config"]
+
+
+@pytest.mark.slow
 @pytest.mark.parametrize("kind", ["all_equal", "three_values", "reverse", "sawtooth", "int_max_heavy"])
 def test_adversarial_inputs_large(ns, cuda, kind):
     """2^26 keys of adversarial shapes through both algorithms: ties everywhere
