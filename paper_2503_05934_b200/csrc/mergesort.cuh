@@ -330,6 +330,15 @@ __device__ __forceinline__ void cta_sort_padded(const Key* in, Key* out, int val
 // the producer/loser loop they fit 64 registers without spills; measured
 // equal for the merge-sort tile and 8 % faster for the 16 M int64 quick-sort
 // bucket tiles (tools/i64_ab.sh)
+// Warp bitonic levels of the skewed tile sort: 4 = 16-lane runs and one more
+// shared-memory merge level than 5 (a warp run).  Measured (tools/ab_all.sh,
+// tools/i64_quick_ab.sh): int32 2^30 tile sort 7.72 -> 7.48 ms, segmented
+// 7.60 -> 7.47 ms; int64 2^28 tile sort 5.06 -> 4.57 ms, int64 16M quick-sort
+// buckets 538 -> 478 us (a bitonic level costs more ALU than a merge level
+// costs shared-memory wavefronts).
+#ifndef NSB_TS_WARP_LEVELS
+#define NSB_TS_WARP_LEVELS 4
+#endif
 #ifndef NSB_SKEW64_K16
 #define NSB_SKEW64_K16 1
 #endif
@@ -351,7 +360,7 @@ template <int NT, int K, class Key>
 __host__ __device__ constexpr int tile_smem_bytes() {
   constexpr int T = NT * K;
   constexpr int pw = padded_words<Key>(T);
-  constexpr int sw = T + (NT > 32 ? NT / 32 : 1) * skew_pad<K>() + 8;
+  constexpr int sw = T + (NT > 32 ? NT / (1 << NSB_TS_WARP_LEVELS) : 1) * skew_pad<K>() + 8;
   return (cta_sort_skewed<NT, K, Key>() && sw > pw ? sw : pw) * (int)sizeof(Key);
 }
 
@@ -379,7 +388,11 @@ __device__ __forceinline__ void cta_sort_skewed_body(const Key* in, Key* out, in
   smem_to_regs<K>(sm, v);
 
   thread_sort<LEAF>(v);  // the network base case (try_base_case, hybrid.hpp:48-56)
-  if constexpr (NT >= 32) warp_bitonic<5>(v, lane);
+  // NSB_TS_WARP_LEVELS bitonic levels: runs of 2^levels lanes (5: one run per
+  // warp; 4: one per half-warp and one more shared-memory level)
+  constexpr int WL = NT > 32 ? NSB_TS_WARP_LEVELS : 5;
+  static_assert(WL == 4 || WL == 5, "the merge levels take half-warp or warp runs");
+  if constexpr (NT >= 32) warp_bitonic<WL>(v, lane);
 
   if constexpr (NT <= 32) {
     __syncthreads();
@@ -398,9 +411,12 @@ __device__ __forceinline__ void cta_sort_skewed_body(const Key* in, Key* out, in
     constexpr int KB = (int)sizeof(Key);
     constexpr int KM = K + 1;
     const int warp = tid >> 5;
+    constexpr int L0 = K << WL;             // run length after the warp stage
+    constexpr int LPR = 1 << WL;            // lanes per run
     __syncthreads();  // every thread is done reading the padded tile
     {
-      Key* dst = sm + warp * (W + GAP) + K * lane;
+      const int run = (warp << (5 - WL)) + (lane >> WL);
+      Key* dst = sm + run * (L0 + GAP) + K * (lane & (LPR - 1));
 #pragma unroll
       for (int q = 0; q < K / PV; ++q) {
         Key e[PV];
@@ -408,7 +424,8 @@ __device__ __forceinline__ void cta_sort_skewed_body(const Key* in, Key* out, in
         for (int u = 0; u < PV; ++u) e[u] = v[q * PV + u];
         *reinterpret_cast<int4*>(dst + q * PV) = pack16<Key>(e);
       }
-      for (int i = lane; i < GAP; i += 32) sm[warp * (W + GAP) + W + i] = KeyT<Key>::kMax;
+      const int li = lane & (LPR - 1);
+      for (int i = li; i < GAP; i += LPR) sm[run * (L0 + GAP) + L0 + i] = KeyT<Key>::kMax;
     }
     __syncthreads();
     auto skew_of = [](int l) { return S == 2 * K ? ((l >> 1) & (K - 1)) : (l & (S - 1)); };
@@ -416,7 +433,7 @@ __device__ __forceinline__ void cta_sort_skewed_body(const Key* in, Key* out, in
     const int cnt = lane == 31 ? W - (K * 31 + skew_of(31)) : K + skew_of(lane + 1) - skew;
     const char* smc = reinterpret_cast<const char*>(sm);
 #pragma unroll 1
-    for (int R = W; R < T; R *= 2) {
+    for (int R = L0; R < T; R *= 2) {
       const int S = R + GAP, S2 = 2 * R + GAP;
       const int wpp = 2 * R / W;  // warps per output run
       const int p = warp / wpp, wi = warp - p * wpp;
