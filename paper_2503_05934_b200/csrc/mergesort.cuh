@@ -355,12 +355,25 @@ __host__ __device__ constexpr bool cta_sort_skewed() {
 template <int K>
 __host__ __device__ constexpr int skew_pad() { return K + 4; }
 
+// Bitonic levels of the skewed tile sort and its sentinel pad (see
+// cta_sort_skewed_body).
+template <int NT, int K, class Key>
+__host__ __device__ constexpr int ts_warp_levels() {
+  return NT <= 32 ? 5
+         : (NSB_TS_WARP_LEVELS >= 4 || 128 / (int)sizeof(Key) == K) ? NSB_TS_WARP_LEVELS
+                                                                      : 4;
+}
+template <int NT, int K, class Key>
+__host__ __device__ constexpr int ts_gap() {
+  return (ts_warp_levels<NT, K, Key>() == 3 && sizeof(Key) == 4) ? 48 : skew_pad<K>();
+}
+
 // Dynamic shared memory of a tile-sort CTA (either layout).
 template <int NT, int K, class Key>
 __host__ __device__ constexpr int tile_smem_bytes() {
   constexpr int T = NT * K;
   constexpr int pw = padded_words<Key>(T);
-  constexpr int sw = T + (NT > 32 ? NT / (1 << NSB_TS_WARP_LEVELS) : 1) * skew_pad<K>() + 8;
+  constexpr int sw = T + (NT > 32 ? (NT >> ts_warp_levels<NT, K, Key>()) : 1) * ts_gap<NT, K, Key>() + 8;
   return (cta_sort_skewed<NT, K, Key>() && sw > pw ? sw : pw) * (int)sizeof(Key);
 }
 
@@ -390,8 +403,10 @@ __device__ __forceinline__ void cta_sort_skewed_body(const Key* in, Key* out, in
   thread_sort<LEAF>(v);  // the network base case (try_base_case, hybrid.hpp:48-56)
   // NSB_TS_WARP_LEVELS bitonic levels: runs of 2^levels lanes (5: one run per
   // warp; 4: one per half-warp and one more shared-memory level)
-  constexpr int WL = NT > 32 ? NSB_TS_WARP_LEVELS : 5;
-  static_assert(WL == 4 || WL == 5, "the merge levels take half-warp or warp runs");
+  // 3 levels only where a bank row holds exactly K keys (int32 x 32, int64 x 16):
+  // the sub-warp merge level's skew pattern is proven for that shape alone
+  constexpr int WL = ts_warp_levels<NT, K, Key>();
+  static_assert(WL >= 3 && WL <= 5, "the merge levels take runs of 8, 16 or 32 lanes");
   if constexpr (NT >= 32) warp_bitonic<WL>(v, lane);
 
   if constexpr (NT <= 32) {
@@ -406,7 +421,11 @@ __device__ __forceinline__ void cta_sort_skewed_body(const Key* in, Key* out, in
     constexpr int S = 128 / (int)sizeof(Key);
     static_assert(S == 2 * K || S == K, "skew pattern needs 128/sizeof(Key) in {K, 2K}");
     constexpr int W = 32 * K;  // warp run
-    constexpr int GAP = skew_pad<K>();  // sentinels; keeps every run 16-byte aligned
+    // sentinels after every run; keeps every run 16-byte aligned.  With two
+    // output runs per warp (8-lane input runs, int32) the second run's
+    // stores must land 16 banks away from the first's: GAP = 16 (mod 32)
+    constexpr int GAP = ts_gap<NT, K, Key>();
+    static_assert(GAP >= K + 2 && GAP % 4 == 0, "sentinel pad");
     constexpr int PV = kpv<Key>();
     constexpr int KB = (int)sizeof(Key);
     constexpr int KM = K + 1;
@@ -429,15 +448,21 @@ __device__ __forceinline__ void cta_sort_skewed_body(const Key* in, Key* out, in
     }
     __syncthreads();
     auto skew_of = [](int l) { return S == 2 * K ? ((l >> 1) & (K - 1)) : (l & (S - 1)); };
-    const int skew = skew_of(lane);
-    const int cnt = lane == 31 ? W - (K * 31 + skew_of(31)) : K + skew_of(lane + 1) - skew;
     const char* smc = reinterpret_cast<const char*>(sm);
 #pragma unroll 1
     for (int R = L0; R < T; R *= 2) {
       const int S = R + GAP, S2 = 2 * R + GAP;
-      const int wpp = 2 * R / W;  // warps per output run
-      const int p = warp / wpp, wi = warp - p * wpp;
-      const int d = W * wi + K * lane + skew;
+      // G lanes per output run (a run of 2R keys; G = 32 and several warps
+      // per run once 2R >= W)
+      const int G = 2 * R / K < 32 ? 2 * R / K : 32;
+      const int li = lane & (G - 1);
+      const int RW = G * K;  // outputs of one lane group
+      const int skew = skew_of(li);
+      const int cnt = li == G - 1 ? RW - (K * (G - 1) + skew_of(G - 1)) : K + skew_of(li + 1) - skew;
+      const int wpp = G < 32 ? 1 : 2 * R / W;  // warps per output run
+      const int p = G < 32 ? warp * (32 / G) + (lane / G) : warp / wpp;
+      const int wi = G < 32 ? 0 : warp - p * wpp;
+      const int d = W * wi + K * li + skew;
       const int a_pos = 2 * p * S, b_pos = a_pos + S;
       const int a = merge_path<int>(sm + a_pos, R, sm + b_pos, R, d);
       // Producer/loser form of the merge: m is the head of the run that did
@@ -468,7 +493,7 @@ __device__ __forceinline__ void cta_sort_skewed_body(const Key* in, Key* out, in
       for (int k = 0; k < KM; ++k)
         if (k < cnt) o[k] = w[k];
       if (wi == 0)
-        for (int i = lane; i < GAP; i += 32) sm[p * S2 + 2 * R + i] = KeyT<Key>::kMax;
+        for (int i = li; i < GAP; i += G) sm[p * S2 + 2 * R + i] = KeyT<Key>::kMax;
       __syncthreads();
     }
     // the sorted tile is sm[0, T)
