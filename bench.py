@@ -1,29 +1,34 @@
 #!/usr/bin/env python
 """bench.py — B200 hybrid network-base-case sort, one JSON line on rank 0.
 
-Workload (BASELINE.json configs[4], the largest single-GPU configuration of
-the metric "sorted int32 Gkeys/s at n=10K-1G"): ONE uniform-random int32
-array of n = 2^30 keys (values int32(SplitMix64(42).next() >> 33), generated
-on the device, identical to the oracle's stream), sorted by merge sort with
-the 6To8 network base case.  At N = 1 that is the single-GPU merge sort of
-1 G keys; under torchrun with N > 1 the array is sharded evenly and sorted by
-the sample sort (local merge sort -> 255 regular samples per GPU -> NCCL
-all-gather + all-to-all -> g-way merge): total work fixed, scaling "strong".
+Headline workload (BASELINE.json configs[4], the largest single-GPU
+configuration of the metric "sorted int32 Gkeys/s at n=10K-1G"): ONE
+uniform-random int32 array of n = 2^30 keys (int32(SplitMix64(42).next() >>
+33), generated on the device), merge sort with the 6To8 network base case.
+Under torchrun with N > 1 the same array is sharded evenly and sample-sorted
+(local merge sort -> 255 regular samples per GPU -> splitters -> all-to-all
+over NVLink -> g-way merge): total work fixed, scaling "strong".
 
-  value  : n / (device time of the sort), inputs resident in HBM, CUDA events
-           on the launching stream, max over ranks; the input is restored by
-           an untimed device copy before every step (4 GiB >> 126 MB L2, so
-           no step sees a warm L2 for its input).
-  e2e    : the same metric through the public API with HOST buffers: pinned
-           int32 numpy array -> optimized_merge_sort(array, 6To8) (C ABI
-           ns_merge_sort_host_i32: H2D, sort, D2H, sync) timed by wall clock.
-  roofline: dominant kernel (merge_pass_kernel) — algorithmic bytes per
-           launch (8 B/key: read + write every key once) / its average launch
-           time from the library's own per-launch CUDA events, vs the measured
-           HBM copy bandwidth in MEASURED_PEAKS.json.
-  cpu_baseline: the reference itself (oracle/_ref, compiled from
-           /root/reference) — optimized_merge_sort<int32_t>(6To8) on one core,
-           on a 2^24-key sample of the same distribution.
+  value   : n / device time of the sort (CUDA events on the launching stream,
+            max over ranks), inputs resident in HBM; the input is restored by
+            an untimed D2D copy before every step (4 GiB >> 126 MB L2).
+  e2e     : the same metric through the public API with HOST buffers (pinned
+            numpy array -> optimized_merge_sort -> ns_merge_sort_host_i32:
+            H2D, sort, D2H, sync), wall clock.
+  roofline: the dominant kernel's algorithmic bytes per launch (8 B/key) over
+            its average launch time (the library's per-launch CUDA events),
+            vs the measured HBM bandwidth in MEASURED_PEAKS.json.
+  configs : every other BASELINE cell (configs[0..3]: MS 6To8 at 10K, 25K /
+            100K / 1M x random / sorted / nearly sorted, QS 3To5 at 10K / 1M /
+            16M x sorted / random, the 2^24-array base-case batch, the
+            65,536 x 16,384 segmented batch): device time, byte-model fraction,
+            verification against SHA-256 digests of the REFERENCE's own sorted
+            output (tests/golden/golden.json), e2e at 10K and 1M, and the
+            reference's time on ONE pinned core for the same input.
+  cpu_baseline / --impl reference: the reference itself (oracle/_ref, built
+            from /root/reference by oracle/Makefile) on one pinned core in a
+            child process (oracle/cpu_ref_bench.py), CPU time with the
+            reference harness's doubling-batch policy (bench.cpp:39-89).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 """
@@ -118,101 +123,89 @@ class Clocks:
 
 
 # ---------------------------------------------------------------------------
-# CPU baseline: the reference (oracle/_ref) or the C port (oracle)
+# CPU arm: the reference (oracle/_ref) on ONE pinned core, in a child process
+# (oracle/cpu_ref_bench.py: CLOCK_PROCESS_CPUTIME_ID, the reference harness's
+# doubling-batch policy restated at int32, bench.cpp:39-89)
 # ---------------------------------------------------------------------------
-def cpu_baseline(seconds: float = 10.0, n: int = 1 << 24):
-    import numpy as np
-    from oracle import oracle as O
-    a = O.generate_i32("random", n, SEED)
-    mask, vs = O.CONFIGS["6To8"]
-    if O.ref_available():
-        fn = lambda x: O.ref().ref_merge_sort_i32(x, len(x), mask, vs, None)  # noqa: E731
-        kind = "reference"
-    else:
-        fn = lambda x: O.lib().oracle_merge_sort_i32(x, 0, len(x) - 1, mask, vs, None)  # noqa
-        kind = "port"
-    times = []
-    t_total = time.perf_counter()
-    while True:
-        w = a.copy()
-        t0 = time.perf_counter()
-        fn(w)
-        times.append(time.perf_counter() - t0)
-        if time.perf_counter() - t_total > seconds or len(times) >= 8:
-            break
-    assert np.all(w[:-1] <= w[1:])
-    best = min(times)
-    return {"value": n / best / 1e9, "unit": "Gkeys/s", "cores": 1, "kind": kind,
-            "sample": f"optimized_merge_sort<int32_t>(6To8) on {n} uniform-random keys "
-                      f"(seed {SEED}), 1 thread, best of {len(times)} runs",
-            "cpu": _cpu_model()}
-
-
-def _cpu_model():
+def cpu_child(extra, timeout=900):
+    cmd = [sys.executable, os.path.join(ROOT, "oracle", "cpu_ref_bench.py")] + extra
     try:
-        with open("/proc/cpuinfo") as f:
-            for ln in f:
-                if ln.startswith("model name"):
-                    return ln.split(":", 1)[1].strip()
-    except Exception:
-        pass
-    return None
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, cwd=ROOT)
+        lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+        if r.returncode != 0 or not lines:
+            return {"unavailable": f"cpu_ref_bench rc={r.returncode}: {r.stderr[-300:]}"}
+        return json.loads(lines[-1])
+    except Exception as e:  # noqa: BLE001 - reported in the line
+        return {"unavailable": f"cpu_ref_bench failed: {e!r}"[:300]}
+
+
+HEADLINE_CPU_CELL = "merge:6To8:random:16777216"
+
+
+def cpu_baseline_from(cells):
+    """cpu_baseline object of the headline: the reference's merge sort 6To8 on
+    a 2^24-key uniform-random sample of the 2^30 workload, one pinned core."""
+    if "cells" not in cells or HEADLINE_CPU_CELL not in cells["cells"]:
+        return {"value": None, "unit": "Gkeys/s", "cores": 1, "kind": "reference",
+                "sample": "unavailable", "detail": cells.get("unavailable")}
+    c = cells["cells"][HEADLINE_CPU_CELL]
+    return {"value": c["gkeys_per_s"], "unit": "Gkeys/s", "cores": 1, "kind": "reference",
+            "sample": "optimized_merge_sort<int32_t>(6To8) from oracle/_ref (the reference "
+                      "compiled from its own sources) on a 2^24-key uniform-random sample "
+                      f"(seed {SEED}) of the 2^30 workload; {c['iterations']} timed call(s) "
+                      f"after one untimed warm-up, CPU time {c['cpu_ms']:.1f} ms per call "
+                      f"(wall {c['wall_ms']:.1f} ms); a 2^30 array would take ~27/21 of the "
+                      "per-key time (merge levels), so this overstates the CPU",
+            "core": cells.get("core"), "nproc": cells.get("nproc"), "cpu": cells.get("cpu"),
+            "clock": cells.get("clock")}
+
+
+def workload_config(n, world, exchange):
+    return {"workload": ("merge sort 6To8" if world == 1 else
+                         "sample sort (local merge sort 6To8 + " +
+                         ("pull-merge over NVLink peer memory)" if exchange == "p2p"
+                          else "NCCL all-to-all)")) +
+                        f", one uniform-random int32 array, n={n} (BASELINE configs[4])",
+            "n": n, "keys_per_gpu": n // world, "distribution": "uniform [0, 2^31), seed 42",
+            "parallelism": "shards over NCCL/NVLink" if world > 1 else "single GPU",
+            "l2": f"input {4 * n / 2**30:.2f} GiB vs 126 MB L2; restored by an untimed D2D "
+                  "copy before each step"}
 
 
 def run_reference(args, metric):
-    """--impl reference: the reference's CPU merge sort (oracle/_ref, else the
-    oracle port) on the host cores, one independent 2^22-key sample of the
-    workload's distribution per thread per step (the reference is
-    single-threaded per array, bench.hpp:53-57)."""
+    """--impl reference: the reference's own CPU merge sort (oracle/_ref) on
+    ONE pinned core — its path is single-threaded (bench.hpp:53-57) — each
+    step a 2^24-key uniform-random sample of the 2^30 workload, CPU time per
+    call.  An all-cores figure (independent arrays, one per core) is reported
+    beside it as all_cores_not_reference_path.  Under torchrun only rank 0
+    runs."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    import numpy as np
-    from oracle import oracle as O
-    O.build()
-    threads = len(os.sched_getaffinity(0))
-    m = 1 << 22
-    mask, vs = O.CONFIGS["6To8"]
-    if O.ref_available():
-        kind = "reference"
-        fn = lambda x: O.ref().ref_merge_sort_i32(x, len(x), mask, vs, None)  # noqa: E731
-    else:
-        kind = "port"
-        fn = lambda x: O.lib().oracle_merge_sort_i32(x, 0, len(x) - 1, mask, vs, None)  # noqa
-    pristine = [O.generate_i32("random", m, SEED + t) for t in range(threads)]
-    work = [p.copy() for p in pristine]
-
-    def step():
-        for w, p in zip(work, pristine):
-            np.copyto(w, p)
-        ths = [threading.Thread(target=fn, args=(w,)) for w in work]
-        t0 = time.perf_counter()
-        for t in ths:
-            t.start()
-        for t in ths:
-            t.join()
-        return time.perf_counter() - t0
-
-    for _ in range(args.warmup):
-        step()
-    dt = [step() for _ in range(args.steps)]
-    for w in work:
-        assert np.all(w[:-1] <= w[1:])
-    total = sum(dt)
-    v = threads * m * args.steps / total / 1e9
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    m = 1 << 24
+    r = cpu_child(["--steps", str(args.steps), "--warmup", str(args.warmup), "--n", str(m)],
+                  timeout=1800)
+    if "unavailable" in r:
+        print(json.dumps({"impl": "reference", "unavailable": r["unavailable"]}), flush=True)
+        return
+    ms = r["cpu_ms_per_step"]
+    v = m / (ms * 1e-3) / 1e9
     line = {"metric": metric, "value": v, "unit": "Gkeys/s", "impl": "reference",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": total / args.steps * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-            "config": {"workload": "merge sort 6To8, uniform-random int32 (BASELINE configs[4] "
-                                   "distribution), bounded CPU sample",
-                       "keys_per_thread_per_step": m, "threads": threads},
-            "cpu_baseline": {"value": v, "unit": "Gkeys/s", "cores": threads, "kind": kind,
-                             "sample": f"{threads} threads x optimized_merge_sort<int32_t>(6To8) "
-                                       f"on independent {m}-key arrays per step",
-                             "cpu": _cpu_model()},
+            "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+            "config": workload_config(args.n, world, args.exchange),
+            "cpu_baseline": {"value": v, "unit": "Gkeys/s", "cores": 1, "kind": "reference",
+                             "sample": f"each step: optimized_merge_sort<int32_t>(6To8) from "
+                                       f"oracle/_ref on a {m}-key uniform-random sample of the "
+                                       f"workload, one pinned core, CPU time "
+                                       f"(CLOCK_PROCESS_CPUTIME_ID), refill untimed",
+                             "core": r.get("core"), "nproc": r.get("nproc"), "cpu": r.get("cpu"),
+                             "wall_ms_per_step": r.get("wall_ms_per_step")},
             "e2e": {"value": v, "unit": "Gkeys/s", "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0}}
+                    "d2h_bytes_per_step": 0},
+            "all_cores_not_reference_path": r.get("all_cores")}
     print(json.dumps(line), flush=True)
 
 
@@ -284,10 +277,40 @@ def run_ours(args, metric):
         keys.copy_(pristine)
         out = step()
     torch.cuda.synchronize()
-    # correctness of the last warm-up step (size-independent properties)
+    # correctness of the last warm-up step (size-independent properties):
+    # every rank's slice sorted, the ranks' slices in order across rank
+    # boundaries, and the multiset of all output keys == that of all input
+    # keys (sum and xor of mix64(key), combined over ranks)
     local_ok = ns.count_inversions(out) == 0
+    d_out = ns.multiset_digest(out) if out.numel() else (0, 0)
     if world == 1:
-        local_ok = local_ok and ns.multiset_digest(out) == d_in
+        local_ok = local_ok and d_out == d_in
+    else:
+        import numpy as _np
+        cnt = out.numel()
+        mine = torch.tensor([cnt, int(out[0]) if cnt else 0, int(out[-1]) if cnt else 0,
+                             d_in[0] - 2**63, d_in[1] - 2**63, d_out[0] - 2**63,
+                             d_out[1] - 2**63], dtype=torch.int64)
+        parts = [torch.empty_like(mine) for _ in range(world)]
+        if dist.get_backend() == "gloo":
+            dist.all_gather(parts, mine)
+        else:
+            pd = [p.to(dev) for p in parts]
+            dist.all_gather(pd, mine.to(dev))
+            parts = [p.cpu() for p in pd]
+        rows = [[int(x) for x in p.tolist()] for p in parts]
+        u = lambda v: (v + 2**63) % 2**64  # noqa: E731
+        sin = sum(u(r[3]) for r in rows) % 2**64
+        sout = sum(u(r[5]) for r in rows) % 2**64
+        xin = xout = 0
+        for r in rows:
+            xin ^= u(r[4])
+            xout ^= u(r[6])
+        nonempty = [r for r in rows if r[0] > 0]
+        order_ok = all(a[2] <= b[1] for a, b in zip(nonempty, nonempty[1:]))
+        count_ok = sum(r[0] for r in rows) == n
+        local_ok = local_ok and sin == sout and xin == xout and order_ok and count_ok
+        del _np
 
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
@@ -428,75 +451,272 @@ def run_ours(args, metric):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "int32", "data": "synthetic",
-            "config": {"workload": ("merge sort 6To8" if world == 1 else
-                                    "sample sort (local merge sort 6To8 + " +
-                                    ("pull-merge over NVLink peer memory)"
-                                     if exchange["mode"] == "p2p" else "NCCL all-to-all)")) +
-                       f", one uniform-random int32 array, n={n} (BASELINE configs[4])",
-                       "n": n, "keys_per_gpu": m, "distribution": "uniform [0, 2^31), seed 42",
-                       "parallelism": "replicas/shards over NCCL" if world > 1 else "single GPU",
-                       "l2": f"input {4 * n / 2**30:.2f} GiB vs 126 MB L2; restored by an "
-                             "untimed D2D copy before each step"},
+            "config": workload_config(n, world, exchange["mode"]),
             "exchange": exchange if world > 1 else None,
             "gpu_launches": int(launches), "wall_ms_timed_region": wall * 1e3,
             "roofline": roofline, "byte_model": model, "kernel_profile": prof,
             "e2e": e2e, "clocks": clk, "verified": bool(ok.item())}
     if nvlink is not None:
         line["nvlink"] = nvlink
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline()
     if rank == 0 and world == 1 and not args.no_size_sweep:
         line["size_sweep"] = size_sweep(ns, L, dev, peak)
-    if rank == 0 and world == 1 and not args.no_batch:
-        line["base_case_batch"] = base_case_batch(ns, L, dev, peak)
+    if rank == 0 and world == 1 and not args.no_configs:
+        line["configs"] = all_configs(ns, L, dev, peak)
     if rank == 0 and world == 1 and args.extra:
         line["other_configs"] = other_configs(ns, L, dev)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cells = cpu_child(["--cells", "all"])
+        line["cpu_baseline"] = cpu_baseline_from(cells)
+        if "configs" in line:
+            attach_cpu(line["configs"], cells)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
 
 
-def base_case_batch(ns, L, dev, peak):
-    """BASELINE configs[1], the base-case kernel alone: 2^24 independent int32
-    arrays, lengths uniform in {3..8}, packed with a uint32 offsets array,
-    each sorted by its size-specific network.  Kernel time from the library's
-    own launch events (median of 7; the call adds one 4-byte validation
-    read-back), algorithmic bytes 8 per key + 4 per offset, checked against
-    the oracle (the checker only)."""
-    import ctypes as C
+# ---------------------------------------------------------------------------
+# BASELINE configs[0..3] (configs[4] is the headline): every cell timed on the
+# device, checked against the REFERENCE's own sorted output (SHA-256 digests in
+# tests/golden/golden.json, made from oracle/_ref by tests/golden/make_golden.py),
+# with its byte model and, after the CPU child has run, the reference's
+# 1-core time on the same input.
+# ---------------------------------------------------------------------------
+QS_GRAPH_SAFE = False     # quick sort synchronises per partition level (v1)
+BATCH_GRAPH_SAFE = False  # the batch call reads its validation flag back
+
+
+def _golden():
+    with open(os.path.join(ROOT, "tests", "golden", "golden.json")) as f:
+        return json.load(f)
+
+
+def _sha(a):
+    import hashlib
     import numpy as np
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def _profile(L, fn):
+    """Per-kind (device ms, launches) of one call, from the library's events."""
+    import ctypes as C
     import torch
     from paper_2503_05934_b200._lib import check
-    from oracle import oracle as O
-    offs, keys = O.generate_batch_i32(1 << 24, SEED)
-    k = torch.from_numpy(keys).to(dev)
-    o = torch.from_numpy(offs.view("int32")).to(dev)
-    w = k.clone()
-    ns.sort_small_batch(w, o)
-    ok = bool(np.array_equal(w.cpu().numpy(), O.sort_small_batch(keys, offs)))
+    torch.cuda.synchronize()
+    check(L.ns_profile_enable(1), "profile")
+    fn()
+    torch.cuda.synchronize()
+    out = {}
+    for k in range(L.ns_profile_kinds()):
+        t, c = C.c_double(), C.c_uint64()
+        check(L.ns_profile_read(k, C.byref(t), C.byref(c)), "profile read")
+        if c.value:
+            out[L.ns_profile_kind_name(k).decode()] = {"ms": t.value, "launches": c.value}
+    check(L.ns_profile_enable(0), "profile")
+    return out
+
+
+def device_ms(fn, restore, graph_safe, reps):
+    """Device time of one call: CUDA-graph replay of (restore; call) minus
+    replay of (restore) when the call is stream-ordered without host syncs,
+    else CUDA events around each call (host round trips inside the call are
+    then part of the time).  Median-free mean over `reps` replays."""
+    import statistics as st
+    import torch
+    for _ in range(3):
+        restore()
+        fn()
+    torch.cuda.synchronize()
+    if graph_safe:
+        out = []
+        for body in ((restore, fn), (restore,)):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                for f in body:
+                    f()
+            g.replay()
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            for _ in range(reps):
+                g.replay()
+            b.record()
+            torch.cuda.synchronize()
+            out.append(a.elapsed_time(b) / reps)
+            del g
+        return max(out[0] - out[1], 1e-6), "cuda-graph replay, restore copy subtracted"
     ts = []
-    for _ in range(7):
-        w.copy_(k)
+    for _ in range(reps):
+        restore()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
         torch.cuda.synchronize()
-        check(L.ns_profile_enable(1), "profile")
-        ns.sort_small_batch(w, o)
-        torch.cuda.synchronize()
-        tot = 0.0
-        for kind in range(L.ns_profile_kinds()):
-            t, c = C.c_double(), C.c_uint64()
-            check(L.ns_profile_read(kind, C.byref(t), C.byref(c)), "profile read")
-            tot += t.value
-        check(L.ns_profile_enable(0), "profile")
-        ts.append(tot)
-    ms = statistics.median(ts)
+        ts.append(a.elapsed_time(b))
+    return st.median(ts), "CUDA events per call (median; host round trips inside the call count)"
+
+
+def e2e_ms(fn_host, src, reps=20):
+    """The reference's call shape: a pageable host numpy array sorted in place
+    through the public API (H2D, sort, D2H, sync inside), wall clock, median."""
+    import statistics as st
+    import numpy as np
+    w = src.copy()
+    for _ in range(3):
+        np.copyto(w, src)
+        fn_host(w)
+    ts = []
+    for _ in range(reps):
+        np.copyto(w, src)
+        t0 = time.perf_counter()
+        fn_host(w)
+        ts.append((time.perf_counter() - t0) * 1e3)
+    return st.median(ts), w
+
+
+def all_configs(ns, L, dev, peak):
+    import numpy as np
+    import torch
+    gold = _golden()
+    gcase = {(c["algo"], c["config"], c["dist"], c["n"]): c["output_sha256"]
+             for c in gold["cases"]}
+    res = {}
+
+    def single(cell, algo, cfgname, dist, n, e2e=False):
+        a = ns.generate(dist, n, SEED)
+        d = torch.from_numpy(a).to(dev)
+        w = d.clone()
+        cfg = ns.find_config(cfgname)
+        sort = ns.optimized_merge_sort if algo == "merge" else ns.optimized_quick_sort
+        fn = lambda: sort(w, cfg)  # noqa: E731
+        restore = lambda: w.copy_(d)  # noqa: E731
+        reps = max(5, min(50, (1 << 26) // n))
+        ms, how = device_ms(fn, restore, algo == "merge" or QS_GRAPH_SAFE, reps)
+        restore()
+        prof = _profile(L, fn)
+        got = w.cpu().numpy()
+        rec = {"config": cfgname, "algorithm": algo, "dist": dist, "n": n, "device_ms": ms,
+               "timing": how, "gkeys_per_s": n / (ms * 1e-3) / 1e9,
+               "verified": _sha(got) == gcase.get((algo, cfgname, dist, n)),
+               "verified_against": "SHA-256 of the reference's sorted output (golden.json)",
+               "kernel_launches": int(sum(v["launches"] for v in prof.values())),
+               "kernel_profile": prof}
+        if algo == "merge":
+            passes = (prof.get("tile_sort", {}).get("launches", 0) +
+                      prof.get("merge_pass", {}).get("launches", 0))
+            nbytes = 8 * n * passes
+            rec["byte_model"] = f"8n x {passes} passes (tile sort + merge passes)"
+        else:
+            lv = prof.get("qs_count", {}).get("launches", 0)
+            nbytes = 12 * n * lv + 8 * n
+            rec["byte_model"] = (f"{lv} partition level(s) x (count 4n + scatter 8n) + "
+                                 "8n bucket sorts (upper bound: every level over all n keys)")
+        rec["model_bytes"] = nbytes
+        rec["hbm_frac"] = nbytes / (ms * 1e-3) / 1e9 / peak
+        rec["l2_resident"] = 8 * n < 100 * 2**20
+        if e2e:
+            host = ns.optimized_merge_sort if algo == "merge" else ns.optimized_quick_sort
+            ems, hw = e2e_ms(lambda x: host(x, cfg), a)
+            rec["e2e"] = {"ms": ems, "gkeys_per_s": n / (ems * 1e-3) / 1e9,
+                          "path": f"optimized_{algo}_sort(pageable numpy int32, {cfgname}) -> "
+                                  f"ns_{algo}_sort_host_i32", "h2d_bytes": 4 * n,
+                          "d2h_bytes": 4 * n, "verified": bool(np.array_equal(hw, got))}
+        res[cell] = rec
+        del d, w
+
+    single("merge:6To8:random:10000", "merge", "6To8", "random", 10_000, e2e=True)
+    for n in (25_000, 100_000, 1_000_000):
+        for dist in ("random", "sorted", "nearly_sorted"):
+            single(f"merge:6To8:{dist}:{n}", "merge", "6To8", dist, n,
+                   e2e=(n == 1_000_000 and dist == "random"))
+    for n in (10_000, 1_000_000, 16_777_216):
+        for dist in ("sorted", "random"):
+            single(f"quick:3To5:{dist}:{n}", "quick", "3To5", dist, n,
+                   e2e=(n <= 1_000_000))
+    torch.cuda.empty_cache()
+
+    # configs[1]: the base-case kernel alone, 2^24 ragged arrays
+    b = gold["batch"]
+    offs, keys = ns.generate_batch(1 << 24, SEED)
+    k = torch.from_numpy(keys).to(dev)
+    o = torch.from_numpy(offs.view(np.int32)).to(dev)
+    w = k.clone()
+    fn = lambda: ns.sort_small_batch(w, o)  # noqa: E731
+    restore = lambda: w.copy_(k)  # noqa: E731
+    ms, how = device_ms(fn, restore, BATCH_GRAPH_SAFE, 10)
+    restore()
+    prof = _profile(L, fn)
+    kms = prof.get("batch", {}).get("ms")
     nbytes = 8 * len(keys) + 4 * len(offs)
-    gbs = nbytes / (ms * 1e-3) / 1e9
-    return {"workload": "BASELINE configs[1]: 2^24 ragged int32 arrays, lengths U{3..8}, "
-                        "uint32 offsets, size-specific networks",
-            "num_arrays": 1 << 24, "num_keys": int(len(keys)), "kernel_ms": ms,
-            "gkeys_per_s": len(keys) / (ms * 1e-3) / 1e9, "bytes": nbytes,
-            "achieved_gbs": gbs, "peak_gbs": peak, "frac": gbs / peak, "verified": ok}
+    res["batch:6To8:random:16777216"] = {
+        "workload": "BASELINE configs[1]: 2^24 ragged int32 arrays, lengths U{3..8}, uint32 "
+                    "offsets, each sorted by its size-specific network",
+        "num_arrays": 1 << 24, "num_keys": int(len(keys)), "device_ms": ms, "timing": how,
+        "kernel_ms": kms, "gkeys_per_s": len(keys) / (ms * 1e-3) / 1e9, "model_bytes": nbytes,
+        "byte_model": "8 B per key (read + write) + 4 B per offset",
+        "hbm_frac": nbytes / (ms * 1e-3) / 1e9 / peak,
+        "kernel_hbm_frac": nbytes / (kms * 1e-3) / 1e9 / peak if kms else None,
+        "verified": _sha(w.cpu().numpy()) == b["output_sha256"],
+        "verified_against": "SHA-256 of the reference's sort_small output (golden.json)"}
+    del k, o, w
+    torch.cuda.empty_cache()
+
+    # configs[3] segmented: 65,536 x 16,384 uniform-random keys (one 2^30 stream)
+    g = gold["segmented"]
+    nseg, seg = g["full_num_segments"], g["seg_len"]
+    n = nseg * seg
+    src = torch.empty(n, dtype=torch.int32, device=dev)
+    from paper_2503_05934_b200._lib import check
+    check(L.ns_generate_i32(src.data_ptr(), n, 0, SEED, torch.cuda.current_stream().cuda_stream),
+          "generate")
+    w = src.clone()
+    cfg = ns.find_config(g["config"])
+    fn = lambda: ns.segmented_sort(w, seg, cfg, ns.Algorithm.quick_sort)  # noqa: E731
+    restore = lambda: w.copy_(src)  # noqa: E731
+    ms, how = device_ms(fn, restore, True, 5)
+    restore()
+    prof = _profile(L, fn)
+    pre = w[: g["num_segments_checked"] * seg].cpu().numpy()
+    v = w.view(nseg, seg)
+    seg_sorted = bool((v[:, 1:] >= v[:, :-1]).all().item())
+    ok = (_sha(pre) == g["output_prefix_sha256"] and seg_sorted and
+          ns.multiset_digest(w) == ns.multiset_digest(src))
+    res["segmented:3To5:65536x16384"] = {
+        "workload": "BASELINE configs[3] segmented batch: 65,536 independent uniform-random "
+                    "int32 arrays of 16,384 keys, quick sort 3To5 per segment",
+        "n": n, "device_ms": ms, "timing": how, "gkeys_per_s": n / (ms * 1e-3) / 1e9,
+        "model_bytes": 8 * n, "byte_model": "8n: one on-chip pass (read + write every key once)",
+        "hbm_frac": 8 * n / (ms * 1e-3) / 1e9 / peak, "kernel_profile": prof,
+        "verified": bool(ok),
+        "verified_against": "SHA-256 of the reference's output on the first 1,024 segments "
+                            "(golden.json) + every segment sorted + multiset digest"}
+    del src, w, v
+    ns.release_scratch()
+    torch.cuda.empty_cache()
+    return res
+
+
+def attach_cpu(configs, cells):
+    """Reference 1-core time per cell (same inputs) and the device speed-up."""
+    if "cells" not in cells:
+        return
+    for name, rec in configs.items():
+        key = name if name in cells["cells"] else name + ":1024"
+        c = cells["cells"].get(key)
+        if not c:
+            continue
+        cpu_ms = c["cpu_ms"]
+        keys_gpu = rec.get("n") or rec.get("num_keys")
+        if name.startswith("segmented"):  # 1,024 of the segments timed: per-key rate
+            cpu_ms = cpu_ms * keys_gpu / c["keys_per_call"]
+        rec["cpu_ref"] = {"ms": cpu_ms, "cores": 1, "kind": "reference",
+                          "iterations": c["iterations"], "wall_ms": c["wall_ms"]}
+        if c.get("note"):
+            rec["cpu_ref"]["note"] = c["note"]
+        rec["speedup_vs_ref_1core"] = cpu_ms / rec["device_ms"]
+        if "e2e" in rec:
+            rec["e2e"]["speedup_vs_ref_1core"] = cpu_ms / rec["e2e"]["ms"]
 
 
 def size_sweep(ns, L, dev, peak):
@@ -554,153 +774,48 @@ def size_sweep(ns, L, dev, peak):
 
 
 def other_configs(ns, L, dev):
-    """The other BASELINE configs.  Merge sort (no host round trip inside) is
-    timed as a CUDA-graph replay of the C-ABI call, i.e. pure device time with
-    the input restored inside the graph by a D2D copy whose own time is
-    subtracted; quick sort and the batch (one D2H read each by design) are
-    timed per call with CUDA events on the stream (host round trip included)
-    and also reported as the sum of their kernels' device time from the
-    library's per-launch events."""
-    import ctypes as C
+    """--extra: the §8(f) widenings — int64 keys (the reference's own benchmark
+    type, full 64-bit values) and the stable key-value sort."""
+    import numpy as np
     import torch
-    from paper_2503_05934_b200._lib import check
-    from oracle import oracle as O
+    peak = measured_peaks()[0]
     res = {}
-    s = torch.cuda.current_stream().cuda_stream
 
-    def kernel_ms(fn, restore):
-        restore()
-        fn()  # warm: lazy module loading and smem attributes stay out of the profile
-        restore()
-        torch.cuda.synchronize()
-        check(L.ns_profile_enable(1), "profile")
-        fn()
-        torch.cuda.synchronize()
-        tot = 0.0
-        for k in range(L.ns_profile_kinds()):
-            t, c = C.c_double(), C.c_uint64()
-            check(L.ns_profile_read(k, C.byref(t), C.byref(c)), "profile read")
-            tot += t.value
-        check(L.ns_profile_enable(0), "profile")
-        return tot
-
-    def call_ms(fn, restore, reps=10):
-        for _ in range(3):
-            restore()
-            fn()
-        ts = []
-        for _ in range(reps):
-            restore()
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record()
-            fn()
-            b.record()
-            torch.cuda.synchronize()
-            ts.append(a.elapsed_time(b))
-        return statistics.median(ts)
-
-    def graph_ms(fn, restore, reps=20):
-        for _ in range(3):
-            restore()
-            fn()
-        torch.cuda.synchronize()
-        g_full, g_copy = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g_full):
-            restore()
-            fn()
-        with torch.cuda.graph(g_copy):
-            restore()
-        out = []
-        for g in (g_full, g_copy):
-            g.replay()
-            torch.cuda.synchronize()
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record()
-            for _ in range(reps):
-                g.replay()
-            b.record()
-            torch.cuda.synchronize()
-            out.append(a.elapsed_time(b) / reps)
-        return max(out[0] - out[1], 1e-6)
-
-    def single(name, algo, cfgname, dist, n, key="i32"):
-        gen = O.generate_i32 if key == "i32" else O.generate_i64
-        a = torch.from_numpy(gen(dist, n, SEED)).to(dev)
+    def single(name, algo, n):
+        a = torch.from_numpy(ns.generate("random", n, SEED, dtype=np.int64)).to(dev)
         w = a.clone()
-        cfg = ns.find_config(cfgname)
-        fn = lambda: (ns.optimized_merge_sort if algo == "merge"  # noqa: E731
-                      else ns.optimized_quick_sort)(w, cfg)
+        cfg = ns.find_config("6To8" if algo == "merge" else "3To5")
+        sort = ns.optimized_merge_sort if algo == "merge" else ns.optimized_quick_sort
+        fn = lambda: sort(w, cfg)  # noqa: E731
         restore = lambda: w.copy_(a)  # noqa: E731
-        rec = {"n": n, "kernel_ms": kernel_ms(fn, restore), "call_ms": call_ms(fn, restore)}
-        if algo == "merge":
-            rec["graph_ms"] = graph_ms(fn, restore)
-            rec["gkeys_per_s"] = n / (rec["graph_ms"] * 1e-3) / 1e9
-        else:
-            rec["gkeys_per_s"] = n / (rec["call_ms"] * 1e-3) / 1e9
+        ms, how = device_ms(fn, restore, algo == "merge" or QS_GRAPH_SAFE, 5)
         w.copy_(a)
         fn()
-        rec["sorted"] = ns.count_inversions(w) == 0
-        if key == "i64":
-            rec["key"] = "int64 (the reference's own benchmark type, full 64-bit values)"
-            if algo == "merge" and n > (1 << 14):
-                # byte model: 16 B per key per pass (one tile pass + one pass
-                # per doubling from the 8192-key tile)
-                passes = 1 + max(0, (n - 1).bit_length() - 13)
-                rec["hbm_frac_all_passes"] = 16 * n * passes / (rec["graph_ms"] * 1e-3) / 1e9 \
-                    / measured_peaks()[0]
+        rec = {"n": n, "device_ms": ms, "timing": how, "gkeys_per_s": n / (ms * 1e-3) / 1e9,
+               "sorted": ns.count_inversions(w) == 0,
+               "key": "int64 (the reference's own benchmark type, full 64-bit values)"}
+        if algo == "merge" and n > (1 << 14):
+            passes = 1 + max(0, (n - 1).bit_length() - 13)
+            rec["hbm_frac_all_passes"] = 16 * n * passes / (ms * 1e-3) / 1e9 / peak
         res[name] = rec
+        del a, w
 
-    single("ms_6to8_random_10k", "merge", "6To8", "random", 10_000)
-    for n in (25_000, 100_000, 1_000_000):
-        for d in ("random", "sorted", "nearly_sorted"):
-            single(f"ms_6to8_{d}_{n}", "merge", "6To8", d, n)
-    for n in (10_000, 1_000_000, 16_777_216):
-        for d in ("sorted", "random"):
-            single(f"qs_3to5_{d}_{n}", "quick", "3To5", d, n)
-    # int64 keys (SURVEY.md §8(f) row 1)
     for n in (1_000_000, 1 << 28):
-        single(f"ms_6to8_random_i64_{n}", "merge", "6To8", "random", n, key="i64")
+        single(f"ms_6to8_random_i64_{n}", "merge", n)
     for n in (1_000_000, 16_777_216):
-        single(f"qs_3to5_random_i64_{n}", "quick", "3To5", "random", n, key="i64")
+        single(f"qs_3to5_random_i64_{n}", "quick", n)
     torch.cuda.empty_cache()
-    # stable key-value sort (int32 keys + 4-byte payload), SURVEY.md §8(f) row 4
     n = 1 << 26
-    kk = torch.from_numpy(O.generate_i32("random", n, SEED)).to(dev)
+    kk = torch.from_numpy(ns.generate("random", n, SEED)).to(dev)
     vv = torch.arange(n, dtype=torch.int32, device=dev)
     wk, wv = kk.clone(), vv.clone()
     fn = lambda: ns.sort_pairs(wk, wv)  # noqa: E731
     restore = lambda: (wk.copy_(kk), wv.copy_(vv))  # noqa: E731
-    ms = graph_ms(fn, restore, reps=5)
-    res["sort_pairs_i32_random_2^26"] = {"n": n, "graph_ms": ms,
+    ms, how = device_ms(fn, restore, True, 5)
+    res["sort_pairs_i32_random_2^26"] = {"n": n, "device_ms": ms, "timing": how,
                                          "gkeys_per_s": n / (ms * 1e-3) / 1e9}
     del kk, vv, wk, wv
     torch.cuda.empty_cache()
-    # base-case batch, 2^24 ragged arrays
-    offs, keys = O.generate_batch_i32(1 << 24, SEED)
-    k = torch.from_numpy(keys).to(dev)
-    o = torch.from_numpy(offs.view("int32")).to(dev)
-    w = k.clone()
-    fn = lambda: ns.sort_small_batch(w, o)  # noqa: E731
-    restore = lambda: w.copy_(k)  # noqa: E731
-    kms, cms = kernel_ms(fn, restore), call_ms(fn, restore)
-    nbytes = 8 * len(keys) + 4 * len(offs)
-    res["base_case_batch_2^24"] = {"num_arrays": 1 << 24, "num_keys": int(len(keys)),
-                                   "kernel_ms": kms, "call_ms": cms,
-                                   "gkeys_per_s": len(keys) / (cms * 1e-3) / 1e9,
-                                   "kernel_hbm_gbs": nbytes / (kms * 1e-3) / 1e9}
-    # segmented quick sort 65536 x 16384
-    n = 65536 * 16384
-    seg = torch.empty(n, dtype=torch.int32, device=dev)
-    check(L.ns_generate_i32(seg.data_ptr(), n, 0, SEED, s), "generate")
-    w = seg.clone()
-    cfg = ns.find_config("3To5")
-    fn = lambda: ns.segmented_sort(w, 16384, cfg, ns.Algorithm.quick_sort)  # noqa: E731
-    restore = lambda: w.copy_(seg)  # noqa: E731
-    ms = graph_ms(fn, restore, reps=5)
-    res["qs_3to5_segmented_65536x16384"] = {"n": n, "graph_ms": ms,
-                                            "gkeys_per_s": n / (ms * 1e-3) / 1e9,
-                                            "hbm_gbs": 8 * n / (ms * 1e-3) / 1e9}
-    del seg, w
     return res
 
 
@@ -714,8 +829,8 @@ def main():
                     help="total keys (--keys under torchrun: its parser claims --n)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--extra", action="store_true", help="also time the other BASELINE configs")
-    ap.add_argument("--no-batch", action="store_true",
-                    help="skip the base-case batch kernel (BASELINE configs[1]) object")
+    ap.add_argument("--no-configs", action="store_true",
+                    help="skip the per-config objects (BASELINE configs[0..3])")
     ap.add_argument("--no-size-sweep", action="store_true",
                     help="skip the n = 10K..256M merge-sort sweep (N=1 only)")
     ap.add_argument("--exchange", choices=["p2p", "nccl"], default="p2p",

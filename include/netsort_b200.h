@@ -209,6 +209,18 @@ int ns_count_inversions_i64(const int64_t* d_keys, size_t n, unsigned long long*
  * element (datagen.hpp:29-42 narrowed as in SURVEY.md §8(d)); kind 1 = the
  * ramp 0..n-1.  Identical to oracle_generate_i32 for the same (kind, seed). */
 int ns_generate_i32(int32_t* d_out, size_t n, int kind, uint64_t seed, void* stream);
+/* Host-side forms (datagen.cpp): kind 0 random, 1 sorted (ramp), 2 nearly
+ * sorted = the ramp after floor(p*n) seeded index-pair swaps (at least one
+ * when p > 0) — generate(), src/datagen.cpp:18-50, at int32 (random =
+ * int32(next() >> 33)) or at the reference's own int64 (random = next()).
+ * The ragged batch of BASELINE config 2: lengths 3 + next() % 6 from stream
+ * `seed`, keys int32(next() >> 33) from stream seed ^ 0x5bd1e995; writes
+ * num_arrays + 1 offsets and returns the key count (either pointer may be
+ * NULL to query it). */
+int ns_generate_host_i32(int32_t* h_out, size_t n, int kind, uint64_t seed, double p);
+int ns_generate_host_i64(int64_t* h_out, size_t n, int kind, uint64_t seed, double p);
+size_t ns_generate_batch_host_i32(size_t num_arrays, uint64_t seed, uint32_t* h_offsets,
+                                  int32_t* h_keys);
 
 /* ---- instrumentation ----------------------------------------------------
  * ns_launch_count: kernels this library has launched since load (process-

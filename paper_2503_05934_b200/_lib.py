@@ -67,6 +67,9 @@ SIGNATURES = {
     "ns_multiset_digest_i64": (_i32, [_vp, _sz, _vp, _vp]),
     "ns_count_inversions_i64": (_i32, [_vp, _sz, _vp, _vp]),
     "ns_generate_i32": (_i32, [_vp, _sz, _i32, C.c_uint64, _vp]),
+    "ns_generate_host_i32": (_i32, [_vp, _sz, _i32, C.c_uint64, C.c_double]),
+    "ns_generate_host_i64": (_i32, [_vp, _sz, _i32, C.c_uint64, C.c_double]),
+    "ns_generate_batch_host_i32": (_sz, [_sz, C.c_uint64, _vp, _vp]),
     "ns_launch_count": (C.c_uint64, []),
     "ns_profile_enable": (_i32, [_i32]),
     "ns_profile_kinds": (_i32, []),

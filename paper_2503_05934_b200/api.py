@@ -398,3 +398,32 @@ def count_inversions(keys) -> int:
                                                        out.data_ptr(), _stream_ptr(keys)),
           "count_inversions")
     return int(out.item())
+
+
+# ---- seeded inputs (generate, src/datagen.cpp:18-50) -------
+
+_DIST = {"random": 0, "sorted": 1, "nearly_sorted": 2}
+
+
+def generate(dist: str, n: int, seed: int = 42, p: float = 0.01, dtype=np.int32) -> np.ndarray:
+    """Host array of the reference's distributions: random (int32: next() >> 33,
+    int64: next()), sorted 0..n-1, nearly_sorted (ramp + floor(p*n) swaps)."""
+    if dist not in _DIST:
+        raise ValueError(f"unknown distribution {dist!r}")
+    a = np.empty(int(n), dtype=dtype)
+    sfx = "i64" if a.dtype == np.int64 else "i32"
+    check(getattr(lib(), f"ns_generate_host_{sfx}")(a.ctypes.data, a.size, _DIST[dist],
+                                                     int(seed) % 2**64, float(p)), "generate")
+    return a
+
+
+def generate_batch(num_arrays: int, seed: int = 42):
+    """(offsets uint32[num_arrays + 1], keys int32[K]) of the ragged base-case
+    batch (lengths U{3..8})."""
+    L = lib()
+    k = L.ns_generate_batch_host_i32(int(num_arrays), int(seed) % 2**64, None, None)
+    offs = np.empty(int(num_arrays) + 1, dtype=np.uint32)
+    keys = np.empty(int(k), dtype=np.int32)
+    L.ns_generate_batch_host_i32(int(num_arrays), int(seed) % 2**64, offs.ctypes.data,
+                                 keys.ctypes.data)
+    return offs, keys

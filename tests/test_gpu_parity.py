@@ -561,7 +561,8 @@ def test_bench_multi_rank_code_path_on_one_gpu(exchange):
 def test_bench_single_gpu_line_contract():
     """bench.py at N=1 on a small array: one JSON line with the keys the
     driver reads (value, timing, roofline, byte model, e2e with its copy
-    bytes, launches, clocks, the base-case batch object) and a verified sort."""
+    bytes, launches, clocks, every BASELINE config cell verified against the
+    reference's digests) and a verified sort."""
     import json
     import os
     import subprocess
@@ -575,13 +576,17 @@ def test_bench_single_gpu_line_contract():
     line = json.loads(lines[0])
     for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
               "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config",
-              "roofline", "byte_model", "e2e", "gpu_launches", "clocks", "base_case_batch"):
+              "roofline", "byte_model", "e2e", "gpu_launches", "clocks", "configs"):
         assert k in line, k
     assert line["n_gpus"] == 1 and line["steps"] == 2 and line["warmup"] == 3
     assert line["verified"] is True and line["value"] > 0 and line["gpu_launches"] > 0
     assert line["roofline"]["bound"] == "hbm" and 0 < line["roofline"]["frac"] < 2
     assert line["e2e"]["h2d_bytes_per_step"] == 4 << 24 == line["e2e"]["d2h_bytes_per_step"]
-    assert line["base_case_batch"]["verified"] is True
+    cells = line["configs"]
+    assert len(cells) == 18, sorted(cells)
+    for name, rec in cells.items():
+        assert rec["verified"] is True, name
+        assert rec["device_ms"] > 0 and rec["hbm_frac"] > 0, name
     assert "workload" in line["config"]
 
 

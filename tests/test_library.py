@@ -180,3 +180,28 @@ def test_merge_sort_dispatch_stats_match_reference(oracle):
     big = ns.merge_sort_dispatch_stats(1 << 24, ns.find_config("6To8"))
     assert big.network_hits[8] == 2_097_152 and big.max_depth == 22
     assert ns.merge_sort_dispatch_stats(0, ns.find_config("6To8")).max_depth == 0
+
+
+def test_host_generator_matches_oracle_and_golden(ns, oracle, golden):
+    """ns.generate / ns.generate_batch (the library's host generator, row
+    a19) reproduce the oracle's streams and the golden input digests (the
+    reference's datagen.cpp:18-50 narrowed to int32; int64 unnarrowed)."""
+    import hashlib
+    sha = lambda a: hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()  # noqa: E731
+    for dist in ("random", "sorted", "nearly_sorted"):
+        for n in (0, 1, 2, 3, 1000, 65537):
+            assert np.array_equal(ns.generate(dist, n, 42), oracle.generate_i32(dist, n, 42))
+            assert np.array_equal(ns.generate(dist, n, 7, dtype=np.int64),
+                                  oracle.generate_i64(dist, n, 7))
+    seen = 0
+    for c in golden["cases"]:
+        if c["n"] <= 1_000_000 and c["seed"] == 42:
+            assert sha(ns.generate(c["dist"], c["n"], c["seed"])) == c["input_sha256"], c
+            seen += 1
+    assert seen >= 14
+    offs, keys = ns.generate_batch(40, 7)
+    assert offs.tolist() == golden["small_batch"]["offsets"]
+    o2, k2 = oracle.generate_batch_i32(40, 7)
+    assert np.array_equal(keys, k2)
+    with pytest.raises(ValueError):
+        ns.generate("nearly_sorted", 10, 1, p=1.5)
