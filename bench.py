@@ -482,7 +482,7 @@ def run_ours(args, metric):
 # with its byte model and, after the CPU child has run, the reference's
 # 1-core time on the same input.
 # ---------------------------------------------------------------------------
-QS_GRAPH_SAFE = False     # quick sort synchronises per partition level (v1)
+QS_GRAPH_SAFE = True      # quick sort is planned on the device (no host sync)
 BATCH_GRAPH_SAFE = False  # the batch call reads its validation flag back
 
 

@@ -94,11 +94,12 @@ int ns_merge_sort_i64(int64_t* d_keys, size_t n, uint32_t width_mask, int varsor
                       void* d_temp, size_t temp_bytes, void* stream);
 
 /* optimized_quick_sort — include/netsort/hybrid.hpp:197-216.  GPU form: a
- * sampled-splitter partition (the many-pivot analogue of median_of_three +
- * hoare_partition, hybrid.hpp:105-133) recursing until buckets fit one CTA,
- * whose in-shared-memory sort uses the config's network base case.  May
- * synchronise `stream` once per partition level (bucket sizes drive the
- * launch plan, as the partition split drives the reference recursion). */
+ * sampled-pivot partition (the many-pivot analogue of median_of_three +
+ * hoare_partition, hybrid.hpp:105-133; up to 127 pivots per segment and
+ * level) recursing until buckets fit one CTA, whose on-chip sort uses the
+ * config's network base case.  Bucket sizes are planned ON THE DEVICE (work
+ * lists, upper-bound grids): the call never synchronises and can be captured
+ * in a CUDA graph.  n < 2^32 per array. */
 size_t ns_quick_sort_temp_bytes(size_t n);
 int ns_quick_sort_i32(int32_t* d_keys, size_t n, uint32_t width_mask, int varsort_max,
                       void* d_temp, size_t temp_bytes, void* stream);
@@ -135,7 +136,11 @@ int ns_argsort_i32(const int32_t* d_keys, uint32_t* d_perm, size_t n, void* d_te
 
 /* Segmented sort of num_segments independent arrays of seg_len keys each,
  * stored back to back (BASELINE config 4's 65,536 x 16,384 batch).  The
- * reference would run `algorithm` once per segment. */
+ * reference would run `algorithm` once per segment.  Segments of up to 16384
+ * keys are one CTA each; longer ones, with NS_QUICK_SORT, are all level-0
+ * segments of ONE device-planned partition (no per-segment host loop);
+ * NS_MERGE_SORT runs one stream-ordered merge sort per long segment.
+ * num_segments * seg_len overflowing is NS_ERR_INVALID. */
 size_t ns_segmented_sort_temp_bytes(size_t num_segments, size_t seg_len);
 int ns_segmented_sort_i32(int32_t* d_keys, size_t num_segments, size_t seg_len,
                           int algorithm, uint32_t width_mask, int varsort_max, void* d_temp,

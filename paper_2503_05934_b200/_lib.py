@@ -13,7 +13,9 @@ import os
 import subprocess
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "lib", "libnetsort_b200.so")
+# NETSORT_B200_LIB: an alternative build of the same library (A/B runs of a
+# compile-time variant, tools/build_variant.sh); the ABI is identical
+LIB_PATH = os.environ.get("NETSORT_B200_LIB") or os.path.join(PKG, "lib", "libnetsort_b200.so")
 CSRC = os.path.join(PKG, "csrc")
 
 NS_OK, NS_ERR_INVALID, NS_ERR_CUDA, NS_ERR_OOM, NS_ERR_TEMP = 0, 1, 2, 3, 4

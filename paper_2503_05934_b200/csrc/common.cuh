@@ -25,6 +25,7 @@ enum ProfKind {
   PK_QS_BUCKET,      // bucket_sort_kernel
   PK_PSRS,           // multi-GPU sample-sort helpers
   PK_CHECK,          // digest / inversions / generator
+  PK_QS_PLAN,        // quick-sort level planning (bucket positions, work lists)
   PK_NUM_KINDS
 };
 
@@ -143,5 +144,12 @@ int merge_existing_runs(int32_t* keys, int32_t* tmp, size_t n, int64_t R0, void*
 int merge_existing_runs(int64_t* keys, int64_t* tmp, size_t n, int64_t R0, void* d_temp,
                         cudaStream_t s, int64_t** result);
 constexpr int kSmallTile = 16384;  // largest array one CTA sorts on chip
+// quick sort of nseg back-to-back segments of len (> kSmallTile) keys each,
+// planned on the device (quicksort.cu)
+size_t quick_sort_segments_temp(size_t nseg, size_t len, size_t key_bytes);
+int quick_sort_segments_device(int32_t* keys, size_t nseg, size_t len, int leaf, void* d_temp,
+                               size_t temp_bytes, cudaStream_t s);
+int quick_sort_segments_device(int64_t* keys, size_t nseg, size_t len, int leaf, void* d_temp,
+                               size_t temp_bytes, cudaStream_t s);
 
 }  // namespace nsb

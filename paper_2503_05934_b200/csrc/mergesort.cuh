@@ -390,24 +390,43 @@ __device__ __forceinline__ void cta_sort(const Key* in, Key* out, int valid, Key
 }
 
 template <int NT, int K, int LEAF, class Key>
+__device__ __forceinline__ void cta_sort_regs(Key (&v)[K], Key* out, int valid, Key* sm);
+
+template <int NT, int K, int LEAF, class Key>
 __device__ __forceinline__ void cta_sort_skewed_body(const Key* in, Key* out, int valid, Key* sm) {
   constexpr int T = NT * K;
-  const int tid = threadIdx.x;
-  const int lane = tid & 31;
-
   tile_load<NT, T>(in, valid, sm);
   __syncthreads();
   Key v[K];
   smem_to_regs<K>(sm, v);
+  cta_sort_regs<NT, K, LEAF>(v, out, valid, sm);
+}
 
-  thread_sort<LEAF>(v);  // the network base case (try_base_case, hybrid.hpp:48-56)
-  // NSB_TS_WARP_LEVELS bitonic levels: runs of 2^levels lanes (5: one run per
-  // warp; 4: one per half-warp and one more shared-memory level)
-  // 3 levels only where a bank row holds exactly K keys (int32 x 32, int64 x 16):
-  // the sub-warp merge level's skew pattern is proven for that shape alone
+// The skewed tile sort from registers: thread t holds K of the tile's T keys
+// (any assignment — the result is the sorted multiset; pad with the key
+// maximum), `valid` keys are stored to out (nullptr: left in sm[0, T)).
+template <int NT, int K, int LEAF, class Key>
+__device__ __forceinline__ void cta_sort_regs(Key (&v)[K], Key* out, int valid, Key* sm) {
+  static_assert(cta_sort_skewed<NT, K, Key>(), "cta_sort_regs is the skewed layout");
+  constexpr int T = NT * K;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+
+  // Tile positions >= valid hold the key maximum at every stage (a sorted run
+  // keeps its pads at its end), so a warp whose keys are all padding skips the
+  // register stage and a lane whose outputs all lie at or past `valid` writes
+  // the maximum without merging: a partial tile costs about its valid keys.
+  const bool warp_pad = (tid & ~31) * K >= valid;
   constexpr int WL = ts_warp_levels<NT, K, Key>();
   static_assert(WL >= 3 && WL <= 5, "the merge levels take runs of 8, 16 or 32 lanes");
-  if constexpr (NT >= 32) warp_bitonic<WL>(v, lane);
+  if (!warp_pad) {
+    thread_sort<LEAF>(v);  // the network base case (try_base_case, hybrid.hpp:48-56)
+    // NSB_TS_WARP_LEVELS bitonic levels: runs of 2^levels lanes (5: one run per
+    // warp; 4: one per half-warp and one more shared-memory level)
+    // 3 levels only where a bank row holds exactly K keys (int32 x 32, int64 x 16):
+    // the sub-warp merge level's skew pattern is proven for that shape alone
+    if constexpr (NT >= 32) warp_bitonic<WL>(v, lane);
+  }
 
   if constexpr (NT <= 32) {
     __syncthreads();
@@ -464,6 +483,11 @@ __device__ __forceinline__ void cta_sort_skewed_body(const Key* in, Key* out, in
       const int wi = G < 32 ? 0 : warp - p * wpp;
       const int d = W * wi + K * li + skew;
       const int a_pos = 2 * p * S, b_pos = a_pos + S;
+      Key w[KM];
+      if (p * 2 * R + d >= valid) {  // every output of this lane is padding
+#pragma unroll
+        for (int k = 0; k < KM; ++k) w[k] = KeyT<Key>::kMax;
+      } else {
       const int a = merge_path<int>(sm + a_pos, R, sm + b_pos, R, d);
       // Producer/loser form of the merge: m is the head of the run that did
       // not emit the last key, ptr the next key of the run that did, mnext
@@ -476,7 +500,6 @@ __device__ __forceinline__ void cta_sort_skewed_body(const Key* in, Key* out, in
       uint32_t ptr = (uint32_t)(a_pos + a) * KB;
       uint32_t mnext = (uint32_t)(b_pos + d - a + 1) * KB;
       Key m = sm[b_pos + d - a];
-      Key w[KM];
 #pragma unroll
       for (int k = 0; k < KM; ++k) {
         const Key x = *reinterpret_cast<const Key*>(smc + ptr);
@@ -487,6 +510,7 @@ __device__ __forceinline__ void cta_sort_skewed_body(const Key* in, Key* out, in
         mnext = t ? mnext : q;
         m = t ? m : x;
       }
+      }
       __syncthreads();  // every thread is done reading this level's input
       Key* o = sm + p * S2 + d;
 #pragma unroll
@@ -496,7 +520,9 @@ __device__ __forceinline__ void cta_sort_skewed_body(const Key* in, Key* out, in
         for (int i = li; i < GAP; i += G) sm[p * S2 + 2 * R + i] = KeyT<Key>::kMax;
       __syncthreads();
     }
-    // the sorted tile is sm[0, T)
+    // the sorted tile is sm[0, T); out == nullptr leaves it there (the
+    // quick-sort splitter selection and big-bucket fallback read it on chip)
+    if (out == nullptr) return;
     if (valid == T && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
       fence_proxy_async_smem();
       __syncthreads();

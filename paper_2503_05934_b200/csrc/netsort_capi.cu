@@ -686,6 +686,35 @@ static int grid_for(int64_t n, int nt) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sms * 8));
 }
 
+// Segments of up to one CTA (16384 keys) are tile-sorted one CTA each; larger
+// segments go, all at once, through the quick sort's device-planned partition
+// (every segment is a level-0 segment of one batched launch sequence) or, for
+// the merge sort, through one merge sort per segment (stream-ordered).
+template <class Key>
+static size_t segmented_temp(size_t num_segments, size_t seg_len) {
+  if (seg_len <= (size_t)kSmT || num_segments == 0) return 0;
+  if (num_segments > SIZE_MAX / seg_len) return 0;
+  const size_t ms = sizeof(Key) == 4 ? merge_sort_temp(seg_len) : merge_sort_temp_i64(seg_len);
+  return std::max(ms, quick_sort_segments_temp(num_segments, seg_len, sizeof(Key)));
+}
+
+template <class Key>
+static int segmented_sort(Key* d_keys, size_t num_segments, size_t seg_len, int algorithm,
+                          uint32_t width_mask, int varsort_max, void* d_temp, size_t temp_bytes,
+                          cudaStream_t s) {
+  if (algorithm != NS_MERGE_SORT && algorithm != NS_QUICK_SORT) return NS_ERR_INVALID;
+  if (num_segments == 0 || seg_len <= 1) return NS_OK;
+  if (!d_keys) return NS_ERR_INVALID;
+  if (num_segments > (size_t)INT64_MAX / sizeof(Key) / seg_len) return NS_ERR_INVALID;
+  const int leaf = leaf_of(width_mask, varsort_max);
+  if (seg_len <= (size_t)kSmT) return tile_sort_segments_t(d_keys, num_segments, seg_len, leaf, s);
+  if (algorithm == NS_QUICK_SORT)
+    return quick_sort_segments_device(d_keys, num_segments, seg_len, leaf, d_temp, temp_bytes, s);
+  for (size_t g = 0; g < num_segments; ++g)
+    NSB_TRY(merge_sort_device(d_keys + g * seg_len, seg_len, leaf, d_temp, temp_bytes, s));
+  return NS_OK;
+}
+
 }  // namespace nsb
 
 using namespace nsb;
@@ -771,56 +800,25 @@ int ns_sort_small_batch_i32(int32_t* d_keys, const uint32_t* d_offsets, size_t n
 }
 
 size_t ns_segmented_sort_temp_bytes(size_t num_segments, size_t seg_len) {
-  (void)num_segments;
-  if (seg_len <= (size_t)kSmT) return 0;
-  return std::max(merge_sort_temp(seg_len), ns_quick_sort_temp_bytes(seg_len));
+  return segmented_temp<int32_t>(num_segments, seg_len);
 }
 
 int ns_segmented_sort_i32(int32_t* d_keys, size_t num_segments, size_t seg_len, int algorithm,
                           uint32_t width_mask, int varsort_max, void* d_temp,
                           size_t temp_bytes, void* stream) {
-  if (algorithm != NS_MERGE_SORT && algorithm != NS_QUICK_SORT) return NS_ERR_INVALID;
-  if (num_segments == 0 || seg_len <= 1) return NS_OK;
-  if (!d_keys) return NS_ERR_INVALID;
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const int leaf = leaf_of(width_mask, varsort_max);
-  if (seg_len <= (size_t)kSmT) return tile_sort_segments(d_keys, num_segments, seg_len, leaf, s);
-  // Segments larger than one CTA: one device sort per segment.
-  for (size_t g = 0; g < num_segments; ++g) {
-    int32_t* seg = d_keys + g * seg_len;
-    const int st = algorithm == NS_MERGE_SORT
-                       ? merge_sort_device(seg, seg_len, leaf, d_temp, temp_bytes, s)
-                       : ns_quick_sort_i32(seg, seg_len, width_mask, varsort_max, d_temp,
-                                           temp_bytes, stream);
-    if (st != NS_OK) return st;
-  }
-  return NS_OK;
+  return segmented_sort(d_keys, num_segments, seg_len, algorithm, width_mask, varsort_max, d_temp,
+                        temp_bytes, static_cast<cudaStream_t>(stream));
 }
 
 size_t ns_segmented_sort_temp_bytes_i64(size_t num_segments, size_t seg_len) {
-  (void)num_segments;
-  if (seg_len <= (size_t)kSmT) return 0;
-  return std::max(merge_sort_temp_i64(seg_len), ns_quick_sort_temp_bytes_i64(seg_len));
+  return segmented_temp<int64_t>(num_segments, seg_len);
 }
 
 int ns_segmented_sort_i64(int64_t* d_keys, size_t num_segments, size_t seg_len, int algorithm,
                           uint32_t width_mask, int varsort_max, void* d_temp,
                           size_t temp_bytes, void* stream) {
-  if (algorithm != NS_MERGE_SORT && algorithm != NS_QUICK_SORT) return NS_ERR_INVALID;
-  if (num_segments == 0 || seg_len <= 1) return NS_OK;
-  if (!d_keys) return NS_ERR_INVALID;
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const int leaf = leaf_of(width_mask, varsort_max);
-  if (seg_len <= (size_t)kSmT) return tile_sort_segments_t(d_keys, num_segments, seg_len, leaf, s);
-  for (size_t g = 0; g < num_segments; ++g) {
-    int64_t* seg = d_keys + g * seg_len;
-    const int st = algorithm == NS_MERGE_SORT
-                       ? merge_sort_device(seg, seg_len, leaf, d_temp, temp_bytes, s)
-                       : ns_quick_sort_i64(seg, seg_len, width_mask, varsort_max, d_temp,
-                                           temp_bytes, stream);
-    if (st != NS_OK) return st;
-  }
-  return NS_OK;
+  return segmented_sort(d_keys, num_segments, seg_len, algorithm, width_mask, varsort_max, d_temp,
+                        temp_bytes, static_cast<cudaStream_t>(stream));
 }
 
 int ns_multiset_digest_i32(const int32_t* d_keys, size_t n, uint64_t* d_out, void* stream) {

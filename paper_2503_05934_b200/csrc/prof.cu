@@ -97,7 +97,8 @@ static void prof_clear() {
 
 static const char* kKindNames[PK_NUM_KINDS] = {
     "tile_sort", "merge_partition", "merge_pass", "sort_small_batch", "qs_sample",
-    "qs_count",  "qs_scatter",      "qs_bucket_sort", "psrs",         "check"};
+    "qs_count",  "qs_scatter",      "qs_bucket_sort", "psrs",         "check",
+    "qs_plan"};
 
 // SplitMix64 output i of a stream seeded with `seed` is mix(seed + (i+1)*gamma)
 // (include/netsort/datagen.hpp:33-38), so the stream is counter-based and the

@@ -1,32 +1,48 @@
-// quicksort.cu — the quick-sort layer on sm_100a.
+// quicksort.cu — the quick-sort layer on sm_100a, planned entirely on the
+// device (no host round trip, so ns_quick_sort_* is stream-ordered and can
+// be captured in a CUDA graph).
 //
 // Replaces /root/reference/proj/include/netsort/hybrid.hpp:105-150
 // (median_of_three + hoare_partition + quick_sort_rec).  A single pivot and
-// a two-cursor scan are inherently sequential, so the GPU partition step uses
-// B-1 sampled splitters at once (a many-pivot quick sort, i.e. sample sort):
-//   1. sample_kernel      : S = 16*B regularly spaced (jittered) keys;
-//   2. the samples are sorted on chip and B-1 splitters picked at regular
-//      ranks (the many-pivot analogue of median-of-three: a pivot is a
-//      sample median, so sorted input still splits evenly);
-//   3. count_kernel       : every key is classified into one of 2B-1 buckets
-//      — "between" buckets (s[j-1] < k < s[j]) and "equal" buckets (k ==
-//      s[j]); equal buckets are constant, which keeps heavy duplicates from
-//      unbalancing the recursion (the job hoare_partition's j==high fix-up
-//      does for a single pivot, hybrid.hpp:130);
-//   4. scatter_kernel     : keys move to their bucket (warp-aggregated
-//      atomics reserve slots);
-//   5. bucket_sort_kernel : every bucket that fits one CTA is sorted on chip
-//      by cta_sort with the config's network base case (try_base_case,
-//      hybrid.hpp:48-56); larger buckets recurse (quick_sort_rec).
+// a two-cursor scan are inherently sequential, so one GPU partition level
+// uses up to 255 sampled pivots at once (a many-pivot quick sort, i.e. a
+// sample sort) on every oversized segment of the level:
+//   sample  : one CTA per segment draws 16 jittered, regularly spaced samples
+//             per bucket, sorts them on chip with the tile sort and keeps
+//             every 16th as a pivot (the many-pivot analogue of
+//             median_of_three: sorted input still splits evenly);
+//   count   : every key is classified into 2B-1 buckets — "between" buckets
+//             (s[j-1] < k < s[j]) and "equal" buckets (k == s[j]); an equal
+//             bucket is constant, which keeps heavy duplicates from
+//             unbalancing the recursion (the job of hoare_partition's j==high
+//             fix-up for one pivot, hybrid.hpp:130);
+//   plan    : one CTA per segment scans its bucket counts into positions and
+//             sorts the buckets out: the ones that fit a CTA become leaf jobs
+//             (neighbouring small buckets packed into one tile, since they
+//             hold disjoint ascending key ranges), large constant buckets are
+//             already sorted, large between buckets become the next level's
+//             segments (quick_sort_rec's two recursive calls, hybrid.hpp:
+//             145-148), appended to device-side work lists;
+//   scatter : keys move to their buckets through a shared-memory multisplit,
+//             so each bucket's keys leave a CTA as one contiguous run
+//             (coalesced stores) at a range reserved with one global atomic
+//             per (CTA, bucket).
+// The number of levels follows from n alone (each level divides a segment by
+// up to 256); after the last level every leaf job is sorted on chip by
+// cta_sort with the config's network base case (try_base_case,
+// hybrid.hpp:48-56).  Launch grids are upper bounds and every kernel walks
+// the device-side lists, so the host never reads a count.  A segment still
+// larger than one CTA after the last level (only possible for adversarial
+// sampling) is sorted by one CTA in global memory — correct, just slow.
 // Parity with the reference is on the sorted bytes, which are unique.
 #include <cuda_runtime.h>
 
 #include <algorithm>
-#include <cstdlib>
-#include <utility>
 #include <climits>
 #include <cstdint>
+#include <mutex>
 #include <type_traits>
+#include <utility>
 #include <vector>
 
 #include "common.cuh"
@@ -34,52 +50,103 @@
 
 namespace nsb {
 
-constexpr int kQsMaxB = 4096;        // splitter slots (B-1 used, last is +inf pad)
-#ifndef NSB_QS_OVERSAMPLE
-#define NSB_QS_OVERSAMPLE 16
-#endif
-constexpr int kQsOversample = NSB_QS_OVERSAMPLE;  // samples per bucket
-constexpr int kQsTarget = 4096;      // target mean bucket size
-constexpr int kQsNT = 512;
-constexpr int kQsChunk = kQsNT * 32;  // keys per CTA in count / scatter
-constexpr int kQsLut = 4096;          // prefix table slots
+constexpr int kQsNT = 512;                   // count / scatter / plan threads
+constexpr int kQsPer = 16;                   // keys per thread in count / scatter
+constexpr int kQsChunk = kQsNT * kQsPer;     // keys per chunk (one CTA iteration)
+constexpr int kQsMaxB = 128;                 // pivot slots per segment (B-1 real + pad):
+                                             // 2B-1 <= 255 buckets, so a bucket id is one byte
+constexpr int kQsOver = 16;                  // samples per bucket
+constexpr int64_t kQsTarget = 4096;          // mean bucket size a level aims for
 
-struct QsAux {  // carved from the caller's scratch, after the n-key buffer
-  int32_t* samples;     // kQsMaxB * kQsOversample
-  void* sample_temp;    // merge_sort_temp(samples)
-  size_t sample_temp_bytes;
-  int32_t* splitters;   // kQsMaxB
-  uint32_t* totals;     // 2*kQsMaxB
-  unsigned long long* fill;  // 2*kQsMaxB
-  int64_t* jobs;        // 2 * 2*kQsMaxB
-  int16_t* lut;         // kQsLut + 1 entries + {base, shift} header
-};
-
-static size_t qs_aux_bytes() {
-  const size_t S = (size_t)kQsMaxB * kQsOversample;
-  return align_up(S * 4, 256) + align_up(merge_sort_temp(S), 256) + align_up(kQsMaxB * 4, 256) +
-         align_up(2 * kQsMaxB * 4, 256) + align_up(2 * kQsMaxB * 8, 256) +
-         align_up(4 * kQsMaxB * 8, 256) + align_up((kQsLut + 1) * 2 + 16, 256);
+// Buckets a segment of len keys is split into: the smallest power of two
+// B >= 2 with B * kQsTarget >= len, at most kQsMaxB.
+__host__ __device__ inline int qs_buckets(int64_t len) {
+  int B = 2;
+  while (B < kQsMaxB && (int64_t)B * kQsTarget < len) B <<= 1;
+  return B;
 }
 
-static QsAux carve_aux(char* p) {
-  QsAux a;
-  const size_t S = (size_t)kQsMaxB * kQsOversample;
-  a.samples = reinterpret_cast<int32_t*>(p);
-  p += align_up(S * 4, 256);
-  a.sample_temp = p;
-  a.sample_temp_bytes = merge_sort_temp(S);
-  p += align_up(a.sample_temp_bytes, 256);
-  a.splitters = reinterpret_cast<int32_t*>(p);
-  p += align_up(kQsMaxB * 4, 256);
-  a.totals = reinterpret_cast<uint32_t*>(p);
-  p += align_up(2 * kQsMaxB * 4, 256);
-  a.fill = reinterpret_cast<unsigned long long*>(p);
-  p += align_up(2 * kQsMaxB * 8, 256);
-  a.jobs = reinterpret_cast<int64_t*>(p);
-  p += align_up(4 * kQsMaxB * 8, 256);
-  a.lut = reinterpret_cast<int16_t*>(p);
-  return a;
+// Partition levels for segments of len keys: expected bucket size after
+// each level, until it fits one CTA.
+static int qs_levels(int64_t len) {
+  int levels = 0;
+  for (int64_t s = len; s > kSmallTile / 2; s /= qs_buckets(s)) ++levels;
+  return std::max(levels, 1);
+}
+
+struct QsSeg {
+  int64_t start, len;
+  int64_t chunk0;   // first chunk of this segment in its level's chunk list
+  int64_t cnt_off;  // first bucket counter (2B-1 of them)
+  int64_t spl_off;  // first pivot slot (B of them)
+  int32_t B, nchunks;
+};
+
+struct QsJob {
+  int64_t start, len;
+  int32_t flags;  // bit 0: source is tmp; bits 1-2: 0 sort, 1 copy, 2 big
+  int32_t pad;
+};
+enum { kJobSort = 0, kJobCopy = 1, kJobBig = 2 };
+
+struct QsCounters {  // device-side list lengths
+  unsigned long long nseg[2], nchunk[2], nbkt[2], nspl[2];
+  unsigned long long njobs[3];
+};
+
+template <class Key>
+struct QsCtx {
+  Key* keys;
+  Key* tmp;
+  int64_t n;
+  // level 0: nseg0 uniform segments of len0 keys (no list: arithmetic)
+  int64_t nseg0, len0, cps0;
+  int32_t B0;
+  QsCounters* ctr;
+  QsSeg* segs[2];
+  int32_t* chunk_seg[2];
+  Key* spl[2];
+  uint16_t* cells[2];  // 16 per pivot slot: the classifier's prefix cells
+  uint8_t* ids;        // bucket id of every key of the level (count -> scatter)
+  uint32_t* cnt[2];
+  unsigned long long* fill[2];  // bucket write cursors (absolute positions)
+  QsJob* jobs[3];
+  int64_t max_segs, max_chunks, max_bkt, max_spl, max_jobs;
+};
+
+// ---- level geometry (device) ----------------------------------------------
+template <class Key>
+__device__ __forceinline__ QsSeg qs_seg(const QsCtx<Key>& c, int level, int64_t s) {
+  if (level == 0) {
+    QsSeg g;
+    g.start = s * c.len0;
+    g.len = c.len0;
+    g.B = c.B0;
+    g.nchunks = (int32_t)c.cps0;
+    g.chunk0 = s * c.cps0;
+    g.cnt_off = s * (2 * c.B0 - 1);
+    g.spl_off = s * c.B0;
+    return g;
+  }
+  return c.segs[level & 1][s];
+}
+template <class Key>
+__device__ __forceinline__ int64_t qs_nseg(const QsCtx<Key>& c, int level) {
+  return level == 0 ? c.nseg0 : (int64_t)*(volatile unsigned long long*)&c.ctr->nseg[level & 1];
+}
+template <class Key>
+__device__ __forceinline__ int64_t qs_nchunk(const QsCtx<Key>& c, int level) {
+  return level == 0 ? c.nseg0 * c.cps0
+                    : (int64_t)*(volatile unsigned long long*)&c.ctr->nchunk[level & 1];
+}
+template <class Key>
+__device__ __forceinline__ int64_t qs_seg_of_chunk(const QsCtx<Key>& c, int level, int64_t ch) {
+  return level == 0 ? ch / c.cps0 : (int64_t)c.chunk_seg[level & 1][ch];
+}
+// keys of level l live in X_l: the caller's buffer at even levels, tmp at odd
+template <class Key>
+__device__ __forceinline__ Key* qs_src(const QsCtx<Key>& c, int level) {
+  return (level & 1) ? c.tmp : c.keys;
 }
 
 __device__ __forceinline__ uint32_t hash32(uint32_t x) {
@@ -91,848 +158,895 @@ __device__ __forceinline__ uint32_t hash32(uint32_t x) {
   return x;
 }
 
-__global__ void sample_kernel(const int32_t* __restrict__ keys, int64_t n, int S,
-                              int32_t* __restrict__ samples) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= S) return;
-  const int64_t stride = n / S;
-  const int64_t pos = (int64_t)i * stride + (stride > 1 ? hash32((uint32_t)i) % stride : 0);
-  samples[i] = keys[pos];
+// ---- 1. sample + pivots -----------------------------------------------------
+// Sample i of a segment sits at i*stride + jitter(i) (stride = len / S), so
+// sorted input still yields evenly spaced pivots.
+__device__ __forceinline__ int64_t qs_sample_pos(int i, int64_t stride, int level) {
+  return (int64_t)i * stride +
+         (stride > 1 ? (int64_t)(hash32((uint32_t)i * 2654435761u + (uint32_t)level) %
+                                 (uint64_t)stride)
+                     : 0);
 }
 
-// spl[j] = samples[(j+1)*S/B - 1] for j < B-1; spl[B-1] = INT_MAX (pad).
-__global__ void splitter_kernel(const int32_t* __restrict__ samples, int S, int B,
-                                int32_t* __restrict__ spl) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= B) return;
-  spl[j] = j < B - 1 ? samples[(int64_t)(j + 1) * S / B - 1] : INT_MAX;
-}
-
-// Prefix lookup table that shortcuts the splitter search: keys are bucketed
-// by (key - base) >> shift into kQsLut slots spanning [spl[0], spl[B-2]];
-// lut[p] = number of splitters < base + (p << shift).  A key's lower_bound
-// then lies in [lut[p], lut[p+1]] (p < kQsLut-1) — usually 0..2 candidates —
-// instead of needing log2(B) dependent shared-memory loads.  Layout in global:
-// int32 header {base, shift} then kQsLut+1 int16 entries.
-__global__ void lut_kernel(const int32_t* __restrict__ spl, int B, int16_t* __restrict__ lut) {
-  const int p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p > kQsLut) return;
-  const int32_t base = spl[0];
-  const int64_t span = (int64_t)spl[max(B - 2, 0)] - base + 1;
+// The classifier's prefix cells (see "classification" below): the pivots'
+// key range [lo, hi] = [piv[0], piv[B-2]] cut into 16 B cells of 2^shift keys.
+template <class Key>
+__device__ __forceinline__ int qs_cell_shift(Key lo, Key hi, int ncell) {
+  using U = std::make_unsigned_t<Key>;
+  const U span = (U)hi - (U)lo;
   int shift = 0;
-  while ((span >> shift) > kQsLut) ++shift;
-  if (p == 0) {
-    int32_t* hdr = reinterpret_cast<int32_t*>(lut);
-    hdr[0] = base;
-    hdr[1] = shift;
-  }
-  const int64_t bound = (int64_t)base + ((int64_t)p << shift);
-  int lo = 0, hi = B - 1;  // lower_bound over the B-1 real splitters
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if ((int64_t)spl[mid] < bound) lo = mid + 1;
-    else hi = mid;
-  }
-  lut[8 + p] = (int16_t)lo;
+  while ((span >> shift) >= (U)ncell) ++shift;
+  return shift;
+}
+template <class Key>
+__device__ __forceinline__ int qs_cell_of(Key p, Key lo, int shift, int ncell) {
+  using U = std::make_unsigned_t<Key>;
+  const U cidx = ((U)p - (U)lo) >> shift;
+  return cidx < (U)ncell ? (int)cidx : ncell - 1;
 }
 
-struct Classifier {
-  const int32_t* spl;  // smem, B entries (spl[B-1] = +inf pad)
-  const int16_t* lut;  // smem, kQsLut+1 entries
-  int B;
-  int32_t base;
-  int shift;
-  // equal/between bucket id in [0, 2B-1)
-  __device__ __forceinline__ int operator()(int32_t key) const {
-    const int64_t d = (int64_t)key - base;
-    int lo, hi;
-    if (d < 0) {
-      lo = hi = 0;
-    } else {
-      const int64_t pp = d >> shift;
-      if (pp >= kQsLut - 1) {
-        lo = lut[kQsLut - 1];
-        hi = B - 1;
-      } else {
-        lo = lut[pp];
-        hi = lut[pp + 1];
+// Pivot j of S = 16 B sorted samples is sample 16 (j+1) - 1; slot B-1 is the
+// key-maximum pad.  Also clears the segment's bucket counters.
+template <class Key>
+__device__ __forceinline__ void qs_write_pivots_zero(const QsCtx<Key>& c, int level, const QsSeg& g,
+                                                     int i, int stride) {
+  uint32_t* cnt = c.cnt[level & 1] + g.cnt_off;
+  for (int b = i; b < 2 * g.B - 1; b += stride) cnt[b] = 0;
+}
+
+template <class Key>
+__global__ void __launch_bounds__(256) qs_sample_kernel(QsCtx<Key> c, int level) {
+  __shared__ Key sub[512];
+  __shared__ Key piv[kQsMaxB];
+  __shared__ uint32_t ccount[16 * kQsMaxB];
+  __shared__ uint32_t wsum[8];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (blockIdx.x == 0 && tid == 0) {
+    // the next level's lists are appended by this level's plan kernel
+    const int nx = (level + 1) & 1;
+    c.ctr->nseg[nx] = 0;
+    c.ctr->nchunk[nx] = 0;
+    c.ctr->nbkt[nx] = 0;
+    c.ctr->nspl[nx] = 0;
+    if (level == 0) c.ctr->njobs[0] = c.ctr->njobs[1] = c.ctr->njobs[2] = 0;
+  }
+  const Key* X = qs_src(c, level);
+  Key* splb = c.spl[level & 1];
+  const int64_t nseg = qs_nseg(c, level);
+  for (int64_t base = (int64_t)blockIdx.x * 8; base < nseg; base += (int64_t)gridDim.x * 8) {
+    // segments of B <= 32 pivots (S <= 512 samples): one warp each, sorted in
+    // registers (16 per lane, network base case + warp bitonic stage)
+    const int64_t s = base + warp;
+    if (s < nseg) {
+      const QsSeg g = qs_seg(c, level, s);
+      if (g.B <= 32) {
+        const int S = kQsOver * g.B;
+        const int64_t stride = g.len / S;
+        Key v[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          const int i = lane * 16 + u;
+          v[u] = i < S ? X[g.start + qs_sample_pos(i, stride, level)] : KeyT<Key>::kMax;
+        }
+        thread_sort<8>(v);
+        warp_bitonic<5>(v, lane);
+        // lane l holds sorted samples [16 l, 16 l + 16): pivot j is lane j's last
+        if (lane < g.B) splb[g.spl_off + lane] = lane < g.B - 1 ? v[15] : KeyT<Key>::kMax;
+        qs_write_pivots_zero(c, level, g, lane, 32);
+        // prefix cells: j0(c) = #pivots whose cell < c (cells of the sorted
+        // pivots are non-decreasing: a 5-step shuffle search), k = j0(c+1) - j0(c)
+        const Key lo = __shfl_sync(kFull, v[15], 0), hi = __shfl_sync(kFull, v[15], g.B - 2);
+        const int ncell = 16 * g.B;
+        const int shift = qs_cell_shift(lo, hi, ncell);
+        const int cj = lane < g.B - 1 ? qs_cell_of(v[15], lo, shift, ncell) : ncell;
+        uint16_t* cells = c.cells[level & 1] + 16 * g.spl_off;
+        for (int c0 = 0; c0 < ncell; c0 += 32) {
+          const int cc = c0 + lane;
+          auto j0_of = [&](int x) {
+            int l = 0, h = g.B - 1;
+#pragma unroll
+            for (int it = 0; it < 5; ++it) {
+              const int m = (l + h) >> 1;
+              const int cm = __shfl_sync(kFull, cj, m);
+              if (l < h) {
+                if (cm < x) l = m + 1;
+                else h = m;
+              }
+            }
+            return l;
+          };
+          const int j0 = j0_of(cc), j1 = j0_of(cc + 1);
+          if (cc < ncell) cells[cc] = (uint16_t)(j0 | ((j1 - j0) << 8));
+        }
       }
     }
-    while (lo < hi) {  // lower_bound in spl[lo..hi)
-      const int mid = (lo + hi) >> 1;
-      if (spl[mid] < key) lo = mid + 1;
-      else hi = mid;
-    }
-    return (lo < B - 1 && spl[lo] == key) ? 2 * lo + 1 : 2 * lo;
   }
-};
-
-__device__ __forceinline__ Classifier load_classifier(int32_t* sm, const int32_t* gspl,
-                                                      const int16_t* glut, int B) {
-  int32_t* spl = sm;
-  int16_t* lut = reinterpret_cast<int16_t*>(sm + B);
-  for (int i = threadIdx.x; i < B; i += blockDim.x) spl[i] = gspl[i];
-  for (int i = threadIdx.x; i <= kQsLut; i += blockDim.x) lut[i] = glut[8 + i];
-  const int32_t* hdr = reinterpret_cast<const int32_t*>(glut);
-  return Classifier{spl, lut, B, hdr[0], hdr[1]};
+  // larger segments (B = 64, 128: S = 1024, 2048 samples), one CTA each: S/512 warps each
+    // sort 512 samples in registers and keep every (S/512)-th; warp 0 sorts
+    // those 512 regular sub-samples and takes the pivots at regular ranks
+    // (regular sampling of regular samples: PSRS-style quantile bounds)
+  for (int64_t sb = blockIdx.x; sb < nseg; sb += gridDim.x) {
+    {
+      const QsSeg g = qs_seg(c, level, sb);
+      if (g.B <= 32) continue;
+      const int S = kQsOver * g.B;
+      const int nw = S / 512;
+      const int64_t stride = g.len / S;
+      if (warp < nw) {
+        Key v[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u)
+          v[u] = X[g.start + qs_sample_pos(warp * 512 + lane * 16 + u, stride, level)];
+        thread_sort<8>(v);
+        warp_bitonic<5>(v, lane);
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          const int r = lane * 16 + u;
+          if (r % nw == nw - 1) sub[warp * (512 / nw) + r / nw] = v[u];
+        }
+      }
+      __syncthreads();
+      const int ncell = 16 * g.B;
+      for (int i = tid; i < ncell; i += 256) ccount[i] = 0;
+      if (warp == 0) {
+        Key v[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) v[u] = sub[lane * 16 + u];
+        thread_sort<8>(v);
+        warp_bitonic<5>(v, lane);
+        const int step = 512 / g.B;
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          const int r = lane * 16 + u + 1;
+          if (r % step == 0) {
+            const int j = r / step - 1;
+            const Key pv = j < g.B - 1 ? v[u] : KeyT<Key>::kMax;
+            splb[g.spl_off + j] = pv;
+            piv[j] = pv;
+          }
+        }
+      }
+      qs_write_pivots_zero(c, level, g, tid, 256);
+      __syncthreads();
+      // prefix cells: count the pivots per cell, exclusive scan -> j0
+      const Key lo = piv[0], hi = piv[g.B - 2];
+      const int shift = qs_cell_shift(lo, hi, ncell);
+      for (int j = tid; j < g.B - 1; j += 256) atomicAdd(&ccount[qs_cell_of(piv[j], lo, shift, ncell)], 1u);
+      __syncthreads();
+      {
+        const int per = ncell / 256;  // 4 .. 16 cells per thread
+        uint32_t run[16];
+        uint32_t tot = 0;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          run[q] = q < per ? ccount[tid * per + q] : 0u;
+          tot += run[q];
+        }
+        // block exclusive scan of the per-thread totals (8 warps)
+        uint32_t x = tot;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(kFull, x, o);
+          if (lane >= o) x += y;
+        }
+        if (lane == 31) wsum[warp] = x;
+        __syncthreads();
+        uint32_t before = 0;
+        for (int w = 0; w < warp; ++w) before += wsum[w];
+        uint32_t j0 = before + x - tot;
+        uint16_t* cells = c.cells[level & 1] + 16 * g.spl_off;
+#pragma unroll
+        for (int q = 0; q < 16; ++q)
+          if (q < per) {
+            cells[tid * per + q] = (uint16_t)(j0 | (run[q] << 8));
+            j0 += run[q];
+          }
+      }
+      __syncthreads();  // sub / piv / ccount are reused by the next segment
+    }
+  }
 }
 
-constexpr int kQsClassifierWords = kQsMaxB + (kQsLut + 2) / 2 + 2;
-
-// Runs of equal bucket ids among consecutive lanes (consecutive keys in
-// memory): one ballot finds the run heads, so a run — one lane for random
-// input, the whole warp for sorted input — is charged with ONE shared-memory
-// atomic by its head lane.  Equal ids in different runs of a warp just issue
-// separate atomics.  (Replaces __match_any_sync, which measured as the
-// bottleneck of these kernels.)  Lanes with b < 0 form their own runs and
-// are skipped by the callers.
-struct WarpRun {
-  int head_lane;  // first lane of my run
-  int len;        // my run's length (valid on every lane of the run)
-  bool head;
-};
-__device__ __forceinline__ WarpRun warp_run(int b) {
-  const int lane = threadIdx.x & 31;
-  const int prev = __shfl_up_sync(kFull, b, 1);
-  const bool head = lane == 0 || b != prev;
-  const unsigned heads = __ballot_sync(kFull, head);
-  const unsigned upto = heads & (0xffffffffu >> (31 - lane));      // heads at lanes <= mine
-  const int hl = 31 - __clz(upto);
-  const unsigned after = heads & ~(0xffffffffu >> (31 - lane));    // heads at lanes > mine
-  const int next = after ? __ffs(after) - 1 : 32;
-  return WarpRun{hl, next - hl, head};
+// ---- classification ----------------------------------------------------------
+// bucket(key): j = number of real pivots < key (lower_bound over the B-1 real
+// pivots; slot B-1 is the key-maximum pad); equal bucket 2j+1 when
+// piv[j] == key, else between bucket 2j.  Every key is classified ONCE per
+// level (count kernel); its one-byte bucket id is stored for the scatter.
+//
+// Per segment every CTA loads, into shared memory,
+//   - the pivot table REPLICATED across the banks: pivot i of lane l sits at
+//     word i*R + l%R (R = 32 int32 / 16 int64 copies), so data-dependent
+//     probes of the 32 lanes always hit 32 different banks (one copy: ~3.5
+//     wavefronts per probe; ncu measured 76 % bank-conflict wavefronts);
+//   - the prefix cells built by the sample kernel: the pivots' key range
+//     [piv[0], piv[B-2]] cut into 16 B cells, cell c = (j0 = #pivots below
+//     the cell, k = #pivots inside it).  A key finds its cell with one shift
+//     and compares with the k pivots of its cell — usually none or one —
+//     instead of log2(B) dependent probes.
+template <class Key>
+__host__ __device__ constexpr int qs_rep() { return sizeof(Key) == 4 ? 32 : 16; }
+constexpr int kQsCellsMax = 16 * kQsMaxB;
+template <class Key>
+__host__ __device__ constexpr int qs_table_bytes() {
+  return kQsMaxB * qs_rep<Key>() * (int)sizeof(Key) + kQsCellsMax * 2;
 }
 
-// 2 CTAs/SM (<= 64 registers; the classifier + histogram take 57 KiB of
-// shared memory each): measured at 112 registers and ONE CTA/SM the kernel
-// ran at 25 % occupancy and 0.6 TB/s.
-#ifndef NSB_QS_COUNT_MINB
-#define NSB_QS_COUNT_MINB 2
-#endif
-__global__ void __launch_bounds__(kQsNT, NSB_QS_COUNT_MINB)
-    count_kernel(const int32_t* __restrict__ keys, int64_t n, const int32_t* __restrict__ gspl,
-                 const int16_t* __restrict__ glut, int B, uint32_t* __restrict__ totals) {
-  extern __shared__ int32_t qsm[];
-  const Classifier cls = load_classifier(qsm, gspl, glut, B);
-  uint32_t* hist = reinterpret_cast<uint32_t*>(qsm + kQsClassifierWords);
-  const int NB = 2 * B - 1;
-  for (int i = threadIdx.x; i < NB; i += kQsNT) hist[i] = 0;
-  __syncthreads();
-  const int64_t c0 = (int64_t)blockIdx.x * kQsChunk;
-  const int64_t c1 = min(n, c0 + kQsChunk);
-  constexpr int kU = kQsChunk / kQsNT;  // keys per thread
-  constexpr int kG = 8;                 // loaded in groups of 8
+template <class Key>
+struct QsClassifier {
+  const Key* tab;        // replicated pivots, this lane's column
+  const uint16_t* cell;  // j0 | k << 8
+  Key lo;
+  int shift, ncell, B;
+  __device__ __forceinline__ int operator()(Key key) const {
+    constexpr int R = qs_rep<Key>();
+    using U = std::make_unsigned_t<Key>;
+    const U cd = ((U)key - (U)lo) >> shift;
+    // keys below the first pivot use cell 0 (j0 = 0; its first candidate is
+    // the first pivot, which they do not exceed)
+    const int ci = key < lo ? 0 : (cd < (U)ncell ? (int)cd : ncell - 1);
+    const uint32_t e = cell[ci];
+    int j = (int)(e & 255u);
+    int k = (int)(e >> 8);
+    Key t = tab[j * R];
 #pragma unroll 1
-  for (int g0 = 0; g0 < kU; g0 += kG) {
-    int32_t k[kG];
-#pragma unroll
-    for (int u = 0; u < kG; ++u) {
-      const int64_t i = c0 + (g0 + u) * kQsNT + threadIdx.x;
-      k[u] = i < c1 ? __ldg(keys + i) : 0;
+    while (k > 0 && t < key) {
+      ++j;
+      --k;
+      t = tab[j * R];
     }
-#pragma unroll
-    for (int u = 0; u < kG; ++u) {
-      const int64_t i = c0 + (g0 + u) * kQsNT + threadIdx.x;
-      const int b = i < c1 ? cls(k[u]) : -1;
-      const WarpRun r = warp_run(b);
-      if (b >= 0 && r.head) atomicAdd(&hist[b], (uint32_t)r.len);
-    }
+    return 2 * j + ((j < B - 1) & (t == key));
   }
-  __syncthreads();
-  for (int i = threadIdx.x; i < NB; i += kQsNT)
-    if (hist[i]) atomicAdd(&totals[i], hist[i]);
+};
+
+// Loads both tables of one segment (all threads of the CTA; the caller
+// synchronises before and after).  The cells were built by the sample kernel.
+template <class Key>
+__device__ __forceinline__ QsClassifier<Key> qs_load_classifier(unsigned char* raw,
+                                                                 const Key* __restrict__ spl,
+                                                                 const uint16_t* __restrict__ cells,
+                                                                 int B) {
+  constexpr int R = qs_rep<Key>();
+  Key* tab = reinterpret_cast<Key*>(raw);
+  uint16_t* cell = reinterpret_cast<uint16_t*>(raw + kQsMaxB * R * sizeof(Key));
+  const Key lo = __ldg(spl), hi = __ldg(spl + (B >= 2 ? B - 2 : 0));
+  const int ncell = 16 * B;
+#pragma unroll 4
+  for (int i = threadIdx.x; i < B * R; i += blockDim.x) tab[i] = __ldg(spl + i / R);
+#pragma unroll 4
+  for (int i = threadIdx.x; i < ncell; i += blockDim.x) cell[i] = __ldg(cells + i);
+  return QsClassifier<Key>{tab + (threadIdx.x & (R - 1)), cell, lo, qs_cell_shift(lo, hi, ncell),
+                           ncell, B};
 }
 
-// Scatter with one global reservation per (CTA, bucket): the CTA classifies
-// its chunk once (bucket ids stay in registers), builds a shared-memory
-// histogram, reserves each non-empty bucket's range with ONE global atomic,
-// then places every key at base + warp-aggregated shared-memory rank.
-#ifndef NSB_QS_SNT
-#define NSB_QS_SNT 512
+// ---- 2. count (classify once, store the ids) ----------------------------------
+// One shared increment per key: ptxas emits ATOMS.POPC.INC, which charges all
+// lanes of a warp that hit the same bucket in one operation (sorted input).
+__device__ __forceinline__ void qs_hist_add(uint32_t* hist, int b) {
+  if (b >= 0) atomicAdd(&hist[b], 1u);
+}
+
+template <bool FULL, class Key>
+__device__ __forceinline__ void qs_count_chunk(const Key* __restrict__ X, uint8_t* __restrict__ ids,
+                                               int64_t c0, int64_t c1,
+                                               const QsClassifier<Key>& cls, uint32_t* hist) {
+  Key k[kQsPer];
+#pragma unroll
+  for (int u = 0; u < kQsPer; ++u) {
+    const int64_t i = c0 + u * kQsNT + threadIdx.x;
+    k[u] = (FULL || i < c1) ? __ldg(X + i) : Key(0);
+  }
+#pragma unroll
+  for (int u = 0; u < kQsPer; ++u) {
+    const int64_t i = c0 + u * kQsNT + threadIdx.x;
+    const bool in = FULL || i < c1;
+    const int b = in ? cls(k[u]) : -1;
+    if (in) ids[i] = (uint8_t)b;
+    qs_hist_add(hist, b);
+  }
+}
+
+template <class Key>
+__global__ void __launch_bounds__(kQsNT, 2) qs_count_kernel(QsCtx<Key> c, int level) {
+  extern __shared__ __align__(16) unsigned char qs_raw[];
+  __shared__ uint32_t hist[2 * kQsMaxB];
+  const Key* X = qs_src(c, level);
+  const int64_t nch = qs_nchunk(c, level);
+  int64_t cur = -1;  // segment whose tables are loaded
+  QsClassifier<Key> cls{};
+  for (int64_t ch = blockIdx.x; ch < nch; ch += gridDim.x) {
+    const int64_t sid = qs_seg_of_chunk(c, level, ch);
+    const QsSeg g = qs_seg(c, level, sid);
+    const int NB = 2 * g.B - 1;
+    __syncthreads();  // the previous chunk is done with the tables / hist
+    if (sid != cur)
+      cls = qs_load_classifier<Key>(qs_raw, c.spl[level & 1] + g.spl_off,
+                                    c.cells[level & 1] + 16 * g.spl_off, g.B);
+    cur = sid;
+    for (int i = threadIdx.x; i < NB; i += kQsNT) hist[i] = 0;
+    __syncthreads();
+    const int64_t c0 = g.start + (ch - g.chunk0) * kQsChunk;
+    const int64_t c1 = min(g.start + g.len, c0 + kQsChunk);
+    if (c1 - c0 == kQsChunk) qs_count_chunk<true>(X, c.ids, c0, c1, cls, hist);
+    else qs_count_chunk<false>(X, c.ids, c0, c1, cls, hist);
+    __syncthreads();
+    uint32_t* cnt = c.cnt[level & 1] + g.cnt_off;
+    for (int b = threadIdx.x; b < NB; b += kQsNT)
+      if (hist[b]) atomicAdd(&cnt[b], hist[b]);
+  }
+}
+
+// ---- 3. plan ---------------------------------------------------------------------
+// Block-wide exclusive scan of one value per thread (kQsNT threads) under an
+// associative op with identity `id`.
+template <class T, class Op>
+__device__ __forceinline__ T qs_block_scan(T v, T id, Op op, T* warp_tot) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  T x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const T y = __shfl_up_sync(kFull, x, o);
+    if (lane >= o) x = op(y, x);
+  }
+  if (lane == 31) warp_tot[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    T t = lane < kQsNT / 32 ? warp_tot[lane] : id;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const T y = __shfl_up_sync(kFull, t, o);
+      if (lane >= o) t = op(y, t);
+    }
+    if (lane < kQsNT / 32) warp_tot[lane] = t;  // inclusive over warps
+  }
+  __syncthreads();
+  T ex = __shfl_up_sync(kFull, x, 1);
+  if (lane == 0) ex = id;
+  const T r = warp > 0 ? op(warp_tot[warp - 1], ex) : ex;
+  __syncthreads();  // warp_tot is reused by the caller's next scan
+  return r;
+}
+__device__ __forceinline__ int64_t qs_block_scan(uint32_t v, int64_t* warp_tot) {
+  return qs_block_scan<int64_t>((int64_t)v, 0, [](int64_t a, int64_t b) { return a + b; },
+                                warp_tot);
+}
+
+#ifndef NSB_QS_PACK
+#define NSB_QS_PACK 4096
 #endif
-constexpr int kQsSNT = NSB_QS_SNT;          // scatter threads (1024 measured no faster)
-constexpr int kQsPer = 16;                  // keys per thread in scatter
-constexpr int kQsSChunk = kQsPer * kQsSNT;  // keys per CTA in scatter
+// Leaf packing: neighbouring buckets of <= kQsPack keys whose start offsets
+// in the segment fall in the same kQsPack-key window form one leaf job, so a
+// job is < 2 kQsPack keys; the rule is evaluated by every bucket in parallel.
+constexpr int kQsPack = NSB_QS_PACK;
+static_assert(2 * kQsPack <= kSmallTile, "packed jobs must fit one tile");
 
-__global__ void __launch_bounds__(kQsSNT, 2)
-    scatter_kernel(const int32_t* __restrict__ keys, int64_t n, const int32_t* __restrict__ gspl,
-                   const int16_t* __restrict__ glut, int B, uint32_t* __restrict__ fill,
-                   int32_t* __restrict__ out) {
-  extern __shared__ int32_t qsm[];
-  const Classifier cls = load_classifier(qsm, gspl, glut, B);
-  // 32-bit counters and positions: the single-level path sorts < 2^32 keys
-  // (64-bit shared atomics measured as the bottleneck of this kernel)
-  uint32_t* pos = reinterpret_cast<uint32_t*>(qsm + kQsClassifierWords);
-  const int NB = 2 * B - 1;
-  for (int i = threadIdx.x; i < NB; i += kQsSNT) pos[i] = 0;
-  __syncthreads();
-  const int64_t c0 = (int64_t)blockIdx.x * kQsSChunk;
-  const int lane = threadIdx.x & 31;
-  int32_t k[kQsPer];
-  int bk[kQsPer];
-#pragma unroll
-  for (int u = 0; u < kQsPer; ++u) {
-    const int64_t i = c0 + u * kQsSNT + threadIdx.x;
-    k[u] = i < n ? __ldcs(keys + i) : 0;
-  }
-#pragma unroll
-  for (int u = 0; u < kQsPer; ++u) {
-    const int64_t i = c0 + u * kQsSNT + threadIdx.x;
-    bk[u] = i < n ? cls(k[u]) : -1;
-    const WarpRun r = warp_run(bk[u]);
-    if (bk[u] >= 0 && r.head) atomicAdd(&pos[bk[u]], (uint32_t)r.len);
-  }
-  __syncthreads();
-  {
-    // one global reservation per (CTA, bucket); a thread's atomics are all
-    // issued before any result is used, so their L2 round trips overlap
-    // (one after another they were the kernel's critical path)
-    constexpr int kR = (2 * kQsMaxB + kQsSNT - 1) / kQsSNT;
-    uint32_t c[kR], r[kR];
-#pragma unroll
-    for (int q = 0; q < kR; ++q) {
-      const int b = threadIdx.x + q * kQsSNT;
-      c[q] = b < NB ? pos[b] : 0u;
+__device__ __forceinline__ int qs_class_of(int64_t len) {
+  return len <= 4096 ? 0 : len <= 8192 ? 1 : 2;
+}
+
+template <class Key>
+__global__ void __launch_bounds__(kQsNT) qs_plan_kernel(QsCtx<Key> c, int level, int last) {
+  __shared__ int64_t s_wtot[kQsNT / 32];
+  __shared__ uint32_t s_cnt[kQsNT];
+  __shared__ int64_t s_pos[kQsNT];
+  __shared__ uint8_t s_flag[kQsNT];  // 0 empty, 1 packed member, 2 job head, 3 big
+  __shared__ uint32_t s_ccnt[3], s_nn;
+  __shared__ uint32_t s_chunks, s_bk, s_sp;  // per segment: < 2^32 (32-bit shared atomics)
+  __shared__ unsigned long long s_jbase[3], s_sbase, s_kbase, s_bbase, s_pbase;
+  const int tid = threadIdx.x;
+  const int nx = (level + 1) & 1;
+  // buckets of this level land in Y_l (the scatter destination): tmp at even levels
+  const int src_flag = (level & 1) ? 0 : 1;
+  const int64_t nseg = qs_nseg(c, level);
+  for (int64_t s = blockIdx.x; s < nseg; s += gridDim.x) {
+    const QsSeg g = qs_seg(c, level, s);
+    const int NB = 2 * g.B - 1;
+    const uint32_t v = tid < NB ? __ldcg(c.cnt[level & 1] + g.cnt_off + tid) : 0u;
+    const int64_t pos = g.start + qs_block_scan(v, s_wtot);
+    // previous non-empty bucket (exclusive max-scan of indices)
+    const int64_t prev = qs_block_scan<int64_t>(v ? tid : -1, -1,
+                                                [](int64_t a, int64_t b) { return a > b ? a : b; },
+                                                s_wtot);
+    s_cnt[tid] = v;
+    s_pos[tid] = pos;
+    if (tid < NB) c.fill[level & 1][g.cnt_off + tid] = (unsigned long long)pos;
+    if (tid == 0) {
+      s_ccnt[0] = s_ccnt[1] = s_ccnt[2] = 0;
+      s_nn = 0;
+      s_chunks = s_bk = s_sp = 0;
     }
-#pragma unroll
-    for (int q = 0; q < kR; ++q) r[q] = c[q] ? atomicAdd(&fill[threadIdx.x + q * kQsSNT], c[q]) : 0u;
-#pragma unroll
-    for (int q = 0; q < kR; ++q)
-      if (c[q]) pos[threadIdx.x + q * kQsSNT] = r[q];
-  }
-  __syncthreads();
-#pragma unroll
-  for (int u = 0; u < kQsPer; ++u) {
-    const int b = bk[u];
-    const WarpRun r = warp_run(b);
-    uint32_t base = 0;
-    if (b >= 0 && r.head) base = atomicAdd(&pos[b], (uint32_t)r.len);
-    base = __shfl_sync(kFull, base, r.head_lane);
-    if (b >= 0) out[base + (lane - r.head_lane)] = k[u];
+    __syncthreads();
+    const bool small = v > 0 && v <= (uint32_t)kQsPack;
+    const int64_t win = (pos - g.start) / kQsPack;
+    bool head = false;
+    if (small) {
+      head = prev < 0 || s_cnt[prev] > (uint32_t)kQsPack || (s_pos[prev] - g.start) / kQsPack != win;
+    }
+    s_flag[tid] = head ? 2 : small ? 1 : v > 0 ? 3 : 0;
+    __syncthreads();
+    // this thread's job (packed run, own bucket, copy, fallback) or new segment
+    int cls = -1, type = kJobSort;
+    int64_t jstart = pos, jlen = 0;
+    uint32_t jlocal = 0;
+    int32_t nB = 0, nch = 0;
+    uint32_t slocal = 0;
+    uint32_t koff = 0, boff = 0, poff = 0;
+    if (head) {
+      int b = tid + 1;
+      while (b < NB && s_flag[b] <= 1) ++b;
+      jlen = (b < NB ? s_pos[b] : g.start + g.len) - pos;
+      cls = qs_class_of(jlen);
+    } else if (v > (uint32_t)kQsPack) {
+      jlen = v;
+      if (v <= (uint32_t)kSmallTile) {
+        cls = qs_class_of(jlen);
+      } else if (tid & 1) {  // constant bucket: already sorted; moved only if it sits in tmp
+        if (src_flag) {
+          cls = 2;
+          type = kJobCopy;
+        }
+      } else if (!last) {
+        nB = qs_buckets(jlen);
+        nch = (int32_t)((jlen + kQsChunk - 1) / kQsChunk);
+        slocal = atomicAdd(&s_nn, 1u);
+        koff = atomicAdd(&s_chunks, (uint32_t)nch);
+        boff = atomicAdd(&s_bk, (uint32_t)(2 * nB - 1));
+        poff = atomicAdd(&s_sp, (uint32_t)nB);
+      } else {
+        cls = 2;
+        type = kJobBig;
+      }
+    }
+    if (cls >= 0) jlocal = atomicAdd(&s_ccnt[cls], 1u);
+    __syncthreads();
+    if (tid < 3) s_jbase[tid] = s_ccnt[tid] ? atomicAdd(&c.ctr->njobs[tid], (unsigned long long)s_ccnt[tid]) : 0ull;
+    if (tid == 3 && s_nn) {
+      s_sbase = atomicAdd(&c.ctr->nseg[nx], (unsigned long long)s_nn);
+      s_kbase = atomicAdd(&c.ctr->nchunk[nx], (unsigned long long)s_chunks);
+      s_bbase = atomicAdd(&c.ctr->nbkt[nx], (unsigned long long)s_bk);
+      s_pbase = atomicAdd(&c.ctr->nspl[nx], (unsigned long long)s_sp);
+    }
+    __syncthreads();
+    if (cls >= 0) {
+      const unsigned long long at = s_jbase[cls] + jlocal;
+      if (at < (unsigned long long)c.max_jobs)
+        c.jobs[cls][at] = QsJob{jstart, jlen, src_flag | (type << 1), 0};
+    }
+    if (nB) {
+      const unsigned long long sid = s_sbase + slocal, k0 = s_kbase + koff;
+      if (sid < (unsigned long long)c.max_segs) {
+        QsSeg ns;
+        ns.start = jstart;
+        ns.len = jlen;
+        ns.chunk0 = (int64_t)k0;
+        ns.cnt_off = (int64_t)(s_bbase + boff);
+        ns.spl_off = (int64_t)(s_pbase + poff);
+        ns.B = nB;
+        ns.nchunks = nch;
+        c.segs[nx][sid] = ns;
+        for (int j = 0; j < nch; ++j)
+          if (k0 + j < (unsigned long long)c.max_chunks) c.chunk_seg[nx][k0 + j] = (int32_t)sid;
+      }
+    }
+    __syncthreads();
   }
 }
 
-// One CTA per job (start, len <= T): sorts src[start..start+len) into dst.
+// ---- 4. scatter (shared-memory multisplit, coalesced bucket runs) -------------
+template <class Key>
+__host__ __device__ constexpr int qs_scatter_smem() {
+  return kQsChunk * (int)sizeof(Key) + kQsChunk;  // keys + one-byte bucket ids
+}
+
+template <class Key>
+__global__ void __launch_bounds__(kQsNT, 2) qs_scatter_kernel(QsCtx<Key> c, int level) {
+  __shared__ uint32_t hist[2 * kQsMaxB];    // counts, then local starts
+  __shared__ long long delta[2 * kQsMaxB];  // global position - local start
+  __shared__ int64_t wtot[kQsNT / 32];
+  extern __shared__ __align__(16) unsigned char qs_raw[];
+  Key* skey = reinterpret_cast<Key*>(qs_raw);
+  uint8_t* sbid = qs_raw + kQsChunk * sizeof(Key);
+  const int tid = threadIdx.x, lane = tid & 31;
+  const Key* X = qs_src(c, level);
+  Key* Y = qs_src(c, level + 1);
+  const int64_t nch = qs_nchunk(c, level);
+  for (int64_t ch = blockIdx.x; ch < nch; ch += gridDim.x) {
+    const QsSeg g = qs_seg(c, level, qs_seg_of_chunk(c, level, ch));
+    const int NB = 2 * g.B - 1;
+    __syncthreads();
+    for (int i = tid; i < NB; i += kQsNT) hist[i] = 0;
+    __syncthreads();
+    const int64_t c0 = g.start + (ch - g.chunk0) * kQsChunk;
+    const int64_t c1 = min(g.start + g.len, c0 + kQsChunk);
+    Key k[kQsPer];
+    int b[kQsPer];
+#pragma unroll
+    for (int u = 0; u < kQsPer; ++u) {
+      const int64_t i = c0 + u * kQsNT + tid;
+      const bool in = i < c1;
+      k[u] = in ? __ldcs(X + i) : Key(0);
+      b[u] = in ? (int)__ldcs(c.ids + i) : -1;
+    }
+    uint32_t pk[kQsPer];  // rank-in-bucket << 8 | bucket, 0xffffffff = no key
+#pragma unroll
+    for (int u = 0; u < kQsPer; ++u) {
+      const int b0 = __shfl_sync(kFull, b[u], 0);
+      uint32_t r;
+      if (__all_sync(kFull, b[u] == b0)) {  // one bucket for the whole warp
+        uint32_t base = 0;
+        if (lane == 0 && b0 >= 0) base = atomicAdd(&hist[b0], 32u);
+        r = __shfl_sync(kFull, base, 0) + (uint32_t)lane;
+      } else {
+        r = b[u] >= 0 ? atomicAdd(&hist[b[u]], 1u) : 0u;
+      }
+      pk[u] = b[u] >= 0 ? (r << 8) | (uint32_t)b[u] : 0xffffffffu;
+    }
+    __syncthreads();
+    // local bucket starts (exclusive scan) and one global reservation per bucket
+    const uint32_t cnt = tid < NB ? hist[tid] : 0u;
+    const int64_t ls = qs_block_scan(cnt, wtot);
+    unsigned long long* fill = c.fill[level & 1] + g.cnt_off;
+    if (tid < NB) {
+      const unsigned long long gb = cnt ? atomicAdd(&fill[tid], (unsigned long long)cnt) : 0ull;
+      hist[tid] = (uint32_t)ls;
+      delta[tid] = (long long)gb - (long long)ls;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < kQsPer; ++u) {
+      if (pk[u] != 0xffffffffu) {
+        const int bb = (int)(pk[u] & 0xffu);
+        const int p = (int)hist[bb] + (int)(pk[u] >> 8);
+        skey[p] = k[u];
+        sbid[p] = (uint8_t)bb;
+      }
+    }
+    __syncthreads();
+    const int total = (int)(c1 - c0);
+    for (int i = tid; i < total; i += kQsNT) Y[delta[sbid[i]] + i] = skey[i];
+  }
+}
+
+// ---- 5. leaf jobs ---------------------------------------------------------------
+// One CTA sorts a segment of any length in global memory (the fallback for a
+// bucket still larger than one CTA after the last level): tiles sorted on
+// chip, then pairwise merges of runs ping-ponging between the two buffers'
+// ranges, the last pass landing in `keys`.  Plain loads/stores only (every
+// key is re-read by this same CTA).
+template <int NT, int K, int LEAF, class Key>
+__device__ void qs_big_sort(Key* keys, Key* tmp, int64_t st, int64_t len, bool src_tmp, Key* sm) {
+  static_assert(cta_sort_skewed<NT, K, Key>(), "the fallback reads the skewed tile from smem");
+  constexpr int T = NT * K;
+  const int tid = threadIdx.x;
+  const int64_t tiles = (len + T - 1) / T;
+  int passes = 0;
+  for (int64_t r = tiles; r > 1; r = (r + 1) / 2) ++passes;
+  Key* kb = keys + st;
+  Key* tb = tmp + st;
+  const Key* src = src_tmp ? tb : kb;
+  Key* A = (passes & 1) ? tb : kb;
+  Key* Bf = (passes & 1) ? kb : tb;
+  for (int64_t t = 0; t < tiles; ++t) {
+    const int valid = (int)min((int64_t)T, len - t * T);
+    cta_sort<NT, K, LEAF>(src + t * T, (Key*)nullptr, valid, sm);
+    __syncthreads();
+    for (int i = tid; i < valid; i += NT) A[t * T + i] = sm[i];
+    __syncthreads();
+  }
+  __shared__ int64_t s_split[2];
+  constexpr int M = NT * 4;  // outputs per merge chunk, 4 per thread
+  for (int64_t R = T; R < len; R *= 2) {
+    for (int64_t p = 0; p < len; p += 2 * R) {
+      const Key* a = A + p;
+      const int64_t la = min(R, len - p);
+      const Key* b = a + la;
+      const int64_t lb = max((int64_t)0, min(R, len - p - R));
+      for (int64_t d0 = 0; d0 < la + lb; d0 += M) {
+        const int64_t d1 = min(d0 + M, la + lb);
+        if (tid < 2) {
+          const int64_t d = tid ? d1 : d0;
+          int64_t lo = d > lb ? d - lb : 0, hi = d < la ? d : la;
+          while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (__ldcg(a + mid) <= __ldcg(b + d - 1 - mid)) lo = mid + 1;
+            else hi = mid;
+          }
+          s_split[tid] = lo;
+        }
+        __syncthreads();
+        const int64_t a0 = s_split[0], a1 = s_split[1];
+        const int na = (int)(a1 - a0), nb = (int)((d1 - a1) - (d0 - a0));
+        for (int i = tid; i < na; i += NT) sm[i] = __ldcg(a + a0 + i);
+        for (int i = tid; i < nb; i += NT) sm[na + i] = __ldcg(b + (d0 - a0) + i);
+        __syncthreads();
+        const int dd = min(tid * 4, na + nb);
+        int lo = dd > nb ? dd - nb : 0, hi = dd < na ? dd : na;
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (sm[mid] <= sm[na + dd - 1 - mid]) lo = mid + 1;
+          else hi = mid;
+        }
+        int ia = lo, ib = dd - lo;
+        for (int k = 0; k < 4 && dd + k < na + nb; ++k) {
+          const bool ta = ib >= nb || (ia < na && sm[ia] <= sm[na + ib]);
+          Bf[p + d0 + dd + k] = ta ? sm[ia++] : sm[na + ib++];
+        }
+        __syncthreads();
+      }
+    }
+    std::swap(A, Bf);
+  }
+}
+
 template <int NT, int K, int LEAF, class Key>
 __global__ void __launch_bounds__(NT, (bs_min_blocks_tput<NT, K, Key>()))
-    bucket_sort_kernel(const Key* __restrict__ src, Key* __restrict__ dst,
-                       const int64_t* __restrict__ jobs) {
-  extern __shared__ __align__(16) unsigned char bsm_raw[];
-  Key* sm = reinterpret_cast<Key*>(bsm_raw);
-  const int64_t start = jobs[2 * blockIdx.x];
-  const int len = (int)jobs[2 * blockIdx.x + 1];
-  cta_sort<NT, K, LEAF>(src + start, dst + start, len, sm);
-}
-
-template <int NT, int K, int LEAF, class Key>
-static int launch_bucket_sort(const Key* src, Key* dst, const int64_t* jobs, int njobs,
-                              cudaStream_t s) {
-  if (njobs == 0) return NS_OK;
-  constexpr int smem = tile_smem_bytes<NT, K, Key>();
-  auto* kern = bucket_sort_kernel<NT, K, LEAF, Key>;
-  NSB_TRY(ensure_smem_attr(reinterpret_cast<const void*>(kern), smem,
-                           "cudaFuncSetAttribute(bucket_sort)"));
-  {
-    Prof prof(PK_QS_BUCKET, s);
-    kern<<<njobs, NT, smem, s>>>(src, dst, jobs);
-  }
-  return check_launch("bucket_sort_kernel");
-}
-
-// Job classes 1..3 (buckets of <= 4096, 8192, 16384 keys; class 0 is launched
-// by the caller with <128,16>): int32 tiles as 32 keys per thread when
-// seg_k32_enabled(), else 16.
-template <int LF, class Key>
-static int bucket_sort_classes(const Key* src, Key* dst, const int64_t* jobs, const int* off,
-                               cudaStream_t s) {
-  if (std::is_same_v<Key, int32_t> && seg_k32_enabled()) {
-    NSB_TRY((launch_bucket_sort<128, 32, LF>(src, dst, jobs + 2 * off[1], off[2] - off[1], s)));
-    NSB_TRY((launch_bucket_sort<256, 32, LF>(src, dst, jobs + 2 * off[2], off[3] - off[2], s)));
-    return launch_bucket_sort<512, 32, LF>(src, dst, jobs + 2 * off[3], off[4] - off[3], s);
-  }
-  NSB_TRY((launch_bucket_sort<256, 16, LF>(src, dst, jobs + 2 * off[1], off[2] - off[1], s)));
-  NSB_TRY((launch_bucket_sort<512, 16, LF>(src, dst, jobs + 2 * off[2], off[3] - off[2], s)));
-  return launch_bucket_sort<1024, 16, LF>(src, dst, jobs + 2 * off[3], off[4] - off[3], s);
-}
-
-// n <= kSmallTile at the top level: the merge sort (one CTA up to 8192
-// keys, else two tiles and a merge pass in the caller's scratch, which
-// quick_sort_temp sizes for it).
-template <class Key>
-static int small_sort(Key* d_keys, size_t n, int leaf, void* d_temp, size_t temp_bytes,
-                      cudaStream_t s) {
-  return merge_sort_device(d_keys, n, leaf, d_temp, temp_bytes, s);
-}
-
-// Leaf jobs of a partition level.  Consecutive buckets hold disjoint,
-// ascending key ranges, so a run of NEIGHBOURING buckets sorted as one tile
-// is each bucket sorted: small buckets are packed greedily into tiles of up
-// to kPackKeys keys, which removes the per-bucket tile padding (buckets of
-// ~4 K keys in 4 K/8 K tiles wasted about a third of the bucket-sort work).
-// Jobs are grouped by tile size class: <=2048, <=4096, <=8192, <=16384 keys.
-constexpr int64_t kPackKeys = 8192;
-struct JobPacker {
-  std::vector<int64_t> cls[4];
-  int64_t js = 0, jl = 0;
-  static int class_of(int64_t len) { return len <= 2048 ? 0 : len <= 4096 ? 1 : len <= 8192 ? 2 : 3; }
-  void flush() {
-    if (jl > 0) {
-      auto& c = cls[class_of(jl)];
-      c.push_back(js);
-      c.push_back(jl);
+    qs_leaf_kernel(QsCtx<Key> c, int cls) {
+  extern __shared__ __align__(16) unsigned char qs_raw[];
+  Key* sm = reinterpret_cast<Key*>(qs_raw);
+  const int64_t nj = (int64_t)*(volatile unsigned long long*)&c.ctr->njobs[cls];
+  const QsJob* jobs = c.jobs[cls];
+  for (int64_t j = blockIdx.x; j < nj; j += gridDim.x) {
+    const QsJob jb = jobs[j];
+    const bool src_tmp = jb.flags & 1;
+    const int type = (jb.flags >> 1) & 3;
+    const Key* src = (src_tmp ? c.tmp : c.keys) + jb.start;
+    Key* dst = c.keys + jb.start;
+    if (type == kJobSort) {
+      cta_sort<NT, K, LEAF>(src, dst, (int)jb.len, sm);
+    } else if (type == kJobCopy) {
+      for (int64_t i = threadIdx.x; i < jb.len; i += NT) dst[i] = src[i];
+    } else {
+      if constexpr (cta_sort_skewed<NT, K, Key>()) qs_big_sort<NT, K, LEAF>(c.keys, c.tmp, jb.start, jb.len, src_tmp, sm);
     }
-    jl = 0;
+    __syncthreads();
   }
-  // bucket [st, st+len), len <= kSmallTile
-  void add(int64_t st, int64_t len) {
-    if (len == 0) return;
-    if (len > kPackKeys) {  // alone in the 16 K class
-      flush();
-      cls[3].push_back(st);
-      cls[3].push_back(len);
-      return;
+}
+
+// ---- host side ---------------------------------------------------------------------
+// Side streams + fork/join events for the concurrent leaf classes: one set
+// per (host thread, device), so concurrent callers never share an event.
+struct QsSide {
+  cudaStream_t s[2] = {nullptr, nullptr};
+  cudaEvent_t fork = nullptr, join[2] = {nullptr, nullptr};
+};
+struct QsSideSet {
+  QsSide d[64];
+  ~QsSideSet() {
+    for (auto& x : d) {
+      for (int i = 0; i < 2; ++i) {
+        if (x.s[i]) cudaStreamDestroy(x.s[i]);
+        if (x.join[i]) cudaEventDestroy(x.join[i]);
+      }
+      if (x.fork) cudaEventDestroy(x.fork);
     }
-    if (jl > 0 && (js + jl != st || jl + len > kPackKeys)) flush();
-    if (jl == 0) js = st;
-    jl += len;
   }
 };
+static thread_local QsSideSet t_side;
 
-// Sorts keys[0..n) in place; tmp holds n keys of scratch; aux is reused by
-// recursive calls only after this level has enqueued all its work.
-static int quick_sort_level(int32_t* keys, int32_t* tmp, size_t n, int leaf, const QsAux& aux,
-                            cudaStream_t s) {
-  if (n <= (size_t)kSmallTile) return merge_sort_device(keys, n, leaf, nullptr, 0, s);  // one CTA
-  int B = 2;
-  while (B < kQsMaxB && (size_t)B * kQsTarget < n) B *= 2;
-  const int S = B * kQsOversample;
-  const int NB = 2 * B - 1;
-
-  {
-    Prof prof(PK_QS_SAMPLE, s);
-    sample_kernel<<<(S + 255) / 256, 256, 0, s>>>(keys, (int64_t)n, S, aux.samples);
-  }
-  NSB_TRY(check_launch("sample_kernel"));
-  NSB_TRY(merge_sort_device(aux.samples, (size_t)S, 8, aux.sample_temp, aux.sample_temp_bytes, s));
-  {
-    Prof prof(PK_QS_SAMPLE, s);
-    splitter_kernel<<<(B + 255) / 256, 256, 0, s>>>(aux.samples, S, B, aux.splitters);
-  }
-  NSB_TRY(check_launch("splitter_kernel"));
-  {
-    Prof prof(PK_QS_SAMPLE, s);
-    lut_kernel<<<(kQsLut + 1 + 255) / 256, 256, 0, s>>>(aux.splitters, B, aux.lut);
-  }
-  NSB_TRY(check_launch("lut_kernel"));
-
-  NSB_TRY(check_cuda(cudaMemsetAsync(aux.totals, 0, NB * sizeof(uint32_t), s), "memset"));
-  const int64_t ctas = (int64_t)((n + kQsChunk - 1) / kQsChunk);
-  const int count_smem = (kQsClassifierWords + NB) * 4;
-  const int scatter_smem = (kQsClassifierWords + NB) * 4;
-  NSB_TRY(ensure_smem_attr(reinterpret_cast<const void*>(count_kernel),
-                           (kQsClassifierWords + 2 * kQsMaxB) * 4, "cudaFuncSetAttribute(count)"));
-  NSB_TRY(ensure_smem_attr(reinterpret_cast<const void*>(scatter_kernel),
-                           (kQsClassifierWords + 2 * kQsMaxB) * 4,
-                           "cudaFuncSetAttribute(scatter)"));
-  {
-    Prof prof(PK_QS_COUNT, s);
-    count_kernel<<<(unsigned)ctas, kQsNT, count_smem, s>>>(keys, (int64_t)n, aux.splitters,
-                                                           aux.lut, B, aux.totals);
-  }
-  NSB_TRY(check_launch("count_kernel"));
-
-  // One device->host read per partition level: the bucket sizes drive the
-  // launch plan, as the split point drives quick_sort_rec (hybrid.hpp:145-148).
-  std::vector<uint32_t> totals(NB);
-  NSB_TRY(check_cuda(cudaMemcpyAsync(totals.data(), aux.totals, NB * sizeof(uint32_t),
-                                     cudaMemcpyDeviceToHost, s),
-                     "cudaMemcpyAsync(totals)"));
-  NSB_TRY(check_cuda(cudaStreamSynchronize(s), "cudaStreamSynchronize"));
-
-  std::vector<uint32_t> starts(NB);
-  uint64_t acc = 0;
-  for (int b = 0; b < NB; ++b) {
-    starts[b] = (uint32_t)acc;
-    acc += totals[b];
-  }
-  if (acc != n) return NS_ERR_CUDA;  // classification lost keys: a device fault
-  NSB_TRY(check_cuda(cudaMemcpyAsync(aux.fill, starts.data(), NB * sizeof(uint32_t),
-                                     cudaMemcpyHostToDevice, s),
-                     "cudaMemcpyAsync(fill)"));
-  {
-    Prof prof(PK_QS_SCATTER, s);
-    scatter_kernel<<<(unsigned)((n + kQsSChunk - 1) / kQsSChunk), kQsSNT, scatter_smem, s>>>(
-        keys, (int64_t)n, aux.splitters, aux.lut, B, reinterpret_cast<uint32_t*>(aux.fill), tmp);
-  }
-  NSB_TRY(check_launch("scatter_kernel"));
-
-  // Size classes: one CTA shape per class so small buckets do not pay for a
-  // 16K-key tile.  Classes: <=2048, <=4096, <=8192, <=16384, larger.
-  JobPacker pk;
-  std::vector<int> big;
-  for (int b = 0; b < NB; ++b) {
-    const int64_t len = totals[b];
-    if (len == 0) continue;
-    if (len <= kSmallTile) {
-      pk.add((int64_t)starts[b], len);
-    } else {
-      pk.flush();
-      big.push_back(b);
+static int qs_side_streams(QsSide** out) {
+  int dev = 0;
+  NSB_TRY(check_cuda(cudaGetDevice(&dev), "cudaGetDevice"));
+  if (dev < 0 || dev >= 64) return NS_ERR_INVALID;
+  QsSide& x = t_side.d[dev];
+  if (!x.fork) {
+    for (int i = 0; i < 2; ++i) {
+      NSB_TRY(check_cuda(cudaStreamCreateWithFlags(&x.s[i], cudaStreamNonBlocking), "cudaStreamCreate"));
+      NSB_TRY(check_cuda(cudaEventCreateWithFlags(&x.join[i], cudaEventDisableTiming), "cudaEventCreate"));
     }
+    NSB_TRY(check_cuda(cudaEventCreateWithFlags(&x.fork, cudaEventDisableTiming), "cudaEventCreate"));
   }
-  pk.flush();
-  auto& cls = pk.cls;
-  std::vector<int64_t> jobs;
-  int off[5] = {0, 0, 0, 0, 0};
-  for (int c = 0; c < 4; ++c) {
-    off[c] = (int)(jobs.size() / 2);
-    jobs.insert(jobs.end(), cls[c].begin(), cls[c].end());
-  }
-  off[4] = (int)(jobs.size() / 2);
-  if (!jobs.empty())
-    NSB_TRY(check_cuda(cudaMemcpyAsync(aux.jobs, jobs.data(), jobs.size() * sizeof(int64_t),
-                                       cudaMemcpyHostToDevice, s),
-                       "cudaMemcpyAsync(jobs)"));
-  NSB_TRY(with_leaf(leaf, [&](auto L) {
-    constexpr int LF = decltype(L)::value;
-    NSB_TRY((launch_bucket_sort<128, 16, LF>(tmp, keys, aux.jobs + 2 * off[0], off[1] - off[0], s)));
-    return bucket_sort_classes<LF>(tmp, keys, aux.jobs, off, s);
-  }));
-  // Oversized buckets: equal buckets are already sorted (constant); between
-  // buckets recurse, using their own slice of tmp as scratch.
-  for (int b : big) {
-    const size_t st = starts[b], len = totals[b];
-    NSB_TRY(check_cuda(cudaMemcpyAsync(keys + st, tmp + st, len * 4, cudaMemcpyDeviceToDevice, s),
-                       "cudaMemcpyAsync(bucket)"));
-    if ((b & 1) == 0) NSB_TRY(quick_sort_level(keys + st, tmp + st, len, leaf, aux, s));
-  }
+  *out = &x;
   return NS_OK;
 }
 
-// ===========================================================================
-// Multi-level, multi-segment partition (default).  Every level partitions ALL
-// oversized segments at once with at most 256 splitters per segment, so the
-// count/scatter kernels stay cheap (8-step search, <= 511 buckets, coalesced
-// ~32-key runs per bucket per CTA) and a whole level costs one host read,
-// instead of one per bucket.  Segments ping-pong between the key buffer and
-// tmp at fixed positions; buckets that fit one CTA are sorted straight into
-// the key buffer (jobs), constant "equal" buckets are copied, the rest form
-// the next level's segments.  Random input of 16M keys: 2 levels.
-// ===========================================================================
-constexpr int kMlMaxB = 256;
+static int sm_count() {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms;
+}
 
-struct MlSeg {
-  int64_t start, len;
-  int B, spl_off, cnt_off;
-  int64_t chunk0;  // first count/scatter chunk of this segment
-  int64_t smp_off;
+// Resident CTAs per SM of a kernel at (threads, dynamic smem), cached per device.
+static int occupancy(const void* kern, int nt, int smem) {
+  static std::mutex mu;
+  static std::vector<std::pair<std::pair<int, const void*>, int>> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  for (const auto& e : cache)
+    if (e.first.first == dev && e.first.second == kern) return e.second;
+  int b = 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, nt, smem) != cudaSuccess || b < 1) b = 1;
+  cache.push_back({{dev, kern}, b});
+  return b;
+}
+
+static unsigned grid_of(const void* kern, int nt, int smem, int64_t upper) {
+  const int64_t g = (int64_t)sm_count() * occupancy(kern, nt, smem);
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>(g, upper));
+}
+
+struct QsSizes {
+  int64_t max_segs, max_chunks, max_bkt, max_spl, max_jobs;
 };
 
-template <class Key>
-struct MlAux {
-  MlSeg* segs;
-  Key* samples;
-  Key* spl;
-  uint32_t* counts;
-  unsigned long long* fill;
-  int64_t* jobs;
-  size_t max_segs, max_samples, max_spl, max_cnt, max_jobs;
-};
-
-static size_t ml_max_segs(size_t n) { return n / (kSmallTile + 1) + 4; }
-static size_t ml_max_spl(size_t n) { return n / 2048 + 2 * kMlMaxB * ml_max_segs(n) / 64 + 1024; }
-
-static size_t ml_aux_bytes(size_t n, size_t kb = 4) {
-  const size_t segs = ml_max_segs(n), spl = n / 2048 + 512 * segs / 64 + 4096;
-  return align_up(segs * sizeof(MlSeg), 256) + align_up(16 * spl * kb, 256) +
-         align_up(spl * kb, 256) + align_up(2 * spl * 4, 256) + align_up(2 * spl * 8, 256) +
-         align_up(2 * (2 * spl + segs) * 8, 256);
+static QsSizes qs_sizes(int64_t nseg0, int64_t len0) {
+  const int64_t n = nseg0 * len0;
+  const int levels = qs_levels(len0);
+  QsSizes z;
+  // level >= 1 segments are buckets of > kSmallTile keys; level 0 is given
+  z.max_segs = std::max<int64_t>(nseg0, n / (kSmallTile + 1) + 1);
+  z.max_chunks = n / kQsChunk + z.max_segs + 1;
+  // 2B-1 <= 4 len / kQsTarget + 3 buckets, B <= 2 len / kQsTarget + 2 pivots
+  z.max_bkt = std::max<int64_t>(nseg0 * (2 * qs_buckets(len0) - 1), 4 * n / kQsTarget + 3 * z.max_segs) + 64;
+  z.max_spl = std::max<int64_t>(nseg0 * qs_buckets(len0), 2 * n / kQsTarget + 2 * z.max_segs) + 64;
+  // every job holds at least one non-empty bucket of one level
+  z.max_jobs = std::max<int64_t>(nseg0 * (2 * qs_buckets(len0) - 1), 0) +
+               (int64_t)levels * (4 * n / kQsTarget + 3 * z.max_segs) + 64;
+  return z;
 }
 
 template <class Key>
-static MlAux<Key> carve_ml(char* p, size_t n) {
-  MlAux<Key> a;
-  a.max_segs = ml_max_segs(n);
-  a.max_spl = n / 2048 + 512 * a.max_segs / 64 + 4096;
-  a.max_samples = 16 * a.max_spl;
-  a.max_cnt = 2 * a.max_spl;
-  a.max_jobs = 2 * a.max_spl + a.max_segs;
-  a.segs = reinterpret_cast<MlSeg*>(p);
-  p += align_up(a.max_segs * sizeof(MlSeg), 256);
-  a.samples = reinterpret_cast<Key*>(p);
-  p += align_up(a.max_samples * sizeof(Key), 256);
-  a.spl = reinterpret_cast<Key*>(p);
-  p += align_up(a.max_spl * sizeof(Key), 256);
-  a.counts = reinterpret_cast<uint32_t*>(p);
-  p += align_up(a.max_cnt * 4, 256);
-  a.fill = reinterpret_cast<unsigned long long*>(p);
-  p += align_up(a.max_cnt * 8, 256);
-  a.jobs = reinterpret_cast<int64_t*>(p);
-  return a;
-}
-
-__device__ __forceinline__ int seg_of_chunk(const MlSeg* segs, int nseg, int64_t c) {
-  int lo = 0, hi = nseg - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (segs[mid].chunk0 <= c) lo = mid;
-    else hi = mid - 1;
-  }
-  return lo;
-}
-
-__device__ __forceinline__ int seg_of_sample(const MlSeg* segs, int nseg, int64_t i) {
-  int lo = 0, hi = nseg - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (segs[mid].smp_off <= i) lo = mid;
-    else hi = mid - 1;
-  }
-  return lo;
+static size_t qs_temp_bytes(int64_t nseg0, int64_t len0) {
+  const int64_t n = nseg0 * len0;
+  const QsSizes z = qs_sizes(nseg0, len0);
+  size_t b = align_up((size_t)n * sizeof(Key), 256) + align_up(sizeof(QsCounters), 256);
+  b += align_up((size_t)n, 256);
+  b += 2 * align_up((size_t)z.max_segs * sizeof(QsSeg), 256);
+  b += 2 * align_up((size_t)z.max_chunks * 4, 256);
+  b += 2 * align_up((size_t)z.max_spl * sizeof(Key), 256);
+  b += 2 * align_up((size_t)z.max_spl * 16 * 2, 256);
+  b += 2 * align_up((size_t)z.max_bkt * 4, 256);
+  b += 2 * align_up((size_t)z.max_bkt * 8, 256);
+  b += 3 * align_up((size_t)z.max_jobs * sizeof(QsJob), 256);
+  return b;
 }
 
 template <class Key>
-__global__ void ml_sample_kernel(const Key* __restrict__ X, const MlSeg* __restrict__ segs,
-                                 int nseg, int64_t total, Key* __restrict__ samples) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= total) return;
-  const MlSeg sg = segs[seg_of_sample(segs, nseg, i)];
-  const int S = kQsOversample * sg.B;
-  const int64_t j = i - sg.smp_off;
-  const int64_t stride = sg.len / S;
-  const int64_t pos = j * stride + (stride > 1 ? hash32((uint32_t)j) % stride : 0);
-  samples[i] = X[sg.start + pos];
+static QsCtx<Key> qs_carve(Key* keys, void* d_temp, int64_t nseg0, int64_t len0) {
+  const int64_t n = nseg0 * len0;
+  const QsSizes z = qs_sizes(nseg0, len0);
+  char* p = static_cast<char*>(d_temp);
+  auto take = [&](size_t bytes) {
+    char* r = p;
+    p += align_up(bytes, 256);
+    return r;
+  };
+  QsCtx<Key> c;
+  c.keys = keys;
+  c.tmp = reinterpret_cast<Key*>(take((size_t)n * sizeof(Key)));
+  c.n = n;
+  c.nseg0 = nseg0;
+  c.len0 = len0;
+  c.cps0 = (len0 + kQsChunk - 1) / kQsChunk;
+  c.B0 = qs_buckets(len0);
+  c.ctr = reinterpret_cast<QsCounters*>(take(sizeof(QsCounters)));
+  c.ids = reinterpret_cast<uint8_t*>(take((size_t)n));
+  for (int i = 0; i < 2; ++i) c.segs[i] = reinterpret_cast<QsSeg*>(take((size_t)z.max_segs * sizeof(QsSeg)));
+  for (int i = 0; i < 2; ++i) c.chunk_seg[i] = reinterpret_cast<int32_t*>(take((size_t)z.max_chunks * 4));
+  for (int i = 0; i < 2; ++i) c.spl[i] = reinterpret_cast<Key*>(take((size_t)z.max_spl * sizeof(Key)));
+  for (int i = 0; i < 2; ++i) c.cells[i] = reinterpret_cast<uint16_t*>(take((size_t)z.max_spl * 16 * 2));
+  for (int i = 0; i < 2; ++i) c.cnt[i] = reinterpret_cast<uint32_t*>(take((size_t)z.max_bkt * 4));
+  for (int i = 0; i < 2; ++i) c.fill[i] = reinterpret_cast<unsigned long long*>(take((size_t)z.max_bkt * 8));
+  for (int i = 0; i < 3; ++i) c.jobs[i] = reinterpret_cast<QsJob*>(take((size_t)z.max_jobs * sizeof(QsJob)));
+  c.max_segs = z.max_segs;
+  c.max_chunks = z.max_chunks;
+  c.max_bkt = z.max_bkt;
+  c.max_spl = z.max_spl;
+  c.max_jobs = z.max_jobs;
+  return c;
 }
 
+// Leaf tile shapes per class (4096 / 8192 / 16384 keys): int32 at 32 keys per
+// thread, int64 at 16.
+template <class Key, int CLS> struct QsLeafShape;
+template <> struct QsLeafShape<int32_t, 0> { static constexpr int NT = 128, K = 32; };
+template <> struct QsLeafShape<int32_t, 1> { static constexpr int NT = 256, K = 32; };
+template <> struct QsLeafShape<int32_t, 2> { static constexpr int NT = 512, K = 32; };
+template <> struct QsLeafShape<int64_t, 0> { static constexpr int NT = 256, K = 16; };
+template <> struct QsLeafShape<int64_t, 1> { static constexpr int NT = 512, K = 16; };
+template <> struct QsLeafShape<int64_t, 2> { static constexpr int NT = 1024, K = 16; };
+
+template <int CLS, int LF, class Key>
+static int qs_launch_leaf(const QsCtx<Key>& c, int64_t upper, cudaStream_t s) {
+  constexpr int NT = QsLeafShape<Key, CLS>::NT, K = QsLeafShape<Key, CLS>::K;
+  constexpr int smem = tile_smem_bytes<NT, K, Key>();
+  auto* kern = qs_leaf_kernel<NT, K, LF, Key>;
+  NSB_TRY(ensure_smem_attr(reinterpret_cast<const void*>(kern), smem, "cudaFuncSetAttribute(qs_leaf)"));
+  {
+    Prof prof(PK_QS_BUCKET, s);
+    kern<<<grid_of(reinterpret_cast<const void*>(kern), NT, smem, upper), NT, smem, s>>>(c, CLS);
+  }
+  return check_launch("qs_leaf_kernel");
+}
+
+// Sorts nseg0 back-to-back segments of len0 (> kSmallTile) keys each.
 template <class Key>
-__global__ void ml_splitter_kernel(const Key* __restrict__ samples,
-                                   const MlSeg* __restrict__ segs, int nseg,
-                                   Key* __restrict__ spl) {
-  const int sgi = blockIdx.x;
-  if (sgi >= nseg) return;
-  const MlSeg sg = segs[sgi];
-  const int S = kQsOversample * sg.B;
-  for (int j = threadIdx.x; j < sg.B; j += blockDim.x)
-    spl[sg.spl_off + j] =
-        j < sg.B - 1 ? samples[sg.smp_off + (int64_t)(j + 1) * S / sg.B - 1] : KeyT<Key>::kMax;
-}
-
-template <int LOGB, class Key>
-__device__ __forceinline__ int ml_classify(const Key* spl, Key key) {
-  constexpr int B = 1 << LOGB;
-  int j = 0;
-#pragma unroll
-  for (int step = B >> 1; step >= 1; step >>= 1)
-    if (spl[j + step - 1] < key) j += step;
-  return (j < B - 1 && spl[j] == key) ? 2 * j + 1 : 2 * j;
-}
-
-constexpr int kMlNT = 512, kMlPer = 16, kMlChunk = kMlNT * kMlPer;
-
-// Per-warp private histograms: a warp's lanes that share a bucket are
-// combined with __match_any_sync and one lane updates the warp's own row, so
-// no shared-memory atomics contend (with only 2B-1 <= 511 buckets, 16 warps
-// hammering one shared histogram serialised on the atomic unit).
-constexpr int kMlWarps = kMlNT / 32;
-
-// Lanes of the warp holding the same bucket id, from one ballot per id bit
-// (cheaper than __match_any_sync, which measured as the bottleneck of the
-// count/scatter kernels).  Ids are < 2^nbits; an invalid lane passes -1 and
-// lands in the all-ones group, which callers never use as a real id.
-template <int NBITS>
-__device__ __forceinline__ unsigned warp_peers(int b) {
-  unsigned m = kFull;
-#pragma unroll
-  for (int i = 0; i < NBITS; ++i) {
-    const bool bit = (b >> i) & 1;
-    const unsigned bal = __ballot_sync(kFull, bit);
-    m &= bit ? bal : ~bal;
-  }
-  return m;
-}
-
-// Per-CTA bucket histogram: runs of equal ids among consecutive lanes are
-// found with one ballot (warp_run) and charged with ONE shared atomic by the
-// run's head lane; equal ids in different runs just add separately.
-template <int LOGB, class Key>
-__device__ __forceinline__ void ml_hist(const Key* spl, const Key (&k)[kMlPer],
-                                        int (&bk)[kMlPer], int64_t c0, int64_t c1,
-                                        uint32_t* hist) {
-#pragma unroll
-  for (int u = 0; u < kMlPer; ++u) {
-    const int64_t i = c0 + u * kMlNT + threadIdx.x;
-    bk[u] = i < c1 ? ml_classify<LOGB>(spl, k[u]) : -1;
-    const WarpRun r = warp_run(bk[u]);
-    if (bk[u] >= 0 && r.head) atomicAdd(&hist[bk[u]], (uint32_t)r.len);
-  }
-}
-
-template <int LOGB, class Key>
-__device__ __noinline__ void ml_count_body(const Key* __restrict__ X, const MlSeg& sg,
-                                              const Key* spl, uint32_t* hist,
-                                              uint32_t* __restrict__ counts) {
-  const int NB = 2 * sg.B - 1;
-  const int64_t c0 = sg.start + (blockIdx.x - sg.chunk0) * (int64_t)kMlChunk;
-  const int64_t c1 = min(sg.start + sg.len, c0 + kMlChunk);
-  Key k[kMlPer];
-  int bk[kMlPer];
-#pragma unroll
-  for (int u = 0; u < kMlPer; ++u) {
-    const int64_t i = c0 + u * kMlNT + threadIdx.x;
-    k[u] = i < c1 ? __ldg(X + i) : 0;
-  }
-  ml_hist<LOGB>(spl, k, bk, c0, c1, hist);
-  __syncthreads();
-  for (int b = threadIdx.x; b < NB; b += kMlNT) {
-    const uint32_t t = hist[b];
-    if (t) atomicAdd(&counts[sg.cnt_off + b], t);
-  }
-}
-
-#define NSB_LOGB_DISPATCH(B, CALL)        \
-  switch (B) {                            \
-    case 2: CALL(1); break;               \
-    case 4: CALL(2); break;               \
-    case 8: CALL(3); break;               \
-    case 16: CALL(4); break;              \
-    case 32: CALL(5); break;              \
-    case 64: CALL(6); break;              \
-    case 128: CALL(7); break;             \
-    default: CALL(8); break;              \
-  }
-
-template <class Key>
-__global__ void __launch_bounds__(kMlNT, 2)
-    ml_count_kernel(const Key* __restrict__ X, const MlSeg* __restrict__ segs, int nseg,
-                    const Key* __restrict__ gspl, uint32_t* __restrict__ counts) {
-  __shared__ Key spl[kMlMaxB];
-  __shared__ uint32_t hist[2 * kMlMaxB];
-  const MlSeg sg = segs[seg_of_chunk(segs, nseg, blockIdx.x)];
-  for (int i = threadIdx.x; i < sg.B; i += kMlNT) spl[i] = gspl[sg.spl_off + i];
-  for (int i = threadIdx.x; i < 2 * sg.B - 1; i += kMlNT) hist[i] = 0;
-  __syncthreads();
-#define NSB_COUNT_CALL(L) ml_count_body<L>(X, sg, spl, hist, counts)
-  NSB_LOGB_DISPATCH(sg.B, NSB_COUNT_CALL)
-#undef NSB_COUNT_CALL
-}
-
-template <int LOGB, class Key>
-__device__ __noinline__ void ml_scatter_body(const Key* __restrict__ X, const MlSeg& sg,
-                                                const Key* spl, uint32_t* hist,
-                                                unsigned long long* __restrict__ fill,
-                                                Key* __restrict__ Y) {
-  const int NB = 2 * sg.B - 1;
-  const int lane = threadIdx.x & 31;
-  const int64_t c0 = sg.start + (blockIdx.x - sg.chunk0) * (int64_t)kMlChunk;
-  const int64_t c1 = min(sg.start + sg.len, c0 + kMlChunk);
-  Key k[kMlPer];
-  int bk[kMlPer];
-#pragma unroll
-  for (int u = 0; u < kMlPer; ++u) {
-    const int64_t i = c0 + u * kMlNT + threadIdx.x;
-    k[u] = i < c1 ? __ldcs(X + i) : 0;
-  }
-  ml_hist<LOGB>(spl, k, bk, c0, c1, hist);
-  __syncthreads();
-  // one global reservation per (CTA, bucket); cursors relative to the segment
-  for (int b = threadIdx.x; b < NB; b += kMlNT) {
-    const uint32_t t = hist[b];
-    if (t)
-      hist[b] = (uint32_t)(atomicAdd(&fill[sg.cnt_off + b], (unsigned long long)t) -
-                           (unsigned long long)sg.start);
-  }
-  __syncthreads();
-  Key* Ys = Y + sg.start;
-#pragma unroll
-  for (int u = 0; u < kMlPer; ++u) {
-    const int b = bk[u];
-    const WarpRun r = warp_run(b);
-    uint32_t base = 0;
-    if (b >= 0 && r.head) base = atomicAdd(&hist[b], (uint32_t)r.len);
-    base = __shfl_sync(kFull, base, r.head_lane);
-    if (b >= 0) Ys[base + (lane - r.head_lane)] = k[u];
-  }
-}
-
-template <class Key>
-__global__ void __launch_bounds__(kMlNT, 2)
-    ml_scatter_kernel(const Key* __restrict__ X, const MlSeg* __restrict__ segs, int nseg,
-                      const Key* __restrict__ gspl, unsigned long long* __restrict__ fill,
-                      Key* __restrict__ Y) {
-  __shared__ Key spl[kMlMaxB];
-  __shared__ uint32_t hist[2 * kMlMaxB];  // counts, then cursors (relative to the segment)
-  const MlSeg sg = segs[seg_of_chunk(segs, nseg, blockIdx.x)];
-  for (int i = threadIdx.x; i < sg.B; i += kMlNT) spl[i] = gspl[sg.spl_off + i];
-  for (int i = threadIdx.x; i < 2 * sg.B - 1; i += kMlNT) hist[i] = 0;
-  __syncthreads();
-#define NSB_SCATTER_CALL(L) ml_scatter_body<L>(X, sg, spl, hist, fill, Y)
-  NSB_LOGB_DISPATCH(sg.B, NSB_SCATTER_CALL)
-#undef NSB_SCATTER_CALL
-}
-
-// Copies jobs (start, len) from src to dst (constant "equal" buckets).
-template <class Key>
-__global__ void copy_jobs_kernel(const Key* __restrict__ src, Key* __restrict__ dst,
-                                 const int64_t* __restrict__ jobs) {
-  const int64_t st = jobs[2 * blockIdx.x], len = jobs[2 * blockIdx.x + 1];
-  for (int64_t i = threadIdx.x; i < len; i += blockDim.x) dst[st + i] = src[st + i];
-}
-
-template <class Key>
-static int ml_quick_sort(Key* keys, Key* tmp, size_t n, int leaf, const MlAux<Key>& ax,
-                         cudaStream_t s) {
-  std::vector<std::pair<int64_t, int64_t>> cur{{0, (int64_t)n}};
-  Key* X = keys;
-  Key* Y = tmp;
-  std::vector<MlSeg> segs;
-  std::vector<uint32_t> counts;
-  std::vector<unsigned long long> fill;
-  while (!cur.empty()) {
-    // ---- plan the level
-    segs.clear();
-    int spl = 0, cnt = 0;
-    int64_t chunks = 0, smp = 0;
-    for (auto [st, len] : cur) {
-      MlSeg g{};
-      g.start = st;
-      g.len = len;
-      int B = 2;
-      while (B < kMlMaxB && (int64_t)B * kQsTarget < len) B *= 2;
-      g.B = B;
-      g.spl_off = spl;
-      g.cnt_off = cnt;
-      g.chunk0 = chunks;
-      g.smp_off = smp;
-      spl += B;
-      cnt += 2 * B - 1;
-      chunks += (len + kMlChunk - 1) / kMlChunk;
-      smp += kQsOversample * B;
-      segs.push_back(g);
-    }
-    const int nseg = (int)segs.size();
-    if ((size_t)nseg > ax.max_segs || (size_t)spl > ax.max_spl || (size_t)cnt > ax.max_cnt ||
-        (size_t)smp > ax.max_samples)
-      return NS_ERR_TEMP;
-    NSB_TRY(check_cuda(cudaMemcpyAsync(ax.segs, segs.data(), nseg * sizeof(MlSeg),
-                                       cudaMemcpyHostToDevice, s),
-                       "H2D(segs)"));
-    // ---- splitters: sample, sort each segment's samples on chip, pick
+static int quick_sort_segments(Key* keys, int64_t nseg0, int64_t len0, int leaf, void* d_temp,
+                               size_t temp_bytes, cudaStream_t s) {
+  if (!d_temp || temp_bytes < qs_temp_bytes<Key>(nseg0, len0)) return NS_ERR_TEMP;
+  const QsCtx<Key> c = qs_carve<Key>(keys, d_temp, nseg0, len0);
+  const QsSizes z = qs_sizes(nseg0, len0);
+  const int levels = qs_levels(len0);
+  constexpr int sample_smem = 0;
+  constexpr int scatter_smem = qs_scatter_smem<Key>();
+  constexpr int count_smem = qs_table_bytes<Key>();
+  NSB_TRY(ensure_smem_attr(reinterpret_cast<const void*>(qs_count_kernel<Key>), count_smem,
+                           "cudaFuncSetAttribute(qs_count)"));
+  NSB_TRY(ensure_smem_attr(reinterpret_cast<const void*>(qs_scatter_kernel<Key>), scatter_smem,
+                           "cudaFuncSetAttribute(qs_scatter)"));
+  for (int l = 0; l < levels; ++l) {
+    const int64_t segs_ub = l == 0 ? nseg0 : z.max_segs;
+    const int64_t chunks_ub = l == 0 ? nseg0 * c.cps0 : z.max_chunks;
     {
       Prof prof(PK_QS_SAMPLE, s);
-      ml_sample_kernel<Key><<<(unsigned)((smp + 255) / 256), 256, 0, s>>>(X, ax.segs, nseg, smp,
-                                                                       ax.samples);
+      qs_sample_kernel<Key><<<grid_of(reinterpret_cast<const void*>(qs_sample_kernel<Key>), 256, sample_smem,
+                                      segs_ub),
+                              256, sample_smem, s>>>(c, l);
     }
-    NSB_TRY(check_launch("ml_sample_kernel"));
-    std::vector<int64_t> sjobs;
-    for (const auto& g : segs) {
-      sjobs.push_back(g.smp_off);
-      sjobs.push_back(kQsOversample * g.B);
-    }
-    NSB_TRY(check_cuda(cudaMemcpyAsync(ax.jobs, sjobs.data(), sjobs.size() * 8,
-                                       cudaMemcpyHostToDevice, s),
-                       "H2D(sample jobs)"));
-    NSB_TRY((launch_bucket_sort<256, 16, 8>(ax.samples, ax.samples, ax.jobs, nseg, s)));
-    {
-      Prof prof(PK_QS_SAMPLE, s);
-      ml_splitter_kernel<Key><<<nseg, 256, 0, s>>>(ax.samples, ax.segs, nseg, ax.spl);
-    }
-    NSB_TRY(check_launch("ml_splitter_kernel"));
-    // ---- count
-    NSB_TRY(check_cuda(cudaMemsetAsync(ax.counts, 0, cnt * 4, s), "memset"));
+    NSB_TRY(check_launch("qs_sample_kernel"));
     {
       Prof prof(PK_QS_COUNT, s);
-      ml_count_kernel<Key><<<(unsigned)chunks, kMlNT, 0, s>>>(X, ax.segs, nseg, ax.spl, ax.counts);
+      qs_count_kernel<Key><<<grid_of(reinterpret_cast<const void*>(qs_count_kernel<Key>), kQsNT, count_smem,
+                                     chunks_ub),
+                             kQsNT, count_smem, s>>>(c, l);
     }
-    NSB_TRY(check_launch("ml_count_kernel"));
-    // One device->host read per LEVEL: bucket sizes drive the plan, as the
-    // split point drives quick_sort_rec (hybrid.hpp:145-148).
-    counts.resize(cnt);
-    NSB_TRY(check_cuda(cudaMemcpyAsync(counts.data(), ax.counts, cnt * 4, cudaMemcpyDeviceToHost,
-                                       s),
-                       "D2H(counts)"));
-    NSB_TRY(check_cuda(cudaStreamSynchronize(s), "cudaStreamSynchronize"));
-    // ---- plan buckets: fill positions, jobs, next level
-    fill.resize(cnt);
-    JobPacker pk;
-    std::vector<int64_t> copies;
-    std::vector<std::pair<int64_t, int64_t>> next;
-    for (const auto& g : segs) {
-      int64_t acc = g.start;
-      const int NB = 2 * g.B - 1;
-      for (int b = 0; b < NB; ++b) {
-        const int64_t len = counts[g.cnt_off + b];
-        fill[g.cnt_off + b] = (unsigned long long)acc;
-        if (len > 0) {
-          if (len <= kSmallTile) {
-            // leaf (a constant bucket too: sorting it from Y is its copy)
-            pk.add(acc, len);
-          } else if (b & 1) {  // large constant bucket: already sorted
-            pk.flush();
-            if (Y != keys) {
-              copies.push_back(acc);
-              copies.push_back(len);
-            }
-          } else {
-            pk.flush();
-            next.push_back({acc, len});
-          }
-        }
-        acc += len;
-      }
-      if (acc != g.start + g.len) return NS_ERR_CUDA;  // lost keys: a device fault
+    NSB_TRY(check_launch("qs_count_kernel"));
+    {
+      Prof prof(PK_QS_PLAN, s);
+      qs_plan_kernel<Key><<<grid_of(reinterpret_cast<const void*>(qs_plan_kernel<Key>), kQsNT, 0, segs_ub),
+                            kQsNT, 0, s>>>(c, l, l == levels - 1);
     }
-    NSB_TRY(check_cuda(cudaMemcpyAsync(ax.fill, fill.data(), cnt * 8, cudaMemcpyHostToDevice, s),
-                       "H2D(fill)"));
+    NSB_TRY(check_launch("qs_plan_kernel"));
     {
       Prof prof(PK_QS_SCATTER, s);
-      ml_scatter_kernel<Key><<<(unsigned)chunks, kMlNT, 0, s>>>(X, ax.segs, nseg, ax.spl, ax.fill, Y);
+      qs_scatter_kernel<Key><<<grid_of(reinterpret_cast<const void*>(qs_scatter_kernel<Key>), kQsNT,
+                                       scatter_smem, chunks_ub),
+                               kQsNT, scatter_smem, s>>>(c, l);
     }
-    NSB_TRY(check_launch("ml_scatter_kernel"));
-    pk.flush();
-    auto& cls = pk.cls;
-    // ---- leaf buckets -> key buffer
-    std::vector<int64_t> jobs;
-    int off[6] = {0, 0, 0, 0, 0, 0};
-    for (int c = 0; c < 4; ++c) {
-      off[c] = (int)(jobs.size() / 2);
-      jobs.insert(jobs.end(), cls[c].begin(), cls[c].end());
-    }
-    off[4] = (int)(jobs.size() / 2);
-    jobs.insert(jobs.end(), copies.begin(), copies.end());
-    off[5] = (int)(jobs.size() / 2);
-    if ((size_t)off[5] > ax.max_jobs) return NS_ERR_TEMP;
-    if (!jobs.empty())
-      NSB_TRY(check_cuda(cudaMemcpyAsync(ax.jobs, jobs.data(), jobs.size() * 8,
-                                         cudaMemcpyHostToDevice, s),
-                         "H2D(jobs)"));
-    NSB_TRY(with_leaf(leaf, [&](auto L) {
-      constexpr int LF = decltype(L)::value;
-      NSB_TRY((launch_bucket_sort<128, 16, LF>(Y, keys, ax.jobs + 2 * off[0], off[1] - off[0], s)));
-      return bucket_sort_classes<LF>(Y, keys, ax.jobs, off, s);
-    }));
-    if (off[5] > off[4]) {
-      copy_jobs_kernel<Key><<<off[5] - off[4], 256, 0, s>>>(Y, keys, ax.jobs + 2 * off[4]);
-      NSB_TRY(check_launch("copy_jobs_kernel"));
-    }
-    // the jobs/fill/segs buffers are rewritten by the next level: the stream
-    // orders that after this level's kernels; the host vectors are copied
-    // by value into pageable H2D copies (staged before cudaMemcpyAsync returns)
-    cur.swap(next);
-    std::swap(X, Y);
+    NSB_TRY(check_launch("qs_scatter_kernel"));
+  }
+  // The three leaf classes are independent: they run concurrently on two
+  // side streams forked from (and joined back into) the caller's stream, so
+  // a small sort pays one tile-sort latency instead of three (the fork/join
+  // is event-based and therefore also valid inside a CUDA-graph capture).
+  QsSide* side = nullptr;
+  NSB_TRY(qs_side_streams(&side));
+  NSB_TRY(check_cuda(cudaEventRecord(side->fork, s), "cudaEventRecord(fork)"));
+  for (int i = 0; i < 2; ++i)
+    NSB_TRY(check_cuda(cudaStreamWaitEvent(side->s[i], side->fork, 0), "cudaStreamWaitEvent"));
+  NSB_TRY(with_leaf(leaf, [&](auto L) {
+    constexpr int LF = decltype(L)::value;
+    NSB_TRY((qs_launch_leaf<0, LF>(c, z.max_jobs, side->s[0])));
+    NSB_TRY((qs_launch_leaf<1, LF>(c, z.max_jobs, side->s[1])));
+    return qs_launch_leaf<2, LF>(c, z.max_jobs, s);
+  }));
+  for (int i = 0; i < 2; ++i) {
+    NSB_TRY(check_cuda(cudaEventRecord(side->join[i], side->s[i]), "cudaEventRecord(join)"));
+    NSB_TRY(check_cuda(cudaStreamWaitEvent(s, side->join[i], 0), "cudaStreamWaitEvent"));
   }
   return NS_OK;
 }
 
 size_t quick_sort_temp(size_t n) {
   if (n <= (size_t)kSmallTile) return merge_sort_temp(n);
-  return align_up(n * 4, 256) + std::max(qs_aux_bytes(), ml_aux_bytes(n));
+  return qs_temp_bytes<int32_t>(1, (int64_t)n);
 }
-
-// int64 keys always take the multi-level partition (its classifier is a
-// plain splitter search; the single-level prefix table is int32-specific)
 size_t quick_sort_temp_i64(size_t n) {
   if (n <= (size_t)kSmallTile) return merge_sort_temp_i64(n);
-  return align_up(n * 8, 256) + ml_aux_bytes(n, 8);
+  return qs_temp_bytes<int64_t>(1, (int64_t)n);
+}
+size_t quick_sort_segments_temp(size_t nseg, size_t len, size_t key_bytes) {
+  if (len <= (size_t)kSmallTile) return 0;
+  return key_bytes == 8 ? qs_temp_bytes<int64_t>((int64_t)nseg, (int64_t)len)
+                        : qs_temp_bytes<int32_t>((int64_t)nseg, (int64_t)len);
+}
+int quick_sort_segments_device(int32_t* keys, size_t nseg, size_t len, int leaf, void* d_temp,
+                               size_t temp_bytes, cudaStream_t s) {
+  return quick_sort_segments(keys, (int64_t)nseg, (int64_t)len, leaf, d_temp, temp_bytes, s);
+}
+int quick_sort_segments_device(int64_t* keys, size_t nseg, size_t len, int leaf, void* d_temp,
+                               size_t temp_bytes, cudaStream_t s) {
+  return quick_sort_segments(keys, (int64_t)nseg, (int64_t)len, leaf, d_temp, temp_bytes, s);
 }
 
 }  // namespace nsb
@@ -946,24 +1060,14 @@ size_t ns_quick_sort_temp_bytes(size_t n) { return quick_sort_temp(n); }
 int ns_quick_sort_i32(int32_t* d_keys, size_t n, uint32_t width_mask, int varsort_max,
                       void* d_temp, size_t temp_bytes, void* stream) {
   if (n > 0 && d_keys == nullptr) return NS_ERR_INVALID;
+  if (n > (size_t)INT64_MAX / 8) return NS_ERR_INVALID;
   if (n <= 1) return NS_OK;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int leaf = leaf_of(width_mask, varsort_max);
-  if (n <= (size_t)kSmallTile) return small_sort(d_keys, n, leaf, d_temp, temp_bytes, s);
-  if (!d_temp || temp_bytes < quick_sort_temp(n)) return NS_ERR_TEMP;
-  int32_t* tmp = static_cast<int32_t*>(d_temp);
-  char* auxp = static_cast<char*>(d_temp) + align_up(n * 4, 256);
-  // Single level (up to 4096 splitters, measured faster while its buckets
-  // fit one CTA) up to 2^25 keys; the multi-level partition above that,
-  // where a single level would leave thousands of oversized buckets.
-  // NSB_QS=1 / 2 forces one or the other.
-  static const int mode = [] {
-    const char* e = getenv("NSB_QS");
-    return e ? atoi(e) : 0;
-  }();
-  const bool single = mode == 1 || (mode == 0 && n <= (size_t(1) << 25));
-  if (single) return quick_sort_level(d_keys, tmp, n, leaf, carve_aux(auxp), s);
-  return ml_quick_sort(d_keys, tmp, n, leaf, carve_ml<int32_t>(auxp, n), s);
+  // n <= kSmallTile: one CTA (or two tiles and a merge) — the merge sort's
+  // small path, whose tile sort is this layer's base case
+  if (n <= (size_t)kSmallTile) return merge_sort_device(d_keys, n, leaf, d_temp, temp_bytes, s);
+  return quick_sort_segments(d_keys, 1, (int64_t)n, leaf, d_temp, temp_bytes, s);
 }
 
 size_t ns_quick_sort_temp_bytes_i64(size_t n) { return quick_sort_temp_i64(n); }
@@ -971,14 +1075,12 @@ size_t ns_quick_sort_temp_bytes_i64(size_t n) { return quick_sort_temp_i64(n); }
 int ns_quick_sort_i64(int64_t* d_keys, size_t n, uint32_t width_mask, int varsort_max,
                       void* d_temp, size_t temp_bytes, void* stream) {
   if (n > 0 && d_keys == nullptr) return NS_ERR_INVALID;
+  if (n > (size_t)INT64_MAX / 16) return NS_ERR_INVALID;
   if (n <= 1) return NS_OK;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int leaf = leaf_of(width_mask, varsort_max);
-  if (n <= (size_t)kSmallTile) return small_sort(d_keys, n, leaf, d_temp, temp_bytes, s);
-  if (!d_temp || temp_bytes < quick_sort_temp_i64(n)) return NS_ERR_TEMP;
-  int64_t* tmp = static_cast<int64_t*>(d_temp);
-  char* auxp = static_cast<char*>(d_temp) + align_up(n * 8, 256);
-  return ml_quick_sort(d_keys, tmp, n, leaf, carve_ml<int64_t>(auxp, n), s);
+  if (n <= (size_t)kSmallTile) return merge_sort_device(d_keys, n, leaf, d_temp, temp_bytes, s);
+  return quick_sort_segments(d_keys, 1, (int64_t)n, leaf, d_temp, temp_bytes, s);
 }
 
 }  // extern "C"

@@ -1,0 +1,145 @@
+"""GPU parity of the device-planned quick sort (quicksort.cu): every partition
+path — one and several levels, many segments per level, packed leaf jobs of
+every size class, constant ("equal") buckets moved or left in place, and the
+one-CTA fallback for a bucket that is still oversized after the last level —
+against the CPU oracle (optimized_quick_sort restated, hybrid.hpp:137-150)
+and numpy.  The call must also be capturable in a CUDA graph (no host
+synchronisation inside)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _dev(a, cuda):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(a)).to(cuda)
+
+
+def _hash32(x):
+    x &= 0xFFFFFFFF
+    x ^= x >> 16
+    x = (x * 0x7FEB352D) & 0xFFFFFFFF
+    x ^= x >> 15
+    x = (x * 0x846CA68B) & 0xFFFFFFFF
+    x ^= x >> 16
+    return x
+
+
+def _buckets(n):
+    b = 2
+    while b < 128 and b * 4096 < n:
+        b *= 2
+    return b
+
+
+def _sample_positions(n, level=0):
+    """The level's sample positions (qs_sample_kernel), to build inputs that
+    defeat the sampling on purpose."""
+    B = _buckets(n)
+    S = 16 * B
+    stride = n // S
+    return [i * stride + (_hash32((i * 2654435761 + level) & 0xFFFFFFFF) % stride
+                          if stride > 1 else 0) for i in range(S)]
+
+
+@pytest.mark.parametrize("n", [16385, 20000, 65536, 100_003, 1 << 20, 3_000_001, 5_000_000])
+@pytest.mark.parametrize("dist", ["random", "sorted", "nearly_sorted"])
+def test_quick_sort_levels_match_oracle(ns, cuda, oracle, n, dist):
+    a = oracle.generate_i32(dist, n, 11)
+    t = _dev(a, cuda)
+    ns.optimized_quick_sort(t, ns.find_config("3To5"))
+    assert np.array_equal(t.cpu().numpy(), oracle.quick_sort(a, "3To5"))
+
+
+@pytest.mark.parametrize("kind", ["few_values", "one_heavy", "two_values", "all_equal",
+                                  "extremes", "runs"])
+def test_quick_sort_duplicate_shapes(ns, cuda, kind):
+    """Equal buckets (constant) of every size, including > 16384 keys moved
+    from tmp to the caller's buffer, and INT_MIN / INT_MAX keys (INT_MAX is
+    the pivot pad)."""
+    rng = np.random.default_rng(5)
+    n = 2_000_000
+    if kind == "few_values":
+        a = rng.integers(0, 37, n).astype(np.int32)
+    elif kind == "one_heavy":
+        a = rng.integers(0, 2**31 - 1, n).astype(np.int32)
+        a[rng.random(n) < 0.6] = 12345
+    elif kind == "two_values":
+        a = np.where(rng.random(n) < 0.5, -7, 2**31 - 1).astype(np.int32)
+    elif kind == "all_equal":
+        a = np.full(n, 42, np.int32)
+    elif kind == "extremes":
+        a = rng.choice(np.array([-2**31, -1, 0, 2**31 - 1], np.int32), n)
+    else:
+        a = (np.arange(n) // 50000).astype(np.int32)[::-1].copy()
+    t = _dev(a, cuda)
+    ns.optimized_quick_sort(t, ns.find_config("3To5"))
+    assert np.array_equal(t.cpu().numpy(), np.sort(a))
+
+
+def test_quick_sort_oversized_bucket_fallback(ns, cuda):
+    """Pivots drawn from an input built against the sampling positions: every
+    sampled key is spread over a wide range, every other key is distinct and
+    falls between the first two pivots, so after the (single) level one
+    bucket holds ~all keys — the one-CTA global-memory fallback sorts it."""
+    n = 300_000
+    pos = _sample_positions(n)
+    rng = np.random.default_rng(3)
+    a = rng.permutation(np.arange(10, 10 + n, dtype=np.int64)).astype(np.int32)
+    spread = np.linspace(0, 2**31 - 2, len(pos)).astype(np.int64)
+    spread[0] = 5  # first pivot region: everything else lands above it
+    a[np.array(pos)] = spread.astype(np.int32)
+    a[np.array(pos[1:])] = (spread[1:] + 10_000_000).clip(max=2**31 - 2).astype(np.int32)
+    t = _dev(a, cuda)
+    ns.optimized_quick_sort(t, ns.find_config("3To5"))
+    assert np.array_equal(t.cpu().numpy(), np.sort(a))
+
+
+@pytest.mark.parametrize("nseg,seg_len", [(3, 16385), (5, 70_000), (40, 30_000), (2, 1_000_000)])
+def test_segmented_quick_sort_large_segments(ns, cuda, oracle, nseg, seg_len):
+    """Segments above one CTA: all of them are level-0 segments of ONE
+    device-planned partition (no per-segment host loop)."""
+    a = oracle.generate_i32("random", nseg * seg_len, 9)
+    t = _dev(a, cuda)
+    ns.segmented_sort(t, seg_len, ns.find_config("3To5"), ns.Algorithm.quick_sort)
+    want = np.sort(a.reshape(nseg, seg_len), axis=1).reshape(-1)
+    assert np.array_equal(t.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("cfg_name", ["Classic", "3To5", "6To8", "VarSort3"])
+def test_quick_sort_every_leaf_shape(ns, cuda, oracle, cfg_name):
+    a = oracle.generate_i32("random", 1_500_000, 4)
+    t = _dev(a, cuda)
+    ns.optimized_quick_sort(t, ns.find_config(cfg_name))
+    assert np.array_equal(t.cpu().numpy(), oracle.quick_sort(a, cfg_name))
+
+
+def test_quick_sort_in_cuda_graph(ns, cuda):
+    """No host synchronisation inside ns_quick_sort_i32: the call is captured
+    in a CUDA graph and replayed on fresh input."""
+    import torch
+    n = 3_000_000
+    a = _dev(np.random.default_rng(1).integers(-2**31, 2**31 - 1, n).astype(np.int32), cuda)
+    w = a.clone()
+    cfg = ns.find_config("3To5")
+    ns.optimized_quick_sort(w, cfg)  # warm: scratch + attributes
+    w.copy_(a)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        w.copy_(a)
+        ns.optimized_quick_sort(w, cfg)
+    for _ in range(3):
+        w.zero_()
+        g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(w, torch.sort(a).values)
+
+
+def test_quick_sort_i64_levels(ns, cuda, oracle):
+    for n in (20000, 1 << 20, 3_000_001):
+        a = oracle.generate_i64("random", n, 2)
+        t = _dev(a, cuda)
+        ns.optimized_quick_sort(t, ns.find_config("3To5"))
+        assert np.array_equal(t.cpu().numpy(), np.sort(a))
