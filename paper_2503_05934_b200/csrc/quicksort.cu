@@ -160,12 +160,12 @@ __device__ __forceinline__ uint32_t hash32(uint32_t x) {
 
 // ---- 1. sample + pivots -----------------------------------------------------
 // Sample i of a segment sits at i*stride + jitter(i) (stride = len / S), so
-// sorted input still yields evenly spaced pivots.
+// sorted input still yields evenly spaced pivots; the jitter is a hash scaled
+// into [0, stride) with one multiply-high (a 64-bit modulo here measured as
+// most of the sample kernel's time).
 __device__ __forceinline__ int64_t qs_sample_pos(int i, int64_t stride, int level) {
-  return (int64_t)i * stride +
-         (stride > 1 ? (int64_t)(hash32((uint32_t)i * 2654435761u + (uint32_t)level) %
-                                 (uint64_t)stride)
-                     : 0);
+  const uint32_t st = stride > 0xffffffffll ? 0xffffffffu : (uint32_t)stride;
+  return (int64_t)i * stride + (int64_t)__umulhi(hash32((uint32_t)i * 2654435761u + (uint32_t)level), st);
 }
 
 // The classifier's prefix cells (see "classification" below): the pivots'

@@ -39,8 +39,8 @@ def _sample_positions(n, level=0):
     B = _buckets(n)
     S = 16 * B
     stride = n // S
-    return [i * stride + (_hash32((i * 2654435761 + level) & 0xFFFFFFFF) % stride
-                          if stride > 1 else 0) for i in range(S)]
+    return [i * stride + ((_hash32((i * 2654435761 + level) & 0xFFFFFFFF) * min(stride, 2**32 - 1))
+                          >> 32) for i in range(S)]
 
 
 @pytest.mark.parametrize("n", [16385, 20000, 65536, 100_003, 1 << 20, 3_000_001, 5_000_000])
