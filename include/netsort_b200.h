@@ -43,7 +43,9 @@ typedef enum ns_status {
   NS_ERR_INVALID = 1, /* bad argument / config (reference: std::invalid_argument) */
   NS_ERR_CUDA = 2,    /* CUDA runtime / launch error, or no device */
   NS_ERR_OOM = 3,     /* device or pinned-host allocation failed */
-  NS_ERR_TEMP = 4     /* caller scratch smaller than *_temp_bytes */
+  NS_ERR_TEMP = 4,    /* caller scratch smaller than *_temp_bytes (or an output
+                         buffer smaller than the result, see sample sort) */
+  NS_ERR_NCCL = 5     /* NCCL unavailable or an NCCL call failed */
 } ns_status;
 
 typedef enum ns_algorithm { NS_MERGE_SORT = 0, NS_QUICK_SORT = 1 } ns_algorithm;
@@ -114,9 +116,16 @@ int ns_quick_sort_i64(int64_t* d_keys, size_t n, uint32_t width_mask, int varsor
  * independent arrays packed contiguously, array i = d_keys[d_offsets[i] ..
  * d_offsets[i+1]); every length must lie in [0, 8].  Each array of length
  * 2..8 is sorted by its own size-specific network; 0/1 are no-ops (the
- * reference's apply_varsort rule, networks.hpp:166-176).  Lengths outside
- * [0, 8] are NS_ERR_INVALID (checked on the device; the call then
- * synchronises to report it). */
+ * reference's apply_varsort rule, networks.hpp:166-176).  A validation pass
+ * over all offsets runs first: if any length lies outside [0, 8] NO key is
+ * modified and the status is NS_ERR_INVALID.
+ *   ns_sort_small_batch_async_i32: stream-ordered, never synchronises (CUDA-
+ *     graph capturable); the status (NS_OK / NS_ERR_INVALID) is written to the
+ *     caller's device word *d_status.
+ *   ns_sort_small_batch_i32: the same, then reads the status back (one
+ *     4-byte D2H + stream synchronise) and returns it. */
+int ns_sort_small_batch_async_i32(int32_t* d_keys, const uint32_t* d_offsets, size_t num_arrays,
+                                  int* d_status, void* stream);
 int ns_sort_small_batch_i32(int32_t* d_keys, const uint32_t* d_offsets, size_t num_arrays,
                             void* stream);
 
@@ -187,6 +196,62 @@ size_t ns_merge_pairs_temp_bytes(int64_t total, int npairs);
 int ns_merge_pairs_i32(const int32_t* const* a_ptrs, const int64_t* a_lens,
                        const int32_t* const* b_ptrs, const int64_t* b_lens, int npairs,
                        int32_t* d_out, void* d_temp, size_t temp_bytes, void* stream);
+
+/* ---- multi-GPU, one host thread --------------
+ * The sample sort of BASELINE config 5 over ngpu devices driven by ONE host
+ * thread: shard d = d_shards[d][0 .. counts[d]) on device devices[d], its
+ * stream streams[d] and scratch d_temps[d] (temp_bytes each, from
+ * ns_sample_sort_multi_temp_bytes(ngpu, max shard, out_capacity)).  Steps:
+ * local merge sort (the config's network base case) -> 255 regular samples
+ * per shard -> all-gather -> g-1 common splitters -> bucket bounds ->
+ * exchange -> g-way merge.  Device d receives the d-th key range of the
+ * sorted array in d_out[d][0 .. out_counts[d]); concatenated in device order
+ * the outputs are the sorted input.  The shards are sorted in place as a
+ * side effect.
+ *   exchange NS_EXCHANGE_NCCL: grouped ncclSend / ncclRecv over `comms`
+ *     (one communicator per device, e.g. ns_nccl_comms_init_all = the
+ *     single-process ncclCommInitAll), then a merge of the received runs;
+ *   exchange NS_EXCHANGE_P2P: no receive buffer — each device merges the
+ *     runs destined to it directly out of its peers' memory over NVLink
+ *     (peer access; comms may be NULL; devices may repeat, e.g. several
+ *     virtual ranks on one GPU).
+ * The bucket bounds come to the host once (they size the exchange) and the
+ * call synchronises every stream before returning (peers read the shards).
+ * A result larger than out_capacity returns NS_ERR_TEMP with out_counts set.
+ * NCCL is loaded at run time (libnccl.so.2); ns_nccl_available() says
+ * whether it could be. */
+typedef struct ncclComm* ns_nccl_comm; /* == ncclComm_t */
+typedef enum ns_exchange { NS_EXCHANGE_NCCL = 0, NS_EXCHANGE_P2P = 1 } ns_exchange;
+int ns_nccl_available(void);
+int ns_nccl_comms_init_all(int ngpu, const int* devices, ns_nccl_comm* comms);
+int ns_nccl_comms_destroy(int ngpu, ns_nccl_comm* comms);
+/* Host-only exchange plan: bounds is ngpu rows of ngpu+1 bucket bounds (row
+ * src = the sorted shard src cut for every destination); writes, per
+ * destination dst, recv_offsets[dst*(ngpu+1) + src] = where src's run starts
+ * in dst's output (row ends with the total) and recv_totals[dst]. */
+int ns_sample_sort_plan(int ngpu, const int64_t* bounds, int64_t* recv_offsets,
+                        int64_t* recv_totals);
+size_t ns_sample_sort_multi_temp_bytes(int ngpu, size_t shard_keys, size_t out_capacity);
+int ns_sample_sort_multi_i32(int ngpu, const int* devices, ns_nccl_comm* comms, int exchange,
+                             int32_t* const* d_shards, const size_t* counts, int32_t* const* d_out,
+                             size_t out_capacity, size_t* out_counts, uint32_t width_mask,
+                             int varsort_max, void* const* d_temps, size_t temp_bytes,
+                             void* const* streams);
+/* Shard by array (BASELINE configs 2 and 4: independent arrays, no
+ * collective).  ns_shard_batch_plan cuts a ragged batch (host offsets,
+ * num_arrays + 1 entries) into nshards contiguous array ranges of about
+ * equal key counts: shard k = arrays [array_begin[k], array_begin[k+1]).
+ * The multi entry points then run the single-device call on every device's
+ * shard (offsets rebased to the shard's first key; status per device). */
+int ns_shard_batch_plan(const uint32_t* h_offsets, size_t num_arrays, int nshards,
+                        size_t* array_begin);
+int ns_sort_small_batch_multi_i32(int ngpu, const int* devices, int32_t* const* d_keys,
+                                  const uint32_t* const* d_offsets, const size_t* num_arrays,
+                                  int* const* d_status, void* const* streams);
+int ns_segmented_sort_multi_i32(int ngpu, const int* devices, int32_t* const* d_keys,
+                                const size_t* num_segments, size_t seg_len, int algorithm,
+                                uint32_t width_mask, int varsort_max, void* const* d_temps,
+                                const size_t* temp_bytes, void* const* streams);
 
 /* CUDA IPC for the pull-based exchange: export the allocation that contains
  * d_ptr (64-byte handle + byte offset of d_ptr inside it), map a peer's

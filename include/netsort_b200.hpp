@@ -218,4 +218,16 @@ void device_merge_sort(std::int64_t* d_keys, size_t n, const NetworkConfig& cfg,
 void device_quick_sort(std::int64_t* d_keys, size_t n, const NetworkConfig& cfg,
                        DeviceScratch& scratch, void* stream = nullptr);
 
+// ---- several GPUs, one host thread (BASELINE config 5) ---------------------
+// optimized_merge_sort's call shape (a HOST array sorted in place,
+// hybrid.hpp:174-177) over several devices: the array is cut into even
+// shards, one per entry of `devices`, uploaded, sample-sorted
+// (ns_sample_sort_multi_i32) and the devices' key ranges are read back in
+// order.  Exchange::nccl creates single-process communicators
+// (ncclCommInitAll; devices must be distinct); Exchange::p2p merges out of
+// the peers' memory over NVLink (devices may repeat).
+enum class Exchange { nccl = NS_EXCHANGE_NCCL, p2p = NS_EXCHANGE_P2P };
+void sample_sort_multi(std::span<std::int32_t> a, const std::vector<int>& devices,
+                       const NetworkConfig& cfg, Exchange exchange = Exchange::nccl);
+
 }  // namespace netsort_b200

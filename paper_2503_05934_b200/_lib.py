@@ -18,7 +18,8 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("NETSORT_B200_LIB") or os.path.join(PKG, "lib", "libnetsort_b200.so")
 CSRC = os.path.join(PKG, "csrc")
 
-NS_OK, NS_ERR_INVALID, NS_ERR_CUDA, NS_ERR_OOM, NS_ERR_TEMP = 0, 1, 2, 3, 4
+NS_OK, NS_ERR_INVALID, NS_ERR_CUDA, NS_ERR_OOM, NS_ERR_TEMP, NS_ERR_NCCL = 0, 1, 2, 3, 4, 5
+NS_EXCHANGE_NCCL, NS_EXCHANGE_P2P = 0, 1
 NS_MERGE_SORT, NS_QUICK_SORT = 0, 1
 
 _vp, _sz, _u32, _i32, _i64 = C.c_void_p, C.c_size_t, C.c_uint32, C.c_int, C.c_int64
@@ -44,6 +45,7 @@ SIGNATURES = {
     "ns_quick_sort_i64": (_i32, [_vp, _sz, _u32, _i32, _vp, _sz, _vp]),
     "ns_quick_sort_i32": (_i32, [_vp, _sz, _u32, _i32, _vp, _sz, _vp]),
     "ns_sort_small_batch_i32": (_i32, [_vp, _vp, _sz, _vp]),
+    "ns_sort_small_batch_async_i32": (_i32, [_vp, _vp, _sz, _vp, _vp]),
     "ns_sort_pairs_temp_bytes_i32": (_sz, [_sz]),
     "ns_sort_pairs_i32": (_i32, [_vp, _vp, _sz, _vp, _sz, _vp]),
     "ns_argsort_temp_bytes_i32": (_sz, [_sz]),
@@ -61,6 +63,17 @@ SIGNATURES = {
     "ns_merge_runs_i64": (_i32, [_vp, _vp, _i32, _vp, _sz, _vp]),
     "ns_merge_pairs_temp_bytes": (_sz, [_i64, _i32]),
     "ns_merge_pairs_i32": (_i32, [_vp, _vp, _vp, _vp, _i32, _vp, _vp, _sz, _vp]),
+    "ns_nccl_available": (_i32, []),
+    "ns_nccl_comms_init_all": (_i32, [_i32, _vp, _vp]),
+    "ns_nccl_comms_destroy": (_i32, [_i32, _vp]),
+    "ns_sample_sort_plan": (_i32, [_i32, _vp, _vp, _vp]),
+    "ns_sample_sort_multi_temp_bytes": (_sz, [_i32, _sz, _sz]),
+    "ns_sample_sort_multi_i32": (_i32, [_i32, _vp, _vp, _i32, _vp, _vp, _vp, _sz, _vp, _u32, _i32,
+                                        _vp, _sz, _vp]),
+    "ns_shard_batch_plan": (_i32, [_vp, _sz, _i32, _vp]),
+    "ns_sort_small_batch_multi_i32": (_i32, [_i32, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "ns_segmented_sort_multi_i32": (_i32, [_i32, _vp, _vp, _vp, _sz, _i32, _u32, _i32, _vp, _vp,
+                                           _vp]),
     "ns_ipc_get_handle": (_i32, [_vp, _vp, C.POINTER(C.c_uint64)]),
     "ns_ipc_open_handle": (_i32, [_vp, C.POINTER(C.c_void_p)]),
     "ns_ipc_close": (_i32, [_vp]),

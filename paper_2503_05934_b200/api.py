@@ -20,6 +20,7 @@ from __future__ import annotations
 
 import ctypes as C
 import enum
+import threading
 from dataclasses import dataclass, field
 from typing import Optional, Sequence
 
@@ -158,22 +159,52 @@ def leaf_width(cfg: NetworkConfig) -> int:
 
 
 # ---- device scratch -------------------------------------------------------
+# One cached scratch buffer per (device, stream): a sort's kernels only ever
+# touch the scratch of the stream they run on, so sorts on different streams
+# never share one, and the caching allocator's stream bookkeeping stays exact
+# (the buffer is allocated while its stream is current and used only there).
+# Calls that enqueue on the same stream from several host threads are
+# serialised by a per-(device, stream) lock held across the enqueue, so one
+# sort's kernels are all queued before the next sort's.
 
 _SCRATCH: dict = {}
+_LOCKS: dict = {}
+_LOCKS_GUARD = threading.Lock()
 
 
-def scratch(nbytes: int, device) -> int:
-    """Device pointer to >= nbytes of cached scratch on `device` (0 if none)."""
+def _key(device, stream: int):
+    d = torch.device(device)
+    return (d.index if d.index is not None else torch.cuda.current_device(), int(stream))
+
+
+def _lock(key):
+    with _LOCKS_GUARD:
+        lk = _LOCKS.get(key)
+        if lk is None:
+            lk = _LOCKS[key] = threading.RLock()
+        return lk
+
+
+def scratch(nbytes: int, device, stream: Optional[int] = None) -> int:
+    """Device pointer to >= nbytes of cached scratch for (device, stream)."""
     if nbytes == 0:
         return 0
-    key = torch.device(device).index if torch.device(device).index is not None else \
-        torch.cuda.current_device()
+    if stream is None:
+        stream = torch.cuda.current_stream(torch.device(device)).cuda_stream
+    key = _key(device, stream)
     buf = _SCRATCH.get(key)
     if buf is None or buf.numel() < nbytes:
         _SCRATCH.pop(key, None)
-        buf = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{key}")
+        buf = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{key[0]}")
         _SCRATCH[key] = buf
     return buf.data_ptr()
+
+
+def _with_scratch(nbytes: int, t, fn):
+    """fn(scratch_ptr, stream_ptr) under the (device, stream) lock."""
+    strm = _stream_ptr(t)
+    with _lock(_key(t.device, strm)):
+        return fn(scratch(nbytes, t.device, strm), strm)
 
 
 def release_scratch() -> None:
@@ -229,9 +260,9 @@ def _sort(algo: int, a, left, right, cfg: NetworkConfig):
         ptr = a.data_ptr() + a.element_size() * left
         sfx = "" if t == "i32" else "_i64"
         tb = getattr(L, f"ns_{alg}_sort_temp_bytes{sfx}")(cnt)
-        st = getattr(L, f"ns_{alg}_sort_{t}")(ptr, cnt, cfg.width_mask, cfg.varsort_max,
-                                             scratch(tb, a.device), tb, _stream_ptr(a))
-        check(st, what)
+        fn = getattr(L, f"ns_{alg}_sort_{t}")
+        check(_with_scratch(tb, a, lambda tmp, strm: fn(ptr, cnt, cfg.width_mask,
+                                                         cfg.varsort_max, tmp, tb, strm)), what)
     else:
         t = _check_host(a)
         ptr = a.ctypes.data + a.itemsize * left
@@ -270,10 +301,10 @@ def merge(a, left: int, mid: int, right: int):
         offs = (C.c_int64 * 3)(0, mid - left + 1, cnt)
         sfx = "" if t == "i32" else "_i64"
         tb = getattr(L, f"ns_merge_runs_temp_bytes{sfx}")(cnt, 2)
-        check(getattr(L, f"ns_merge_runs_{t}")(a.data_ptr() + a.element_size() * left,
-                                               C.cast(offs, C.c_void_p), 2,
-                                               scratch(tb, a.device), tb, _stream_ptr(a)),
-              "merge")
+        fn = getattr(L, f"ns_merge_runs_{t}")
+        base = a.data_ptr() + a.element_size() * left
+        check(_with_scratch(tb, a, lambda tmp, strm: fn(base, C.cast(offs, C.c_void_p), 2, tmp,
+                                                         tb, strm)), "merge")
     else:
         t = _check_host(a)
         check(getattr(L, f"ns_merge_host_{t}")(a.ctypes.data + a.itemsize * left,
@@ -314,14 +345,25 @@ def run_variant(variant: SortVariant, a, stats: Optional[DispatchStats] = None):
 
 # ---- batch entry points (BASELINE configs 2 and 4) -------------------------
 
-def sort_small_batch(keys, offsets):
+def sort_small_batch(keys, offsets, status=None):
     """Sort every ragged array keys[offsets[i]:offsets[i+1]] (length <= 8) with
     its size-specific network.  keys: CUDA int32, offsets: CUDA int32/uint32
-    (num_arrays + 1 entries, read as uint32)."""
+    (num_arrays + 1 entries, read as uint32).  Without `status` the call
+    reads the validation result back and raises ValueError on a bad length;
+    with `status` (a CUDA int32 tensor of >= 1 element) it stays stream-
+    ordered (graph-capturable) and writes 0 / NS_ERR_INVALID to status[0].
+    A bad length leaves every key untouched."""
     _check_tensor(keys)
     if offsets.dtype not in (torch.int32, torch.uint32) or not offsets.is_cuda:
         raise ValueError("offsets must be a CUDA int32/uint32 tensor")
     num = offsets.numel() - 1
+    if status is not None:
+        if status.dtype != torch.int32 or not status.is_cuda or status.numel() < 1:
+            raise ValueError("status must be a CUDA int32 tensor")
+        check(lib().ns_sort_small_batch_async_i32(keys.data_ptr(), offsets.data_ptr(),
+                                                  max(num, 0), status.data_ptr(),
+                                                  _stream_ptr(keys)), "sort_small_batch")
+        return keys
     check(lib().ns_sort_small_batch_i32(keys.data_ptr(), offsets.data_ptr(), max(num, 0),
                                         _stream_ptr(keys)), "sort_small_batch")
     return keys
@@ -337,9 +379,10 @@ def segmented_sort(keys, seg_len: int, cfg: NetworkConfig,
     L = lib()
     sfx = "" if t == "i32" else "_i64"
     tb = getattr(L, f"ns_segmented_sort_temp_bytes{sfx}")(nseg, seg_len)
-    check(getattr(L, f"ns_segmented_sort_{t}")(keys.data_ptr(), nseg, seg_len, algorithm.value,
-                                               cfg.width_mask, cfg.varsort_max,
-                                               scratch(tb, keys.device), tb, _stream_ptr(keys)),
+    fn = getattr(L, f"ns_segmented_sort_{t}")
+    check(_with_scratch(tb, keys, lambda tmp, strm: fn(keys.data_ptr(), nseg, seg_len,
+                                                        algorithm.value, cfg.width_mask,
+                                                        cfg.varsort_max, tmp, tb, strm)),
           "segmented_sort")
     return keys
 
@@ -359,8 +402,10 @@ def sort_pairs(keys, values=None):
             raise ValueError("values must be a contiguous 4-byte CUDA tensor of len(keys)")
     L = lib()
     tb = L.ns_sort_pairs_temp_bytes_i32(n)
-    check(L.ns_sort_pairs_i32(keys.data_ptr(), values.data_ptr() if values is not None else None,
-                              n, scratch(tb, keys.device), tb, _stream_ptr(keys)), "sort_pairs")
+    vptr = values.data_ptr() if values is not None else None
+    check(_with_scratch(tb, keys, lambda tmp, strm: L.ns_sort_pairs_i32(keys.data_ptr(), vptr, n,
+                                                                         tmp, tb, strm)),
+          "sort_pairs")
     return keys, values
 
 
@@ -372,8 +417,9 @@ def argsort(keys):
     perm = torch.empty(n, dtype=torch.int32, device=keys.device)
     L = lib()
     tb = L.ns_argsort_temp_bytes_i32(n)
-    check(L.ns_argsort_i32(keys.data_ptr(), perm.data_ptr(), n, scratch(tb, keys.device), tb,
-                           _stream_ptr(keys)), "argsort")
+    check(_with_scratch(tb, keys, lambda tmp, strm: L.ns_argsort_i32(keys.data_ptr(),
+                                                                      perm.data_ptr(), n, tmp,
+                                                                      tb, strm)), "argsort")
     return perm.to(torch.int64) if n < 2**31 else perm.view(torch.uint32).to(torch.int64)
 
 

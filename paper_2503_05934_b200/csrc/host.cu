@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstring>
 
 #include "../../include/netsort_b200.hpp"
 #include "common.cuh"
@@ -22,11 +23,18 @@ constexpr int kMaxChunks = 8;
 struct HostCache {
   void* dev = nullptr;
   size_t bytes = 0;
+  // small arrays (<= kSmallTile keys): pinned, device-mapped staging that the
+  // one-CTA sort reads and writes in place over PCIe (zero-copy): one launch
+  // and one synchronise per call, no DMA round trips
+  void* pinned = nullptr;
+  void* mapped = nullptr;
   cudaStream_t stream = nullptr;  // compute
   cudaStream_t copy = nullptr;    // host->device chunks
   cudaEvent_t ev[kMaxChunks] = {};
   ~HostCache() { release(); }
   void release() {
+    if (pinned) cudaFreeHost(pinned);
+    pinned = mapped = nullptr;
     if (dev) cudaFree(dev);
     if (stream) cudaStreamDestroy(stream);
     if (copy) cudaStreamDestroy(copy);
@@ -38,6 +46,12 @@ struct HostCache {
     stream = nullptr;
     copy = nullptr;
   }
+  int ensure_pinned() {
+    if (pinned) return NS_OK;
+    NSB_TRY(check_cuda(cudaHostAlloc(&pinned, (size_t)kSmallTile * 8, cudaHostAllocMapped),
+                       "cudaHostAlloc"));
+    return check_cuda(cudaHostGetDevicePointer(&mapped, pinned, 0), "cudaHostGetDevicePointer");
+  }
   int ensure(size_t need) {
     if (!stream) {
       NSB_TRY(check_cuda(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking),
@@ -48,6 +62,7 @@ struct HostCache {
         NSB_TRY(check_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming),
                            "cudaEventCreate"));
     }
+    if (need == 0) return NS_OK;
     if (bytes >= need) return NS_OK;
     if (dev) cudaFree(dev);
     dev = nullptr;
@@ -57,7 +72,19 @@ struct HostCache {
     return NS_OK;
   }
 };
-static thread_local HostCache g_host;
+// One cache per (host thread, device): a thread that switches devices gets
+// that device's own buffers and streams.
+struct HostCaches {
+  HostCache d[64];
+};
+static thread_local HostCaches g_hosts;
+static int host_cache(HostCache** out) {
+  int dev = 0;
+  NSB_TRY(check_cuda(cudaGetDevice(&dev), "cudaGetDevice"));
+  if (dev < 0 || dev >= 64) return NS_ERR_INVALID;
+  *out = &g_hosts.d[dev];
+  return NS_OK;
+}
 
 // Host-buffer sort.  Large merge sorts overlap the PCIe upload with compute:
 // the array is cut into up to 8 chunks (multiples of the 8192-key tile); each
@@ -87,6 +114,22 @@ static int host_sort(Key* h_keys, size_t n, uint32_t mask, int vs, int algorithm
   if (n <= 1) return NS_OK;
   if (!h_keys) return NS_ERR_INVALID;
   constexpr size_t KB = sizeof(Key);
+  HostCache* hc = nullptr;
+  NSB_TRY(host_cache(&hc));
+  HostCache& g_host = *hc;
+  if (n <= (size_t)kSmallTile) {
+    // one CTA sorts the keys in the mapped staging buffer (no scratch: the
+    // merge sort's single-tile path; quick sort delegates to it at this size)
+    NSB_TRY(g_host.ensure(0));
+    NSB_TRY(g_host.ensure_pinned());
+    std::memcpy(g_host.pinned, h_keys, n * KB);
+    const int st = dev_sort(static_cast<Key*>(g_host.mapped), n, mask, vs, nullptr, 0, algorithm,
+                            g_host.stream);
+    NSB_TRY(check_cuda(cudaStreamSynchronize(g_host.stream), "cudaStreamSynchronize"));
+    if (st != NS_OK) return st;
+    std::memcpy(h_keys, g_host.pinned, n * KB);
+    return NS_OK;
+  }
   const size_t kb = align_up(n * KB, 256);
   const size_t tb = dev_temp(h_keys, algorithm, n);
   NSB_TRY(g_host.ensure(kb + tb));
@@ -147,6 +190,9 @@ static int host_merge(Key* h_keys, size_t n_left, size_t n) {
   constexpr size_t KB = sizeof(Key);
   const size_t kb = align_up(n * KB, 256);
   const size_t tb = merge_temp(h_keys, n);
+  HostCache* hc = nullptr;
+  NSB_TRY(host_cache(&hc));
+  HostCache& g_host = *hc;
   NSB_TRY(g_host.ensure(kb + tb));
   cudaStream_t s = g_host.stream;
   Key* d = static_cast<Key*>(g_host.dev);
@@ -192,7 +238,7 @@ int ns_quick_sort_host_i64(int64_t* h_keys, size_t n, uint32_t width_mask, int v
 }
 
 int ns_release_cache(void) {
-  nsb::g_host.release();
+  for (auto& c : nsb::g_hosts.d) c.release();
   return NS_OK;
 }
 
@@ -245,6 +291,87 @@ void device_quick_sort(std::int64_t* d_keys, size_t n, const NetworkConfig& cfg,
   void* t = scratch.reserve(tb);
   detail::check(ns_quick_sort_i64(d_keys, n, cfg.width_mask, cfg.varsort_max, t, tb, stream),
                 "device_quick_sort");
+}
+
+void sample_sort_multi(std::span<std::int32_t> a, const std::vector<int>& devices,
+                       const NetworkConfig& cfg, Exchange exchange) {
+  const int g = (int)devices.size();
+  if (g < 1) throw std::invalid_argument("sample_sort_multi: no devices");
+  const size_t n = a.size();
+  std::vector<size_t> counts(g), start(g + 1, 0);
+  for (int d = 0; d < g; ++d) {
+    start[d + 1] = n * (size_t)(d + 1) / (size_t)g;
+    counts[d] = start[d + 1] - start[d];
+  }
+  const size_t shard_max = *std::max_element(counts.begin(), counts.end());
+  size_t cap = std::min(n, 2 * shard_max + (size_t)4096 * g);
+  if (cap == 0) cap = 1;
+  std::vector<int32_t*> shards(g, nullptr), outs(g, nullptr);
+  std::vector<void*> temps(g, nullptr), streams(g, nullptr);
+  std::vector<ns_nccl_comm> comms(g, nullptr);
+  int prev = 0;
+  cudaGetDevice(&prev);
+  auto cleanup = [&] {
+    for (int d = 0; d < g; ++d) {
+      cudaSetDevice(devices[d]);
+      if (shards[d]) cudaFree(shards[d]);
+      if (outs[d]) cudaFree(outs[d]);
+      if (temps[d]) cudaFree(temps[d]);
+      if (streams[d]) cudaStreamDestroy(static_cast<cudaStream_t>(streams[d]));
+    }
+    if (exchange == Exchange::nccl && comms[0]) ns_nccl_comms_destroy(g, comms.data());
+    cudaSetDevice(prev);
+  };
+  int st = NS_OK;
+  size_t tb = 0;
+  std::vector<size_t> oc(g, 0);
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    tb = ns_sample_sort_multi_temp_bytes(g, shard_max, cap);
+    for (int d = 0; d < g && st == NS_OK; ++d) {
+      st = nsb::check_cuda(cudaSetDevice(devices[d]), "cudaSetDevice");
+      cudaStream_t s = static_cast<cudaStream_t>(streams[d]);
+      if (st == NS_OK && !s) {
+        st = nsb::check_cuda(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate");
+        streams[d] = s;
+      }
+      if (st == NS_OK && !shards[d])
+        st = nsb::check_cuda(cudaMalloc(&shards[d], std::max<size_t>(counts[d], 1) * 4), "cudaMalloc");
+      if (outs[d]) cudaFree(outs[d]);
+      if (temps[d]) cudaFree(temps[d]);
+      outs[d] = nullptr;
+      temps[d] = nullptr;
+      if (st == NS_OK) st = nsb::check_cuda(cudaMalloc(&outs[d], cap * 4), "cudaMalloc");
+      if (st == NS_OK) st = nsb::check_cuda(cudaMalloc(&temps[d], tb), "cudaMalloc");
+      if (st == NS_OK)
+        st = nsb::check_cuda(cudaMemcpyAsync(shards[d], a.data() + start[d], counts[d] * 4,
+                                             cudaMemcpyHostToDevice, s),
+                             "H2D");
+    }
+    if (st == NS_OK && exchange == Exchange::nccl && !comms[0])
+      st = ns_nccl_comms_init_all(g, devices.data(), comms.data());
+    if (st == NS_OK)
+      st = ns_sample_sort_multi_i32(g, devices.data(),
+                                    exchange == Exchange::nccl ? comms.data() : nullptr,
+                                    (int)exchange, shards.data(), counts.data(), outs.data(), cap,
+                                    oc.data(), cfg.width_mask, cfg.varsort_max, temps.data(), tb,
+                                    streams.data());
+    if (st == NS_ERR_TEMP && *std::max_element(oc.begin(), oc.end()) > cap) {
+      cap = *std::max_element(oc.begin(), oc.end());  // a bucket above the PSRS estimate
+      st = NS_OK;
+      continue;
+    }
+    break;
+  }
+  size_t at = 0;
+  for (int d = 0; d < g && st == NS_OK; ++d) {
+    st = nsb::check_cuda(cudaSetDevice(devices[d]), "cudaSetDevice");
+    if (st == NS_OK && oc[d])
+      st = nsb::check_cuda(cudaMemcpy(a.data() + at, outs[d], oc[d] * 4, cudaMemcpyDeviceToHost), "D2H");
+    at += oc[d];
+  }
+  cleanup();
+  detail::check(st, "sample_sort_multi");
+  if (at != n) throw std::runtime_error("sample_sort_multi: lost keys");
 }
 
 }  // namespace netsort_b200

@@ -430,9 +430,25 @@ __device__ __forceinline__ unsigned match_len4(int len) {
   return eq;
 }
 
+// Length check of the whole batch BEFORE any key moves (networks.hpp:99-103
+// throws before touching the window): *status = NS_ERR_INVALID if some array
+// is longer than 8 keys or its offsets decrease.  The sort kernel reads the
+// word first and leaves every key untouched when it is set.
+__global__ void batch_validate_kernel(const uint32_t* __restrict__ offsets, int64_t num_arrays,
+                                      int* __restrict__ status) {
+  bool bad = false;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < num_arrays;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t a = __ldg(offsets + i), b = __ldg(offsets + i + 1);
+    bad |= b < a || b - a > 8u;
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicExch(status, NS_ERR_INVALID);
+}
+
 __global__ void __launch_bounds__(kBaNT, NSB_BATCH_MINB)
     sort_small_batch_kernel(int32_t* __restrict__ keys, const uint32_t* __restrict__ offsets,
                             int64_t num_arrays, int* __restrict__ bad) {
+  if (*reinterpret_cast<volatile int*>(bad)) return;  // the validation pass found a bad length
   constexpr int NW = kBaNT / 32;
   __shared__ __align__(16) int32_t sk[kBaArr * 8 + 8];
   // length-grouped order: (shared-memory key offset << 4) | length per slot
@@ -522,8 +538,8 @@ __global__ void __launch_bounds__(kBaNT, NSB_BATCH_MINB)
     if (len >= 0 && (eq & ((1u << lane) - 1u)) == 0) wcnt[warp][len][r] = __popc(eq);
   }
   __syncthreads();
-  if (s_bad) {
-    if (tid == 0) atomicExch(bad, 1);
+  if (s_bad) {  // unreachable after batch_validate_kernel; kept as a bounds guard
+    if (tid == 0) atomicExch(bad, NS_ERR_INVALID);
     return;
   }
   // exclusive scan in (length, round, warp) order (stable): each of the
@@ -728,6 +744,7 @@ const char* ns_status_string(int status) {
     case NS_ERR_CUDA: return "CUDA error";
     case NS_ERR_OOM: return "out of memory";
     case NS_ERR_TEMP: return "scratch buffer too small";
+    case NS_ERR_NCCL: return "NCCL unavailable or failed";
     default: return "unknown status";
   }
 }
@@ -777,6 +794,29 @@ int ns_merge_sort_i64(int64_t* d_keys, size_t n, uint32_t width_mask, int varsor
                            static_cast<cudaStream_t>(stream));
 }
 
+int ns_sort_small_batch_async_i32(int32_t* d_keys, const uint32_t* d_offsets, size_t num_arrays,
+                                  int* d_status, void* stream) {
+  if (!d_status) return NS_ERR_INVALID;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  NSB_TRY(check_cuda(cudaMemsetAsync(d_status, 0, sizeof(int), s), "cudaMemsetAsync"));
+  if (num_arrays == 0) return NS_OK;
+  if (!d_keys || !d_offsets) return NS_ERR_INVALID;
+  if (num_arrays >= (size_t)UINT32_MAX) return NS_ERR_INVALID;
+  {
+    Prof prof(PK_BATCH, s);
+    batch_validate_kernel<<<grid_for((int64_t)num_arrays, 256), 256, 0, s>>>(
+        d_offsets, (int64_t)num_arrays, d_status);
+  }
+  NSB_TRY(check_launch("batch_validate_kernel"));
+  const int64_t ctas = (int64_t)((num_arrays + kBaArr - 1) / kBaArr);
+  {
+    Prof prof(PK_BATCH, s);
+    sort_small_batch_kernel<<<(unsigned)ctas, kBaNT, 0, s>>>(d_keys, d_offsets,
+                                                              (int64_t)num_arrays, d_status);
+  }
+  return check_launch("sort_small_batch_kernel");
+}
+
 int ns_sort_small_batch_i32(int32_t* d_keys, const uint32_t* d_offsets, size_t num_arrays,
                             void* stream) {
   if (num_arrays == 0) return NS_OK;
@@ -784,15 +824,8 @@ int ns_sort_small_batch_i32(int32_t* d_keys, const uint32_t* d_offsets, size_t n
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   BatchFlag* f = nullptr;
   NSB_TRY(batch_flag(&f));
-  NSB_TRY(check_cuda(cudaMemsetAsync(f->dev, 0, sizeof(int), s), "cudaMemsetAsync"));
-  const int64_t ctas = (int64_t)((num_arrays + kBaArr - 1) / kBaArr);
-  {
-    Prof prof(PK_BATCH, s);
-    sort_small_batch_kernel<<<(unsigned)ctas, kBaNT, 0, s>>>(d_keys, d_offsets,
-                                                              (int64_t)num_arrays, f->dev);
-  }
-  NSB_TRY(check_launch("sort_small_batch_kernel"));
-  // The length check is the only device->host traffic of this call.
+  NSB_TRY(ns_sort_small_batch_async_i32(d_keys, d_offsets, num_arrays, f->dev, stream));
+  // reading the status back is the only device->host traffic of this call
   NSB_TRY(check_cuda(cudaMemcpyAsync(f->host, f->dev, sizeof(int), cudaMemcpyDeviceToHost, s),
                      "cudaMemcpyAsync"));
   NSB_TRY(check_cuda(cudaStreamSynchronize(s), "cudaStreamSynchronize"));

@@ -216,6 +216,35 @@ static void device_side() {
     CHECK(back64 == e64);
     cudaFree(d64);
   }
+
+  // several GPUs behind one host thread (BASELINE config 5's shape): the NCCL
+  // exchange on the devices present, the peer-memory exchange with several
+  // virtual ranks on device 0 (both checked against std::sort)
+  {
+    int ndev = 0;
+    cudaGetDeviceCount(&ndev);
+    std::mt19937 r32(5);
+    for (size_t n : {size_t(0), size_t(1), size_t(1000), size_t(3000017)}) {
+      std::vector<int32_t> in(n);
+      for (auto& x : in) x = static_cast<int32_t>(r32() >> 1);
+      auto expect = in;
+      std::sort(expect.begin(), expect.end());
+      std::vector<int> all;
+      for (int d = 0; d < ndev; ++d) all.push_back(d);
+      if (ns_nccl_available()) {
+        auto v = in;
+        ns::sample_sort_multi(std::span<int32_t>(v), all, *ns::find_config("6To8"),
+                              ns::Exchange::nccl);
+        CHECK(v == expect);
+      }
+      for (int g : {1, 2, 3, 4}) {
+        auto v = in;
+        ns::sample_sort_multi(std::span<int32_t>(v), std::vector<int>(g, 0),
+                              *ns::find_config("6To8"), ns::Exchange::p2p);
+        CHECK(v == expect);
+      }
+    }
+  }
 }
 
 int main(int argc, char** argv) {
