@@ -112,9 +112,15 @@ class NetsortError(RuntimeError):
 _LIB = None
 
 
-def build(verbose: bool = False) -> str:
-    """Compile the sm_100a library in-tree (nvcc cross-compiles without a GPU)."""
-    subprocess.run(["make", "-s", "-C", CSRC, f"-j{os.cpu_count() or 4}"], check=True,
+CHECKED_LIB_PATH = os.path.join(PKG, "lib", "libnetsort_b200_checked.so")
+
+
+def build(verbose: bool = False, checked: bool = True) -> str:
+    """Compile the sm_100a library in-tree (nvcc cross-compiles without a GPU)
+    and, with `checked`, its bounds-checked twin (NSB_CHECKED=1, used only by
+    tests/test_checked_build.py)."""
+    targets = ["all", "checked"] if checked else ["all"]
+    subprocess.run(["make", "-s", "-C", CSRC, f"-j{os.cpu_count() or 4}"] + targets, check=True,
                    stdout=None if verbose else subprocess.DEVNULL)
     return LIB_PATH
 

@@ -8,6 +8,33 @@
 
 #include "../../include/netsort_b200.h"
 
+// Checked build (NSB_CHECKED=1, libnetsort_b200_checked.so): device-side
+// bounds checks on every data-dependent shared / global index of the hot
+// kernels (merge cursors against their slice + sentinel pad, staged slice
+// extents, bucket ids and scatter positions, job-list capacities).  A failed
+// check prints the condition and traps (cudaErrorLaunchFailure for the
+// caller).  This stands in for compute-sanitizer, which this GPU pool does
+// not allow (tests/test_checked_build.py); the default build compiles the
+// checks out.
+#ifndef NSB_CHECKED
+#define NSB_CHECKED 0
+#endif
+#if NSB_CHECKED
+#include <cstdio>
+#define NSB_DCHECK(...)                                                                 \
+  do {                                                                                  \
+    if (!(__VA_ARGS__)) {                                                                      \
+      printf("NSB_DCHECK failed %s:%d: %s (block %d, thread %d)\n", __FILE__, __LINE__, \
+             #__VA_ARGS__, (int)blockIdx.x, (int)threadIdx.x);                                 \
+      __trap();                                                                         \
+    }                                                                                   \
+  } while (0)
+#else
+#define NSB_DCHECK(...) \
+  do {                   \
+  } while (0)
+#endif
+
 namespace nsb {
 
 void set_last_error(const char* where, cudaError_t e);
@@ -63,17 +90,6 @@ inline int check_cuda(cudaError_t e, const char* where) {
   } while (0)
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
-
-// int32 segment / bucket tiles of 4097..16384 keys as 32 keys per thread
-// (<128,32>, <256,32>, <512,32>: 1024-key warp runs, one shared-memory merge
-// level fewer than 16 keys per thread).  NSB_SEG_K32=0 restores <.., 16>.
-inline bool seg_k32_enabled() {
-  static const bool on = [] {
-    const char* e = getenv("NSB_SEG_K32");
-    return e ? atoi(e) != 0 : true;
-  }();
-  return on;
-}
 
 // Programmatic dependent launch (sm_90+): kernels of one sort are launched
 // with programmatic stream serialization, so the next kernel's CTAs can be

@@ -500,8 +500,12 @@ __device__ __forceinline__ void cta_sort_regs(Key (&v)[K], Key* out, int valid, 
       uint32_t ptr = (uint32_t)(a_pos + a) * KB;
       uint32_t mnext = (uint32_t)(b_pos + d - a + 1) * KB;
       Key m = sm[b_pos + d - a];
+      NSB_DCHECK(a >= 0 && a <= R && d - a >= 0 && d - a <= R);
 #pragma unroll
       for (int k = 0; k < KM; ++k) {
+        // a cursor stays inside its run + GAP sentinels (runs at a_pos, b_pos)
+        NSB_DCHECK((ptr >= (uint32_t)a_pos * KB && ptr < (uint32_t)(a_pos + R + GAP) * KB) ||
+                   (ptr >= (uint32_t)b_pos * KB && ptr < (uint32_t)(b_pos + R + GAP) * KB));
         const Key x = *reinterpret_cast<const Key*>(smc + ptr);
         const bool t = x <= m;
         w[k] = t ? x : m;
@@ -513,6 +517,7 @@ __device__ __forceinline__ void cta_sort_regs(Key (&v)[K], Key* out, int valid, 
       }
       __syncthreads();  // every thread is done reading this level's input
       Key* o = sm + p * S2 + d;
+      NSB_DCHECK(p * S2 + 2 * R + GAP <= tile_smem_bytes<NT, K, Key>() / KB && d + cnt <= 2 * R);
 #pragma unroll
       for (int k = 0; k < KM; ++k)
         if (k < cnt) o[k] = w[k];
@@ -740,6 +745,8 @@ __device__ __forceinline__ void merge_staged_tile(Key* sm, int a_pos, int la, in
   const Key* SA = sm + a_pos;
   const Key* SB = sm + b_pos;
   const int total = la + lb;
+  NSB_DCHECK(la >= 0 && lb >= 0 && total <= TM &&
+             (a_pos + la + PAD <= b_pos || b_pos + lb + PAD <= a_pos));
   // full tiles (every tile but the last of a pair) give every thread exactly
   // K outputs: that path has no per-output guard at all
   const int d = min(tid * K, total);
@@ -754,6 +761,8 @@ __device__ __forceinline__ void merge_staged_tile(Key* sm, int a_pos, int la, in
   uint32_t mnext = (uint32_t)(b_pos + d - a + 1) * KB;
   Key m = *reinterpret_cast<const Key*>(smc + mnext - KB);
   auto step = [&]() {
+    NSB_DCHECK((ptr >= (uint32_t)a_pos * KB && ptr < (uint32_t)(a_pos + la + PAD) * KB) ||
+               (ptr >= (uint32_t)b_pos * KB && ptr < (uint32_t)(b_pos + lb + PAD) * KB));
     const Key x = *reinterpret_cast<const Key*>(smc + ptr);
     const bool t = x <= m;
     const Key out = t ? x : m;
@@ -1003,6 +1012,9 @@ __global__ void __launch_bounds__(NT, v2_min_blocks(NT, K, (int)sizeof(Key)))
   }
   const int la = (int)(a1 - a0);
   const int lb = (int)((g.diag1 - a1) - (g.diag0 - a0));
+  // the splits lie on the pair's merge path and the slices fit the tile
+  NSB_DCHECK(a0 >= 0 && a0 <= a1 && a1 <= g.a_len && g.diag0 - a0 >= 0 && g.diag1 - a1 <= g.b_len &&
+             lb >= 0 && la + lb == (int)(g.diag1 - g.diag0) && la + lb <= TM);
   const Key* A = src + g.pair_base + a0;
   const Key* B = src + g.pair_base + g.a_len + (g.diag0 - a0);
   const Key* lo = src;
@@ -1017,6 +1029,7 @@ __global__ void __launch_bounds__(NT, v2_min_blocks(NT, K, (int)sizeof(Key)))
   const int a_words = (a_shift + la + PV - 1) & ~(PV - 1), b_words = (b_shift + lb + PV - 1) & ~(PV - 1);
   const bool a_tma = la > 0 && (a_addr % KB) == 0 && a_cov >= lo && a_cov + a_words <= hi;
   const bool b_tma = lb > 0 && (b_addr % KB) == 0 && b_cov >= lo && b_cov + b_words <= hi;
+  NSB_DCHECK(b_off + b_words + v2_pad(K) <= v2_smem_words(TM, K) && a_shift + la + v2_pad(K) <= b_off);
 
   // the output offset crosses the merge loop through shared memory, so no
   // 64-bit geometry stays live in registers next to the K outputs

@@ -1,5 +1,6 @@
 // netsort_capi.cu — C-ABI entry points of the merge layer, the base-case
 // batch, the segmented sort and the checking helpers (include/netsort_b200.h).
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -40,57 +41,38 @@ static int launch_blocksort(const Key* src, Key* dst, int64_t n, int stride, int
   return check_launch("blocksort_kernel");
 }
 
-// Tuning knobs (read once; the defaults are the measured best on B200).
-//   NSB_TILE  = 8192 | 16384 | 32768 : keys per tile-sort CTA
-constexpr int kV2NT = 256, kV2K = 29, kV2T = kV2NT * kV2K;  // 7424 keys per tile (<256,29> measured 0.5-4 % faster than <256,31> from 2^24 to 2^30: tools/shape_ab2.sh)
-// int64 keys (NSB_V2_64=0): 3840 keys (30 KiB) per tile; K odd keeps the
-// half-warp 64-bit cursor accesses on distinct banks
-constexpr int kV2K64 = 15;
+// Merge-pass tile shape: <256,29> = 7424 keys per tile (measured 0.5-4 %
+// faster than <256,31> from 2^24 to 2^30, profiles/r01_tile_sort_v6_ab.txt);
+// int64 keys take odd K as well (half-warp 64-bit cursors on distinct banks).
+constexpr int kV2NT = 256, kV2K = 29, kV2T = kV2NT * kV2K;
+// Run-time knobs (read once).  Only knobs that select between code paths
+// every build carries anyway; the measured-dead tile shapes of round 1 are
+// gone (DESIGN.md §4 lists what was measured).
+//   NSB_FUSED_MAX     : passes with at most this many tiles search their
+//                       merge-path splits in-kernel (no partition launch)
+//   NSB_PART_WARP_MAX : passes of at most this many tiles find their splits
+//                       with one warp per tile (merge_partition_v4_kernel),
+//                       larger ones with one thread per tile (v3 / v2)
+//   NSB_SAMPLES=0     : partition without the block samples (plain search)
+//   NSB_SINGLE_MAX    : largest n sorted by one CTA (<= 16384; measured
+//                       10,000 keys 22.9 us in one 1024-thread CTA, 15.9 us
+//                       as two 8192-key tiles and one merge pass)
+// The sanitizer-style tests use them to force every partition path at small
+// sizes.
 struct MergeTuning {
-  int tile = 0;  // NSB_TILE forces a tile size; 0 = by size (below)
-  int64_t fused_max_tiles = 4096;  // passes with fewer tiles search in-kernel (measured crossover)
-  int v2 = -1;  // NSB_V2 forces one tile shape (see v2_pass); -1 = by size
-  int samples = 1;  // NSB_SAMPLES=0: plain partition search on every pass
-  // NSB_TILE64: int64 tile sort 1 = <1024,8>, 2 = <512,16> (16384-key
-  // <1024,16> tiles measured slower: 2^28 tile sort 5.05 -> 6.92 ms for one
-  // pass fewer, sort 14.8 -> 16.0 ms; tools/tile64_ab.sh)
-  // (measured at 2^28: 7.5 vs 5.1 ms -- the 256-key warp runs need a fifth
-  // shared-memory level and the CTA fits once per SM)
-  int tile64 = 2;
-  // NSB_K32=0: int32 tiles as 16 keys per thread (512-key warp runs)
-  // instead of 32 (1024-key warp runs, one shared-memory level fewer per
-  // tile; measured 2 % faster at 2^26..2^30)
-  int k32tile = 1;
-  // NSB_SINGLE_MAX: largest n sorted by one CTA (<= 16384); above it the
-  // tiled path (measured, tools/small_ab.sh: 10,000 keys 22.9 us in one
-  // 1024-thread CTA, 15.9 us as two 8192-key tiles and one merge pass).
-  // NSB_SMALL_K32=1: single-CTA int32 shapes at 32 keys/thread (slower).
+  int64_t fused_max_tiles = 4096;
+  int samples = 1;
   int64_t single_max = kBsT;
-  int small_k32 = 0;
-  // NSB_PART_WARP_MAX: passes of at most this many tiles find their splits
-  // with one warp per tile (merge_partition_v4_kernel), larger ones with one
-  // thread per tile (v3 / v2)
   int64_t part_warp_max = 16384;
   MergeTuning() {
     if (const char* e = getenv("NSB_PART_WARP_MAX")) part_warp_max = atoll(e);
     if (const char* e = getenv("NSB_SINGLE_MAX")) single_max = std::min<int64_t>(atoll(e), kSmT);
-    if (const char* e = getenv("NSB_SMALL_K32")) small_k32 = atoi(e);
-    if (const char* e = getenv("NSB_V2")) v2 = atoi(e);
     if (const char* e = getenv("NSB_SAMPLES")) samples = atoi(e);
-    if (const char* e = getenv("NSB_TILE64")) tile64 = atoi(e);
-    if (const char* e = getenv("NSB_K32")) k32tile = atoi(e);
     if (const char* e = getenv("NSB_FUSED_MAX")) fused_max_tiles = atoll(e);
-    if (const char* e = getenv("NSB_TILE")) {
-      const int t = atoi(e);
-      tile = (t == 32768 || t == 16384 || t == 4096 || t == 2048 || t == 1024) ? t : 8192;
-    }
   }
 };
 static const MergeTuning& tuning() {
-  static const MergeTuning t = [] {
-    MergeTuning m;
-    return m;
-  }();
+  static const MergeTuning t;
   return t;
 }
 
@@ -212,45 +194,20 @@ static int v2_pass_t(const Key* src, Key* dst, int64_t n, int64_t R, int64_t* mp
 }
 
 // One pairwise merge pass (v2): runs of R in src -> runs of 2R in dst.
-// Tile shape by array size (tests/size_sweep.py, tools/mid_sweep.sh on B200):
-// up to 2^23 keys a pass is latency bound and smaller tiles (<128,23>, 2944
-// keys, 12 CTAs/SM) win by 5-10 %; above, <256,29> (7424 keys, 6 CTAs/SM;
-// tools/shape_ab2.sh: 2^24 411 -> 396 us, 2^30 28.10 -> 27.97 ms against
-// <256,31>, the previous default, now NSB_V2=14).
+// Tile shape by array size (tools/mid_sweep.sh on B200): up to 2^23 keys a
+// pass is latency bound and smaller tiles (<128,23>, 2944 keys, 12 CTAs/SM)
+// win by 5-10 %; above, <256,29>.  int64 (tools/i64_sweep.sh): <128,15> up
+// to 2^20 keys, <128,23> up to 2^25, <128,31> above.
 static int v2_pass(const int32_t* src, int32_t* dst, int64_t n, int64_t R, int64_t* mp,
                    cudaStream_t s, SmpCtx* sc = nullptr) {
-  switch (tuning().v2) {
-    case 0: return v2_pass_t<kV2NT, kV2K>(src, dst, n, R, mp, s, sc);
-    case 1: return v2_pass_t<512, 15>(src, dst, n, R, mp, s, sc);
-    case 2: return v2_pass_t<384, 21>(src, dst, n, R, mp, s, sc);
-    case 3: return v2_pass_t<128, 31>(src, dst, n, R, mp, s, sc);
-    case 5: return v2_pass_t<128, 47>(src, dst, n, R, mp, s, sc);
-    case 6: return v2_pass_t<128, 23>(src, dst, n, R, mp, s, sc);
-    case 9: return v2_pass_t<128, 63>(src, dst, n, R, mp, s, sc);
-    case 11: return v2_pass_t<128, 55>(src, dst, n, R, mp, s, sc);
-    case 13: return v2_pass_t<256, 27>(src, dst, n, R, mp, s, sc);
-    case 14: return v2_pass_t<256, 31>(src, dst, n, R, mp, s, sc);
-    default:
-      return n <= (int64_t(1) << 23) ? v2_pass_t<128, 23>(src, dst, n, R, mp, s, sc)
-                                     : v2_pass_t<kV2NT, kV2K>(src, dst, n, R, mp, s, sc);
-  }
+  return n <= (int64_t(1) << 23) ? v2_pass_t<128, 23>(src, dst, n, R, mp, s, sc)
+                                 : v2_pass_t<kV2NT, kV2K>(src, dst, n, R, mp, s, sc);
 }
 static int v2_pass(const int64_t* src, int64_t* dst, int64_t n, int64_t R, int64_t* mp,
                    cudaStream_t s, SmpCtx* sc = nullptr) {
-  static const int shape = [] {
-    const char* e = getenv("NSB_V2_64");
-    return e ? atoi(e) : -1;
-  }();
-  switch (shape) {
-    case 0: return v2_pass_t<kV2NT, kV2K64>(src, dst, n, R, mp, s, sc);
-    case 1: return v2_pass_t<128, 23>(src, dst, n, R, mp, s, sc);
-    case 2: return v2_pass_t<128, 31>(src, dst, n, R, mp, s, sc);
-    case 3: return v2_pass_t<128, 15>(src, dst, n, R, mp, s, sc);
-    default:  // by size (tools/i64_sweep.sh on B200)
-      if (n <= (int64_t(1) << 20)) return v2_pass_t<128, 15>(src, dst, n, R, mp, s, sc);
-      if (n <= (int64_t(1) << 25)) return v2_pass_t<128, 23>(src, dst, n, R, mp, s, sc);
-      return v2_pass_t<128, 31>(src, dst, n, R, mp, s, sc);
-  }
+  if (n <= (int64_t(1) << 20)) return v2_pass_t<128, 15>(src, dst, n, R, mp, s, sc);
+  if (n <= (int64_t(1) << 25)) return v2_pass_t<128, 23>(src, dst, n, R, mp, s, sc);
+  return v2_pass_t<128, 31>(src, dst, n, R, mp, s, sc);
 }
 
 // Pairwise passes over existing sorted runs of length R0 (the last may be
@@ -288,13 +245,6 @@ static int merge_sort_device_t(Key* d_keys, size_t n, int leaf, void* d_temp, si
     // (also up to 16384 keys when the caller passes no scratch)
     return with_leaf(leaf, [&](auto L) {
       constexpr int LF = decltype(L)::value;
-      if constexpr (k32) {
-        if (tuning().small_k32 && n > 2048) {
-          if (n <= 4096) return launch_blocksort<128, 32, LF>(d_keys, d_keys, (int64_t)n, 4096, 1, s);
-          if (n <= 8192) return launch_blocksort<256, 32, LF>(d_keys, d_keys, (int64_t)n, 8192, 1, s);
-          return launch_blocksort<512, 32, LF>(d_keys, d_keys, (int64_t)n, kSmT, 1, s);
-        }
-      }
       if (n <= 512) return launch_blocksort<32, 16, LF>(d_keys, d_keys, (int64_t)n, 512, 1, s);
       if (n <= 2048) return launch_blocksort<128, 16, LF>(d_keys, d_keys, (int64_t)n, 2048, 1, s);
       if (n <= 4096) return launch_blocksort<256, 16, LF>(d_keys, d_keys, (int64_t)n, 4096, 1, s);
@@ -307,13 +257,10 @@ static int merge_sort_device_t(Key* d_keys, size_t n, int leaf, void* d_temp, si
   Key* tmp = static_cast<Key*>(d_temp);
   int64_t* mp = reinterpret_cast<int64_t*>(static_cast<char*>(d_temp) +
                                            align_up(n * sizeof(Key), 256));
-  const MergeTuning& tu = tuning();
-  // int32 tile: 16384 keys from 2^21 keys up (one merge pass fewer; with 32
-  // keys per thread it has the 8192-key tile's four shared-memory levels),
-  // 8192 below; int64: 8192
-  const int T = !k32 ? kBsT
-                     : tu.tile ? tu.tile
-                               : (tu.k32tile && n >= (size_t(1) << 21) ? kSmT : kBsT);
+  // int32 tile: 16384 keys (<512,32>) from 2^21 keys up (one merge pass
+  // fewer; with 32 keys per thread it has the 8192-key tile's four
+  // shared-memory levels), 8192 (<256,32>) below; int64: 8192 (<512,16>)
+  const int T = (k32 && n >= (size_t(1) << 21)) ? kSmT : kBsT;
   const int64_t tiles = (int64_t)((n + T - 1) / T);
   // pairwise passes until one run remains
   int passes = 0;
@@ -324,22 +271,11 @@ static int merge_sort_device_t(Key* d_keys, size_t n, int leaf, void* d_temp, si
   NSB_TRY(with_leaf(leaf, [&](auto L) {
     constexpr int LF = decltype(L)::value;
     if constexpr (!k32) {
-      if (tu.tile64 == 1) return launch_blocksort<1024, 8, LF>(d_keys, cur, (int64_t)n, T, tiles, s);
-      if (tu.tile64 == 2) return launch_blocksort<512, 16, LF>(d_keys, cur, (int64_t)n, T, tiles, s);
+      return launch_blocksort<512, 16, LF>(d_keys, cur, (int64_t)n, T, tiles, s);
+    } else {
+      if (T == kBsT) return launch_blocksort<256, 32, LF>(d_keys, cur, (int64_t)n, T, tiles, s);
+      return launch_blocksort<512, 32, LF>(d_keys, cur, (int64_t)n, T, tiles, s);
     }
-    if constexpr (k32) {
-      if (tu.k32tile && T == kBsT)
-        return launch_blocksort<256, 32, LF>(d_keys, cur, (int64_t)n, T, tiles, s);
-      if (tu.k32tile && T == kSmT)
-        return launch_blocksort<512, 32, LF>(d_keys, cur, (int64_t)n, T, tiles, s);
-      if (T == 2 * kSmT)
-        return launch_blocksort<1024, 32, LF>(d_keys, cur, (int64_t)n, T, tiles, s);
-    }
-    if (T == 4096) return launch_blocksort<256, 16, LF>(d_keys, cur, (int64_t)n, T, tiles, s);
-    if (T == 2048) return launch_blocksort<128, 16, LF>(d_keys, cur, (int64_t)n, T, tiles, s);
-    if (T == 1024) return launch_blocksort<64, 16, LF>(d_keys, cur, (int64_t)n, T, tiles, s);
-    return T == kSmT ? launch_blocksort<kSmNT, kSmK, LF>(d_keys, cur, (int64_t)n, T, tiles, s)
-                     : launch_blocksort<kBsNT, kBsK, LF>(d_keys, cur, (int64_t)n, T, tiles, s);
   }));
   SmpCtx sc;
   {
@@ -372,7 +308,6 @@ template <class Key>
 static int tile_sort_segments_t(Key* d_keys, size_t num_segments, size_t seg_len, int leaf,
                                 cudaStream_t s) {
   if (seg_len > (size_t)kSmT) return NS_ERR_INVALID;
-  (void)tuning();
   const int64_t n = (int64_t)(num_segments * seg_len);
   const int st = (int)seg_len;
   const int64_t g = (int64_t)num_segments;
@@ -380,14 +315,17 @@ static int tile_sort_segments_t(Key* d_keys, size_t num_segments, size_t seg_len
     constexpr int LF = decltype(L)::value;
     if (seg_len <= 512) return launch_blocksort<32, 16, LF>(d_keys, d_keys, n, st, g, s);
     if (seg_len <= 2048) return launch_blocksort<128, 16, LF>(d_keys, d_keys, n, st, g, s);
-    if (std::is_same_v<Key, int32_t> && seg_k32_enabled()) {
+    if constexpr (std::is_same_v<Key, int32_t>) {
+      // 32 keys per thread: 1024-key warp runs, one shared-memory merge level
+      // fewer than 16 keys per thread
       if (seg_len <= 4096) return launch_blocksort<128, 32, LF>(d_keys, d_keys, n, st, g, s);
       if (seg_len <= (size_t)kBsT) return launch_blocksort<256, 32, LF>(d_keys, d_keys, n, st, g, s);
       return launch_blocksort<512, 32, LF>(d_keys, d_keys, n, st, g, s);
+    } else {
+      if (seg_len <= 4096) return launch_blocksort<256, 16, LF>(d_keys, d_keys, n, st, g, s);
+      if (seg_len <= (size_t)kBsT) return launch_blocksort<kBsNT, kBsK, LF>(d_keys, d_keys, n, st, g, s);
+      return launch_blocksort<kSmNT, kSmK, LF>(d_keys, d_keys, n, st, g, s);
     }
-    if (seg_len <= 4096) return launch_blocksort<256, 16, LF>(d_keys, d_keys, n, st, g, s);
-    if (seg_len <= (size_t)kBsT) return launch_blocksort<kBsNT, kBsK, LF>(d_keys, d_keys, n, st, g, s);
-    return launch_blocksort<kSmNT, kSmK, LF>(d_keys, d_keys, n, st, g, s);
   });
 }
 int tile_sort_segments(int32_t* d_keys, size_t num_segments, size_t seg_len, int leaf,
@@ -430,25 +368,13 @@ __device__ __forceinline__ unsigned match_len4(int len) {
   return eq;
 }
 
-// Length check of the whole batch BEFORE any key moves (networks.hpp:99-103
-// throws before touching the window): *status = NS_ERR_INVALID if some array
-// is longer than 8 keys or its offsets decrease.  The sort kernel reads the
-// word first and leaves every key untouched when it is set.
-__global__ void batch_validate_kernel(const uint32_t* __restrict__ offsets, int64_t num_arrays,
-                                      int* __restrict__ status) {
-  bool bad = false;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < num_arrays;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t a = __ldg(offsets + i), b = __ldg(offsets + i + 1);
-    bad |= b < a || b - a > 8u;
-  }
-  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicExch(status, NS_ERR_INVALID);
-}
-
-__global__ void __launch_bounds__(kBaNT, NSB_BATCH_MINB)
-    sort_small_batch_kernel(int32_t* __restrict__ keys, const uint32_t* __restrict__ offsets,
-                            int64_t num_arrays, int* __restrict__ bad) {
-  if (*reinterpret_cast<volatile int*>(bad)) return;  // the validation pass found a bad length
+// One chunk of kBaArr consecutive arrays (first = its first array), sorted
+// by one CTA.  Returns false (keys untouched) if a length is out of range —
+// unreachable after the validation phase, kept as a bounds guard.
+__device__ __forceinline__ bool batch_chunk(int32_t* __restrict__ keys,
+                                            const uint32_t* __restrict__ offsets,
+                                            int64_t num_arrays, int64_t first, uint64_t* bar,
+                                            uint32_t& tma_uses) {
   constexpr int NW = kBaNT / 32;
   __shared__ __align__(16) int32_t sk[kBaArr * 8 + 8];
   // length-grouped order: (shared-memory key offset << 4) | length per slot
@@ -458,10 +384,8 @@ __global__ void __launch_bounds__(kBaNT, NSB_BATCH_MINB)
   __shared__ int wcnt[NW][9][kBaPer];
   __shared__ int s_bad;
   __shared__ uint32_t s_k0, s_k1, s_kt;
-  __shared__ __align__(8) uint64_t bar;
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
-  const int64_t first = (int64_t)blockIdx.x * kBaArr;
   const int cnt = (int)min((int64_t)kBaArr, num_arrays - first);
   if (tid == 0) {
     s_bad = 0;
@@ -469,8 +393,6 @@ __global__ void __launch_bounds__(kBaNT, NSB_BATCH_MINB)
     s_k1 = __ldg(offsets + first + cnt);
     s_kt = __ldg(offsets + num_arrays);  // end of the key array
     if (s_k1 < s_k0 || s_k1 - s_k0 > 8u * (uint32_t)cnt) s_bad = 1;
-    mbar_init(&bar, 1);
-    fence_mbar_init();
   }
   __syncthreads();
   const uint32_t k0 = s_k0;
@@ -489,8 +411,8 @@ __global__ void __launch_bounds__(kBaNT, NSB_BATCH_MINB)
   const bool use_tma = nk > 0 && cov >= keys && cov + cov_words <= keys + s_kt;
   if (use_tma) {
     if (tid == 0) {
-      mbar_arrive_expect_tx(&bar, (uint32_t)cov_words * 4u);
-      tma_load_1d(sk, cov, (uint32_t)cov_words * 4u, &bar);
+      mbar_arrive_expect_tx(bar, (uint32_t)cov_words * 4u);
+      tma_load_1d(sk, cov, (uint32_t)cov_words * 4u, bar);
     }
   } else {
     for (int i = tid; i < nk; i += kBaNT) sk[phase + i] = __ldcs(kp + i);
@@ -510,7 +432,8 @@ __global__ void __launch_bounds__(kBaNT, NSB_BATCH_MINB)
     if (lane != 31) ofb[r] = nx;
   }
   int4* sk4 = reinterpret_cast<int4*>(sk + phase + head);  // 16-byte aligned
-  if (use_tma) mbar_wait(&bar, 0);
+  // the barrier (initialised once per CTA) completes one phase per staged chunk
+  if (use_tma) mbar_wait(bar, tma_uses++ & 1u);
   __syncthreads();
   // validate (lengths outside [0, 8] -> error, nothing is touched) and count
   // lengths per (round, warp) with ballots
@@ -538,10 +461,7 @@ __global__ void __launch_bounds__(kBaNT, NSB_BATCH_MINB)
     if (len >= 0 && (eq & ((1u << lane) - 1u)) == 0) wcnt[warp][len][r] = __popc(eq);
   }
   __syncthreads();
-  if (s_bad) {  // unreachable after batch_validate_kernel; kept as a bounds guard
-    if (tid == 0) atomicExch(bad, NS_ERR_INVALID);
-    return;
-  }
+  if (s_bad) return false;  // unreachable after the validation phase
   // exclusive scan in (length, round, warp) order (stable): each of the
   // 9*kBaPer rows of NW counts is scanned by one thread, then one warp scans
   // the row totals
@@ -596,6 +516,7 @@ __global__ void __launch_bounds__(kBaNT, NSB_BATCH_MINB)
       const uint32_t pk = perm[slot];  // one load: no second look at the offsets
       const int off = (int)(pk >> 4);
       const int len = (int)(pk & 15u);
+      NSB_DCHECK(len <= 8 && off + len <= kBaArr * 8 + 8);
       sort_small_in_place(sk + off, len);  // warp-uniform almost always (grouped by length)
     }
   }
@@ -612,6 +533,47 @@ __global__ void __launch_bounds__(kBaNT, NSB_BATCH_MINB)
   }
   if (tid < head) kw[tid] = sk[phase + tid];
   if (tid < tail) kw[head + 4 * body + tid] = sk[phase + head + 4 * body + tid];
+  // the shared buffers are reused by this CTA's next chunk, whose staging
+  // bulk copy (async proxy) overwrites keys this chunk wrote generically
+  fence_proxy_async_smem();
+  __syncthreads();
+  return true;
+}
+
+// Length check of the whole batch BEFORE any key moves (networks.hpp:99-103
+// throws before touching the window), fused with the sort: the kernel is a
+// cooperative (all CTAs resident) grid-stride loop over the chunks.  Phase 1:
+// every CTA checks the offsets of the chunks it will sort, in the order it
+// will sort them (the re-read in phase 2 mostly hits L2); a bad length (> 8
+// keys or decreasing offsets) sets *status = NS_ERR_INVALID.  One grid-wide
+// barrier.  Phase 2: if *status is set no CTA touches a key; otherwise each
+// sorts its chunks.  *status is zeroed by the caller (the launch wrapper).
+__global__ void __launch_bounds__(kBaNT, NSB_BATCH_MINB)
+    sort_small_batch_kernel(int32_t* __restrict__ keys, const uint32_t* __restrict__ offsets,
+                            int64_t num_arrays, int* __restrict__ status) {
+  const int64_t nch = (num_arrays + kBaArr - 1) / kBaArr;
+  bool bad = false;
+  for (int64_t ch = blockIdx.x; ch < nch; ch += gridDim.x) {
+    const int64_t first = ch * kBaArr;
+    const int cnt = (int)min((int64_t)kBaArr, num_arrays - first);
+    for (int j = threadIdx.x; j < cnt; j += kBaNT) {
+      const uint32_t a = __ldg(offsets + first + j), b = __ldg(offsets + first + j + 1);
+      bad |= b < a || b - a > 8u;
+    }
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicExch(status, NS_ERR_INVALID);
+  cooperative_groups::this_grid().sync();
+  if (*reinterpret_cast<volatile int*>(status)) return;
+  __shared__ __align__(8) uint64_t bar;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  uint32_t tma_uses = 0;
+  for (int64_t ch = blockIdx.x; ch < nch; ch += gridDim.x)
+    if (!batch_chunk(keys, offsets, num_arrays, ch * kBaArr, &bar, tma_uses) && threadIdx.x == 0)
+      atomicExch(status, NS_ERR_INVALID);
 }
 
 // Validation flag + pinned host mirror per (host thread, device), allocated
@@ -802,17 +764,23 @@ int ns_sort_small_batch_async_i32(int32_t* d_keys, const uint32_t* d_offsets, si
   if (num_arrays == 0) return NS_OK;
   if (!d_keys || !d_offsets) return NS_ERR_INVALID;
   if (num_arrays >= (size_t)UINT32_MAX) return NS_ERR_INVALID;
+  // cooperative launch: every CTA resident (the grid-wide barrier between
+  // the validation and the sort phases), at most one CTA per chunk
+  const int64_t chunks = (int64_t)((num_arrays + kBaArr - 1) / kBaArr);
+  int dev = 0, sms = 148, per_sm = 1;
+  NSB_TRY(check_cuda(cudaGetDevice(&dev), "cudaGetDevice"));
+  NSB_TRY(check_cuda(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "attr"));
+  NSB_TRY(check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sort_small_batch_kernel,
+                                                                   kBaNT, 0),
+                     "cudaOccupancyMaxActiveBlocksPerMultiprocessor"));
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(chunks, (int64_t)sms * per_sm));
+  int64_t na = (int64_t)num_arrays;
+  void* args[] = {&d_keys, const_cast<uint32_t**>(&d_offsets), &na, &d_status};
   {
     Prof prof(PK_BATCH, s);
-    batch_validate_kernel<<<grid_for((int64_t)num_arrays, 256), 256, 0, s>>>(
-        d_offsets, (int64_t)num_arrays, d_status);
-  }
-  NSB_TRY(check_launch("batch_validate_kernel"));
-  const int64_t ctas = (int64_t)((num_arrays + kBaArr - 1) / kBaArr);
-  {
-    Prof prof(PK_BATCH, s);
-    sort_small_batch_kernel<<<(unsigned)ctas, kBaNT, 0, s>>>(d_keys, d_offsets,
-                                                              (int64_t)num_arrays, d_status);
+    const cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(sort_small_batch_kernel),
+                                                      dim3(grid), dim3(kBaNT), args, 0, s);
+    if (e != cudaSuccess) return check_cuda(e, "sort_small_batch_kernel");
   }
   return check_launch("sort_small_batch_kernel");
 }

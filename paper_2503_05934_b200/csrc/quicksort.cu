@@ -440,6 +440,7 @@ __device__ __forceinline__ void qs_count_chunk(const Key* __restrict__ X, uint8_
     const int64_t i = c0 + u * kQsNT + threadIdx.x;
     const bool in = FULL || i < c1;
     const int b = in ? cls(k[u]) : -1;
+    NSB_DCHECK(b < 2 * cls.B - 1);
     if (in) ids[i] = (uint8_t)b;
     qs_hist_add(hist, b);
   }
@@ -608,11 +609,15 @@ __global__ void __launch_bounds__(kQsNT) qs_plan_kernel(QsCtx<Key> c, int level,
     __syncthreads();
     if (cls >= 0) {
       const unsigned long long at = s_jbase[cls] + jlocal;
+      NSB_DCHECK(at < (unsigned long long)c.max_jobs);
       if (at < (unsigned long long)c.max_jobs)
         c.jobs[cls][at] = QsJob{jstart, jlen, src_flag | (type << 1), 0};
     }
     if (nB) {
       const unsigned long long sid = s_sbase + slocal, k0 = s_kbase + koff;
+      NSB_DCHECK(sid < (unsigned long long)c.max_segs && k0 + nch <= (unsigned long long)c.max_chunks &&
+                 s_bbase + boff + 2 * nB - 1 <= (unsigned long long)c.max_bkt &&
+                 s_pbase + poff + nB <= (unsigned long long)c.max_spl);
       if (sid < (unsigned long long)c.max_segs) {
         QsSeg ns;
         ns.start = jstart;
@@ -696,13 +701,18 @@ __global__ void __launch_bounds__(kQsNT, 2) qs_scatter_kernel(QsCtx<Key> c, int 
       if (pk[u] != 0xffffffffu) {
         const int bb = (int)(pk[u] & 0xffu);
         const int p = (int)hist[bb] + (int)(pk[u] >> 8);
+        NSB_DCHECK(bb < NB && p >= 0 && p < (int)(c1 - c0));
         skey[p] = k[u];
         sbid[p] = (uint8_t)bb;
       }
     }
     __syncthreads();
     const int total = (int)(c1 - c0);
-    for (int i = tid; i < total; i += kQsNT) Y[delta[sbid[i]] + i] = skey[i];
+    for (int i = tid; i < total; i += kQsNT) {
+      // every key lands inside its segment (the reserved bucket ranges)
+      NSB_DCHECK(delta[sbid[i]] + i >= g.start && delta[sbid[i]] + i < g.start + g.len);
+      Y[delta[sbid[i]] + i] = skey[i];
+    }
   }
 }
 
@@ -788,6 +798,8 @@ __global__ void __launch_bounds__(NT, (bs_min_blocks_tput<NT, K, Key>()))
     const QsJob jb = jobs[j];
     const bool src_tmp = jb.flags & 1;
     const int type = (jb.flags >> 1) & 3;
+    NSB_DCHECK(jb.start >= 0 && jb.len >= 0 && jb.start + jb.len <= c.n &&
+               (type != kJobSort || jb.len <= (int64_t)NT * K));
     const Key* src = (src_tmp ? c.tmp : c.keys) + jb.start;
     Key* dst = c.keys + jb.start;
     if (type == kJobSort) {
