@@ -661,7 +661,7 @@ def all_configs(ns, L, dev, peak):
         "kernel_hbm_frac": nbytes / (kms * 1e-3) / 1e9 / peak if kms else None,
         "verified": _sha(w.cpu().numpy()) == b["output_sha256"] and int(st.item()) == 0,
         "verified_against": "SHA-256 of the reference's sort_small output (golden.json)",
-        "path": "ns_sort_small_batch_async_i32 (validation pass + network pass, no host sync)"}
+        "path": "ns_sort_small_batch_async_i32 (validation and network phases in one cooperative kernel, no host sync)"}
     del k, o, w
     torch.cuda.empty_cache()
 

@@ -1,6 +1,5 @@
 // netsort_capi.cu — C-ABI entry points of the merge layer, the base-case
 // batch, the segmented sort and the checking helpers (include/netsort_b200.h).
-#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -374,7 +373,7 @@ __device__ __forceinline__ unsigned match_len4(int len) {
 __device__ __forceinline__ bool batch_chunk(int32_t* __restrict__ keys,
                                             const uint32_t* __restrict__ offsets,
                                             int64_t num_arrays, int64_t first, uint64_t* bar,
-                                            uint32_t& tma_uses) {
+                                            uint32_t& tma_uses, const int* status) {
   constexpr int NW = kBaNT / 32;
   __shared__ __align__(16) int32_t sk[kBaArr * 8 + 8];
   // length-grouped order: (shared-memory key offset << 4) | length per slot
@@ -520,7 +519,13 @@ __device__ __forceinline__ bool batch_chunk(int32_t* __restrict__ keys,
       sort_small_in_place(sk + off, len);  // warp-uniform almost always (grouped by length)
     }
   }
+  // Only now wait for the validation kernel (programmatic dependent launch:
+  // everything above overlapped it) and write nothing if it flagged the batch.
+  pdl_wait();
+  __shared__ int s_skip;
+  if (tid == 0) s_skip = *reinterpret_cast<const volatile int*>(status);
   __syncthreads();
+  if (s_skip) return true;
   int32_t* kw = keys + k0;
   if (body > 0) {  // aligned interior: one bulk store; head/tail keys one by one
     fence_proxy_async_smem();
@@ -541,29 +546,66 @@ __device__ __forceinline__ bool batch_chunk(int32_t* __restrict__ keys,
 }
 
 // Length check of the whole batch BEFORE any key moves (networks.hpp:99-103
-// throws before touching the window), fused with the sort: the kernel is a
-// cooperative (all CTAs resident) grid-stride loop over the chunks.  Phase 1:
-// every CTA checks the offsets of the chunks it will sort, in the order it
-// will sort them (the re-read in phase 2 mostly hits L2); a bad length (> 8
-// keys or decreasing offsets) sets *status = NS_ERR_INVALID.  One grid-wide
-// barrier.  Phase 2: if *status is set no CTA touches a key; otherwise each
-// sorts its chunks.  *status is zeroed by the caller (the launch wrapper).
+// throws before touching the window): *status = NS_ERR_INVALID if some array
+// is longer than 8 keys or its offsets decrease.  A pure stream over the
+// offsets: every thread checks 4 consecutive arrays per 16-byte load (the
+// 5th offset comes from the next lane), 4 loads in flight per thread.
+__global__ void __launch_bounds__(256) batch_validate_kernel(const uint32_t* __restrict__ offsets,
+                                                             int64_t num_arrays,
+                                                             int* __restrict__ status) {
+  pdl_trigger();  // the sort kernel may start staging and sorting right away
+  const int lane = threadIdx.x & 31;
+  bool bad = false;
+  // offsets[0, head) one by one until a 16-byte boundary, then quads
+  const int head = (int)min(num_arrays, (int64_t)(((16 - (reinterpret_cast<uintptr_t>(offsets) & 15)) & 15) >> 2));
+  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
+  if (gtid < head) {
+    const uint32_t a = __ldg(offsets + gtid), b = __ldg(offsets + gtid + 1);
+    bad |= b < a || b - a > 8u;
+  }
+  const uint4* q = reinterpret_cast<const uint4*>(offsets + head);
+  const int64_t nq = (num_arrays - head) / 4;  // whole quads of arrays
+  constexpr int U = 4;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x * U; base < nq; base += nthreads * U) {
+    // one round trip per iteration: the quads and, for the lanes whose
+    // neighbour does not hold it, the 5th offset are all loaded up front
+    uint4 v[U];
+    uint32_t own[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = base + (int64_t)u * blockDim.x + threadIdx.x;
+      v[u] = i < nq ? __ldcs(q + i) : make_uint4(0, 0, 0, 0);
+      own[u] = (i < nq && (lane == 31 || i + 1 >= nq)) ? __ldg(offsets + head + 4 * i + 4) : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = base + (int64_t)u * blockDim.x + threadIdx.x;
+      uint32_t n = __shfl_down_sync(0xffffffffu, v[u].x, 1);
+      if (lane == 31 || i + 1 >= nq) n = own[u];
+      if (i < nq) {
+        const uint4 x = v[u];
+        bad |= x.y < x.x || x.y - x.x > 8u || x.z < x.y || x.z - x.y > 8u || x.w < x.z ||
+               x.w - x.z > 8u || n < x.w || n - x.w > 8u;
+      }
+    }
+  }
+  // the last (num_arrays - head) % 4 arrays one by one
+  const int64_t t0 = head + 4 * nq;
+  if (gtid < num_arrays - t0) {
+    const uint32_t a = __ldg(offsets + t0 + gtid), b = __ldg(offsets + t0 + gtid + 1);
+    bad |= b < a || b - a > 8u;
+  }
+  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicExch(status, NS_ERR_INVALID);
+}
+
+// One CTA per chunk of kBaArr arrays.  Launched as a programmatic dependent
+// of the validation kernel: it stages and sorts its chunk while the
+// validation still runs and writes nothing if the validation flagged the
+// batch (batch_chunk).
 __global__ void __launch_bounds__(kBaNT, NSB_BATCH_MINB)
     sort_small_batch_kernel(int32_t* __restrict__ keys, const uint32_t* __restrict__ offsets,
                             int64_t num_arrays, int* __restrict__ status) {
-  const int64_t nch = (num_arrays + kBaArr - 1) / kBaArr;
-  bool bad = false;
-  for (int64_t ch = blockIdx.x; ch < nch; ch += gridDim.x) {
-    const int64_t first = ch * kBaArr;
-    const int cnt = (int)min((int64_t)kBaArr, num_arrays - first);
-    for (int j = threadIdx.x; j < cnt; j += kBaNT) {
-      const uint32_t a = __ldg(offsets + first + j), b = __ldg(offsets + first + j + 1);
-      bad |= b < a || b - a > 8u;
-    }
-  }
-  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicExch(status, NS_ERR_INVALID);
-  cooperative_groups::this_grid().sync();
-  if (*reinterpret_cast<volatile int*>(status)) return;
   __shared__ __align__(8) uint64_t bar;
   if (threadIdx.x == 0) {
     mbar_init(&bar, 1);
@@ -571,9 +613,10 @@ __global__ void __launch_bounds__(kBaNT, NSB_BATCH_MINB)
   }
   __syncthreads();
   uint32_t tma_uses = 0;
-  for (int64_t ch = blockIdx.x; ch < nch; ch += gridDim.x)
-    if (!batch_chunk(keys, offsets, num_arrays, ch * kBaArr, &bar, tma_uses) && threadIdx.x == 0)
-      atomicExch(status, NS_ERR_INVALID);
+  if (!batch_chunk(keys, offsets, num_arrays, (int64_t)blockIdx.x * kBaArr, &bar, tma_uses,
+                   status) &&
+      threadIdx.x == 0)
+    atomicExch(status, NS_ERR_INVALID);
 }
 
 // Validation flag + pinned host mirror per (host thread, device), allocated
@@ -654,6 +697,13 @@ __global__ void inversions_kernel(const Key* __restrict__ keys, int64_t n,
 #pragma unroll
   for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(kFull, c, o);
   if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
+}
+
+static int sm_count_of_current() {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms;
 }
 
 static int grid_for(int64_t n, int nt) {
@@ -764,22 +814,18 @@ int ns_sort_small_batch_async_i32(int32_t* d_keys, const uint32_t* d_offsets, si
   if (num_arrays == 0) return NS_OK;
   if (!d_keys || !d_offsets) return NS_ERR_INVALID;
   if (num_arrays >= (size_t)UINT32_MAX) return NS_ERR_INVALID;
-  // cooperative launch: every CTA resident (the grid-wide barrier between
-  // the validation and the sort phases), at most one CTA per chunk
-  const int64_t chunks = (int64_t)((num_arrays + kBaArr - 1) / kBaArr);
-  int dev = 0, sms = 148, per_sm = 1;
-  NSB_TRY(check_cuda(cudaGetDevice(&dev), "cudaGetDevice"));
-  NSB_TRY(check_cuda(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "attr"));
-  NSB_TRY(check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sort_small_batch_kernel,
-                                                                   kBaNT, 0),
-                     "cudaOccupancyMaxActiveBlocksPerMultiprocessor"));
-  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(chunks, (int64_t)sms * per_sm));
-  int64_t na = (int64_t)num_arrays;
-  void* args[] = {&d_keys, const_cast<uint32_t**>(&d_offsets), &na, &d_status};
   {
     Prof prof(PK_BATCH, s);
-    const cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(sort_small_batch_kernel),
-                                                      dim3(grid), dim3(kBaNT), args, 0, s);
+    // four CTAs per SM: the sort CTAs share the SMs with it (PDL)
+    const int64_t vg = std::min<int64_t>((int64_t)(num_arrays / 4096 + 1), 4 * sm_count_of_current());
+    batch_validate_kernel<<<(unsigned)vg, 256, 0, s>>>(d_offsets, (int64_t)num_arrays, d_status);
+  }
+  NSB_TRY(check_launch("batch_validate_kernel"));
+  const int64_t ctas = (int64_t)((num_arrays + kBaArr - 1) / kBaArr);
+  {
+    Prof prof(PK_BATCH, s);
+    const cudaError_t e = launch_pdl(0, sort_small_batch_kernel, (unsigned)ctas, kBaNT, 0, s, d_keys,
+                                     d_offsets, (int64_t)num_arrays, d_status);
     if (e != cudaSuccess) return check_cuda(e, "sort_small_batch_kernel");
   }
   return check_launch("sort_small_batch_kernel");
