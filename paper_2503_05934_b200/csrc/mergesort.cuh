@@ -36,15 +36,19 @@ template <int LEVELS, int K, class T>
 __device__ __forceinline__ void warp_bitonic(T (&v)[K], int lane) {
 #pragma unroll
   for (int s = 0; s < LEVELS; ++s) {
-    // flip step: (lane, i) <-> (lane ^ (2^(s+1)-1), K-1-i)
+    // flip step: (lane, i) <-> (lane ^ (2^(s+1)-1), K-1-i).  Positions i and
+    // K-1-i exchange with each other, so they are done as a pair: two
+    // temporaries live instead of K (the 40-register tile sort spilled here)
     {
       const int fm = (2 << s) - 1;
       const bool upper = (lane >> s) & 1;
-      T t[K];
 #pragma unroll
-      for (int i = 0; i < K; ++i) t[i] = __shfl_xor_sync(kFull, v[K - 1 - i], fm);
-#pragma unroll
-      for (int i = 0; i < K; ++i) v[i] = upper ? max(v[i], t[i]) : min(v[i], t[i]);
+      for (int i = 0; i < K / 2; ++i) {
+        const T ti = __shfl_xor_sync(kFull, v[K - 1 - i], fm);
+        const T tj = __shfl_xor_sync(kFull, v[i], fm);
+        v[i] = upper ? max(v[i], ti) : min(v[i], ti);
+        v[K - 1 - i] = upper ? max(v[K - 1 - i], tj) : min(v[K - 1 - i], tj);
+      }
     }
     // cross-lane half-cleaners
 #pragma unroll
@@ -392,13 +396,32 @@ __device__ __forceinline__ void cta_sort(const Key* in, Key* out, int valid, Key
 template <int NT, int K, int LEAF, class Key>
 __device__ __forceinline__ void cta_sort_regs(Key (&v)[K], Key* out, int valid, Key* sm);
 
+// Global -> registers for the skewed tile sort.  A full, 16-byte-aligned
+// tile (every tile of a merge sort but the last) skips the shared-memory
+// staging: the register stage accepts any assignment of keys to threads, so
+// thread t takes vector q*NT + t and every warp-wide load is one coalesced
+// 512-byte row.  Partial or unaligned tiles are staged through shared memory
+// into the BLOCKED assignment (thread t owns [t*K, t*K + K), pads the key
+// maximum), which keeps cta_sort_regs' all-padding-warp skip valid.
 template <int NT, int K, int LEAF, class Key>
 __device__ __forceinline__ void cta_sort_skewed_body(const Key* in, Key* out, int valid, Key* sm) {
   constexpr int T = NT * K;
-  tile_load<NT, T>(in, valid, sm);
-  __syncthreads();
+  constexpr int PV = kpv<Key>();
   Key v[K];
-  smem_to_regs<K>(sm, v);
+  if (valid == T && (reinterpret_cast<uintptr_t>(in) & 15) == 0) {
+    const int4* p = reinterpret_cast<const int4*>(in);
+#pragma unroll
+    for (int q = 0; q < K / PV; ++q) {
+      Key e[PV];
+      unpack16<Key>(__ldcs(p + q * NT + threadIdx.x), e);  // streamed: read once
+#pragma unroll
+      for (int u = 0; u < PV; ++u) v[q * PV + u] = e[u];
+    }
+  } else {
+    tile_load<NT, T>(in, valid, sm);
+    __syncthreads();
+    smem_to_regs<K>(sm, v);
+  }
   cta_sort_regs<NT, K, LEAF>(v, out, valid, sm);
 }
 

@@ -387,9 +387,17 @@ struct QsClassifier {
     const uint32_t e = cell[ci];
     int j = (int)(e & 255u);
     int k = (int)(e >> 8);
-    Key t = tab[j * R];
+    // the first step without a branch (a cell holds 0 or 1 pivot almost
+    // always): both candidate pivots are loaded at once (slot B-1 is the
+    // key-maximum pad, so j + 1 <= B - 1 stays in the table)
+    const Key t0 = tab[j * R];
+    const Key t1 = tab[min(j + 1, B - 1) * R];
+    const bool s1 = (k > 0) & (t0 < key);
+    j += s1;
+    k -= s1;
+    Key t = s1 ? t1 : t0;
 #pragma unroll 1
-    while (k > 0 && t < key) {
+    while (k > 0 && t < key) {  // cells with 2+ pivots (clustered pivots)
       ++j;
       --k;
       t = tab[j * R];
@@ -425,54 +433,126 @@ __device__ __forceinline__ void qs_hist_add(uint32_t* hist, int b) {
   if (b >= 0) atomicAdd(&hist[b], 1u);
 }
 
-template <bool FULL, class Key>
-__device__ __forceinline__ void qs_count_chunk(const Key* __restrict__ X, uint8_t* __restrict__ ids,
-                                               int64_t c0, int64_t c1,
-                                               const QsClassifier<Key>& cls, uint32_t* hist) {
-  Key k[kQsPer];
-#pragma unroll
-  for (int u = 0; u < kQsPer; ++u) {
-    const int64_t i = c0 + u * kQsNT + threadIdx.x;
-    k[u] = (FULL || i < c1) ? __ldg(X + i) : Key(0);
-  }
-#pragma unroll
-  for (int u = 0; u < kQsPer; ++u) {
-    const int64_t i = c0 + u * kQsNT + threadIdx.x;
-    const bool in = FULL || i < c1;
-    const int b = in ? cls(k[u]) : -1;
-    NSB_DCHECK(b < 2 * cls.B - 1);
-    if (in) ids[i] = (uint8_t)b;
-    qs_hist_add(hist, b);
-  }
+// Chunk staging for the count and scatter kernels: one elected thread copies
+// the 16-byte-aligned cover of a chunk's keys (and, for the scatter, its
+// one-byte bucket ids) into shared memory with a bulk copy (TMA 1D, mbarrier
+// completion) as soon as the previous chunk has been moved into registers, so
+// the next chunk's HBM read overlaps this chunk's classification / multisplit.
+// A cover that would leave the array (a misaligned caller pointer at the
+// first chunk, the array's last chunk) is read directly instead.
+template <class T>
+struct QsCover {
+  const T* src;
+  int phase;       // elements of the cover before the chunk's first
+  uint32_t bytes;  // multiple of 16
+  bool ok;
+};
+template <class T>
+__device__ __forceinline__ QsCover<T> qs_cover(const T* X, int64_t n, int64_t c0, int64_t c1) {
+  const uintptr_t x = reinterpret_cast<uintptr_t>(X);
+  const uintptr_t a = reinterpret_cast<uintptr_t>(X + c0) & ~uintptr_t(15);
+  const uintptr_t e = (reinterpret_cast<uintptr_t>(X + c1) + 15) & ~uintptr_t(15);
+  QsCover<T> cv;
+  cv.src = reinterpret_cast<const T*>(a);
+  cv.phase = (int)((reinterpret_cast<uintptr_t>(X + c0) - a) / sizeof(T));
+  cv.bytes = (uint32_t)(e - a);
+  cv.ok = c1 > c0 && a >= x && e <= reinterpret_cast<uintptr_t>(X + n) && x % sizeof(T) == 0;
+  return cv;
+}
+// staging buffer sizes: a chunk plus the cover's slack
+template <class T>
+__host__ __device__ constexpr int qs_stage_elems() { return kQsChunk + 32 / (int)sizeof(T); }
+
+template <class Key>
+__host__ __device__ constexpr int qs_count_smem() {
+  return qs_table_bytes<Key>() + qs_stage_elems<Key>() * (int)sizeof(Key);
 }
 
 template <class Key>
 __global__ void __launch_bounds__(kQsNT, 2) qs_count_kernel(QsCtx<Key> c, int level) {
   extern __shared__ __align__(16) unsigned char qs_raw[];
   __shared__ uint32_t hist[2 * kQsMaxB];
+  __shared__ __align__(8) uint64_t bar;
+  Key* stage = reinterpret_cast<Key*>(qs_raw + qs_table_bytes<Key>());
+  const int tid = threadIdx.x;
   const Key* X = qs_src(c, level);
   const int64_t nch = qs_nchunk(c, level);
   int64_t cur = -1;  // segment whose tables are loaded
   QsClassifier<Key> cls{};
-  for (int64_t ch = blockIdx.x; ch < nch; ch += gridDim.x) {
+  // contiguous chunk ranges per CTA: neighbouring chunks share a segment, so
+  // the tables are reloaded only when the segment changes
+  const int64_t per = (nch + gridDim.x - 1) / gridDim.x;
+  const int64_t ch_begin = (int64_t)blockIdx.x * per;
+  const int64_t ch_end = min(nch, ch_begin + per);
+  auto range = [&](int64_t ch, int64_t& c0, int64_t& c1) {
+    const QsSeg g = qs_seg(c, level, qs_seg_of_chunk(c, level, ch));
+    c0 = g.start + (ch - g.chunk0) * kQsChunk;
+    c1 = min(g.start + g.len, c0 + kQsChunk);
+  };
+  auto issue = [&](int64_t ch) {  // thread 0: stage chunk ch
+    int64_t c0, c1;
+    range(ch, c0, c1);
+    const QsCover<Key> cv = qs_cover(X, c.n, c0, c1);
+    if (cv.ok) {
+      fence_proxy_async_smem();  // the previous chunk's generic reads of the buffer are done
+      mbar_arrive_expect_tx(&bar, cv.bytes);
+      tma_load_1d(stage, cv.src, cv.bytes, &bar);
+    }
+  };
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0 && ch_begin < ch_end) issue(ch_begin);
+  uint32_t parity = 0;
+  for (int64_t ch = ch_begin; ch < ch_end; ++ch) {
     const int64_t sid = qs_seg_of_chunk(c, level, ch);
     const QsSeg g = qs_seg(c, level, sid);
     const int NB = 2 * g.B - 1;
-    __syncthreads();  // the previous chunk is done with the tables / hist
-    if (sid != cur)
-      cls = qs_load_classifier<Key>(qs_raw, c.spl[level & 1] + g.spl_off,
-                                    c.cells[level & 1] + 16 * g.spl_off, g.B);
-    cur = sid;
-    for (int i = threadIdx.x; i < NB; i += kQsNT) hist[i] = 0;
-    __syncthreads();
     const int64_t c0 = g.start + (ch - g.chunk0) * kQsChunk;
     const int64_t c1 = min(g.start + g.len, c0 + kQsChunk);
-    if (c1 - c0 == kQsChunk) qs_count_chunk<true>(X, c.ids, c0, c1, cls, hist);
-    else qs_count_chunk<false>(X, c.ids, c0, c1, cls, hist);
+    const int cnt = (int)(c1 - c0);
+    const QsCover<Key> cv = qs_cover(X, c.n, c0, c1);
+    // this chunk's keys -> registers (from the staging buffer when staged)
+    Key k[kQsPer];
+    if (cv.ok) {
+      mbar_wait(&bar, parity);
+      parity ^= 1u;
+#pragma unroll
+      for (int u = 0; u < kQsPer; ++u) {
+        const int j = u * kQsNT + tid;
+        k[u] = j < cnt ? stage[cv.phase + j] : Key(0);
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < kQsPer; ++u) {
+        const int j = u * kQsNT + tid;
+        k[u] = j < cnt ? __ldg(X + c0 + j) : Key(0);
+      }
+    }
+    __syncthreads();  // buffer, tables and hist free: the previous chunk is done
+    if (tid == 0 && ch + 1 < ch_end) issue(ch + 1);  // overlaps this chunk's work
+    if (sid != cur) {
+      cls = qs_load_classifier<Key>(qs_raw, c.spl[level & 1] + g.spl_off,
+                                    c.cells[level & 1] + 16 * g.spl_off, g.B);
+      cur = sid;
+    }
+    for (int i = tid; i < NB; i += kQsNT) hist[i] = 0;
     __syncthreads();
-    uint32_t* cnt = c.cnt[level & 1] + g.cnt_off;
-    for (int b = threadIdx.x; b < NB; b += kQsNT)
-      if (hist[b]) atomicAdd(&cnt[b], hist[b]);
+#pragma unroll
+    for (int u = 0; u < kQsPer; ++u) {
+      const int j = u * kQsNT + tid;
+      const bool in = j < cnt;
+      const int b = in ? cls(k[u]) : -1;
+      NSB_DCHECK(b < 2 * cls.B - 1);
+      if (in) c.ids[c0 + j] = (uint8_t)b;
+      qs_hist_add(hist, b);
+    }
+    __syncthreads();
+    uint32_t* cn = c.cnt[level & 1] + g.cnt_off;
+    for (int b = tid; b < NB; b += kQsNT)
+      if (hist[b]) atomicAdd(&cn[b], hist[b]);
   }
 }
 
@@ -515,8 +595,9 @@ __device__ __forceinline__ int64_t qs_block_scan(uint32_t v, int64_t* warp_tot) 
 #define NSB_QS_PACK 4096
 #endif
 // Leaf packing: neighbouring buckets of <= kQsPack keys whose start offsets
-// in the segment fall in the same kQsPack-key window form one leaf job, so a
-// job is < 2 kQsPack keys; the rule is evaluated by every bucket in parallel.
+// in the segment fall in the same window of W keys form one leaf job, so a
+// job is < W + kQsPack keys; the rule is evaluated by every bucket in
+// parallel.
 constexpr int kQsPack = NSB_QS_PACK;
 static_assert(2 * kQsPack <= kSmallTile, "packed jobs must fit one tile");
 
@@ -557,10 +638,13 @@ __global__ void __launch_bounds__(kQsNT) qs_plan_kernel(QsCtx<Key> c, int level,
     }
     __syncthreads();
     const bool small = v > 0 && v <= (uint32_t)kQsPack;
-    const int64_t win = (pos - g.start) / kQsPack;
+    // (W = kQsWinBig from kQsBigLeafN keys measured slower: 16M random
+    // 0.45 -> 0.49 ms, the 16384-key leaf tiles cost more than they save)
+    const int64_t W = kQsPack;
+    const int64_t win = (pos - g.start) / W;
     bool head = false;
     if (small) {
-      head = prev < 0 || s_cnt[prev] > (uint32_t)kQsPack || (s_pos[prev] - g.start) / kQsPack != win;
+      head = prev < 0 || s_cnt[prev] > (uint32_t)kQsPack || (s_pos[prev] - g.start) / W != win;
     }
     s_flag[tid] = head ? 2 : small ? 1 : v > 0 ? 3 : 0;
     __syncthreads();
@@ -654,7 +738,9 @@ __global__ void __launch_bounds__(kQsNT, 2) qs_scatter_kernel(QsCtx<Key> c, int 
   const Key* X = qs_src(c, level);
   Key* Y = qs_src(c, level + 1);
   const int64_t nch = qs_nchunk(c, level);
-  for (int64_t ch = blockIdx.x; ch < nch; ch += gridDim.x) {
+  const int64_t per = (nch + gridDim.x - 1) / gridDim.x;  // contiguous chunk ranges
+  const int64_t ch_end = min(nch, ((int64_t)blockIdx.x + 1) * per);
+  for (int64_t ch = (int64_t)blockIdx.x * per; ch < ch_end; ++ch) {
     const QsSeg g = qs_seg(c, level, qs_seg_of_chunk(c, level, ch));
     const int NB = 2 * g.B - 1;
     __syncthreads();
@@ -981,7 +1067,7 @@ static int quick_sort_segments(Key* keys, int64_t nseg0, int64_t len0, int leaf,
   const int levels = qs_levels(len0);
   constexpr int sample_smem = 0;
   constexpr int scatter_smem = qs_scatter_smem<Key>();
-  constexpr int count_smem = qs_table_bytes<Key>();
+  constexpr int count_smem = qs_count_smem<Key>();
   NSB_TRY(ensure_smem_attr(reinterpret_cast<const void*>(qs_count_kernel<Key>), count_smem,
                            "cudaFuncSetAttribute(qs_count)"));
   NSB_TRY(ensure_smem_attr(reinterpret_cast<const void*>(qs_scatter_kernel<Key>), scatter_smem,
