@@ -425,6 +425,32 @@ __device__ __forceinline__ void cta_sort_skewed_body(const Key* in, Key* out, in
   cta_sort_regs<NT, K, LEAF>(v, out, valid, sm);
 }
 
+// v as NQ quads of PV keys: quad i <- quad (i + r) mod NQ, branch-free (one
+// conditional cyclic shift per bit of r, walked cycle by cycle so one
+// temporary quad is live at a time).
+template <int NQ, int PV, class Key, int K>
+__device__ __forceinline__ void rotate_quads(Key (&v)[K], int r) {
+#pragma unroll
+  for (int b = 1; b < NQ; b <<= 1) {
+    const bool on = (r & b) != 0;
+#pragma unroll
+    for (int c0 = 0; c0 < b; ++c0) {  // gcd(NQ, b) = b cycles of length NQ / b
+      Key t[PV];
+#pragma unroll
+      for (int u = 0; u < PV; ++u) t[u] = v[c0 * PV + u];
+#pragma unroll
+      for (int j = 0; j < NQ / b - 1; ++j) {
+        const int i = c0 + j * b, nx = i + b;
+#pragma unroll
+        for (int u = 0; u < PV; ++u) v[i * PV + u] = on ? v[nx * PV + u] : v[i * PV + u];
+      }
+      const int last = c0 + (NQ / b - 1) * b;
+#pragma unroll
+      for (int u = 0; u < PV; ++u) v[last * PV + u] = on ? t[u] : v[last * PV + u];
+    }
+  }
+}
+
 // The skewed tile sort from registers: thread t holds K of the tile's T keys
 // (any assignment — the result is the sorted multiset; pad with the key
 // maximum), `valid` keys are stored to out (nullptr: left in sm[0, T)).
@@ -478,14 +504,23 @@ __device__ __forceinline__ void cta_sort_regs(Key (&v)[K], Key* out, int valid, 
     {
       const int run = (warp << (5 - WL)) + (lane >> WL);
       Key* dst = sm + run * (L0 + GAP) + K * (lane & (LPR - 1));
+      const int li = lane & (LPR - 1);
+      // Lane li's K keys are 16-byte quads at a stride of K*KB bytes, so at
+      // equal q the lanes of a quarter-warp would hit the same 16-byte bank
+      // group (8-way conflict for 128-byte lane blocks).  Each lane rotates
+      // its quads by r (three conditional cyclic shifts, one temporary quad)
+      // and stores quad (q + r) mod NQ at step q: eight distinct groups.
+      constexpr int NQ = K / PV;
+      static_assert(NQ >= 1 && NQ <= 8 && (NQ & (NQ - 1)) == 0, "quads per lane");
+      const int r = NQ == 1 ? 0 : (li / (8 / NQ)) & (NQ - 1);
+      rotate_quads<NQ, PV>(v, r);
 #pragma unroll
-      for (int q = 0; q < K / PV; ++q) {
+      for (int q = 0; q < NQ; ++q) {
         Key e[PV];
 #pragma unroll
         for (int u = 0; u < PV; ++u) e[u] = v[q * PV + u];
-        *reinterpret_cast<int4*>(dst + q * PV) = pack16<Key>(e);
+        *reinterpret_cast<int4*>(dst + ((q + r) & (NQ - 1)) * PV) = pack16<Key>(e);
       }
-      const int li = lane & (LPR - 1);
       for (int i = li; i < GAP; i += LPR) sm[run * (L0 + GAP) + L0 + i] = KeyT<Key>::kMax;
     }
     __syncthreads();
@@ -994,14 +1029,74 @@ __host__ __device__ constexpr int v2_min_blocks(int NT, int K, int key_bytes) {
   return b < 1 ? 1 : b;
 }
 
+// Stage + merge + store of one tile of a pairwise pass whose merge-path
+// splits (a0 at diag0, a1 at diag1) are known: both input slices go to shared
+// memory by bulk copy (TMA 1D, completion on *bar at `parity`), the merge is
+// merge_staged_tile's.  `init_bar`: the caller has not initialised *bar
+// (the one-tile kernel does it here; the persistent flow kernel once).
+template <int NT, int K, class Key>
+__device__ __forceinline__ void merge_tile_v2(const Key* __restrict__ src, Key* __restrict__ dst,
+                                              const PassPlan& P, const TileGeom& g, int64_t a0,
+                                              int64_t a1, BlockSamples<Key> bs, Key* sm,
+                                              uint64_t* bar, uint32_t parity, bool init_bar) {
+  constexpr int TM = NT * K;
+  constexpr int PV = kpv<Key>();
+  constexpr int KB = (int)sizeof(Key);
+  const int tid = threadIdx.x;
+  const int la = (int)(a1 - a0);
+  const int lb = (int)((g.diag1 - a1) - (g.diag0 - a0));
+  // the splits lie on the pair's merge path and the slices fit the tile
+  NSB_DCHECK(a0 >= 0 && a0 <= a1 && a1 <= g.a_len && g.diag0 - a0 >= 0 && g.diag1 - a1 <= g.b_len &&
+             lb >= 0 && la + lb == (int)(g.diag1 - g.diag0) && la + lb <= TM);
+  const Key* A = src + g.pair_base + a0;
+  const Key* B = src + g.pair_base + g.a_len + (g.diag0 - a0);
+  const Key* lo = src;
+  const Key* hi = src + P.n;
+
+  // smem placement mirrors global 16-byte alignment so one bulk copy per slice
+  const uintptr_t a_addr = reinterpret_cast<uintptr_t>(A), b_addr = reinterpret_cast<uintptr_t>(B);
+  const int a_shift = (int)((a_addr & 15) / KB), b_shift = (int)((b_addr & 15) / KB);
+  const int b_off = (a_shift + la + v2_pad(K) + PV - 1) & ~(PV - 1);  // B cover starts 16-byte aligned
+  const Key* a_cov = A - a_shift;
+  const Key* b_cov = B - b_shift;
+  const int a_words = (a_shift + la + PV - 1) & ~(PV - 1), b_words = (b_shift + lb + PV - 1) & ~(PV - 1);
+  const bool a_tma = la > 0 && (a_addr % KB) == 0 && a_cov >= lo && a_cov + a_words <= hi;
+  const bool b_tma = lb > 0 && (b_addr % KB) == 0 && b_cov >= lo && b_cov + b_words <= hi;
+  NSB_DCHECK(b_off + b_words + v2_pad(K) <= v2_smem_words(TM, K) && a_shift + la + v2_pad(K) <= b_off);
+
+  // the output offset crosses the merge loop through shared memory, so no
+  // 64-bit geometry stays live in registers next to the K outputs
+  __shared__ int64_t s_out;
+  if (tid == 0) {
+    if (init_bar) {
+      mbar_init(bar, 1);
+      fence_mbar_init();
+    }
+    s_out = g.pair_base + g.diag0;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    fence_proxy_async_smem();  // earlier generic accesses of sm before the bulk writes
+    const uint32_t bytes = (a_tma ? a_words * (uint32_t)KB : 0u) + (b_tma ? b_words * (uint32_t)KB : 0u);
+    mbar_arrive_expect_tx(bar, bytes);
+    if (a_tma) tma_load_1d(sm, a_cov, a_words * (uint32_t)KB, bar);
+    if (b_tma) tma_load_1d(sm + b_off, b_cov, b_words * (uint32_t)KB, bar);
+  }
+  if (!a_tma)
+    for (int i = tid; i < la; i += NT) sm[a_shift + i] = __ldcs(A + i);
+  if (!b_tma)
+    for (int i = tid; i < lb; i += NT) sm[b_off + b_shift + i] = __ldcs(B + i);
+  mbar_wait(bar, parity);
+  __syncthreads();
+  merge_staged_tile<NT, K>(sm, a_shift, la, b_off + b_shift, lb, dst, &s_out, bs);
+}
+
 template <int NT, int K, bool FUSED = false, class Key = int32_t>
 __global__ void __launch_bounds__(NT, v2_min_blocks(NT, K, (int)sizeof(Key)))
     merge_pass_v2_kernel(const Key* __restrict__ src, Key* __restrict__ dst, PassPlan P,
                          const int64_t* __restrict__ mp, BlockSamples<Key> bs) {
   constexpr int TM = NT * K;
   static_assert(TM % 4 == 0, "tiles must start 16-byte aligned");
-  constexpr int PV = kpv<Key>();           // keys per 16 bytes
-  constexpr int KB = (int)sizeof(Key);
   __shared__ __align__(128) Key sm[v2_smem_words(TM, K)];
   __shared__ __align__(8) uint64_t bar;
   const int tid = threadIdx.x;
@@ -1033,49 +1128,8 @@ __global__ void __launch_bounds__(NT, v2_min_blocks(NT, K, (int)sizeof(Key)))
     a0 = mp[c];
     a1 = last_in_pair ? g.a_len : mp[c + 1];
   }
-  const int la = (int)(a1 - a0);
-  const int lb = (int)((g.diag1 - a1) - (g.diag0 - a0));
-  // the splits lie on the pair's merge path and the slices fit the tile
-  NSB_DCHECK(a0 >= 0 && a0 <= a1 && a1 <= g.a_len && g.diag0 - a0 >= 0 && g.diag1 - a1 <= g.b_len &&
-             lb >= 0 && la + lb == (int)(g.diag1 - g.diag0) && la + lb <= TM);
-  const Key* A = src + g.pair_base + a0;
-  const Key* B = src + g.pair_base + g.a_len + (g.diag0 - a0);
-  const Key* lo = src;
-  const Key* hi = src + P.n;
-
-  // smem placement mirrors global 16-byte alignment so one bulk copy per slice
-  const uintptr_t a_addr = reinterpret_cast<uintptr_t>(A), b_addr = reinterpret_cast<uintptr_t>(B);
-  const int a_shift = (int)((a_addr & 15) / KB), b_shift = (int)((b_addr & 15) / KB);
-  const int b_off = (a_shift + la + v2_pad(K) + PV - 1) & ~(PV - 1);  // B cover starts 16-byte aligned
-  const Key* a_cov = A - a_shift;
-  const Key* b_cov = B - b_shift;
-  const int a_words = (a_shift + la + PV - 1) & ~(PV - 1), b_words = (b_shift + lb + PV - 1) & ~(PV - 1);
-  const bool a_tma = la > 0 && (a_addr % KB) == 0 && a_cov >= lo && a_cov + a_words <= hi;
-  const bool b_tma = lb > 0 && (b_addr % KB) == 0 && b_cov >= lo && b_cov + b_words <= hi;
-  NSB_DCHECK(b_off + b_words + v2_pad(K) <= v2_smem_words(TM, K) && a_shift + la + v2_pad(K) <= b_off);
-
-  // the output offset crosses the merge loop through shared memory, so no
-  // 64-bit geometry stays live in registers next to the K outputs
-  __shared__ int64_t s_out;
-  if (tid == 0) {
-    mbar_init(&bar, 1);
-    fence_mbar_init();
-    s_out = g.pair_base + g.diag0;
-  }
-  __syncthreads();
-  if (tid == 0) {
-    const uint32_t bytes = (a_tma ? a_words * (uint32_t)KB : 0u) + (b_tma ? b_words * (uint32_t)KB : 0u);
-    mbar_arrive_expect_tx(&bar, bytes);
-    if (a_tma) tma_load_1d(sm, a_cov, a_words * (uint32_t)KB, &bar);
-    if (b_tma) tma_load_1d(sm + b_off, b_cov, b_words * (uint32_t)KB, &bar);
-  }
-  if (!a_tma)
-    for (int i = tid; i < la; i += NT) sm[a_shift + i] = __ldcs(A + i);
-  if (!b_tma)
-    for (int i = tid; i < lb; i += NT) sm[b_off + b_shift + i] = __ldcs(B + i);
-  mbar_wait(&bar, 0);
-  __syncthreads();
-  merge_staged_tile<NT, K>(sm, a_shift, la, b_off + b_shift, lb, dst, &s_out, bs);
+  merge_tile_v2<NT, K>(src, dst, P, g, a0, a1, bs, sm, &bar, 0u, true);
 }
+
 
 }  // namespace nsb
