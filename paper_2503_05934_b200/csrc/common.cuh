@@ -124,6 +124,23 @@ inline cudaError_t launch_pdl(int64_t n, void (*kern)(KArgs...), unsigned grid, 
   return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 
+// The same with the attribute chosen by the caller.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl_if(bool on, void (*kern)(KArgs...), unsigned grid, unsigned block,
+                                 size_t smem, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = on ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 // Opt a kernel into `bytes` of dynamic shared memory on the CURRENT device,
 // once per (device, kernel): the attribute is per device, so a process that
 // drives several GPUs must set it on each.

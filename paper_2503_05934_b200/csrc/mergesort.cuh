@@ -282,6 +282,33 @@ __device__ __forceinline__ void tile_store(const Key* sm, Key* out, int valid) {
 // (32-thread tiles, int64 tiles other than 8 or 16 keys per thread).  int32
 // tiles of up to 1024 threads and int64 tiles of 8 / 16 keys per thread use
 // the skewed variant.
+// From registers (thread t holds K of the tile's keys, any assignment, pads
+// the key maximum): the sorted tile is left in padded smem, logical key i at
+// sm[pad_idx(i)].
+template <int NT, int K, int LEAF, class Key>
+__device__ __forceinline__ void cta_sort_padded_regs(Key (&v)[K], Key* sm) {
+  constexpr int T = NT * K;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  thread_sort<LEAF>(v);  // the network base case (try_base_case, hybrid.hpp:48-56)
+  if constexpr (NT >= 32) warp_bitonic<5>(v, lane);
+#pragma unroll 1
+  for (int R = 32 * K; R < T; R *= 2) {
+    __syncthreads();
+    regs_to_smem<K>(sm, v);
+    __syncthreads();
+    const int pos = tid * K;
+    const int pair = pos & ~(2 * R - 1);
+    const int diag = pos - pair;
+    const SmemRun<Key> A{sm, pair}, B{sm, pair + R};
+    const int a = merge_path<int>(A, R, B, R, diag);
+    serial_merge<K>(A, R, B, R, a, diag - a, v);
+  }
+  __syncthreads();
+  regs_to_smem<K>(sm, v);
+  __syncthreads();
+}
+
 template <int NT, int K, int LEAF, class Key>
 __device__ __forceinline__ void cta_sort_padded(const Key* in, Key* out, int valid, Key* sm) {
   constexpr int T = NT * K;

@@ -196,7 +196,9 @@ __device__ __forceinline__ void qs_write_pivots_zero(const QsCtx<Key>& c, int le
 
 template <class Key>
 __global__ void __launch_bounds__(256) qs_sample_kernel(QsCtx<Key> c, int level) {
-  __shared__ Key sub[512];
+  pdl_wait();  // everything below reads the previous kernels' lists / keys
+  pdl_trigger();
+  __shared__ __align__(16) Key tile[padded_words<Key>(2048)];
   __shared__ Key piv[kQsMaxB];
   __shared__ uint32_t ccount[16 * kQsMaxB];
   __shared__ uint32_t wsum[8];
@@ -213,11 +215,13 @@ __global__ void __launch_bounds__(256) qs_sample_kernel(QsCtx<Key> c, int level)
   const Key* X = qs_src(c, level);
   Key* splb = c.spl[level & 1];
   const int64_t nseg = qs_nseg(c, level);
-  for (int64_t base = (int64_t)blockIdx.x * 8; base < nseg; base += (int64_t)gridDim.x * 8) {
-    // segments of B <= 32 pivots (S <= 512 samples): one warp each, sorted in
-    // registers (16 per lane, network base case + warp bitonic stage)
-    const int64_t s = base + warp;
-    if (s < nseg) {
+  // segments of B <= 32 pivots (S <= 512 samples): one warp each, sorted in
+  // registers (16 per lane, network base case + warp bitonic stage); segment
+  // s goes to CTA s mod grid first, so a level of few segments spreads over
+  // the SMs instead of packing 8 warps onto one
+  for (int64_t s = blockIdx.x + (int64_t)warp * gridDim.x; s < nseg;
+       s += (int64_t)gridDim.x * 8) {
+    {
       const QsSeg g = qs_seg(c, level, s);
       if (g.B <= 32) {
         const int S = kQsOver * g.B;
@@ -261,50 +265,30 @@ __global__ void __launch_bounds__(256) qs_sample_kernel(QsCtx<Key> c, int level)
       }
     }
   }
-  // larger segments (B = 64, 128: S = 1024, 2048 samples), one CTA each: S/512 warps each
-    // sort 512 samples in registers and keep every (S/512)-th; warp 0 sorts
-    // those 512 regular sub-samples and takes the pivots at regular ranks
-    // (regular sampling of regular samples: PSRS-style quantile bounds)
+  // larger segments (B = 64, 128: S = 1024, 2048 samples), one CTA each: the
+  // CTA gathers 8 samples per thread and sorts all S of them at once (network
+  // base case, warp bitonic stage, three shared-memory merge levels), so the
+  // pivots are exact regular quantiles of the samples: pivot j = sample
+  // 16 (j+1) - 1 of the sorted S
   for (int64_t sb = blockIdx.x; sb < nseg; sb += gridDim.x) {
     {
       const QsSeg g = qs_seg(c, level, sb);
       if (g.B <= 32) continue;
       const int S = kQsOver * g.B;
-      const int nw = S / 512;
       const int64_t stride = g.len / S;
-      if (warp < nw) {
-        Key v[16];
+      Key v[8];
 #pragma unroll
-        for (int u = 0; u < 16; ++u)
-          v[u] = X[g.start + qs_sample_pos(warp * 512 + lane * 16 + u, stride, level)];
-        thread_sort<8>(v);
-        warp_bitonic<5>(v, lane);
-#pragma unroll
-        for (int u = 0; u < 16; ++u) {
-          const int r = lane * 16 + u;
-          if (r % nw == nw - 1) sub[warp * (512 / nw) + r / nw] = v[u];
-        }
+      for (int u = 0; u < 8; ++u) {
+        const int i = tid * 8 + u;
+        v[u] = i < S ? X[g.start + qs_sample_pos(i, stride, level)] : KeyT<Key>::kMax;
       }
-      __syncthreads();
+      cta_sort_padded_regs<256, 8, 8>(v, tile);
       const int ncell = 16 * g.B;
       for (int i = tid; i < ncell; i += 256) ccount[i] = 0;
-      if (warp == 0) {
-        Key v[16];
-#pragma unroll
-        for (int u = 0; u < 16; ++u) v[u] = sub[lane * 16 + u];
-        thread_sort<8>(v);
-        warp_bitonic<5>(v, lane);
-        const int step = 512 / g.B;
-#pragma unroll
-        for (int u = 0; u < 16; ++u) {
-          const int r = lane * 16 + u + 1;
-          if (r % step == 0) {
-            const int j = r / step - 1;
-            const Key pv = j < g.B - 1 ? v[u] : KeyT<Key>::kMax;
-            splb[g.spl_off + j] = pv;
-            piv[j] = pv;
-          }
-        }
+      for (int j = tid; j < g.B; j += 256) {
+        const Key pv = j < g.B - 1 ? tile[pad_idx<Key>(16 * (j + 1) - 1)] : KeyT<Key>::kMax;
+        splb[g.spl_off + j] = pv;
+        piv[j] = pv;
       }
       qs_write_pivots_zero(c, level, g, tid, 256);
       __syncthreads();
@@ -470,6 +454,8 @@ __host__ __device__ constexpr int qs_count_smem() {
 
 template <class Key>
 __global__ void __launch_bounds__(kQsNT, 2) qs_count_kernel(QsCtx<Key> c, int level) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ __align__(16) unsigned char qs_raw[];
   __shared__ uint32_t hist[2 * kQsMaxB];
   __shared__ __align__(8) uint64_t bar;
@@ -607,6 +593,8 @@ __device__ __forceinline__ int qs_class_of(int64_t len) {
 
 template <class Key>
 __global__ void __launch_bounds__(kQsNT) qs_plan_kernel(QsCtx<Key> c, int level, int last) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ int64_t s_wtot[kQsNT / 32];
   __shared__ uint32_t s_cnt[kQsNT];
   __shared__ int64_t s_pos[kQsNT];
@@ -728,6 +716,8 @@ __host__ __device__ constexpr int qs_scatter_smem() {
 
 template <class Key>
 __global__ void __launch_bounds__(kQsNT, 2) qs_scatter_kernel(QsCtx<Key> c, int level) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ uint32_t hist[2 * kQsMaxB];    // counts, then local starts
   __shared__ long long delta[2 * kQsMaxB];  // global position - local start
   __shared__ int64_t wtot[kQsNT / 32];
@@ -900,6 +890,7 @@ __global__ void __launch_bounds__(NT, (bs_min_blocks_tput<NT, K, Key>()))
 }
 
 // ---- host side ---------------------------------------------------------------------
+constexpr int64_t kQsPdlMaxKeys = int64_t(1) << 22;
 // Side streams + fork/join events for the concurrent leaf classes: one set
 // per (host thread, device), so concurrent callers never share an event.
 struct QsSide {
@@ -1072,34 +1063,47 @@ static int quick_sort_segments(Key* keys, int64_t nseg0, int64_t len0, int leaf,
                            "cudaFuncSetAttribute(qs_count)"));
   NSB_TRY(ensure_smem_attr(reinterpret_cast<const void*>(qs_scatter_kernel<Key>), scatter_smem,
                            "cudaFuncSetAttribute(qs_scatter)"));
+  // programmatic dependent launch between the per-level kernels of
+  // latency-bound sorts (every kernel waits for its predecessor on entry;
+  // only the launch and CTA rasterisation overlap)
+  const bool pdl = pdl_enabled(nseg0 * len0 >= kQsPdlMaxKeys ? INT64_MAX : 0);
   for (int l = 0; l < levels; ++l) {
     const int64_t segs_ub = l == 0 ? nseg0 : z.max_segs;
     const int64_t chunks_ub = l == 0 ? nseg0 * c.cps0 : z.max_chunks;
     {
       Prof prof(PK_QS_SAMPLE, s);
-      qs_sample_kernel<Key><<<grid_of(reinterpret_cast<const void*>(qs_sample_kernel<Key>), 256, sample_smem,
-                                      segs_ub),
-                              256, sample_smem, s>>>(c, l);
+      NSB_TRY(check_cuda(launch_pdl_if(pdl, qs_sample_kernel<Key>,
+                                       grid_of(reinterpret_cast<const void*>(qs_sample_kernel<Key>), 256,
+                                               sample_smem, segs_ub),
+                                       256, sample_smem, s, c, l),
+                         "qs_sample_kernel"));
     }
     NSB_TRY(check_launch("qs_sample_kernel"));
     {
       Prof prof(PK_QS_COUNT, s);
-      qs_count_kernel<Key><<<grid_of(reinterpret_cast<const void*>(qs_count_kernel<Key>), kQsNT, count_smem,
-                                     chunks_ub),
-                             kQsNT, count_smem, s>>>(c, l);
+      NSB_TRY(check_cuda(launch_pdl_if(pdl, qs_count_kernel<Key>,
+                                       grid_of(reinterpret_cast<const void*>(qs_count_kernel<Key>), kQsNT,
+                                               count_smem, chunks_ub),
+                                       kQsNT, count_smem, s, c, l),
+                         "qs_count_kernel"));
     }
     NSB_TRY(check_launch("qs_count_kernel"));
     {
       Prof prof(PK_QS_PLAN, s);
-      qs_plan_kernel<Key><<<grid_of(reinterpret_cast<const void*>(qs_plan_kernel<Key>), kQsNT, 0, segs_ub),
-                            kQsNT, 0, s>>>(c, l, l == levels - 1);
+      NSB_TRY(check_cuda(launch_pdl_if(pdl, qs_plan_kernel<Key>,
+                                       grid_of(reinterpret_cast<const void*>(qs_plan_kernel<Key>), kQsNT, 0,
+                                               segs_ub),
+                                       kQsNT, 0, s, c, l, (int)(l == levels - 1)),
+                         "qs_plan_kernel"));
     }
     NSB_TRY(check_launch("qs_plan_kernel"));
     {
       Prof prof(PK_QS_SCATTER, s);
-      qs_scatter_kernel<Key><<<grid_of(reinterpret_cast<const void*>(qs_scatter_kernel<Key>), kQsNT,
-                                       scatter_smem, chunks_ub),
-                               kQsNT, scatter_smem, s>>>(c, l);
+      NSB_TRY(check_cuda(launch_pdl_if(pdl, qs_scatter_kernel<Key>,
+                                       grid_of(reinterpret_cast<const void*>(qs_scatter_kernel<Key>), kQsNT,
+                                               scatter_smem, chunks_ub),
+                                       kQsNT, scatter_smem, s, c, l),
+                         "qs_scatter_kernel"));
     }
     NSB_TRY(check_launch("qs_scatter_kernel"));
   }
