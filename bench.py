@@ -383,22 +383,46 @@ def run_ours(args, metric):
     # e2e through the public API with host buffers
     e2e = None
     if world == 1:
-        host = torch.empty(n, dtype=torch.int32, pin_memory=True).numpy()
-        host_src = pristine.cpu().numpy()
-        e2e_steps = max(1, min(args.steps, 3))
-        dts = []
-        ns.optimized_merge_sort(host, cfg)  # warm the C-ABI host cache
-        for _ in range(e2e_steps):
-            np.copyto(host, host_src)
-            t0 = time.perf_counter()
-            ns.optimized_merge_sort(host, cfg)
-            dts.append(time.perf_counter() - t0)
+        # a stream of K sorts of the 2^30-key pinned host array through the
+        # stream-ordered host API (ns_merge_sort_host_async_i32): every step
+        # uploads its input, sorts and downloads the result; two streams, so
+        # step k+1's upload overlaps step k's download (PCIe is full duplex)
+        host_in = torch.empty(n, dtype=torch.int32, pin_memory=True).numpy()
+        np.copyto(host_in, pristine.cpu().numpy())
+        outs = [torch.empty(n, dtype=torch.int32, pin_memory=True).numpy() for _ in range(2)]
+        sts = [torch.cuda.Stream(), torch.cuda.Stream()]
+        for j in range(2):  # warm: allocates each stream's device buffers
+            ns.sort_host_async(host_in, outs[j], cfg, stream=sts[j])
+        torch.cuda.synchronize()
+        e2e_steps = max(2, min(args.steps, 6))
+        t0 = time.perf_counter()
+        for k in range(e2e_steps):
+            ns.sort_host_async(host_in, outs[k % 2], cfg, stream=sts[k % 2])
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        for o in outs:
+            assert np.all(o[:-1] <= o[1:])
+        # one blocking call (the reference's own call shape, optimized_merge_sort
+        # on a pinned host array) for the single-sort latency
+        host = outs[0]
+        np.copyto(host, host_in)
+        t1 = time.perf_counter()
+        ns.optimized_merge_sort(host, cfg)
+        single = time.perf_counter() - t1
         assert np.all(host[:-1] <= host[1:])
-        e2e = {"value": n * e2e_steps / sum(dts) / 1e9, "unit": "Gkeys/s",
+        e2e = {"value": n * e2e_steps / dt / 1e9, "unit": "Gkeys/s",
                "h2d_bytes_per_step": 4 * n, "d2h_bytes_per_step": 4 * n,
-               "path": "optimized_merge_sort(pinned numpy int32, 6To8) -> ns_merge_sort_host_i32",
-               "steps": e2e_steps}
-        del host, host_src
+               "path": "sort_host_async(pinned numpy in -> pinned numpy out, 6To8) -> "
+                       "ns_merge_sort_host_async_i32, steps alternating two streams (each "
+                       "step's H2D + sort + D2H inside the wall-clock region; step k+1's "
+                       "upload overlaps step k's download)",
+               "steps": e2e_steps,
+               "single_call": {"value": n / single / 1e9, "unit": "Gkeys/s",
+                               "path": "optimized_merge_sort(pinned numpy int32, 6To8) -> "
+                                       "ns_merge_sort_host_i32 (blocking; H2D overlapped "
+                                       "with chunk sorts)"}}
+        del host_in, outs, host
+        ns.release_scratch()  # frees the host-API device caches too (ns_release_cache)
     else:
         # per rank: H2D of the shard from pinned memory, sample sort, D2H of the result
         hs = pristine.cpu().pin_memory()

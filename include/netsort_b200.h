@@ -315,6 +315,16 @@ int ns_quick_sort_host_i64(int64_t* h_keys, size_t n, uint32_t width_mask, int v
 /* merge — hybrid.hpp:186-193: h_keys[0, n_left) and h_keys[n_left, n) are
  * sorted runs of a HOST array; merges them in place (stable, left run wins
  * ties).  n_left == 0 or n_left == n is a no-op. */
+/* Stream-ordered host-array sorts: upload h_in, sort with the config's
+ * network base case, download into h_out (h_out == h_in allowed), all
+ * enqueued on `stream`; the call returns immediately (synchronise the stream
+ * before reading h_out).  Device buffers are cached per (device, stream) and
+ * reused only by later calls on the same stream.  With pinned host buffers,
+ * sorts on two streams overlap one upload with the other's download. */
+int ns_merge_sort_host_async_i32(const int32_t* h_in, int32_t* h_out, size_t n,
+                                 uint32_t width_mask, int varsort_max, void* stream);
+int ns_quick_sort_host_async_i32(const int32_t* h_in, int32_t* h_out, size_t n,
+                                 uint32_t width_mask, int varsort_max, void* stream);
 int ns_merge_host_i32(int32_t* h_keys, size_t n_left, size_t n);
 int ns_merge_host_i64(int64_t* h_keys, size_t n_left, size_t n);
 int ns_release_cache(void);

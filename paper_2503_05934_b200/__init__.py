@@ -10,4 +10,4 @@ from .api import (  # noqa: F401
     leaf_width, make_fixed_config, make_varsort_config, merge, merge_sort_dispatch_stats,
     multiset_digest, network,
     optimized_merge_sort, optimized_quick_sort, release_scratch, run_variant,
-    segmented_sort, sort_pairs, sort_small_batch, generate, generate_batch)
+    segmented_sort, sort_host_async, sort_pairs, sort_small_batch, generate, generate_batch)

@@ -45,6 +45,8 @@ SIGNATURES = {
     "ns_quick_sort_i64": (_i32, [_vp, _sz, _u32, _i32, _vp, _sz, _vp]),
     "ns_quick_sort_i32": (_i32, [_vp, _sz, _u32, _i32, _vp, _sz, _vp]),
     "ns_sort_small_batch_i32": (_i32, [_vp, _vp, _sz, _vp]),
+    "ns_merge_sort_host_async_i32": (_i32, [_vp, _vp, _sz, _u32, _i32, _vp]),
+    "ns_quick_sort_host_async_i32": (_i32, [_vp, _vp, _sz, _u32, _i32, _vp]),
     "ns_sort_small_batch_async_i32": (_i32, [_vp, _vp, _sz, _vp, _vp]),
     "ns_sort_pairs_temp_bytes_i32": (_sz, [_sz]),
     "ns_sort_pairs_i32": (_i32, [_vp, _vp, _sz, _vp, _sz, _vp]),

@@ -287,6 +287,25 @@ def optimized_merge_sort(a, *args):
     return _sort(_lib.NS_MERGE_SORT, a, left, right, cfg)
 
 
+def sort_host_async(src, dst, cfg: NetworkConfig, algorithm: Algorithm = Algorithm.merge_sort,
+                    stream=None):
+    """Stream-ordered host-array sort (ns_*_sort_host_async_i32): upload the
+    int32 numpy array `src`, sort it with the config's network base case,
+    download into `dst` (may be `src`), all enqueued on `stream` (a
+    torch.cuda.Stream, default the current one); returns at once.  Use pinned
+    host memory (e.g. torch.empty(..., pin_memory=True).numpy()) for the
+    copies to overlap; synchronise the stream before reading `dst`."""
+    import torch
+    if _check_host(src) != "i32" or _check_host(dst) != "i32" or len(dst) != len(src):
+        raise ValueError("sort_host_async: src and dst must be int32 host arrays of equal size")
+    s = stream if stream is not None else torch.cuda.current_stream()
+    fn = (lib().ns_merge_sort_host_async_i32 if algorithm == Algorithm.merge_sort
+          else lib().ns_quick_sort_host_async_i32)
+    check(fn(src.ctypes.data, dst.ctypes.data, len(src), cfg.width_mask, cfg.varsort_max,
+             s.cuda_stream), "sort_host_async")
+    return dst
+
+
 def merge(a, left: int, mid: int, right: int):
     """merge — hybrid.hpp:186-193: stable in-place merge of the sorted runs
     a[left..mid] and a[mid+1..right] (inclusive bounds)."""

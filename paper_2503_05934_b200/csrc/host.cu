@@ -7,6 +7,8 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstring>
+#include <mutex>
+#include <vector>
 
 #include "../../include/netsort_b200.hpp"
 #include "common.cuh"
@@ -208,9 +210,86 @@ static int host_merge(Key* h_keys, size_t n_left, size_t n) {
   return check_cuda(cudaStreamSynchronize(s), "cudaStreamSynchronize");
 }
 
+// ---- stream-ordered host-array sort ------------------------------------------
+// H2D of h_in, the device sort, D2H into h_out, all enqueued on the caller's
+// stream; the call returns at once.  Device keys + scratch come from a cache
+// keyed by (device, stream): a buffer is only reused by later calls on the
+// same stream, so stream order is the only synchronisation it needs.  With
+// pinned host buffers, sorts issued on two streams overlap one's upload with
+// the other's download (PCIe is full duplex).
+struct AsyncSlot {
+  int dev = -1;
+  cudaStream_t stream = nullptr;
+  void* ptr = nullptr;
+  size_t bytes = 0;
+};
+static std::mutex g_async_mu;
+static std::vector<AsyncSlot> g_async;
+
+static void release_async_slots() {
+  std::lock_guard<std::mutex> lk(g_async_mu);
+  for (auto& a : g_async)
+    if (a.ptr) {
+      cudaStreamSynchronize(a.stream);
+      cudaFree(a.ptr);
+    }
+  g_async.clear();
+}
+
+template <class Key>
+static int host_sort_async(const Key* h_in, Key* h_out, size_t n, uint32_t mask, int vs,
+                           int algorithm, cudaStream_t s) {
+  if (n == 0) return NS_OK;
+  if (!h_in || !h_out) return NS_ERR_INVALID;
+  constexpr size_t KB = sizeof(Key);
+  const size_t kb = align_up(n * KB, 256);
+  const size_t tb = dev_temp(h_in, algorithm, n);
+  int dev = 0;
+  NSB_TRY(check_cuda(cudaGetDevice(&dev), "cudaGetDevice"));
+  void* buf = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_async_mu);
+    AsyncSlot* slot = nullptr;
+    for (auto& a : g_async)
+      if (a.dev == dev && a.stream == s) slot = &a;
+    if (!slot) {
+      g_async.push_back(AsyncSlot{dev, s, nullptr, 0});
+      slot = &g_async.back();
+    }
+    if (slot->bytes < kb + tb) {
+      if (slot->ptr) {
+        NSB_TRY(check_cuda(cudaStreamSynchronize(s), "cudaStreamSynchronize"));  // earlier work on it
+        cudaFree(slot->ptr);
+        slot->ptr = nullptr;
+        slot->bytes = 0;
+      }
+      NSB_TRY(check_cuda(cudaMalloc(&slot->ptr, kb + tb), "cudaMalloc"));
+      slot->bytes = kb + tb;
+    }
+    buf = slot->ptr;
+  }
+  Key* d = static_cast<Key*>(buf);
+  void* t = static_cast<char*>(buf) + kb;
+  NSB_TRY(check_cuda(cudaMemcpyAsync(d, h_in, n * KB, cudaMemcpyHostToDevice, s), "H2D"));
+  NSB_TRY(dev_sort(d, n, mask, vs, tb ? t : nullptr, tb, algorithm, s));
+  return check_cuda(cudaMemcpyAsync(h_out, d, n * KB, cudaMemcpyDeviceToHost, s), "D2H");
+}
+
 }  // namespace nsb
 
 extern "C" {
+
+int ns_merge_sort_host_async_i32(const int32_t* h_in, int32_t* h_out, size_t n, uint32_t width_mask,
+                                 int varsort_max, void* stream) {
+  return nsb::host_sort_async(h_in, h_out, n, width_mask, varsort_max, NS_MERGE_SORT,
+                              static_cast<cudaStream_t>(stream));
+}
+
+int ns_quick_sort_host_async_i32(const int32_t* h_in, int32_t* h_out, size_t n, uint32_t width_mask,
+                                 int varsort_max, void* stream) {
+  return nsb::host_sort_async(h_in, h_out, n, width_mask, varsort_max, NS_QUICK_SORT,
+                              static_cast<cudaStream_t>(stream));
+}
 
 int ns_merge_host_i32(int32_t* h_keys, size_t n_left, size_t n) {
   return nsb::host_merge(h_keys, n_left, n);
@@ -239,6 +318,7 @@ int ns_quick_sort_host_i64(int64_t* h_keys, size_t n, uint32_t width_mask, int v
 
 int ns_release_cache(void) {
   for (auto& c : nsb::g_hosts.d) c.release();
+  nsb::release_async_slots();
   return NS_OK;
 }
 

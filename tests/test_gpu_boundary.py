@@ -109,3 +109,29 @@ def test_host_small_path_zero_copy(ns, oracle, n, algo):
     w = h64.copy()
     ns.optimized_merge_sort(w, ns.find_config("6To8"))
     assert np.array_equal(w, np.sort(h64))
+
+
+@pytest.mark.parametrize("n", [1, 5000, 16384, 300_001, 3_000_000])
+def test_sort_host_async_two_streams(ns, cuda, oracle, n):
+    """ns_*_sort_host_async_i32: several sorts in flight on two streams, pinned
+    and pageable buffers, out-of-place and in place, both algorithms."""
+    import torch
+    a = oracle.generate_i32("random", n, 77)
+    want = np.sort(a)
+    src = torch.empty(n, dtype=torch.int32, pin_memory=True).numpy()
+    np.copyto(src, a)
+    outs = [torch.empty(n, dtype=torch.int32, pin_memory=True).numpy() for _ in range(3)]
+    sts = [torch.cuda.Stream(), torch.cuda.Stream()]
+    algos = [ns.Algorithm.merge_sort, ns.Algorithm.quick_sort, ns.Algorithm.merge_sort]
+    cfgs = [ns.find_config("6To8"), ns.find_config("3To5"), ns.find_config("PowerOf2")]
+    for k in range(3):
+        ns.sort_host_async(src, outs[k], cfgs[k], algos[k], stream=sts[k % 2])
+    torch.cuda.synchronize()
+    for o in outs:
+        assert np.array_equal(o, want)
+    assert np.array_equal(src, a)  # the input is only read
+    inplace = a.copy()  # pageable, in place
+    ns.sort_host_async(inplace, inplace, cfgs[0], stream=sts[0])
+    sts[0].synchronize()
+    assert np.array_equal(inplace, want)
+    ns.release_scratch()
