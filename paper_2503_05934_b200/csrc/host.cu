@@ -222,17 +222,30 @@ struct AsyncSlot {
   cudaStream_t stream = nullptr;
   void* ptr = nullptr;
   size_t bytes = 0;
+  cudaStream_t copy = nullptr;  // chunked uploads of large merge sorts
+  cudaEvent_t start = nullptr, ev[kMaxChunks] = {};
 };
 static std::mutex g_async_mu;
 static std::vector<AsyncSlot> g_async;
+// Uploads of the async calls on one device are serialised in issue order
+// (each waits for the previous call's last H2D): one host link cannot upload
+// two arrays faster than one after the other, and staggering them lets call
+// k+1's upload run under call k's download instead of both uploading, then
+// both downloading.
+static cudaEvent_t g_upload_done[64] = {};
 
 static void release_async_slots() {
   std::lock_guard<std::mutex> lk(g_async_mu);
-  for (auto& a : g_async)
+  for (auto& a : g_async) {
     if (a.ptr) {
       cudaStreamSynchronize(a.stream);
       cudaFree(a.ptr);
     }
+    if (a.copy) cudaStreamDestroy(a.copy);  // (g_upload_done events are kept)
+    if (a.start) cudaEventDestroy(a.start);
+    for (auto& e : a.ev)
+      if (e) cudaEventDestroy(e);
+  }
   g_async.clear();
 }
 
@@ -247,15 +260,28 @@ static int host_sort_async(const Key* h_in, Key* h_out, size_t n, uint32_t mask,
   int dev = 0;
   NSB_TRY(check_cuda(cudaGetDevice(&dev), "cudaGetDevice"));
   void* buf = nullptr;
+  AsyncSlot sl;
   {
     std::lock_guard<std::mutex> lk(g_async_mu);
     AsyncSlot* slot = nullptr;
     for (auto& a : g_async)
       if (a.dev == dev && a.stream == s) slot = &a;
     if (!slot) {
-      g_async.push_back(AsyncSlot{dev, s, nullptr, 0});
+      g_async.push_back(AsyncSlot{});
       slot = &g_async.back();
+      slot->dev = dev;
+      slot->stream = s;
+      NSB_TRY(check_cuda(cudaStreamCreateWithFlags(&slot->copy, cudaStreamNonBlocking),
+                         "cudaStreamCreate"));
+      NSB_TRY(check_cuda(cudaEventCreateWithFlags(&slot->start, cudaEventDisableTiming),
+                         "cudaEventCreate"));
+      for (auto& e : slot->ev)
+        NSB_TRY(check_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate"));
     }
+    if (dev < 0 || dev >= 64) return NS_ERR_INVALID;
+    if (!g_upload_done[dev])
+      NSB_TRY(check_cuda(cudaEventCreateWithFlags(&g_upload_done[dev], cudaEventDisableTiming),
+                         "cudaEventCreate"));
     if (slot->bytes < kb + tb) {
       if (slot->ptr) {
         NSB_TRY(check_cuda(cudaStreamSynchronize(s), "cudaStreamSynchronize"));  // earlier work on it
@@ -267,12 +293,49 @@ static int host_sort_async(const Key* h_in, Key* h_out, size_t n, uint32_t mask,
       slot->bytes = kb + tb;
     }
     buf = slot->ptr;
+    sl = *slot;
   }
+  // issue order of the uploads (see g_upload_done); the enqueueing below is
+  // under the lock so two host threads cannot interleave their event chain
+  std::lock_guard<std::mutex> lk(g_async_mu);
+  cudaEvent_t& up = g_upload_done[dev];
   Key* d = static_cast<Key*>(buf);
   void* t = static_cast<char*>(buf) + kb;
-  NSB_TRY(check_cuda(cudaMemcpyAsync(d, h_in, n * KB, cudaMemcpyHostToDevice, s), "H2D"));
-  NSB_TRY(dev_sort(d, n, mask, vs, tb ? t : nullptr, tb, algorithm, s));
-  return check_cuda(cudaMemcpyAsync(h_out, d, n * KB, cudaMemcpyDeviceToHost, s), "D2H");
+  Key* result = d;
+  const size_t chunk_min = (size_t(1) << 24) / KB;  // 16 MiB
+  if (algorithm == NS_MERGE_SORT && n >= 2 * chunk_min) {
+    // as host_sort: chunks uploaded on the slot's copy stream, each merge-
+    // sorted on `s` as soon as it lands, then the chunks merged.  The copy
+    // stream first waits for everything earlier on `s` (the previous sort on
+    // this slot may still be downloading from d).
+    int chunks = (int)std::min<size_t>(kMaxChunks, n / chunk_min);
+    size_t clen = (n + chunks - 1) / chunks;
+    clen = (clen + 8191) / 8192 * 8192;
+    chunks = (int)((n + clen - 1) / clen);
+    NSB_TRY(check_cuda(cudaEventRecord(sl.start, s), "cudaEventRecord"));
+    NSB_TRY(check_cuda(cudaStreamWaitEvent(sl.copy, sl.start, 0), "cudaStreamWaitEvent"));
+    NSB_TRY(check_cuda(cudaStreamWaitEvent(sl.copy, up, 0), "cudaStreamWaitEvent"));
+    for (int c = 0; c < chunks; ++c) {
+      const size_t off = c * clen, len = std::min(clen, n - off);
+      NSB_TRY(check_cuda(cudaMemcpyAsync(d + off, h_in + off, len * KB, cudaMemcpyHostToDevice,
+                                         sl.copy),
+                         "H2D"));
+      NSB_TRY(check_cuda(cudaEventRecord(sl.ev[c], sl.copy), "cudaEventRecord"));
+    }
+    NSB_TRY(check_cuda(cudaEventRecord(up, sl.copy), "cudaEventRecord"));
+    for (int c = 0; c < chunks; ++c) {
+      const size_t off = c * clen, len = std::min(clen, n - off);
+      NSB_TRY(check_cuda(cudaStreamWaitEvent(s, sl.ev[c], 0), "cudaStreamWaitEvent"));
+      NSB_TRY(dev_sort(d + off, len, mask, vs, t, tb, NS_MERGE_SORT, s));
+    }
+    NSB_TRY(merge_existing_runs(d, static_cast<Key*>(t), n, (int64_t)clen, t, s, &result));
+  } else {
+    NSB_TRY(check_cuda(cudaStreamWaitEvent(s, up, 0), "cudaStreamWaitEvent"));
+    NSB_TRY(check_cuda(cudaMemcpyAsync(d, h_in, n * KB, cudaMemcpyHostToDevice, s), "H2D"));
+    NSB_TRY(check_cuda(cudaEventRecord(up, s), "cudaEventRecord"));
+    NSB_TRY(dev_sort(d, n, mask, vs, tb ? t : nullptr, tb, algorithm, s));
+  }
+  return check_cuda(cudaMemcpyAsync(h_out, result, n * KB, cudaMemcpyDeviceToHost, s), "D2H");
 }
 
 }  // namespace nsb

@@ -111,7 +111,7 @@ def test_host_small_path_zero_copy(ns, oracle, n, algo):
     assert np.array_equal(w, np.sort(h64))
 
 
-@pytest.mark.parametrize("n", [1, 5000, 16384, 300_001, 3_000_000])
+@pytest.mark.parametrize("n", [1, 5000, 16384, 300_001, 3_000_000, 9_000_001])
 def test_sort_host_async_two_streams(ns, cuda, oracle, n):
     """ns_*_sort_host_async_i32: several sorts in flight on two streams, pinned
     and pageable buffers, out-of-place and in place, both algorithms."""
