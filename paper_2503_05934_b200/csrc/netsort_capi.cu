@@ -40,6 +40,10 @@ static int launch_blocksort(const Key* src, Key* dst, int64_t n, int stride, int
   return check_launch("blocksort_kernel");
 }
 
+// int32 sorts of at least 2^NSB_TILE16K_MIN_LOG2 keys use 16384-key tiles
+#ifndef NSB_TILE16K_MIN_LOG2
+#define NSB_TILE16K_MIN_LOG2 21
+#endif
 // Merge-pass tile shape: <256,29> = 7424 keys per tile (measured 0.5-4 %
 // faster than <256,31> from 2^24 to 2^30, profiles/r01_tile_sort_v6_ab.txt);
 // int64 keys take odd K as well (half-warp 64-bit cursors on distinct banks).
@@ -259,7 +263,7 @@ static int merge_sort_device_t(Key* d_keys, size_t n, int leaf, void* d_temp, si
   // int32 tile: 16384 keys (<512,32>) from 2^21 keys up (one merge pass
   // fewer; with 32 keys per thread it has the 8192-key tile's four
   // shared-memory levels), 8192 (<256,32>) below; int64: 8192 (<512,16>)
-  const int T = (k32 && n >= (size_t(1) << 21)) ? kSmT : kBsT;
+  const int T = (k32 && n >= (size_t(1) << NSB_TILE16K_MIN_LOG2)) ? kSmT : kBsT;
   const int64_t tiles = (int64_t)((n + T - 1) / T);
   // pairwise passes until one run remains
   int passes = 0;
