@@ -56,7 +56,10 @@ constexpr int kQsChunk = kQsNT * kQsPer;     // keys per chunk (one CTA iteratio
 constexpr int kQsMaxB = 128;                 // pivot slots per segment (B-1 real + pad):
                                              // 2B-1 <= 255 buckets, so a bucket id is one byte
 constexpr int kQsOver = 16;                  // samples per bucket
-constexpr int64_t kQsTarget = 4096;          // mean bucket size a level aims for
+#ifndef NSB_QS_TARGET
+#define NSB_QS_TARGET 4096
+#endif
+constexpr int64_t kQsTarget = NSB_QS_TARGET;  // mean bucket size a level aims for
 
 // Buckets a segment of len keys is split into: the smallest power of two
 // B >= 2 with B * kQsTarget >= len, at most kQsMaxB.
