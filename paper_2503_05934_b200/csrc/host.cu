@@ -120,13 +120,18 @@ static int host_sort(Key* h_keys, size_t n, uint32_t mask, int vs, int algorithm
   NSB_TRY(host_cache(&hc));
   HostCache& g_host = *hc;
   if (n <= (size_t)kSmallTile) {
-    // one CTA sorts the keys in the mapped staging buffer (no scratch: the
-    // merge sort's single-tile path; quick sort delegates to it at this size)
-    NSB_TRY(g_host.ensure(0));
+    // the keys stay in the mapped staging buffer (zero-copy over PCIe: one
+    // launch sequence and one synchronise per call, no DMA round trips); up to
+    // 8192 keys one CTA sorts them there, above that the tiled path reads them
+    // once (tile sort -> device scratch) and writes them once (the merge pass's
+    // bulk store into mapped memory); quick sort delegates to the merge sort
+    // at these sizes
+    const size_t tb = dev_temp(h_keys, algorithm, n);
+    NSB_TRY(g_host.ensure(tb));
     NSB_TRY(g_host.ensure_pinned());
     std::memcpy(g_host.pinned, h_keys, n * KB);
-    const int st = dev_sort(static_cast<Key*>(g_host.mapped), n, mask, vs, nullptr, 0, algorithm,
-                            g_host.stream);
+    const int st = dev_sort(static_cast<Key*>(g_host.mapped), n, mask, vs, tb ? g_host.dev : nullptr,
+                            tb, algorithm, g_host.stream);
     NSB_TRY(check_cuda(cudaStreamSynchronize(g_host.stream), "cudaStreamSynchronize"));
     if (st != NS_OK) return st;
     std::memcpy(h_keys, g_host.pinned, n * KB);
