@@ -767,6 +767,21 @@ const char* ns_status_string(int status) {
 
 int ns_version(void) { return 100; }
 
+#if NSB_CHECKED
+// Checked build only (not in the header): a kernel whose NSB_DCHECK fails on
+// purpose, so the tests can show that the device-side checks are live (the
+// launch must end in a trap and the message must name the condition).
+__global__ void nsb_checked_selftest_kernel(int bound) {
+  const int i = (int)threadIdx.x;
+  NSB_DCHECK(i < bound);
+}
+int ns_checked_selftest(void) {
+  nsb_checked_selftest_kernel<<<1, 32>>>(16);
+  const cudaError_t e = cudaDeviceSynchronize();
+  return e == cudaSuccess ? NS_OK : NS_ERR_CUDA;
+}
+#endif
+
 
 int ns_leaf_width(uint32_t width_mask, int varsort_max) { return leaf_of(width_mask, varsort_max); }
 

@@ -75,3 +75,28 @@ def test_checked_build_all_kernels(env):
     assert "NSB_DCHECK failed" not in text, text[-4000:]
     assert out.returncode == 0, text[-4000:]
     assert "PASSED" in out.stdout, text[-4000:]
+
+
+@pytest.mark.gpu
+def test_checked_build_traps_on_a_failed_check():
+    """Negative control: the checked library's self-test kernel fails an
+    NSB_DCHECK on purpose; the launch must trap and the message must name the
+    condition (so a green run above means the checks ran and held)."""
+    import sys
+    from paper_2503_05934_b200 import _lib
+    build_binary()
+    code = ("import ctypes, sys; L = ctypes.CDLL(sys.argv[1]); "
+            "r = L.ns_checked_selftest(); print('status', r); sys.stdout.flush()")
+    out = subprocess.run([sys.executable, "-c", code, _lib.CHECKED_LIB_PATH],
+                         capture_output=True, text=True, timeout=120)
+    text = out.stdout + out.stderr
+    assert "NSB_DCHECK failed" in text and "i < bound" in text, text[-3000:]
+    assert "status 2" in text, text[-3000:]  # NS_ERR_CUDA
+
+
+def test_selftest_symbol_only_in_checked_build():
+    from paper_2503_05934_b200 import _lib
+    build_binary()
+    nm = lambda p: subprocess.run(["nm", "-D", p], capture_output=True, text=True).stdout  # noqa: E731
+    assert "ns_checked_selftest" in nm(_lib.CHECKED_LIB_PATH)
+    assert "ns_checked_selftest" not in nm(_lib.LIB_PATH)
