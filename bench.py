@@ -482,6 +482,10 @@ def run_ours(args, metric):
             "e2e": e2e, "clocks": clk, "verified": bool(ok.item())}
     if nvlink is not None:
         line["nvlink"] = nvlink
+    if world > 1 and not args.no_configs:
+        sb = sharded_batches(ns, L, dev, world, rank, all_reduce)
+        if rank == 0:
+            line["sharded_batches"] = sb
     if rank == 0 and world == 1 and not args.no_size_sweep:
         line["size_sweep"] = size_sweep(ns, L, dev, peak)
     if rank == 0 and world == 1 and not args.no_configs:
@@ -497,6 +501,82 @@ def run_ours(args, metric):
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------
+# Under torchrun: the two batch configs sharded by array over the ranks
+# (independent arrays, no collective on the data path).
+# Total work is fixed (the 2^24-array batch, the 65,536 x 16,384 segmented
+# batch), each rank sorts its own contiguous share; time = max over ranks.
+# ---------------------------------------------------------------------------
+def sharded_batches(ns, L, dev, world, rank, all_reduce):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2503_05934_b200 import multigpu
+
+    def timed(fn, restore, reps=3):
+        restore()
+        fn()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(reps):
+            restore()  # untimed
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            fn()
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        t = torch.tensor([min(ts)], dtype=torch.float64, device=dev)
+        all_reduce(t, dist.ReduceOp.MAX)
+        return float(t.item())
+
+    out = {"scaling": "strong (fixed total work, arrays / segments split over the ranks)"}
+    # base-case batch: key-balanced contiguous array ranges (ns_shard_batch_plan)
+    offs, keys = ns.generate_batch(1 << 24, SEED)
+    ab = multigpu.shard_batch_plan(offs, world)
+    a0, a1 = int(ab[rank]), int(ab[rank + 1])
+    k0, k1 = int(offs[a0]), int(offs[a1])
+    my_offs = (offs[a0:a1 + 1].astype(np.int64) - k0).astype(np.uint32)
+    src = torch.from_numpy(keys[k0:k1].copy()).to(dev)
+    o = torch.from_numpy(my_offs.view(np.int32)).to(dev)
+    w = src.clone()
+    st = torch.zeros(1, dtype=torch.int32, device=dev)
+
+    ms = timed(lambda: ns.sort_small_batch(w, o, status=st), lambda: w.copy_(src))
+    got = w.cpu().numpy()
+    arr = np.repeat(np.arange(a1 - a0), np.diff(my_offs.astype(np.int64)))
+    want = keys[k0:k1][np.lexsort((keys[k0:k1], arr))]  # checker: per-array sort
+    ok = int(st.item()) == 0 and np.array_equal(got, want)
+    okt = torch.tensor([1 if ok else 0], dtype=torch.int32, device=dev)
+    all_reduce(okt, dist.ReduceOp.MIN)
+    out["batch"] = {"num_arrays": 1 << 24, "num_keys": int(len(keys)), "ms_max_over_ranks": ms,
+                    "gkeys_per_s": len(keys) / (ms * 1e-3) / 1e9, "verified": bool(okt.item()),
+                    "timing": "CUDA events around the call, best of 3, max over ranks"}
+    del keys, offs
+    # segmented batch: 65,536 / world whole segments of 16,384 keys per rank
+    seg, nseg_total = 16384, 65536
+    nseg = nseg_total // world
+    m = nseg * seg
+    x = torch.empty(m, dtype=torch.int32, device=dev)
+    stream = torch.cuda.current_stream().cuda_stream
+    L.ns_generate_i32(x.data_ptr(), m, 0, (SEED + rank * m * GAMMA) % 2**64, stream)
+    d_in = ns.multiset_digest(x)
+    y = x.clone()
+    cfg = ns.find_config("3To5")
+
+    ms2 = timed(lambda: ns.segmented_sort(y, seg, cfg, ns.Algorithm.quick_sort), lambda: y.copy_(x))
+    v = y.view(nseg, seg)
+    ok2 = bool((v[:, 1:] >= v[:, :-1]).all().item()) and ns.multiset_digest(y) == d_in
+    okt = torch.tensor([1 if ok2 else 0], dtype=torch.int32, device=dev)
+    all_reduce(okt, dist.ReduceOp.MIN)
+    out["segmented"] = {"segments": nseg_total, "seg_len": seg, "ms_max_over_ranks": ms2,
+                        "gkeys_per_s": nseg_total * seg / (ms2 * 1e-3) / 1e9,
+                        "verified": bool(okt.item()),
+                        "timing": "CUDA events around the call, best of 3, max over ranks"}
+    del x, y
+    return out
 
 
 # ---------------------------------------------------------------------------

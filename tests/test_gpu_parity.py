@@ -555,6 +555,8 @@ def test_bench_multi_rank_code_path_on_one_gpu(exchange):
     assert line["n_gpus"] == 2 and line["verified"] is True
     assert line["nvlink"]["bytes_per_rank_max"] > 0
     assert line["exchange"]["mode"] == exchange
+    sb = line["sharded_batches"]  # the batch configs split by array over the ranks
+    assert sb["batch"]["verified"] is True and sb["segmented"]["verified"] is True
 
 
 @pytest.mark.slow
