@@ -147,8 +147,10 @@ int ns_argsort_i32(const int32_t* d_keys, uint32_t* d_perm, size_t n, void* d_te
  * stored back to back (BASELINE config 4's 65,536 x 16,384 batch).  The
  * reference would run `algorithm` once per segment.  Segments of up to 16384
  * keys are one CTA each; longer ones, with NS_QUICK_SORT, are all level-0
- * segments of ONE device-planned partition (no per-segment host loop);
- * NS_MERGE_SORT runs one stream-ordered merge sort per long segment.
+ * segments of ONE device-planned partition, with NS_MERGE_SORT one tile-sort
+ * launch over every segment's tiles plus pairwise passes whose run pairs stay
+ * inside their segment (no per-segment host loop either way; the merge path
+ * needs the scratch of a merge sort of all the keys).
  * num_segments * seg_len overflowing is NS_ERR_INVALID. */
 size_t ns_segmented_sort_temp_bytes(size_t num_segments, size_t seg_len);
 int ns_segmented_sort_i32(int32_t* d_keys, size_t num_segments, size_t seg_len,

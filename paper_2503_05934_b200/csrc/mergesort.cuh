@@ -673,11 +673,23 @@ __host__ __device__ constexpr int bs_min_blocks_tput() {
 
 template <int NT, int K, int LEAF, class Key = int32_t>
 __global__ void __launch_bounds__(NT, (bs_min_blocks<NT, K, Key>()))
-    blocksort_kernel(const Key* src, Key* dst, int64_t n, int stride) {  // src == dst ok
+    blocksort_kernel(const Key* src, Key* dst, int64_t n, int stride, int64_t seg_len,
+                     int tiles_per_seg) {  // src == dst ok
   extern __shared__ __align__(16) unsigned char sm_raw[];
   Key* sm = reinterpret_cast<Key*>(sm_raw);
-  const int64_t base = (int64_t)blockIdx.x * stride;
-  const int valid = (int)min((int64_t)stride, n - base);
+  // seg_len > 0: back-to-back segments of seg_len keys, tiles_per_seg tiles
+  // each (the last one of a segment partial); else tiles of `stride` keys
+  int64_t base;
+  int valid;
+  if (seg_len > 0) {
+    const int64_t sg = blockIdx.x / tiles_per_seg;
+    const int t = (int)(blockIdx.x - sg * tiles_per_seg);
+    base = sg * seg_len + (int64_t)t * stride;
+    valid = (int)min((int64_t)stride, seg_len - (int64_t)t * stride);
+  } else {
+    base = (int64_t)blockIdx.x * stride;
+    valid = (int)min((int64_t)stride, n - base);
+  }
   pdl_wait();     // src may be the previous kernel's output
   pdl_trigger();
   cta_sort<NT, K, LEAF>(src + base, dst + base, valid, sm);
@@ -725,6 +737,8 @@ struct PassPlan {
   int tpp;      // tiles per pair
   int tmp;      // keys per tile (<= NT*K, multiple of 4)
   int kp;       // outputs per thread = ceil(tmp / NT)
+  int64_t seg_len = 0;  // > 0: runs live in back-to-back segments of seg_len keys
+  int64_t pps = 0;      // run pairs per segment (segmented passes)
 };
 
 struct TileGeom {
@@ -735,9 +749,17 @@ __device__ __forceinline__ TileGeom tile_geom(const PassPlan& P, int64_t c) {
   TileGeom g;
   const int64_t pair = c / P.tpp;
   const int64_t lt = c - pair * P.tpp;
-  g.pair_base = pair * 2 * P.R;
-  g.a_len = min(P.R, P.n - g.pair_base);
-  g.b_len = max((int64_t)0, min(P.R, P.n - g.pair_base - P.R));
+  int64_t end = P.n;  // end of the keys this pair belongs to
+  if (P.seg_len > 0) {
+    const int64_t sg = pair / P.pps;
+    const int64_t seg0 = sg * P.seg_len;
+    g.pair_base = seg0 + (pair - sg * P.pps) * 2 * P.R;
+    end = seg0 + P.seg_len;
+  } else {
+    g.pair_base = pair * 2 * P.R;
+  }
+  g.a_len = min(P.R, end - g.pair_base);
+  g.b_len = max((int64_t)0, min(P.R, end - g.pair_base - P.R));
   const int64_t pair_len = g.a_len + g.b_len;
   g.diag0 = min(lt * P.tmp, pair_len);
   g.diag1 = min(g.diag0 + P.tmp, pair_len);

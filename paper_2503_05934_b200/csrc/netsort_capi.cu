@@ -27,14 +27,15 @@ static_assert(kSmT == kSmallTile, "small-tile size mismatch");
 
 template <int NT, int K, int LEAF, class Key>
 static int launch_blocksort(const Key* src, Key* dst, int64_t n, int stride, int64_t ctas,
-                            cudaStream_t s) {
+                            cudaStream_t s, int64_t seg_len = 0, int tiles_per_seg = 1) {
   constexpr int smem = tile_smem_bytes<NT, K, Key>();
   auto* kern = blocksort_kernel<NT, K, LEAF, Key>;
   NSB_TRY(ensure_smem_attr(reinterpret_cast<const void*>(kern), smem,
                            "cudaFuncSetAttribute(blocksort)"));
   {
     Prof prof(PK_TILE_SORT, s);
-    const cudaError_t e = launch_pdl(n, kern, (unsigned)ctas, NT, smem, s, src, dst, n, stride);
+    const cudaError_t e = launch_pdl(n, kern, (unsigned)ctas, NT, smem, s, src, dst, n, stride,
+                                     seg_len, tiles_per_seg);
     if (e != cudaSuccess) return check_cuda(e, "blocksort_kernel");
   }
   return check_launch("blocksort_kernel");
@@ -121,7 +122,7 @@ struct SmpCtx {
 // Tiles of exactly NT*K outputs (a multiple of 4 keys, so every tile starts
 // 16-byte aligned); only the last tile of a run pair is partial.  A full tile
 // gives every thread exactly K outputs, which the merge loop exploits.
-static PassPlan plan_pass(int64_t n, int64_t R, int nt = kV2NT, int k = kV2K) {
+static PassPlan plan_pass(int64_t n, int64_t R, int nt = kV2NT, int k = kV2K, int64_t seg_len = 0) {
   PassPlan P;
   P.R = R;
   P.n = n;
@@ -129,16 +130,20 @@ static PassPlan plan_pass(int64_t n, int64_t R, int nt = kV2NT, int k = kV2K) {
   P.tmp = nt * k;
   P.tpp = (int)((two_r + P.tmp - 1) / P.tmp);
   P.kp = k;
+  P.seg_len = seg_len;
+  P.pps = seg_len > 0 ? (seg_len + two_r - 1) / two_r : 0;
   return P;
 }
 
 // One pairwise merge pass (v2): runs of R in src -> runs of 2R in dst.
 template <int NT, int K, class Key>
 static int v2_pass_t(const Key* src, Key* dst, int64_t n, int64_t R, int64_t* mp,
-                     cudaStream_t s, SmpCtx* sc = nullptr) {
+                     cudaStream_t s, SmpCtx* sc = nullptr, int64_t seg_len = 0) {
   const MergeTuning& tu = tuning();
-  const PassPlan P = plan_pass(n, R, NT, K);
-  const int64_t pairs = (n + 2 * R - 1) / (2 * R);
+  const PassPlan P = plan_pass(n, R, NT, K, seg_len);
+  // segmented passes (seg_len > 0): every segment's runs pair up on their own;
+  // they neither read nor record block samples (sc == nullptr)
+  const int64_t pairs = seg_len > 0 ? (n / seg_len) * P.pps : (n + 2 * R - 1) / (2 * R);
   const int64_t mt = pairs * P.tpp;
   // samples: only for the whole array of a sort (sc->n == n); tiles must be
   // whole 256-key blocks (NT*K a multiple of 256)
@@ -202,15 +207,15 @@ static int v2_pass_t(const Key* src, Key* dst, int64_t n, int64_t R, int64_t* mp
 // win by 5-10 %; above, <256,29>.  int64 (tools/i64_sweep.sh): <128,15> up
 // to 2^20 keys, <128,23> up to 2^25, <128,31> above.
 static int v2_pass(const int32_t* src, int32_t* dst, int64_t n, int64_t R, int64_t* mp,
-                   cudaStream_t s, SmpCtx* sc = nullptr) {
-  return n <= (int64_t(1) << 23) ? v2_pass_t<128, 23>(src, dst, n, R, mp, s, sc)
-                                 : v2_pass_t<kV2NT, kV2K>(src, dst, n, R, mp, s, sc);
+                   cudaStream_t s, SmpCtx* sc = nullptr, int64_t seg_len = 0) {
+  return n <= (int64_t(1) << 23) ? v2_pass_t<128, 23>(src, dst, n, R, mp, s, sc, seg_len)
+                                 : v2_pass_t<kV2NT, kV2K>(src, dst, n, R, mp, s, sc, seg_len);
 }
 static int v2_pass(const int64_t* src, int64_t* dst, int64_t n, int64_t R, int64_t* mp,
-                   cudaStream_t s, SmpCtx* sc = nullptr) {
-  if (n <= (int64_t(1) << 20)) return v2_pass_t<128, 15>(src, dst, n, R, mp, s, sc);
-  if (n <= (int64_t(1) << 25)) return v2_pass_t<128, 23>(src, dst, n, R, mp, s, sc);
-  return v2_pass_t<128, 31>(src, dst, n, R, mp, s, sc);
+                   cudaStream_t s, SmpCtx* sc = nullptr, int64_t seg_len = 0) {
+  if (n <= (int64_t(1) << 20)) return v2_pass_t<128, 15>(src, dst, n, R, mp, s, sc, seg_len);
+  if (n <= (int64_t(1) << 25)) return v2_pass_t<128, 23>(src, dst, n, R, mp, s, sc, seg_len);
+  return v2_pass_t<128, 31>(src, dst, n, R, mp, s, sc, seg_len);
 }
 
 // Pairwise passes over existing sorted runs of length R0 (the last may be
@@ -331,6 +336,44 @@ static int tile_sort_segments_t(Key* d_keys, size_t num_segments, size_t seg_len
     }
   });
 }
+// Segments longer than one tile, merge-sorted ALL AT ONCE: one tile-sort
+// launch over every segment's tiles (each segment starts a tile; its last
+// tile is partial), then ceil(log2(tiles per segment)) pairwise passes whose
+// run pairs never cross a segment boundary (PassPlan::seg_len) — no
+// per-segment host loop.  Scratch: that of a merge sort of all the keys.
+template <class Key>
+static int merge_sort_segments_t(Key* d_keys, size_t num_segments, size_t seg_len, int leaf,
+                                 void* d_temp, size_t temp_bytes, cudaStream_t s) {
+  constexpr bool k32 = std::is_same_v<Key, int32_t>;
+  const size_t n = num_segments * seg_len;
+  const size_t need = k32 ? merge_sort_temp(n) : merge_sort_temp_i64(n);
+  if (temp_bytes < need || d_temp == nullptr) return NS_ERR_TEMP;
+  Key* tmp = static_cast<Key*>(d_temp);
+  int64_t* mp = reinterpret_cast<int64_t*>(static_cast<char*>(d_temp) +
+                                           align_up(n * sizeof(Key), 256));
+  const int T = k32 ? kSmT : kBsT;
+  const int tps = (int)((seg_len + T - 1) / T);
+  int passes = 0;
+  for (int64_t runs = tps; runs > 1; runs = (runs + 1) / 2) ++passes;
+  Key* cur = (passes & 1) ? tmp : d_keys;
+  Key* other = (cur == d_keys) ? tmp : d_keys;
+  const int64_t ctas = (int64_t)num_segments * tps;
+  NSB_TRY(with_leaf(leaf, [&](auto L) {
+    constexpr int LF = decltype(L)::value;
+    if constexpr (!k32)
+      return launch_blocksort<512, 16, LF>(d_keys, cur, (int64_t)n, T, ctas, s, (int64_t)seg_len, tps);
+    else
+      return launch_blocksort<512, 32, LF>(d_keys, cur, (int64_t)n, T, ctas, s, (int64_t)seg_len, tps);
+  }));
+  int64_t R = T;
+  for (int pi = 0; pi < passes; ++pi) {
+    NSB_TRY(v2_pass(cur, other, (int64_t)n, R, mp, s, nullptr, (int64_t)seg_len));
+    std::swap(cur, other);
+    R *= 2;
+  }
+  return NS_OK;
+}
+
 int tile_sort_segments(int32_t* d_keys, size_t num_segments, size_t seg_len, int leaf,
                        cudaStream_t s) {
   return tile_sort_segments_t(d_keys, num_segments, seg_len, leaf, s);
@@ -726,7 +769,9 @@ template <class Key>
 static size_t segmented_temp(size_t num_segments, size_t seg_len) {
   if (seg_len <= (size_t)kSmT || num_segments == 0) return 0;
   if (num_segments > SIZE_MAX / seg_len) return 0;
-  const size_t ms = sizeof(Key) == 4 ? merge_sort_temp(seg_len) : merge_sort_temp_i64(seg_len);
+  // the merge path sorts every segment at once: a merge sort's scratch for all keys
+  const size_t n = num_segments * seg_len;
+  const size_t ms = sizeof(Key) == 4 ? merge_sort_temp(n) : merge_sort_temp_i64(n);
   return std::max(ms, quick_sort_segments_temp(num_segments, seg_len, sizeof(Key)));
 }
 
@@ -742,9 +787,7 @@ static int segmented_sort(Key* d_keys, size_t num_segments, size_t seg_len, int 
   if (seg_len <= (size_t)kSmT) return tile_sort_segments_t(d_keys, num_segments, seg_len, leaf, s);
   if (algorithm == NS_QUICK_SORT)
     return quick_sort_segments_device(d_keys, num_segments, seg_len, leaf, d_temp, temp_bytes, s);
-  for (size_t g = 0; g < num_segments; ++g)
-    NSB_TRY(merge_sort_device(d_keys + g * seg_len, seg_len, leaf, d_temp, temp_bytes, s));
-  return NS_OK;
+  return merge_sort_segments_t(d_keys, num_segments, seg_len, leaf, d_temp, temp_bytes, s);
 }
 
 }  // namespace nsb

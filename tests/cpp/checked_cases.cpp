@@ -336,6 +336,9 @@ int main(int argc, char** argv) {
   segmented_case<int32_t>(24, 5000, 0);
   segmented_case<int32_t>(6, 16384, 1);
   segmented_case<int32_t>(3, 40000, 1);
+  segmented_case<int32_t>(3, 40000, 0);
+  segmented_case<int32_t>(2, 70001, 0);
+  segmented_case<int64_t>(3, 20000, 0);
   segmented_case<int64_t>(5, 3000, 0);
   pairs_case(30000);
   merge_runs_case(100000, 3);

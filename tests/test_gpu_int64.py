@@ -125,7 +125,7 @@ def test_i64_full_size_properties(ns, cuda, algo, n):
     torch.cuda.empty_cache()
 
 
-@pytest.mark.parametrize("seg_len", [2, 7, 100, 513, 4096, 9000, 16384, 20000])
+@pytest.mark.parametrize("seg_len", [2, 7, 100, 513, 4096, 9000, 16384, 20000, 70001])
 def test_i64_segmented(ns, cuda, oracle, seg_len):
     import torch
     nseg = max(1, (1 << 18) // seg_len)

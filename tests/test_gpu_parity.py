@@ -185,6 +185,25 @@ def test_segmented_odd_lengths(ns, cuda, oracle):
             assert np.array_equal(from_dev(t), want), (seg, cfg)
 
 
+@pytest.mark.parametrize("nseg,seg", [(7, 16385), (5, 40000), (3, 100_001), (2, (1 << 21) + 3),
+                                      (64, 32768), (40, 50_000)])
+def test_segmented_merge_sort_long_segments_batched(ns, cuda, oracle, nseg, seg):
+    """Segments longer than one tile, merge sort: every segment sorted at once
+    (segment-aligned tiles, passes whose run pairs never cross a segment);
+    sorted, duplicate-heavy and random segments."""
+    for kind in ("random", "dups", "sorted"):
+        if kind == "random":
+            a = oracle.generate_i32("random", nseg * seg, seed=seg + nseg)
+        elif kind == "dups":
+            a = (oracle.generate_i32("random", nseg * seg, seed=seg) % 11).astype(np.int32)
+        else:
+            a = np.tile(np.arange(seg, dtype=np.int32)[::-1], nseg)  # each segment descending
+        want = np.sort(a.reshape(nseg, seg), axis=1).reshape(-1)
+        t = to_dev(a, cuda)
+        ns.segmented_sort(t, seg, ns.find_config("6To8"), ns.Algorithm.merge_sort)
+        assert np.array_equal(from_dev(t), want), (nseg, seg, kind)
+
+
 def test_range_sorts_leave_outside_untouched(ns, cuda, oracle):
     """test_hybrid.cpp:320-342, on the device path and the host path."""
     base = oracle.generate_i32("random", 40000, 17)
