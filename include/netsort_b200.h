@@ -111,6 +111,41 @@ size_t ns_quick_sort_temp_bytes_i64(size_t n);
 int ns_quick_sort_i64(int64_t* d_keys, size_t n, uint32_t width_mask, int varsort_max,
                       void* d_temp, size_t temp_bytes, void* stream);
 
+/* The reference's quick sort executed node for node (qs_trace.cu):
+ * median_of_three (hybrid.hpp:105-114) + hoare_partition (121-133) at every
+ * node of quick_sort_rec (137-150), the same pivots, swaps and splits, so the
+ * DispatchStats counters equal the reference's (optimized_quick_sort(...,
+ * stats), hybrid.hpp:197-204; run_variant 234-243).  out12 = network_hits
+ * [0..8], merges (0), partitions, max_depth; n == 0 leaves them zero (no
+ * call, hybrid.hpp:201).  This is the instrumentation path, not the timed
+ * one: it synchronises the stream once per recursion level above 8192 keys.
+ * n < 2^32.  Temp: ns_quick_sort_traced_temp_bytes(n) (either key type). */
+size_t ns_quick_sort_traced_temp_bytes(size_t n);
+int ns_quick_sort_traced_i32(int32_t* d_keys, size_t n, uint32_t width_mask, int varsort_max,
+                             uint64_t* out12, void* d_temp, size_t temp_bytes, void* stream);
+int ns_quick_sort_traced_i64(int64_t* d_keys, size_t n, uint32_t width_mask, int varsort_max,
+                             uint64_t* out12, void* d_temp, size_t temp_bytes, void* stream);
+/* hoare_partition — hybrid.hpp:121-133, on d_keys[low..high] (inclusive,
+ * 0 <= low < high < n) of a device array of n keys: the same swaps in the
+ * same cells and the same returned split (written to the HOST word *split,
+ * absolute index; the call synchronises).  Two streaming passes, no
+ * sequential scan.  The reference requires the pivot to occur in the range;
+ * here a pivot above every key or below every key (where the reference's scan
+ * would leave the range) is NS_ERR_INVALID with the keys untouched.
+ * Temp: ns_hoare_partition_temp_bytes(high - low + 1). */
+size_t ns_hoare_partition_temp_bytes(size_t len);
+int ns_hoare_partition_i32(int32_t* d_keys, size_t n, int64_t low, int64_t high, int32_t pivot,
+                           int64_t* split, void* d_temp, size_t temp_bytes, void* stream);
+int ns_hoare_partition_i64(int64_t* d_keys, size_t n, int64_t low, int64_t high, int64_t pivot,
+                           int64_t* split, void* d_temp, size_t temp_bytes, void* stream);
+/* median_of_three — hybrid.hpp:105-114: the three compare-exchanges on cells
+ * low, low+(high-low)/2, high (none when high-low < 2), pivot to the HOST
+ * word *pivot (the call synchronises). */
+int ns_median_of_three_i32(int32_t* d_keys, size_t n, int64_t low, int64_t high, int32_t* pivot,
+                           void* stream);
+int ns_median_of_three_i64(int64_t* d_keys, size_t n, int64_t low, int64_t high, int64_t* pivot,
+                           void* stream);
+
 /* Base-case batch (BASELINE config 2; no reference batch API — the
  * reference would loop sort_small, networks.hpp:132-145): num_arrays
  * independent arrays packed contiguously, array i = d_keys[d_offsets[i] ..
@@ -330,6 +365,23 @@ int ns_quick_sort_host_async_i32(const int32_t* h_in, int32_t* h_out, size_t n,
 int ns_merge_host_i32(int32_t* h_keys, size_t n_left, size_t n);
 int ns_merge_host_i64(int64_t* h_keys, size_t n_left, size_t n);
 int ns_release_cache(void);
+/* Host-array forms of the traced quick sort, hoare_partition and
+ * median_of_three above (the reference's optimized_quick_sort(span, low,
+ * high, cfg, stats) / hoare_partition(span, low, high, pivot) /
+ * median_of_three(span, low, high) call shapes): the range goes to the
+ * device, the device call runs, the range comes back; synchronous. */
+int ns_quick_sort_traced_host_i32(int32_t* h_keys, size_t n, uint32_t width_mask, int varsort_max,
+                                  uint64_t* out12);
+int ns_quick_sort_traced_host_i64(int64_t* h_keys, size_t n, uint32_t width_mask, int varsort_max,
+                                  uint64_t* out12);
+int ns_hoare_partition_host_i32(int32_t* h_keys, size_t n, int64_t low, int64_t high,
+                                int32_t pivot, int64_t* split);
+int ns_hoare_partition_host_i64(int64_t* h_keys, size_t n, int64_t low, int64_t high,
+                                int64_t pivot, int64_t* split);
+int ns_median_of_three_host_i32(int32_t* h_keys, size_t n, int64_t low, int64_t high,
+                                int32_t* pivot);
+int ns_median_of_three_host_i64(int64_t* h_keys, size_t n, int64_t low, int64_t high,
+                                int64_t* pivot);
 
 #ifdef __cplusplus
 }

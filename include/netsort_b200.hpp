@@ -134,6 +134,59 @@ void merge_range(std::span<Key> a, std::ptrdiff_t left, std::ptrdiff_t mid, std:
                    static_cast<size_t>(right - left + 1)),
         "merge");
 }
+inline int host_traced(std::int32_t* p, size_t n, const NetworkConfig& c, std::uint64_t* o) {
+  return ns_quick_sort_traced_host_i32(p, n, c.width_mask, c.varsort_max, o);
+}
+inline int host_traced(std::int64_t* p, size_t n, const NetworkConfig& c, std::uint64_t* o) {
+  return ns_quick_sort_traced_host_i64(p, n, c.width_mask, c.varsort_max, o);
+}
+inline int host_mot(std::int32_t* p, size_t n, std::int64_t lo, std::int64_t hi, std::int32_t* v) {
+  return ns_median_of_three_host_i32(p, n, lo, hi, v);
+}
+inline int host_mot(std::int64_t* p, size_t n, std::int64_t lo, std::int64_t hi, std::int64_t* v) {
+  return ns_median_of_three_host_i64(p, n, lo, hi, v);
+}
+inline int host_hoare(std::int32_t* p, size_t n, std::int64_t lo, std::int64_t hi, std::int32_t v,
+                      std::int64_t* j) {
+  return ns_hoare_partition_host_i32(p, n, lo, hi, v, j);
+}
+inline int host_hoare(std::int64_t* p, size_t n, std::int64_t lo, std::int64_t hi, std::int64_t v,
+                      std::int64_t* j) {
+  return ns_hoare_partition_host_i64(p, n, lo, hi, v, j);
+}
+// optimized_quick_sort(a, low, high, cfg, stats) — hybrid.hpp:197-204
+template <class Key>
+void traced_quick_sort(std::span<Key> a, std::ptrdiff_t low, std::ptrdiff_t high,
+                       const NetworkConfig& cfg, DispatchStats& stats) {
+  if (high < low) return;  // hybrid.hpp:201
+  if (low < 0 || high >= static_cast<std::ptrdiff_t>(a.size()))
+    throw std::invalid_argument("optimized_quick_sort: range outside the span");
+  std::uint64_t o[12] = {};
+  check(host_traced(a.data() + low, static_cast<size_t>(high - low + 1), cfg, o),
+        "optimized_quick_sort(stats)");
+  DispatchStats s;
+  for (std::size_t w = 0; w < s.network_hits.size(); ++w) s.network_hits[w] = o[w];
+  s.merges = o[9];
+  s.partitions = o[10];
+  s.max_depth = static_cast<int>(o[11]);
+  add_stats(stats, s);
+}
+template <class Key>
+Key median_of_three(std::span<Key> a, std::ptrdiff_t low, std::ptrdiff_t high) {
+  if (!(low >= 0 && low <= high && high < static_cast<std::ptrdiff_t>(a.size())))
+    throw std::invalid_argument("median_of_three: need 0 <= low <= high < size");
+  Key v{};
+  check(host_mot(a.data(), a.size(), low, high, &v), "median_of_three");
+  return v;
+}
+template <class Key>
+std::ptrdiff_t hoare_partition(std::span<Key> a, std::ptrdiff_t low, std::ptrdiff_t high, Key pivot) {
+  if (!(low >= 0 && low < high && high < static_cast<std::ptrdiff_t>(a.size())))
+    throw std::invalid_argument("hoare_partition: need 0 <= low < high < size");
+  std::int64_t j = 0;
+  check(host_hoare(a.data(), a.size(), low, high, pivot, &j), "hoare_partition");
+  return static_cast<std::ptrdiff_t>(j);
+}
 template <class Key>
 void sort_range(std::span<Key> a, std::ptrdiff_t lo, std::ptrdiff_t hi, const NetworkConfig& cfg,
                 Algorithm alg) {
@@ -171,18 +224,32 @@ void sort_range(std::span<Key> a, std::ptrdiff_t lo, std::ptrdiff_t hi, const Ne
     if (v.algorithm == Algorithm::merge_sort) optimized_merge_sort(a, v.config);          \
     else optimized_quick_sort(a, v.config);                                               \
   }                                                                                       \
-  /* stats overloads (hybrid.hpp:158-165, 234-243): merge sort only */                    \
+  /* stats overloads (hybrid.hpp:158-165, 197-204, 234-243); quick sort runs  */         \
+  /* the reference's recursion node for node on the GPU (qs_trace.cu)          */         \
   inline void optimized_merge_sort(std::span<KEY> a, std::ptrdiff_t left,                 \
                                    std::ptrdiff_t right, const NetworkConfig& cfg,        \
                                    DispatchStats& stats) {                                \
     detail::sort_range(a, left, right, cfg, Algorithm::merge_sort);                       \
     if (right >= left) detail::add_stats(stats, merge_sort_dispatch_stats(right - left + 1, cfg)); \
   }                                                                                       \
+  inline void optimized_quick_sort(std::span<KEY> a, std::ptrdiff_t low,                  \
+                                   std::ptrdiff_t high, const NetworkConfig& cfg,         \
+                                   DispatchStats& stats) {                                \
+    detail::traced_quick_sort(a, low, high, cfg, stats);                                  \
+  }                                                                                       \
   inline void run_variant(const SortVariant& v, std::span<KEY> a, DispatchStats& stats) { \
     if (a.empty()) return;                                                                \
-    if (v.algorithm != Algorithm::merge_sort)                                             \
-      throw std::invalid_argument("run_variant: dispatch stats are defined for merge sort only"); \
-    optimized_merge_sort(a, 0, static_cast<std::ptrdiff_t>(a.size()) - 1, v.config, stats); \
+    const auto hi = static_cast<std::ptrdiff_t>(a.size()) - 1;                            \
+    if (v.algorithm == Algorithm::merge_sort) optimized_merge_sort(a, 0, hi, v.config, stats); \
+    else optimized_quick_sort(a, 0, hi, v.config, stats);                                 \
+  }                                                                                       \
+  /* median_of_three / hoare_partition, hybrid.hpp:105-133 (on the GPU) */                \
+  inline KEY median_of_three(std::span<KEY> a, std::ptrdiff_t low, std::ptrdiff_t high) { \
+    return detail::median_of_three(a, low, high);                                         \
+  }                                                                                       \
+  inline std::ptrdiff_t hoare_partition(std::span<KEY> a, std::ptrdiff_t low,             \
+                                        std::ptrdiff_t high, KEY pivot) {                 \
+    return detail::hoare_partition(a, low, high, pivot);                                  \
   }                                                                                       \
   inline void merge(std::span<KEY> a, std::ptrdiff_t left, std::ptrdiff_t mid,             \
                     std::ptrdiff_t right) {                                               \

@@ -99,6 +99,20 @@ SIGNATURES = {
     "ns_quick_sort_host_i64": (_i32, [_vp, _sz, _u32, _i32]),
     "ns_quick_sort_host_i32": (_i32, [_vp, _sz, _u32, _i32]),
     "ns_release_cache": (_i32, []),
+    "ns_quick_sort_traced_temp_bytes": (_sz, [_sz]),
+    "ns_quick_sort_traced_i32": (_i32, [_vp, _sz, _u32, _i32, _vp, _vp, _sz, _vp]),
+    "ns_quick_sort_traced_i64": (_i32, [_vp, _sz, _u32, _i32, _vp, _vp, _sz, _vp]),
+    "ns_hoare_partition_temp_bytes": (_sz, [_sz]),
+    "ns_hoare_partition_i32": (_i32, [_vp, _sz, _i64, _i64, C.c_int32, _vp, _vp, _sz, _vp]),
+    "ns_hoare_partition_i64": (_i32, [_vp, _sz, _i64, _i64, C.c_int64, _vp, _vp, _sz, _vp]),
+    "ns_median_of_three_i32": (_i32, [_vp, _sz, _i64, _i64, _vp, _vp]),
+    "ns_median_of_three_i64": (_i32, [_vp, _sz, _i64, _i64, _vp, _vp]),
+    "ns_quick_sort_traced_host_i32": (_i32, [_vp, _sz, _u32, _i32, _vp]),
+    "ns_quick_sort_traced_host_i64": (_i32, [_vp, _sz, _u32, _i32, _vp]),
+    "ns_hoare_partition_host_i32": (_i32, [_vp, _sz, _i64, _i64, C.c_int32, _vp]),
+    "ns_hoare_partition_host_i64": (_i32, [_vp, _sz, _i64, _i64, C.c_int64, _vp]),
+    "ns_median_of_three_host_i32": (_i32, [_vp, _sz, _i64, _i64, _vp]),
+    "ns_median_of_three_host_i64": (_i32, [_vp, _sz, _i64, _i64, _vp]),
 }
 
 

@@ -84,8 +84,8 @@ class DispatchStats:
 def merge_sort_dispatch_stats(n: int, cfg: "NetworkConfig") -> DispatchStats:
     """The counters the reference's merge sort records for n keys: its
     recursion shape (hybrid.hpp:81-95) depends on n and the config only.
-    Quick sort's counters depend on the data's pivot splits and have no GPU
-    equivalent."""
+    Quick sort's counters depend on the data's pivot splits: they come from
+    the traced quick sort (quick_sort_traced)."""
     out = (C.c_uint64 * 12)()
     check(lib().ns_merge_sort_dispatch_stats(int(n), cfg.width_mask, cfg.varsort_max,
                                              C.cast(out, C.c_void_p)), "dispatch stats")
@@ -332,11 +332,96 @@ def merge(a, left: int, mid: int, right: int):
 
 
 def optimized_quick_sort(a, *args):
-    """optimized_quick_sort(a, cfg) or optimized_quick_sort(a, low, high, cfg)."""
+    """optimized_quick_sort(a, cfg), optimized_quick_sort(a, low, high, cfg)
+    or optimized_quick_sort(a, low, high, cfg, stats) (hybrid.hpp:197-216).
+    The stats form runs the reference's own recursion on the GPU
+    (quick_sort_traced) and adds its DispatchStats counters."""
     if len(args) == 1:
         return _sort(_lib.NS_QUICK_SORT, a, None, None, args[0])
+    if len(args) == 4:
+        low, high, cfg, stats = args
+        stats.add(quick_sort_traced(a, low, high, cfg))
+        return a
     low, high, cfg = args
     return _sort(_lib.NS_QUICK_SORT, a, low, high, cfg)
+
+
+def quick_sort_traced(a, low, high, cfg: NetworkConfig) -> DispatchStats:
+    """Sort a[low..high] with the reference's quick sort executed node for node
+    on the GPU (median_of_three + hoare_partition at every node of
+    quick_sort_rec, hybrid.hpp:105-150; ns_quick_sort_traced_*) and return its
+    DispatchStats.  high < low is a no-op with zero counters (hybrid.hpp:201).
+    Synchronises (the instrumentation path, not the timed one)."""
+    low, high, n = _range(a, low, high)
+    out = (C.c_uint64 * 12)()
+    if high < low:
+        return DispatchStats()
+    if low < 0 or high >= n:
+        raise ValueError("range outside the array")
+    cnt = high - low + 1
+    L = lib()
+    if _is_device(a):
+        t = _check_tensor(a, allow_i64=True)
+        ptr = a.data_ptr() + a.element_size() * low
+        tb = L.ns_quick_sort_traced_temp_bytes(cnt)
+        fn = getattr(L, f"ns_quick_sort_traced_{t}")
+        check(_with_scratch(tb, a, lambda tmp, strm: fn(ptr, cnt, cfg.width_mask, cfg.varsort_max,
+                                                         C.cast(out, C.c_void_p), tmp, tb, strm)),
+              "optimized_quick_sort(stats)")
+    else:
+        t = _check_host(a)
+        fn = getattr(L, f"ns_quick_sort_traced_host_{t}")
+        check(fn(a.ctypes.data + a.itemsize * low, cnt, cfg.width_mask, cfg.varsort_max,
+                 C.cast(out, C.c_void_p)), "optimized_quick_sort(stats)")
+    return DispatchStats(list(out[:9]), int(out[9]), int(out[10]), int(out[11]))
+
+
+def median_of_three(a, low: int, high: int) -> int:
+    """median_of_three — hybrid.hpp:105-114: the three compare-exchanges on
+    a[low], a[low+(high-low)//2], a[high] (in place, on the GPU) and the pivot
+    a[mid]; ranges of length 1 or 2 yield a[low] untouched."""
+    n = a.numel() if _is_device(a) else len(a)
+    low, high = int(low), int(high)
+    if not (0 <= low <= high < n):
+        raise ValueError("median_of_three: need 0 <= low <= high < size")
+    L = lib()
+    if _is_device(a):
+        t = _check_tensor(a, allow_i64=True)
+        piv = (C.c_int64 if t == "i64" else C.c_int32)()
+        check(getattr(L, f"ns_median_of_three_{t}")(a.data_ptr(), n, low, high, C.addressof(piv),
+                                                   _stream_ptr(a)), "median_of_three")
+    else:
+        t = _check_host(a)
+        piv = (C.c_int64 if t == "i64" else C.c_int32)()
+        check(getattr(L, f"ns_median_of_three_host_{t}")(a.ctypes.data, n, low, high,
+                                                        C.addressof(piv)), "median_of_three")
+    return int(piv.value)
+
+
+def hoare_partition(a, low: int, high: int, pivot: int) -> int:
+    """hoare_partition — hybrid.hpp:121-133 on a[low..high] (low < high): the
+    reference's swaps in the reference's cells, and its split j (low <= j <
+    high, [low..j] <= pivot <= [j+1..high]); computed on the GPU in two
+    streaming passes.  A pivot above or below every key in the range raises
+    ValueError (the reference's scan would leave the range)."""
+    n = a.numel() if _is_device(a) else len(a)
+    low, high = int(low), int(high)
+    if not (0 <= low < high < n):
+        raise ValueError("hoare_partition: need 0 <= low < high < size")
+    L = lib()
+    split = C.c_int64()
+    if _is_device(a):
+        t = _check_tensor(a, allow_i64=True)
+        tb = L.ns_hoare_partition_temp_bytes(high - low + 1)
+        fn = getattr(L, f"ns_hoare_partition_{t}")
+        check(_with_scratch(tb, a, lambda tmp, strm: fn(a.data_ptr(), n, low, high, int(pivot),
+                                                         C.addressof(split), tmp, tb, strm)),
+              "hoare_partition")
+    else:
+        t = _check_host(a)
+        check(getattr(L, f"ns_hoare_partition_host_{t}")(a.ctypes.data, n, low, high, int(pivot),
+                                                        C.addressof(split)), "hoare_partition")
+    return int(split.value)
 
 
 def classical_merge_sort(a):
@@ -348,14 +433,14 @@ def classical_quick_sort(a):
 
 
 def run_variant(variant: SortVariant, a, stats: Optional[DispatchStats] = None):
-    """run_variant (hybrid.hpp:225-243).  With stats: merge sort only (quick
-    sort's counters are data-dependent and have no GPU equivalent)."""
+    """run_variant (hybrid.hpp:225-243).  With stats, quick sort runs the
+    traced reference recursion (quick_sort_traced)."""
     if stats is not None:
         n = a.numel() if _is_device(a) else len(a)
         if n == 0:  # hybrid.hpp:237
             return a
         if variant.algorithm is not Algorithm.merge_sort:
-            raise ValueError("run_variant: dispatch stats are defined for merge sort only")
+            return optimized_quick_sort(a, 0, n - 1, variant.config, stats)
         return optimized_merge_sort(a, 0, n - 1, variant.config, stats)
     if variant.algorithm is Algorithm.merge_sort:
         return optimized_merge_sort(a, variant.config)

@@ -163,14 +163,31 @@ static void device_side() {
     CHECK(std::is_sorted(v.begin(), v.end()));
     CHECK(st.merges == 16383 && st.network_hits[6] == 14688 && st.network_hits[7] == 1696);
     CHECK(st.max_depth == 15);  // SURVEY.md A.2 (100,000 keys, 6To8)
-    bool threw = false;
-    try {
-      ns::run_variant(ns::SortVariant{ns::Algorithm::quick_sort, *ns::find_config("3To5")},
-                      std::span<int32_t>(v), st);
-    } catch (const std::invalid_argument&) {
-      threw = true;
+    // quick sort with stats: the reference recursion traced on the GPU; the
+    // depth bound on sorted input (test_hybrid.cpp:271-281)
+    std::vector<int32_t> sorted_in(10000);
+    std::iota(sorted_in.begin(), sorted_in.end(), 0);
+    for (const char* name : {"Classic", "3To5"}) {
+      ns::DispatchStats qs;
+      auto q = sorted_in;
+      ns::run_variant(ns::SortVariant{ns::Algorithm::quick_sort, *ns::find_config(name)},
+                      std::span<int32_t>(q), qs);
+      CHECK(q == sorted_in);
+      CHECK(qs.partitions > 0 && qs.merges == 0);
+      CHECK(qs.max_depth >= 1 && qs.max_depth <= 4 * 13.3 + 16);
     }
-    CHECK(threw);
+    // hoare_partition / median_of_three contract (test_hybrid.cpp:204-269)
+    for (int t = 0; t < 50; ++t) {
+      auto b = random_values(64, 300 + t);
+      for (auto& x : b) x %= 5;
+      auto u = b;
+      const int32_t p = ns::median_of_three(std::span<int32_t>(u), 3, 60);
+      CHECK(u[3] <= p && p <= u[60] && u[31] == p);
+      const auto j = ns::hoare_partition(std::span<int32_t>(u), 3, 60, p);
+      CHECK(j >= 3 && j < 60);
+      for (std::ptrdiff_t k = 3; k <= j; ++k) CHECK(u[static_cast<size_t>(k)] <= p);
+      for (std::ptrdiff_t k = j + 1; k <= 60; ++k) CHECK(u[static_cast<size_t>(k)] >= p);
+    }
     auto m = random_values(5000, 78);
     std::sort(m.begin(), m.begin() + 2000);
     std::sort(m.begin() + 2000, m.end());

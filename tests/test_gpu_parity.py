@@ -476,8 +476,14 @@ def test_run_variant_with_stats(ns, cuda, oracle):
     assert np.array_equal(t.cpu().numpy(), want)
     assert st.network_hits == list(ost.network_hits) and st.merges == ost.merges
     assert st.max_depth == ost.max_depth
-    with pytest.raises(ValueError):
-        ns.run_variant(ns.SortVariant(ns.Algorithm.quick_sort, ns.find_config("3To5")), t, st)
+    # quick sort: the traced reference recursion (qs_trace.cu), counters added
+    q = ns.DispatchStats()
+    t = torch.from_numpy(a).to(cuda)
+    ns.run_variant(ns.SortVariant(ns.Algorithm.quick_sort, ns.find_config("3To5")), t, q)
+    want, qst = oracle.quick_sort(a, "3To5", stats=True)
+    assert np.array_equal(t.cpu().numpy(), want)
+    assert q.network_hits == list(qst.network_hits) and q.partitions == qst.partitions
+    assert q.max_depth == qst.max_depth and q.merges == 0
 
 
 def test_merge_runs_many_runs_both_key_types(ns, cuda):

@@ -204,6 +204,39 @@ def test_median_and_partition_contract(oracle):
                     assert np.array_equal(u[:lo], base[:lo]) and np.array_equal(u[hi + 1:], base[hi + 1:])
 
 
+def _hoare_closed_form(a, lo, hi, p):
+    """The rank form of hoare_partition that qs_trace.cu computes in
+    parallel: swap the pairs (L_k, R_k) while L_k < R_k (L ascending
+    positions of keys >= p, R descending positions of keys <= p, both on the
+    input), return max(R_{S+1}, L_S) with the j == high fix-up."""
+    seg = a[lo:hi + 1]
+    L = lo + np.flatnonzero(seg >= p)
+    R = (lo + np.flatnonzero(seg <= p))[::-1]
+    m = min(len(L), len(R))
+    ok = L[:m] < R[:m]
+    S = int(np.argmin(ok)) if not ok.all() else m
+    a[L[:S]], a[R[:S]] = a[R[:S]].copy(), a[L[:S]].copy()
+    j = max(int(R[S]) if S < len(R) else -1, int(L[S - 1]) if S else -1)
+    return j if j < hi else hi - 1
+
+
+def test_hoare_closed_form(oracle):
+    """The closed form the GPU partition uses gives the reference loop's
+    cells and split (hybrid.hpp:121-133) on every tested input."""
+    L = oracle.lib()
+    rng = np.random.default_rng(8)
+    for _ in range(3000):
+        n = int(rng.integers(2, 60))
+        a = rng.integers(0, int(rng.choice([2, 3, 5, 1000])), n).astype(np.int32)
+        lo = int(rng.integers(0, n - 1))
+        hi = int(rng.integers(lo + 1, n))
+        p = int(a[rng.integers(lo, hi + 1)])
+        u, v = a.copy(), a.copy()
+        j = L.oracle_hoare_partition_i32(u, lo, hi, p)
+        assert _hoare_closed_form(v, lo, hi, p) == j
+        assert np.array_equal(u, v)
+
+
 def test_quick_sort_depth_bound_sorted(oracle):
     """test_hybrid.cpp:271-281."""
     for name in ("Classic", "3To5"):
