@@ -276,6 +276,7 @@ __global__ void __launch_bounds__(kThreads) swap_kernel(K* __restrict__ a,
     const int64_t k = k0 + i + 1;
     if (k > S) break;
     const int64_t x = lo + posL[lo + k - 1], y = lo + posR[lo + NR - k];
+    NSB_DCHECK(x < y && y <= segs[c.seg].hi);
     const K t = a[x];
     a[x] = a[y];
     a[y] = t;
@@ -351,6 +352,8 @@ __device__ int warp_partition(K* s, uint16_t* sL, uint16_t* sR, int lo, int hi, 
     const K v = ok ? s[x] : K(0);
     const bool fl = ok && v >= p, fr = ok && v <= p;
     const uint32_t bl = __ballot_sync(0xffffffffu, fl), br = __ballot_sync(0xffffffffu, fr);
+    NSB_DCHECK(!fl || lo + nl + __popc(bl & lt) <= hi);
+    NSB_DCHECK(!fr || lo + nr + __popc(br & lt) <= hi);
     if (fl) sL[lo + nl + __popc(bl & lt)] = uint16_t(x);
     if (fr) sR[lo + nr + __popc(br & lt)] = uint16_t(x);
     nl += __popc(bl);
@@ -366,6 +369,7 @@ __device__ int warp_partition(K* s, uint16_t* sL, uint16_t* sR, int lo, int hi, 
   const int S = a;
   for (int k = lane + 1; k <= S; k += 32) {
     const int x = sL[lo + k - 1], y = sR[lo + nr - k];
+    NSB_DCHECK(x >= lo && x < y && y <= hi);
     const K t = s[x];
     s[x] = s[y];
     s[y] = t;
@@ -418,6 +422,7 @@ __global__ void __launch_bounds__(kThreads) small_kernel(K* __restrict__ a,
       if (idx >= ncur) break;
       const uint32_t node = fr[cur * (kTraceSmall / 2) + idx];
       const int lo = node & 0xffff, hi = node >> 16;
+      NSB_DCHECK(lo < hi && hi < g.len);
       const int split = warp_partition(s, sL, sR, lo, hi, lane);
       if (lane == 0) atomicAdd(&sh.parts, 1ull);
       visit(s, fr, sh, nxt, lo, split, depth + 1, mask, vs, lane);

@@ -154,6 +154,49 @@ static void one_sort(const char* tag, int algo, size_t n, int dist) {
   expect_sorted_copy(name, in, d.p, n);
 }
 
+// the traced quick sort (qs_trace.cu): the reference recursion node for
+// node; checked sorted (its counters are checked against the oracle by
+// tests/test_gpu_qs_trace.py)
+template <class T>
+static void traced_case(size_t n, int dist) {
+  char name[96];
+  std::snprintf(name, sizeof name, "traced/%s/n=%zu/dist=%d", sizeof(T) == 4 ? "i32" : "i64", n,
+                dist);
+  if (!run(name)) return;
+  const auto in = values<T>(n, 3000 + n + dist, dist);
+  Dev<T> d(n);
+  CU(cudaMemcpy(d.p, in.data(), n * sizeof(T), cudaMemcpyHostToDevice));
+  uint32_t mask;
+  int vs;
+  CK(ns_find_config("3To5", &mask, &vs));
+  const size_t tb = ns_quick_sort_traced_temp_bytes(n);
+  Dev<char> tmp(tb, true);
+  uint64_t st[12];
+  if constexpr (sizeof(T) == 4)
+    CK(ns_quick_sort_traced_i32(d.p, n, mask, vs, st, tmp.p, tb, nullptr));
+  else
+    CK(ns_quick_sort_traced_i64(d.p, n, mask, vs, st, tmp.p, tb, nullptr));
+  CU(cudaDeviceSynchronize());
+  expect_sorted_copy(name, in, d.p, n);
+  // one explicit-pivot partition over the middle of a fresh copy
+  if (n >= 3) {
+    CU(cudaMemcpy(d.p, in.data(), n * sizeof(T), cudaMemcpyHostToDevice));
+    const size_t hb = ns_hoare_partition_temp_bytes(n);
+    Dev<char> ht(hb, true);
+    int64_t split = -1;
+    const int64_t lo = 1, hi = (int64_t)n - 1;
+    if constexpr (sizeof(T) == 4)
+      CK(ns_hoare_partition_i32(d.p, n, lo, hi, in[n / 2], &split, ht.p, hb, nullptr));
+    else
+      CK(ns_hoare_partition_i64(d.p, n, lo, hi, in[n / 2], &split, ht.p, hb, nullptr));
+    if (split < lo || split >= hi) {
+      std::printf("FAIL %s: split %lld outside [%lld, %lld)\n", name, (long long)split,
+                  (long long)lo, (long long)hi);
+      ++failures;
+    }
+  }
+}
+
 static void batch_case(size_t arrays, bool bad) {
   char name[64];
   std::snprintf(name, sizeof name, "batch/arrays=%zu/%s", arrays, bad ? "invalid" : "valid");
@@ -331,6 +374,10 @@ int main(int argc, char** argv) {
   }
   one_sort<int32_t>("qs", 1, 1500000, 0);
   one_sort<int64_t>("qs", 1, 100000, 0);
+  for (size_t n : {1u, 7u, 3000u, 8192u, 8193u, 60000u}) traced_case<int32_t>(n, 0);
+  traced_case<int32_t>(100000, 1);
+  traced_case<int32_t>(100000, 2);
+  traced_case<int64_t>(30000, 0);
   batch_case(3000, false);
   batch_case(3000, true);
   segmented_case<int32_t>(24, 5000, 0);
