@@ -32,35 +32,6 @@ constexpr unsigned kFull = 0xffffffffu;
 // Warp bitonic merge stage: on entry every lane holds K sorted keys
 // (blocked: lane l owns warp positions [l*K, l*K+K)); after LEVELS levels
 // every aligned group of 2^LEVELS lanes holds one sorted run.
-// One key of a cross-lane compare-exchange: the lower lane keeps min(v, o),
-// the upper one max(v, o).  `upper ? max : min` compiles to two VIMNMX (the
-// second predicated), and the bitonic stage is bound by the half-rate ALU
-// pipe.  With NSB_BITONIC_FMA the maximum is taken as v + o - min(v, o)
-// (exact modulo 2^32) by two multiply-adds on the idle FMA pipe, the second
-// predicated on `upper`; the multipliers +-gridDim.y (1 for every launch of
-// these kernels, held in uniform registers) keep ptxas from folding them back
-// into ALU-pipe adds.
-#ifndef NSB_BITONIC_FMA
-#define NSB_BITONIC_FMA 1
-#endif
-template <class T>
-__device__ __forceinline__ T lane_minmax(T v, T o, bool upper) {
-#if NSB_BITONIC_FMA
-  if constexpr (sizeof(T) == 4) {
-    const int one = (int)gridDim.y, mone = -one;
-    int r = min((int)v, (int)o);
-    const int t = (int)v * one + (int)o;
-    asm("{\n\t.reg .pred p;\n\tsetp.ne.s32 p, %1, 0;\n\t@p mad.lo.s32 %0, %0, %2, %3;\n\t}"
-        : "+r"(r)
-        : "r"((int)upper), "r"(mone), "r"(t));
-    return (T)r;
-  } else
-#endif
-  {
-    return upper ? max(v, o) : min(v, o);
-  }
-}
-
 template <int LEVELS, int K, class T>
 __device__ __forceinline__ void warp_bitonic(T (&v)[K], int lane) {
 #pragma unroll
@@ -75,8 +46,8 @@ __device__ __forceinline__ void warp_bitonic(T (&v)[K], int lane) {
       for (int i = 0; i < K / 2; ++i) {
         const T ti = __shfl_xor_sync(kFull, v[K - 1 - i], fm);
         const T tj = __shfl_xor_sync(kFull, v[i], fm);
-        v[i] = lane_minmax(v[i], ti, upper);
-        v[K - 1 - i] = lane_minmax(v[K - 1 - i], tj, upper);
+        v[i] = upper ? max(v[i], ti) : min(v[i], ti);
+        v[K - 1 - i] = upper ? max(v[K - 1 - i], tj) : min(v[K - 1 - i], tj);
       }
     }
     // cross-lane half-cleaners
@@ -86,7 +57,7 @@ __device__ __forceinline__ void warp_bitonic(T (&v)[K], int lane) {
 #pragma unroll
       for (int i = 0; i < K; ++i) {
         const T o = __shfl_xor_sync(kFull, v[i], 1 << j);
-        v[i] = lane_minmax(v[i], o, upper);
+        v[i] = upper ? max(v[i], o) : min(v[i], o);
       }
     }
     // intra-thread half-cleaners
@@ -402,11 +373,6 @@ __device__ __forceinline__ void cta_sort_padded(const Key* in, Key* out, int val
 #ifndef NSB_SKEW64_K16
 #define NSB_SKEW64_K16 1
 #endif
-// int32 merge levels of the tile sort with the cursor arithmetic on the FMA
-// pipe (see the merge loop of cta_sort_regs)
-#ifndef NSB_TS_FMA_STEP
-#define NSB_TS_FMA_STEP 0
-#endif
 template <int NT, int K, class Key>
 __host__ __device__ constexpr bool cta_sort_skewed() {
   return ((sizeof(Key) == 4 && (K == 16 || K == 32)) || (sizeof(Key) == 8 && (K == 8 || (NSB_SKEW64_K16 && K == 16)))) &&
@@ -620,51 +586,18 @@ __device__ __forceinline__ void cta_sort_regs(Key (&v)[K], Key* out, int valid, 
       uint32_t mnext = (uint32_t)(b_pos + d - a + 1) * KB;
       Key m = sm[b_pos + d - a];
       NSB_DCHECK(a >= 0 && a <= R && d - a >= 0 && d - a <= R);
-#if NSB_TS_FMA_STEP
-      if constexpr (sizeof(Key) == 4) {
-        // The same loop with its cursor arithmetic on the FMA pipe (the tile
-        // sort is bound by the half-rate ALU pipe, the FMA pipe idles).  The
-        // two cursors are kept as ptr and s = ptr + mnext: a step leaves
-        // {ptr, mnext} = {ptr + 4, mnext} in one order or the other, so s
-        // grows by 4 either way, the other run's cursor is s - ptr, and the
-        // select becomes a predicated multiply-add that overwrites it.  The
-        // multiplier `one` (gridDim.y, 1 for every launch of these kernels) is
-        // opaque to ptxas, which would otherwise fold the IMADs back into
-        // ALU-pipe adds.  Per output: LDS, ISETP, 2 VIMNMX (ALU) + 3 IMAD
-        // (FMA) instead of 6 ALU operations.
-        const uint32_t one = gridDim.y;
-        NSB_DCHECK(one == 1u);
-        uint32_t s = ptr + mnext;
 #pragma unroll
-        for (int k = 0; k < KM; ++k) {
-          NSB_DCHECK((ptr >= (uint32_t)a_pos * KB && ptr < (uint32_t)(a_pos + R + GAP) * KB) ||
-                     (ptr >= (uint32_t)b_pos * KB && ptr < (uint32_t)(b_pos + R + GAP) * KB));
-          const int32_t x = *reinterpret_cast<const int32_t*>(smc + ptr);
-          uint32_t nx = s * one - ptr;  // the other run's cursor; ptr + 4 if x is emitted
-          asm("{\n\t.reg .pred p;\n\tsetp.le.s32 p, %1, %2;\n\t@p mad.lo.u32 %0, %3, %4, 4;\n\t}"
-              : "+r"(nx)
-              : "r"(x), "r"((int32_t)m), "r"(ptr), "r"(one));
-          w[k] = min(x, (int32_t)m);
-          m = max(x, (int32_t)m);
-          ptr = nx;
-          s = s * one + 4u;
-        }
-      } else
-#endif
-      {
-#pragma unroll
-        for (int k = 0; k < KM; ++k) {
-          // a cursor stays inside its run + GAP sentinels (runs at a_pos, b_pos)
-          NSB_DCHECK((ptr >= (uint32_t)a_pos * KB && ptr < (uint32_t)(a_pos + R + GAP) * KB) ||
-                     (ptr >= (uint32_t)b_pos * KB && ptr < (uint32_t)(b_pos + R + GAP) * KB));
-          const Key x = *reinterpret_cast<const Key*>(smc + ptr);
-          const bool t = x <= m;
-          w[k] = t ? x : m;
-          const uint32_t q = ptr + (uint32_t)KB;
-          ptr = t ? q : mnext;
-          mnext = t ? mnext : q;
-          m = t ? m : x;
-        }
+      for (int k = 0; k < KM; ++k) {
+        // a cursor stays inside its run + GAP sentinels (runs at a_pos, b_pos)
+        NSB_DCHECK((ptr >= (uint32_t)a_pos * KB && ptr < (uint32_t)(a_pos + R + GAP) * KB) ||
+                   (ptr >= (uint32_t)b_pos * KB && ptr < (uint32_t)(b_pos + R + GAP) * KB));
+        const Key x = *reinterpret_cast<const Key*>(smc + ptr);
+        const bool t = x <= m;
+        w[k] = t ? x : m;
+        const uint32_t q = ptr + (uint32_t)KB;
+        ptr = t ? q : mnext;
+        mnext = t ? mnext : q;
+        m = t ? m : x;
       }
       }
       __syncthreads();  // every thread is done reading this level's input
