@@ -529,14 +529,25 @@ __global__ void __launch_bounds__(kQsNT, 2) qs_count_kernel(QsCtx<Key> c, int le
     }
     for (int i = tid; i < NB; i += kQsNT) hist[i] = 0;
     __syncthreads();
+    uint8_t* idp = c.ids + c0 + tid;
+    if (cnt == kQsChunk) {  // full chunk (all but a segment's last): no per-key guard
 #pragma unroll
-    for (int u = 0; u < kQsPer; ++u) {
-      const int j = u * kQsNT + tid;
-      const bool in = j < cnt;
-      const int b = in ? cls(k[u]) : -1;
-      NSB_DCHECK(b < 2 * cls.B - 1);
-      if (in) c.ids[c0 + j] = (uint8_t)b;
-      qs_hist_add(hist, b);
+      for (int u = 0; u < kQsPer; ++u) {
+        const int b = cls(k[u]);
+        NSB_DCHECK(b >= 0 && b < 2 * cls.B - 1);
+        idp[u * kQsNT] = (uint8_t)b;
+        atomicAdd(&hist[b], 1u);
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < kQsPer; ++u) {
+        const int j = u * kQsNT + tid;
+        const bool in = j < cnt;
+        const int b = in ? cls(k[u]) : -1;
+        NSB_DCHECK(b < 2 * cls.B - 1);
+        if (in) idp[u * kQsNT] = (uint8_t)b;
+        qs_hist_add(hist, b);
+      }
     }
     __syncthreads();
     uint32_t* cn = c.cnt[level & 1] + g.cnt_off;
