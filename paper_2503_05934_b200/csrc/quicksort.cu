@@ -355,30 +355,34 @@ __host__ __device__ constexpr int qs_rep() { return sizeof(Key) == 4 ? 32 : 16; 
 constexpr int kQsCellsMax = 16 * kQsMaxB;
 template <class Key>
 __host__ __device__ constexpr int qs_table_bytes() {
-  return kQsMaxB * qs_rep<Key>() * (int)sizeof(Key) + kQsCellsMax * 2;
+  // one more pivot slot than kQsMaxB: the classifier reads slot j + 1 <= B unclamped
+  return (kQsMaxB + 1) * qs_rep<Key>() * (int)sizeof(Key) + kQsCellsMax * 2;
 }
 
 template <class Key>
 struct QsClassifier {
   const Key* tab;        // replicated pivots, this lane's column
   const uint16_t* cell;  // j0 | k << 8
-  Key lo;
+  Key lo, hi;
   int shift, ncell, B;
   __device__ __forceinline__ int operator()(Key key) const {
     constexpr int R = qs_rep<Key>();
     using U = std::make_unsigned_t<Key>;
-    const U cd = ((U)key - (U)lo) >> shift;
-    // keys below the first pivot use cell 0 (j0 = 0; its first candidate is
-    // the first pivot, which they do not exceed)
-    const int ci = key < lo ? 0 : (cd < (U)ncell ? (int)cd : ncell - 1);
+    // the key clamped into the pivots' range [lo, hi] picks its cell: keys
+    // below the first pivot use cell 0 (j0 = 0; its first candidate is the
+    // first pivot, which they do not exceed), keys above the last pivot the
+    // last pivot's cell (every pivot of it is smaller: j ends at B - 1);
+    // (hi - lo) >> shift < ncell by the choice of shift
+    const Key kc = min(max(key, lo), hi);
+    const int ci = (int)(((U)kc - (U)lo) >> shift);
     const uint32_t e = cell[ci];
     int j = (int)(e & 255u);
     int k = (int)(e >> 8);
     // the first step without a branch (a cell holds 0 or 1 pivot almost
-    // always): both candidate pivots are loaded at once (slot B-1 is the
-    // key-maximum pad, so j + 1 <= B - 1 stays in the table)
+    // always): both candidate pivots are loaded at once (slots B-1 and B are
+    // key-maximum pads, so j + 1 <= B stays in the table)
     const Key t0 = tab[j * R];
-    const Key t1 = tab[min(j + 1, B - 1) * R];
+    const Key t1 = tab[(j + 1) * R];
     const bool s1 = (k > 0) & (t0 < key);
     j += s1;
     k -= s1;
@@ -402,14 +406,15 @@ __device__ __forceinline__ QsClassifier<Key> qs_load_classifier(unsigned char* r
                                                                  int B) {
   constexpr int R = qs_rep<Key>();
   Key* tab = reinterpret_cast<Key*>(raw);
-  uint16_t* cell = reinterpret_cast<uint16_t*>(raw + kQsMaxB * R * sizeof(Key));
+  uint16_t* cell = reinterpret_cast<uint16_t*>(raw + (kQsMaxB + 1) * R * sizeof(Key));
   const Key lo = __ldg(spl), hi = __ldg(spl + (B >= 2 ? B - 2 : 0));
   const int ncell = 16 * B;
 #pragma unroll 4
   for (int i = threadIdx.x; i < B * R; i += blockDim.x) tab[i] = __ldg(spl + i / R);
+  if (threadIdx.x < R) tab[B * R + threadIdx.x] = KeyT<Key>::kMax;  // slot B: read, never selected
 #pragma unroll 4
   for (int i = threadIdx.x; i < ncell; i += blockDim.x) cell[i] = __ldg(cells + i);
-  return QsClassifier<Key>{tab + (threadIdx.x & (R - 1)), cell, lo, qs_cell_shift(lo, hi, ncell),
+  return QsClassifier<Key>{tab + (threadIdx.x & (R - 1)), cell, lo, hi, qs_cell_shift(lo, hi, ncell),
                            ncell, B};
 }
 
