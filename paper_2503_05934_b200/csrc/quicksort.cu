@@ -767,18 +767,41 @@ __global__ void __launch_bounds__(kQsNT, 2) qs_scatter_kernel(QsCtx<Key> c, int 
       b[u] = in ? (int)__ldcs(c.ids + i) : -1;
     }
     uint32_t pk[kQsPer];  // rank-in-bucket << 8 | bucket, 0xffffffff = no key
+    const bool full = c1 - c0 == kQsChunk;  // all but a segment's last chunk: no per-key guards
+    if (full) {
+      const uint32_t hist_s = (uint32_t)__cvta_generic_to_shared(hist);
 #pragma unroll
-    for (int u = 0; u < kQsPer; ++u) {
-      const int b0 = __shfl_sync(kFull, b[u], 0);
-      uint32_t r;
-      if (__all_sync(kFull, b[u] == b0)) {  // one bucket for the whole warp
-        uint32_t base = 0;
-        if (lane == 0 && b0 >= 0) base = atomicAdd(&hist[b0], 32u);
-        r = __shfl_sync(kFull, base, 0) + (uint32_t)lane;
-      } else {
-        r = b[u] >= 0 ? atomicAdd(&hist[b[u]], 1u) : 0u;
+      for (int u = 0; u < kQsPer; ++u) {
+        const int b0 = __shfl_sync(kFull, b[u], 0);
+        uint32_t r;
+        if (__all_sync(kFull, b[u] == b0)) {  // one bucket for the whole warp (sorted input)
+          uint32_t base = 0;
+          // (plain PTX: nvcc wraps a one-lane atomicAdd in its own warp aggregation)
+          if (lane == 0)
+            asm volatile("atom.shared.add.u32 %0, [%1], 32;"
+                         : "=r"(base)
+                         : "r"(hist_s + 4u * (uint32_t)b0)
+                         : "memory");
+          r = __shfl_sync(kFull, base, 0) + (uint32_t)lane;
+        } else {
+          r = atomicAdd(&hist[b[u]], 1u);
+        }
+        pk[u] = (r << 8) | (uint32_t)b[u];
       }
-      pk[u] = b[u] >= 0 ? (r << 8) | (uint32_t)b[u] : 0xffffffffu;
+    } else {
+#pragma unroll
+      for (int u = 0; u < kQsPer; ++u) {
+        const int b0 = __shfl_sync(kFull, b[u], 0);
+        uint32_t r;
+        if (__all_sync(kFull, b[u] == b0)) {  // one bucket for the whole warp
+          uint32_t base = 0;
+          if (lane == 0 && b0 >= 0) base = atomicAdd(&hist[b0], 32u);
+          r = __shfl_sync(kFull, base, 0) + (uint32_t)lane;
+        } else {
+          r = b[u] >= 0 ? atomicAdd(&hist[b[u]], 1u) : 0u;
+        }
+        pk[u] = b[u] >= 0 ? (r << 8) | (uint32_t)b[u] : 0xffffffffu;
+      }
     }
     __syncthreads();
     // local bucket starts (exclusive scan) and one global reservation per bucket
@@ -791,22 +814,40 @@ __global__ void __launch_bounds__(kQsNT, 2) qs_scatter_kernel(QsCtx<Key> c, int 
       delta[tid] = (long long)gb - (long long)ls;
     }
     __syncthreads();
+    if (full) {
 #pragma unroll
-    for (int u = 0; u < kQsPer; ++u) {
-      if (pk[u] != 0xffffffffu) {
+      for (int u = 0; u < kQsPer; ++u) {
         const int bb = (int)(pk[u] & 0xffu);
         const int p = (int)hist[bb] + (int)(pk[u] >> 8);
-        NSB_DCHECK(bb < NB && p >= 0 && p < (int)(c1 - c0));
+        NSB_DCHECK(bb < NB && p >= 0 && p < kQsChunk);
         skey[p] = k[u];
         sbid[p] = (uint8_t)bb;
       }
-    }
-    __syncthreads();
-    const int total = (int)(c1 - c0);
-    for (int i = tid; i < total; i += kQsNT) {
-      // every key lands inside its segment (the reserved bucket ranges)
-      NSB_DCHECK(delta[sbid[i]] + i >= g.start && delta[sbid[i]] + i < g.start + g.len);
-      Y[delta[sbid[i]] + i] = skey[i];
+      __syncthreads();
+#pragma unroll
+      for (int u = 0; u < kQsPer; ++u) {
+        const int i = u * kQsNT + tid;
+        // every key lands inside its segment (the reserved bucket ranges)
+        NSB_DCHECK(delta[sbid[i]] + i >= g.start && delta[sbid[i]] + i < g.start + g.len);
+        Y[delta[sbid[i]] + i] = skey[i];
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < kQsPer; ++u) {
+        if (pk[u] != 0xffffffffu) {
+          const int bb = (int)(pk[u] & 0xffu);
+          const int p = (int)hist[bb] + (int)(pk[u] >> 8);
+          NSB_DCHECK(bb < NB && p >= 0 && p < (int)(c1 - c0));
+          skey[p] = k[u];
+          sbid[p] = (uint8_t)bb;
+        }
+      }
+      __syncthreads();
+      const int total = (int)(c1 - c0);
+      for (int i = tid; i < total; i += kQsNT) {
+        NSB_DCHECK(delta[sbid[i]] + i >= g.start && delta[sbid[i]] + i < g.start + g.len);
+        Y[delta[sbid[i]] + i] = skey[i];
+      }
     }
   }
 }
