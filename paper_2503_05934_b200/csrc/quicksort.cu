@@ -772,15 +772,16 @@ __global__ void __launch_bounds__(kQsNT, 2) qs_scatter_kernel(QsCtx<Key> c, int 
       const uint32_t hist_s = (uint32_t)__cvta_generic_to_shared(hist);
 #pragma unroll
       for (int u = 0; u < kQsPer; ++u) {
-        const int b0 = __shfl_sync(kFull, b[u], 0);
+        int uni;
+        __match_all_sync(kFull, b[u], &uni);
         uint32_t r;
-        if (__all_sync(kFull, b[u] == b0)) {  // one bucket for the whole warp (sorted input)
+        if (uni) {  // one bucket for the whole warp (sorted input)
           uint32_t base = 0;
           // (plain PTX: nvcc wraps a one-lane atomicAdd in its own warp aggregation)
           if (lane == 0)
             asm volatile("atom.shared.add.u32 %0, [%1], 32;"
                          : "=r"(base)
-                         : "r"(hist_s + 4u * (uint32_t)b0)
+                         : "r"(hist_s + 4u * (uint32_t)b[u])
                          : "memory");
           r = __shfl_sync(kFull, base, 0) + (uint32_t)lane;
         } else {
