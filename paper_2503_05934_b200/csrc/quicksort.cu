@@ -56,6 +56,7 @@ constexpr int kQsChunk = kQsNT * kQsPer;     // keys per chunk (one CTA iteratio
 constexpr int kQsMaxB = 128;                 // pivot slots per segment (B-1 real + pad):
                                              // 2B-1 <= 255 buckets, so a bucket id is one byte
 constexpr int kQsOver = 16;                  // samples per bucket
+constexpr int kQsHistStride = 2 * kQsMaxB;   // per-chunk histogram slots (2B-1 <= 255 used)
 #ifndef NSB_QS_TARGET
 #define NSB_QS_TARGET 4096
 #endif
@@ -111,6 +112,7 @@ struct QsCtx {
   Key* spl[2];
   uint16_t* cells[2];  // 16 per pivot slot: the classifier's prefix cells
   uint8_t* ids;        // bucket id of every key of the level (count -> scatter)
+  uint16_t* chist;     // per chunk: its kQsHistStride bucket counts (count -> scatter)
   uint32_t* cnt[2];
   unsigned long long* fill[2];  // bucket write cursors (absolute positions)
   QsJob* jobs[3];
@@ -556,8 +558,12 @@ __global__ void __launch_bounds__(kQsNT, 2) qs_count_kernel(QsCtx<Key> c, int le
     }
     __syncthreads();
     uint32_t* cn = c.cnt[level & 1] + g.cnt_off;
-    for (int b = tid; b < NB; b += kQsNT)
-      if (hist[b]) atomicAdd(&cn[b], hist[b]);
+    uint16_t* chh = c.chist + ch * kQsHistStride;  // a chunk holds <= 8192 keys: counts fit 16 bits
+    for (int b = tid; b < NB; b += kQsNT) {
+      const uint32_t h = hist[b];
+      chh[b] = (uint16_t)h;
+      if (h) atomicAdd(&cn[b], h);
+    }
   }
 }
 
@@ -752,11 +758,9 @@ __global__ void __launch_bounds__(kQsNT, 2) qs_scatter_kernel(QsCtx<Key> c, int 
   for (int64_t ch = (int64_t)blockIdx.x * per; ch < ch_end; ++ch) {
     const QsSeg g = qs_seg(c, level, qs_seg_of_chunk(c, level, ch));
     const int NB = 2 * g.B - 1;
-    __syncthreads();
-    for (int i = tid; i < NB; i += kQsNT) hist[i] = 0;
-    __syncthreads();
     const int64_t c0 = g.start + (ch - g.chunk0) * kQsChunk;
     const int64_t c1 = min(g.start + g.len, c0 + kQsChunk);
+    // this chunk's keys and ids: in flight while the bucket starts are set up
     Key k[kQsPer];
     int b[kQsPer];
 #pragma unroll
@@ -766,16 +770,32 @@ __global__ void __launch_bounds__(kQsNT, 2) qs_scatter_kernel(QsCtx<Key> c, int 
       k[u] = in ? __ldcs(X + i) : Key(0);
       b[u] = in ? (int)__ldcs(c.ids + i) : -1;
     }
-    uint32_t pk[kQsPer];  // rank-in-bucket << 8 | bucket, 0xffffffff = no key
-    const bool full = c1 - c0 == kQsChunk;  // all but a segment's last chunk: no per-key guards
+    // The count kernel left this chunk's bucket counts: their exclusive scan
+    // gives every bucket's start in the staged chunk BEFORE any key is ranked,
+    // so one shared atomic per key returns its final staging position (no
+    // second pass over the keys, no rank kept in registers), and the global
+    // range of every bucket is reserved up front (one atomic per bucket whose
+    // round trip hides under the ranking).
+    const uint32_t cnt = tid < NB ? (uint32_t)__ldcg(c.chist + ch * kQsHistStride + tid) : 0u;
+    __syncthreads();  // the previous chunk's write-out is done with hist / delta / the stage
+    const int64_t ls = qs_block_scan(cnt, wtot);
+    unsigned long long* fill = c.fill[level & 1] + g.cnt_off;
+    unsigned long long gb = 0ull;
+    if (tid < NB) {
+      if (cnt) gb = atomicAdd(&fill[tid], (unsigned long long)cnt);
+      hist[tid] = (uint32_t)ls;
+    }
+    __syncthreads();
+    const int total = (int)(c1 - c0);
+    const bool full = total == kQsChunk;  // all but a segment's last chunk: no per-key guards
+    const uint32_t hist_s = (uint32_t)__cvta_generic_to_shared(hist);
     if (full) {
-      const uint32_t hist_s = (uint32_t)__cvta_generic_to_shared(hist);
 #pragma unroll
       for (int u = 0; u < kQsPer; ++u) {
         int uni;
         __match_all_sync(kFull, b[u], &uni);
-        uint32_t r;
-        if (uni) {  // one bucket for the whole warp (sorted input)
+        uint32_t p;
+        if (uni) {  // one bucket for the whole warp (sorted input): one atomic for 32 keys
           uint32_t base = 0;
           // (plain PTX: nvcc wraps a one-lane atomicAdd in its own warp aggregation)
           if (lane == 0)
@@ -783,48 +803,41 @@ __global__ void __launch_bounds__(kQsNT, 2) qs_scatter_kernel(QsCtx<Key> c, int 
                          : "=r"(base)
                          : "r"(hist_s + 4u * (uint32_t)b[u])
                          : "memory");
-          r = __shfl_sync(kFull, base, 0) + (uint32_t)lane;
+          p = __shfl_sync(kFull, base, 0) + (uint32_t)lane;
         } else {
-          r = atomicAdd(&hist[b[u]], 1u);
+          p = atomicAdd(&hist[b[u]], 1u);
         }
-        pk[u] = (r << 8) | (uint32_t)b[u];
+        NSB_DCHECK(b[u] >= 0 && b[u] < NB && p < (uint32_t)kQsChunk);
+        skey[p] = k[u];
+        sbid[p] = (uint8_t)b[u];
       }
     } else {
 #pragma unroll
-      for (int u = 0; u < kQsPer; ++u) {
-        const int b0 = __shfl_sync(kFull, b[u], 0);
-        uint32_t r;
-        if (__all_sync(kFull, b[u] == b0)) {  // one bucket for the whole warp
+      for (int u = 0; u < kQsPer; ++u) {  // a segment's last chunk: absent keys have b = -1
+        int uni;
+        __match_all_sync(kFull, b[u], &uni);
+        uint32_t p = 0;
+        if (uni) {
           uint32_t base = 0;
-          if (lane == 0 && b0 >= 0) base = atomicAdd(&hist[b0], 32u);
-          r = __shfl_sync(kFull, base, 0) + (uint32_t)lane;
-        } else {
-          r = b[u] >= 0 ? atomicAdd(&hist[b[u]], 1u) : 0u;
+          if (lane == 0 && b[u] >= 0)
+            asm volatile("atom.shared.add.u32 %0, [%1], 32;"
+                         : "=r"(base)
+                         : "r"(hist_s + 4u * (uint32_t)b[u])
+                         : "memory");
+          p = __shfl_sync(kFull, base, 0) + (uint32_t)lane;
+        } else if (b[u] >= 0) {
+          p = atomicAdd(&hist[b[u]], 1u);
         }
-        pk[u] = b[u] >= 0 ? (r << 8) | (uint32_t)b[u] : 0xffffffffu;
+        if (b[u] >= 0) {
+          NSB_DCHECK(b[u] < NB && p < (uint32_t)total);
+          skey[p] = k[u];
+          sbid[p] = (uint8_t)b[u];
+        }
       }
     }
-    __syncthreads();
-    // local bucket starts (exclusive scan) and one global reservation per bucket
-    const uint32_t cnt = tid < NB ? hist[tid] : 0u;
-    const int64_t ls = qs_block_scan(cnt, wtot);
-    unsigned long long* fill = c.fill[level & 1] + g.cnt_off;
-    if (tid < NB) {
-      const unsigned long long gb = cnt ? atomicAdd(&fill[tid], (unsigned long long)cnt) : 0ull;
-      hist[tid] = (uint32_t)ls;
-      delta[tid] = (long long)gb - (long long)ls;
-    }
+    if (tid < NB) delta[tid] = (long long)gb - (long long)ls;
     __syncthreads();
     if (full) {
-#pragma unroll
-      for (int u = 0; u < kQsPer; ++u) {
-        const int bb = (int)(pk[u] & 0xffu);
-        const int p = (int)hist[bb] + (int)(pk[u] >> 8);
-        NSB_DCHECK(bb < NB && p >= 0 && p < kQsChunk);
-        skey[p] = k[u];
-        sbid[p] = (uint8_t)bb;
-      }
-      __syncthreads();
 #pragma unroll
       for (int u = 0; u < kQsPer; ++u) {
         const int i = u * kQsNT + tid;
@@ -833,18 +846,6 @@ __global__ void __launch_bounds__(kQsNT, 2) qs_scatter_kernel(QsCtx<Key> c, int 
         Y[delta[sbid[i]] + i] = skey[i];
       }
     } else {
-#pragma unroll
-      for (int u = 0; u < kQsPer; ++u) {
-        if (pk[u] != 0xffffffffu) {
-          const int bb = (int)(pk[u] & 0xffu);
-          const int p = (int)hist[bb] + (int)(pk[u] >> 8);
-          NSB_DCHECK(bb < NB && p >= 0 && p < (int)(c1 - c0));
-          skey[p] = k[u];
-          sbid[p] = (uint8_t)bb;
-        }
-      }
-      __syncthreads();
-      const int total = (int)(c1 - c0);
       for (int i = tid; i < total; i += kQsNT) {
         NSB_DCHECK(delta[sbid[i]] + i >= g.start && delta[sbid[i]] + i < g.start + g.len);
         Y[delta[sbid[i]] + i] = skey[i];
@@ -1041,6 +1042,7 @@ static size_t qs_temp_bytes(int64_t nseg0, int64_t len0) {
   const QsSizes z = qs_sizes(nseg0, len0);
   size_t b = align_up((size_t)n * sizeof(Key), 256) + align_up(sizeof(QsCounters), 256);
   b += align_up((size_t)n, 256);
+  b += align_up((size_t)z.max_chunks * kQsHistStride * 2, 256);
   b += 2 * align_up((size_t)z.max_segs * sizeof(QsSeg), 256);
   b += 2 * align_up((size_t)z.max_chunks * 4, 256);
   b += 2 * align_up((size_t)z.max_spl * sizeof(Key), 256);
@@ -1071,6 +1073,7 @@ static QsCtx<Key> qs_carve(Key* keys, void* d_temp, int64_t nseg0, int64_t len0)
   c.B0 = qs_buckets(len0);
   c.ctr = reinterpret_cast<QsCounters*>(take(sizeof(QsCounters)));
   c.ids = reinterpret_cast<uint8_t*>(take((size_t)n));
+  c.chist = reinterpret_cast<uint16_t*>(take((size_t)z.max_chunks * kQsHistStride * 2));
   for (int i = 0; i < 2; ++i) c.segs[i] = reinterpret_cast<QsSeg*>(take((size_t)z.max_segs * sizeof(QsSeg)));
   for (int i = 0; i < 2; ++i) c.chunk_seg[i] = reinterpret_cast<int32_t*>(take((size_t)z.max_chunks * 4));
   for (int i = 0; i < 2; ++i) c.spl[i] = reinterpret_cast<Key*>(take((size_t)z.max_spl * sizeof(Key)));
