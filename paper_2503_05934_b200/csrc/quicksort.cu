@@ -739,8 +739,11 @@ __host__ __device__ constexpr int qs_scatter_smem() {
   return kQsChunk * (int)sizeof(Key) + kQsChunk;  // keys + one-byte bucket ids
 }
 
+#ifndef NSB_QS_SCATTER_MINB
+#define NSB_QS_SCATTER_MINB 2
+#endif
 template <class Key>
-__global__ void __launch_bounds__(kQsNT, 2) qs_scatter_kernel(QsCtx<Key> c, int level) {
+__global__ void __launch_bounds__(kQsNT, NSB_QS_SCATTER_MINB) qs_scatter_kernel(QsCtx<Key> c, int level) {
   pdl_wait();
   pdl_trigger();
   __shared__ uint32_t hist[2 * kQsMaxB];    // counts, then local starts
