@@ -15,7 +15,8 @@
 //             (s[j-1] < k < s[j]) and "equal" buckets (k == s[j]); an equal
 //             bucket is constant, which keeps heavy duplicates from
 //             unbalancing the recursion (the job of hoare_partition's j==high
-//             fix-up for one pivot, hybrid.hpp:130);
+//             fix-up for one pivot, hybrid.hpp:130); it stores every key's
+//             one-byte bucket id and every chunk's bucket counts;
 //   plan    : one CTA per segment scans its bucket counts into positions and
 //             sorts the buckets out: the ones that fit a CTA become leaf jobs
 //             (neighbouring small buckets packed into one tile, since they
@@ -26,7 +27,8 @@
 //   scatter : keys move to their buckets through a shared-memory multisplit,
 //             so each bucket's keys leave a CTA as one contiguous run
 //             (coalesced stores) at a range reserved with one global atomic
-//             per (CTA, bucket).
+//             per (chunk, bucket); the chunk's counts are scanned first, so
+//             one shared atomic per key returns its staging position.
 // The number of levels follows from n alone (each level divides a segment by
 // up to 256); after the last level every leaf job is sorted on chip by
 // cta_sort with the config's network base case (try_base_case,
