@@ -156,7 +156,11 @@ static int v2_pass_t(const Key* src, Key* dst, int64_t n, int64_t R, int64_t* mp
   // in-kernel search up to 4096 tiles of <= 4096 keys, 2048 larger tiles
   // (tools/fused_ab.sh: 2^24 keys in 2114 <256,31> tiles 480 -> 473 us with
   // the partition kernel; 2^23 in 2850 <128,23> tiles 235 vs 261 us fused)
-  const int64_t fused_max = NT * K > 4096 ? tu.fused_max_tiles / 2 : tu.fused_max_tiles;
+  // int64 keys: 1024 (measured: 2^23 keys in 2850 <128,23> tiles 540 us fused
+  // vs 419 us with the partition kernel, 2^22 261 vs 242 us; equal below)
+  const int64_t fused_max = sizeof(Key) == 8 ? tu.fused_max_tiles / 4
+                            : NT * K > 4096  ? tu.fused_max_tiles / 2
+                                             : tu.fused_max_tiles;
   if (mt <= fused_max) {
     // few tiles: every CTA finds its own split (no partition launch)
     {
