@@ -314,8 +314,54 @@ int merge_sort_device(int64_t* d_keys, size_t n, int leaf, void* d_temp, size_t 
   return merge_sort_device_t(d_keys, n, leaf, d_temp, temp_bytes, s);
 }
 
+// Segments of up to 512 keys: 2^LV lanes of a warp per segment (16 keys per
+// lane, missing keys padded with the key maximum), so a warp sorts 32 >> LV
+// segments at once and a CTA of 8 warps 256 >> LV of them — a batch of tiny
+// segments is not one 32-thread CTA per segment (2^23 segments of 8 keys:
+// 14.8 ms that way).  Each lane sorts its 16 keys with the config's base case
+// and in-register merges, LV warp-bitonic levels join the lanes of a segment;
+// no shared memory.
+template <int LV, int LEAF, class Key>
+__global__ void __launch_bounds__(256) small_segments_kernel(Key* __restrict__ keys, int64_t nseg,
+                                                             int seg_len) {
+  constexpr int G = 1 << LV;     // lanes per segment
+  constexpr int SPW = 32 >> LV;  // segments per warp
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t seg = ((int64_t)blockIdx.x * 8 + warp) * SPW + (lane >> LV);
+  const int j = lane & (G - 1);
+  pdl_wait();
+  pdl_trigger();
+  const int cnt = seg < nseg ? max(0, min(16, seg_len - 16 * j)) : 0;
+  Key* p = keys + (seg < nseg ? seg * seg_len + 16 * j : 0);
+  // (16-byte vector loads / stores of a lane's 16 keys measured slower: 0.55
+  // vs 0.32 ms for 2^20 segments of 64 keys)
+  Key v[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) v[k] = k < cnt ? p[k] : KeyT<Key>::kMax;
+  thread_sort<LEAF>(v);  // the network base case (try_base_case, hybrid.hpp:48-56)
+  if constexpr (LV > 0) warp_bitonic<LV>(v, lane);
+  // the segment's lanes hold its sorted keys blocked, the pads at the end
+#pragma unroll
+  for (int k = 0; k < 16; ++k)
+    if (k < cnt) p[k] = v[k];
+}
+
+template <int LV, int LEAF, class Key>
+static int launch_small_segments(Key* d_keys, int64_t nseg, int seg_len, cudaStream_t s) {
+  const int64_t per_cta = 8 * (32 >> LV);
+  const int64_t ctas = (nseg + per_cta - 1) / per_cta;
+  if (ctas > INT_MAX) return NS_ERR_INVALID;
+  {
+    Prof prof(PK_TILE_SORT, s);
+    const cudaError_t e = launch_pdl(nseg * seg_len, small_segments_kernel<LV, LEAF, Key>,
+                                     (unsigned)ctas, 256, 0, s, d_keys, nseg, seg_len);
+    if (e != cudaSuccess) return check_cuda(e, "small_segments_kernel");
+  }
+  return check_launch("small_segments_kernel");
+}
+
 // One CTA per segment, the tile sized to the segment (a 100-key segment does
-// not pay for an 8192-key tile).
+// not pay for an 8192-key tile); segments of up to 512 keys share warps.
 template <class Key>
 static int tile_sort_segments_t(Key* d_keys, size_t num_segments, size_t seg_len, int leaf,
                                 cudaStream_t s) {
@@ -325,6 +371,12 @@ static int tile_sort_segments_t(Key* d_keys, size_t num_segments, size_t seg_len
   const int64_t g = (int64_t)num_segments;
   return with_leaf(leaf, [&](auto L) {
     constexpr int LF = decltype(L)::value;
+    if (seg_len <= 16) return launch_small_segments<0, LF>(d_keys, g, st, s);
+    if (seg_len <= 32) return launch_small_segments<1, LF>(d_keys, g, st, s);
+    if (seg_len <= 64) return launch_small_segments<2, LF>(d_keys, g, st, s);
+    if (seg_len <= 128) return launch_small_segments<3, LF>(d_keys, g, st, s);
+    if (seg_len <= 256) return launch_small_segments<4, LF>(d_keys, g, st, s);
+    // (a whole warp per segment: the staged one-warp tile is faster, 0.23 vs 0.39 ms per 2^26 keys)
     if (seg_len <= 512) return launch_blocksort<32, 16, LF>(d_keys, d_keys, n, st, g, s);
     if (seg_len <= 2048) return launch_blocksort<128, 16, LF>(d_keys, d_keys, n, st, g, s);
     if constexpr (std::is_same_v<Key, int32_t>) {

@@ -185,6 +185,33 @@ def test_segmented_odd_lengths(ns, cuda, oracle):
             assert np.array_equal(from_dev(t), want), (seg, cfg)
 
 
+@pytest.mark.parametrize("key_bytes", [4, 8])
+def test_segmented_small_segments_share_warps(ns, cuda, oracle, key_bytes):
+    """Segments of up to 512 keys: 2^LV lanes of a warp per segment, several
+    segments per warp (small_segments_kernel).  Every lane-group size and its
+    boundaries, segment counts that leave warps and CTAs partly empty, every
+    leaf shape, duplicates and the extreme key values (the pad value itself)."""
+    import torch
+    dt = np.int32 if key_bytes == 4 else np.int64
+    info = np.iinfo(dt)
+    rng = np.random.default_rng(7)
+    for seg in (1, 2, 7, 8, 15, 16, 17, 31, 32, 33, 63, 64, 65, 100, 128, 129, 200, 256, 257,
+                300, 511, 512):
+        for nseg in (1, 3, 37, 255, 257, 1000):
+            a = rng.integers(info.min, info.max, size=nseg * seg, dtype=dt, endpoint=True)
+            a[:: max(1, seg // 2)] = info.max   # real keys equal to the pad value
+            a[1:: 5] = info.min
+            if seg > 3:
+                m = min(len(a[2:: 3]), len(a[3:: 3]))
+                a[2:: 3][:m] = a[3:: 3][:m]  # duplicates
+            want = np.sort(a.reshape(nseg, seg), axis=1).reshape(-1)
+            for cfg in ("6To8", "Classic") if nseg == 37 else ("3To5",):
+                for algo in (ns.Algorithm.merge_sort, ns.Algorithm.quick_sort):
+                    t = torch.from_numpy(a.copy()).to(cuda)
+                    ns.segmented_sort(t, seg, ns.find_config(cfg), algo)
+                    assert np.array_equal(t.cpu().numpy(), want), (seg, nseg, cfg, algo)
+
+
 @pytest.mark.parametrize("nseg,seg", [(7, 16385), (5, 40000), (3, 100_001), (2, (1 << 21) + 3),
                                       (64, 32768), (40, 50_000)])
 def test_segmented_merge_sort_long_segments_batched(ns, cuda, oracle, nseg, seg):
