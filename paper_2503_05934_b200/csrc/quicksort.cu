@@ -94,6 +94,7 @@ struct QsJob {
   int32_t pad;
 };
 enum { kJobSort = 0, kJobCopy = 1, kJobBig = 2 };
+constexpr int64_t kQsCopyChunk = 32768;  // keys per copy job of a big constant bucket
 
 struct QsCounters {  // device-side list lengths
   unsigned long long nseg[2], nchunk[2], nbkt[2], nspl[2];
@@ -666,7 +667,7 @@ __global__ void __launch_bounds__(kQsNT) qs_plan_kernel(QsCtx<Key> c, int level,
     // this thread's job (packed run, own bucket, copy, fallback) or new segment
     int cls = -1, type = kJobSort;
     int64_t jstart = pos, jlen = 0;
-    uint32_t jlocal = 0;
+    uint32_t jlocal = 0, njob = 1;
     int32_t nB = 0, nch = 0;
     uint32_t slocal = 0;
     uint32_t koff = 0, boff = 0, poff = 0;
@@ -683,6 +684,9 @@ __global__ void __launch_bounds__(kQsNT) qs_plan_kernel(QsCtx<Key> c, int level,
         if (src_flag) {
           cls = 2;
           type = kJobCopy;
+          // a big constant bucket is copied by many CTAs, kQsCopyChunk keys each
+          // (one job per bucket made all-equal input 25x slower than random)
+          njob = (uint32_t)((jlen + kQsCopyChunk - 1) / kQsCopyChunk);
         }
       } else if (!last) {
         nB = qs_buckets(jlen);
@@ -696,7 +700,7 @@ __global__ void __launch_bounds__(kQsNT) qs_plan_kernel(QsCtx<Key> c, int level,
         type = kJobBig;
       }
     }
-    if (cls >= 0) jlocal = atomicAdd(&s_ccnt[cls], 1u);
+    if (cls >= 0) jlocal = atomicAdd(&s_ccnt[cls], njob);
     __syncthreads();
     if (tid < 3) s_jbase[tid] = s_ccnt[tid] ? atomicAdd(&c.ctr->njobs[tid], (unsigned long long)s_ccnt[tid]) : 0ull;
     if (tid == 3 && s_nn) {
@@ -708,9 +712,18 @@ __global__ void __launch_bounds__(kQsNT) qs_plan_kernel(QsCtx<Key> c, int level,
     __syncthreads();
     if (cls >= 0) {
       const unsigned long long at = s_jbase[cls] + jlocal;
-      NSB_DCHECK(at < (unsigned long long)c.max_jobs);
-      if (at < (unsigned long long)c.max_jobs)
-        c.jobs[cls][at] = QsJob{jstart, jlen, src_flag | (type << 1), 0};
+      NSB_DCHECK(at + njob <= (unsigned long long)c.max_jobs);
+      if (njob == 1) {
+        if (at < (unsigned long long)c.max_jobs)
+          c.jobs[cls][at] = QsJob{jstart, jlen, src_flag | (type << 1), 0};
+      } else {
+        for (uint32_t q = 0; q < njob; ++q)
+          if (at + q < (unsigned long long)c.max_jobs)
+            c.jobs[cls][at + q] =
+                QsJob{jstart + (int64_t)q * kQsCopyChunk,
+                      min((int64_t)kQsCopyChunk, jlen - (int64_t)q * kQsCopyChunk),
+                      src_flag | (type << 1), 0};
+      }
     }
     if (nB) {
       const unsigned long long sid = s_sbase + slocal, k0 = s_kbase + koff;
@@ -1038,6 +1051,8 @@ static QsSizes qs_sizes(int64_t nseg0, int64_t len0) {
   // every job holds at least one non-empty bucket of one level
   z.max_jobs = std::max<int64_t>(nseg0 * (2 * qs_buckets(len0) - 1), 0) +
                (int64_t)levels * (4 * n / kQsTarget + 3 * z.max_segs) + 64;
+  // plus the extra copy jobs of big constant buckets (one per kQsCopyChunk keys)
+  z.max_jobs += (int64_t)levels * (n / kQsCopyChunk + 1);
   return z;
 }
 

@@ -78,6 +78,37 @@ def test_quick_sort_duplicate_shapes(ns, cuda, kind):
     assert np.array_equal(t.cpu().numpy(), np.sort(a))
 
 
+def test_quick_sort_duplicates_are_not_a_cliff(ns, cuda):
+    """A big constant bucket is moved by many CTAs (one copy job per 32768
+    keys), so duplicate-heavy input costs no more than random input: with one
+    copy job per bucket, 16 M equal keys took 25x the random time.  Loose
+    bound (2x) on device time, checked sorted."""
+    import torch
+    n = 1 << 24
+    g = torch.Generator(device="cuda").manual_seed(3)
+    r = torch.randint(0, 2**31 - 1, (n,), device=cuda, dtype=torch.int32, generator=g)
+    cfg = ns.find_config("3To5")
+
+    def timed(a):
+        w = a.clone()
+        best = 1e9
+        for _ in range(3):
+            w.copy_(a)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            ns.optimized_quick_sort(w, cfg)
+            e1.record()
+            torch.cuda.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        assert ns.count_inversions(w) == 0 and ns.multiset_digest(w) == ns.multiset_digest(a)
+        return best
+
+    t_random = timed(r)
+    for a in (torch.full((n,), 7, device=cuda, dtype=torch.int32), r & 1, r & 15,
+              torch.where((r % 100) == 0, r, torch.full_like(r, 123456))):
+        assert timed(a) < 2.0 * t_random
+
+
 def test_quick_sort_oversized_bucket_fallback(ns, cuda):
     """Pivots drawn from an input built against the sampling positions: every
     sampled key is spread over a wide range, every other key is distinct and
