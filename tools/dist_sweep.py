@@ -8,15 +8,16 @@ sys.path.insert(0, '.')
 import paper_2503_05934_b200 as ns  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 1 << 24
+DT = torch.int64 if len(sys.argv) > 2 and sys.argv[2] == 'i64' else torch.int32
 dev = torch.device('cuda')
 g = torch.Generator(device='cuda').manual_seed(1)
-r = torch.randint(0, 2**31 - 1, (n,), device=dev, dtype=torch.int32, generator=g)
-ar = torch.arange(n, device=dev, dtype=torch.int32)
+r = torch.randint(0, 2**31 - 1, (n,), device=dev, dtype=DT, generator=g)
+ar = torch.arange(n, device=dev, dtype=DT)
 shapes = {
     'random': r,
     'sorted': ar,
     'reversed': ar.flip(0).contiguous(),
-    'all_equal': torch.full((n,), 7, device=dev, dtype=torch.int32),
+    'all_equal': torch.full((n,), 7, device=dev, dtype=DT),
     'two_values': (r & 1),
     '16_values': (r & 15),
     '1000_values': (r % 1000),
