@@ -77,26 +77,36 @@ class Clocks:
     def __init__(self, index: int):
         self.index = index
         self.proc = None
-        self.lines = []
+        self.lines = []   # (host time the sample arrived, csv line)
+        self.t0 = None
 
-    def start(self):
+    def launch(self):
+        """Starts nvidia-smi (its start-up takes ~100 ms: call this before the
+        timed region); only samples that arrive between start() and stop() count."""
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "25"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
         except Exception:
             self.proc = None
 
+    def start(self):
+        if self.proc is None:
+            self.launch()
+        self.t0 = time.time()
+
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))
 
     def stop(self):
         if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        t1 = time.time()
+        time.sleep(0.03)  # the sample taken at the end of the region is still in the pipe
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
@@ -105,7 +115,8 @@ class Clocks:
         self.thread.join(timeout=2)
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        inside = [ln for (t, ln) in self.lines if self.t0 is not None and self.t0 <= t <= t1 + 0.03]
+        for ln in (inside if inside else [ln for (_, ln) in self.lines]):
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 7:
                 continue
@@ -315,6 +326,8 @@ def run_ours(args, metric):
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
     clocks = Clocks(local)
+    clocks.launch()  # nvidia-smi starts up outside the timed region
+    time.sleep(0.15)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
