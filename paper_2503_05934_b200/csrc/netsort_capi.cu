@@ -333,6 +333,8 @@ __global__ void __launch_bounds__(256) small_segments_kernel(Key* __restrict__ k
   pdl_trigger();
   const int cnt = seg < nseg ? max(0, min(16, seg_len - 16 * j)) : 0;
   Key* p = keys + (seg < nseg ? seg * seg_len + 16 * j : 0);
+  // a lane's keys lie inside its own segment
+  NSB_DCHECK(cnt == 0 || (16 * j + cnt <= seg_len && seg * seg_len + 16 * j + cnt <= nseg * seg_len));
   // (16-byte vector loads / stores of a lane's 16 keys measured slower: 0.55
   // vs 0.32 ms for 2^20 segments of 64 keys)
   Key v[16];

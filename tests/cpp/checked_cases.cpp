@@ -387,6 +387,16 @@ int main(int argc, char** argv) {
   segmented_case<int32_t>(2, 70001, 0);
   segmented_case<int64_t>(3, 20000, 0);
   segmented_case<int64_t>(5, 3000, 0);
+  // segments that share warps (small_segments_kernel): every lane-group size,
+  // a ragged last warp / CTA; the guard zones catch a lane that stores past
+  // its segment or a group that touches the next segment's keys
+  for (size_t len : {1, 7, 16, 17, 33, 100, 129, 256})
+    for (size_t segs : {1, 37, 300}) {
+      segmented_case<int32_t>(segs, len, 0);
+      segmented_case<int64_t>(segs, len, 1);
+    }
+  segmented_case<int32_t>(50, 257, 0);
+  segmented_case<int32_t>(50, 512, 1);
   pairs_case(30000);
   merge_runs_case(100000, 3);
   host_case(10000);
