@@ -180,6 +180,8 @@ constexpr int kSmallTile = 16384;  // largest array one CTA sorts on chip
 // quick sort of nseg back-to-back segments of len (> kSmallTile) keys each,
 // planned on the device (quicksort.cu)
 size_t quick_sort_segments_temp(size_t nseg, size_t len, size_t key_bytes);
+// largest array / segment the quick sort hands to the merge layer (quicksort.cu)
+size_t qs_base_max();
 int quick_sort_segments_device(int32_t* keys, size_t nseg, size_t len, int leaf, void* d_temp,
                                size_t temp_bytes, cudaStream_t s);
 int quick_sort_segments_device(int64_t* keys, size_t nseg, size_t len, int leaf, void* d_temp,

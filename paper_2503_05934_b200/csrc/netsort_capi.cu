@@ -843,7 +843,9 @@ static int segmented_sort(Key* d_keys, size_t num_segments, size_t seg_len, int 
   if (num_segments > (size_t)INT64_MAX / sizeof(Key) / seg_len) return NS_ERR_INVALID;
   const int leaf = leaf_of(width_mask, varsort_max);
   if (seg_len <= (size_t)kSmT) return tile_sort_segments_t(d_keys, num_segments, seg_len, leaf, s);
-  if (algorithm == NS_QUICK_SORT)
+  // quick sort: segments of up to qs_base_max() keys are its base case (the
+  // merge layer, all segments at once: 0.57-0.9 ms per 2^26 keys against 1.1)
+  if (algorithm == NS_QUICK_SORT && seg_len > qs_base_max())
     return quick_sort_segments_device(d_keys, num_segments, seg_len, leaf, d_temp, temp_bytes, s);
   return merge_sort_segments_t(d_keys, num_segments, seg_len, leaf, d_temp, temp_bytes, s);
 }

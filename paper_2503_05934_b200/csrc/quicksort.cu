@@ -42,6 +42,7 @@
 #include <algorithm>
 #include <climits>
 #include <cstdint>
+#include <cstdlib>
 #include <mutex>
 #include <type_traits>
 #include <utility>
@@ -1213,12 +1214,31 @@ static int quick_sort_segments(Key* keys, int64_t nseg0, int64_t len0, int leaf,
   return NS_OK;
 }
 
+// The quick sort's base case.  Its recursion bottoms out where partitioning
+// stops paying: an array (or segment) of up to qs_base_max() keys is finished
+// by the merge layer — tile sort plus a few pairwise passes — instead of a
+// partition level and bucket sorts.  Measured by graph replay (tools/
+// qs_vs_ms.py): one partition level is a chain of five latency-bound kernels
+// (38-45 us from 24 K to 512 K keys against 21-42 us for the merge layer; at
+// 16385 keys 38 vs 16 us).  Default 2^19; NSB_QS_BASE_MAX overrides it (the
+// tests set 16384 so that every partition path also runs at small sizes).
+size_t qs_base_max() {
+  static const size_t v = [] {
+    const char* e = getenv("NSB_QS_BASE_MAX");
+    const long long x = e ? atoll(e) : (1ll << 19);
+    return (size_t)std::max<long long>(x, kSmallTile);
+  }();
+  return v;
+}
+
 size_t quick_sort_temp(size_t n) {
   if (n <= (size_t)kSmallTile) return merge_sort_temp(n);
+  if (n <= qs_base_max()) return std::max(merge_sort_temp(n), qs_temp_bytes<int32_t>(1, (int64_t)n));
   return qs_temp_bytes<int32_t>(1, (int64_t)n);
 }
 size_t quick_sort_temp_i64(size_t n) {
   if (n <= (size_t)kSmallTile) return merge_sort_temp_i64(n);
+  if (n <= qs_base_max()) return std::max(merge_sort_temp_i64(n), qs_temp_bytes<int64_t>(1, (int64_t)n));
   return qs_temp_bytes<int64_t>(1, (int64_t)n);
 }
 size_t quick_sort_segments_temp(size_t nseg, size_t len, size_t key_bytes) {
@@ -1250,9 +1270,8 @@ int ns_quick_sort_i32(int32_t* d_keys, size_t n, uint32_t width_mask, int varsor
   if (n <= 1) return NS_OK;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int leaf = leaf_of(width_mask, varsort_max);
-  // n <= kSmallTile: one CTA (or two tiles and a merge) — the merge sort's
-  // small path, whose tile sort is this layer's base case
-  if (n <= (size_t)kSmallTile) return merge_sort_device(d_keys, n, leaf, d_temp, temp_bytes, s);
+  // the base case: the merge layer (one CTA, or tiles and a few passes)
+  if (n <= qs_base_max()) return merge_sort_device(d_keys, n, leaf, d_temp, temp_bytes, s);
   return quick_sort_segments(d_keys, 1, (int64_t)n, leaf, d_temp, temp_bytes, s);
 }
 
@@ -1265,7 +1284,7 @@ int ns_quick_sort_i64(int64_t* d_keys, size_t n, uint32_t width_mask, int varsor
   if (n <= 1) return NS_OK;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int leaf = leaf_of(width_mask, varsort_max);
-  if (n <= (size_t)kSmallTile) return merge_sort_device(d_keys, n, leaf, d_temp, temp_bytes, s);
+  if (n <= qs_base_max()) return merge_sort_device(d_keys, n, leaf, d_temp, temp_bytes, s);
   return quick_sort_segments(d_keys, 1, (int64_t)n, leaf, d_temp, temp_bytes, s);
 }
 

@@ -3,6 +3,13 @@ import sys
 
 import pytest
 
+# The quick sort hands arrays / segments of up to 2^19 keys to the merge layer
+# (its base case, quicksort.cu qs_base_max).  The tests lower that to one tile
+# so that every partition path also runs at test sizes; the default policy is
+# checked by tests/test_gpu_quicksort.py::test_quick_sort_default_base_case
+# (a child process without this variable), the bench and smoke().
+os.environ.setdefault("NSB_QS_BASE_MAX", "16384")
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)

@@ -109,6 +109,44 @@ def test_quick_sort_duplicates_are_not_a_cliff(ns, cuda):
         assert timed(a) < 2.0 * t_random
 
 
+def test_quick_sort_default_base_case(cuda):
+    """The shipped policy (no NSB_QS_BASE_MAX): arrays and segments of up to
+    2^19 keys are the quick sort's base case (merge layer), larger ones are
+    partitioned; both sides of the threshold, device, host and segmented entry
+    points, checked against numpy in a child process."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import numpy as np, torch, sys
+sys.path.insert(0, ".")
+import paper_2503_05934_b200 as ns
+cfg = ns.find_config("3To5")
+rng = np.random.default_rng(11)
+for n in (16385, 100003, (1 << 19) - 1, 1 << 19, (1 << 19) + 1, 1_500_000):
+    for dt in (np.int32, np.int64):
+        a = rng.integers(-2**31, 2**31 - 1, n).astype(dt)
+        t = torch.from_numpy(a.copy()).cuda()
+        ns.optimized_quick_sort(t, cfg)
+        assert np.array_equal(t.cpu().numpy(), np.sort(a)), (n, dt)
+    h = rng.integers(-2**31, 2**31 - 1, n).astype(np.int32)
+    w = h.copy()
+    ns.optimized_quick_sort(w, cfg)
+    assert np.array_equal(w, np.sort(h)), n
+for nseg, seg in ((5, 20000), (3, 1 << 19), (2, (1 << 19) + 5)):
+    a = rng.integers(-2**31, 2**31 - 1, nseg * seg).astype(np.int32)
+    t = torch.from_numpy(a.copy()).cuda()
+    ns.segmented_sort(t, seg, cfg, ns.Algorithm.quick_sort)
+    assert np.array_equal(t.cpu().numpy(), np.sort(a.reshape(nseg, seg), axis=1).reshape(-1)), (nseg, seg)
+print("default-policy ok")
+'''
+    env = {k: v for k, v in os.environ.items() if k != "NSB_QS_BASE_MAX"}
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0 and "default-policy ok" in r.stdout, r.stdout + r.stderr
+
+
 def test_quick_sort_oversized_bucket_fallback(ns, cuda):
     """Pivots drawn from an input built against the sampling positions: every
     sampled key is spread over a wide range, every other key is distinct and
